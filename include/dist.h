@@ -1,0 +1,192 @@
+/*
+ * dist.h -- C ABI of the B200-native DIST sphere-tracing hot path.
+ *
+ * One shared library (libdist_b200.so, sm_100a) exports these entry points.
+ * They are the drop-in boundary for the reference package `sdftrace`
+ * (/root/reference/pkg/src/sdftrace): every function below replaces one
+ * reference interface, cited as file:line.  All pointers named *_dev are
+ * device pointers owned by the caller (PyTorch allocates them); the library
+ * never allocates per call.  Every call is stream-ordered on `stream` and does
+ * not synchronise the host.  Return codes:
+ *   DIST_OK            0
+ *   DIST_ERR_CONFIG    2  -> ValueError            (bad shape / config)
+ *   DIST_ERR_NUMERIC   3  -> FloatingPointError    (non-finite gradient)
+ *   DIST_ERR_CUDA      4  -> RuntimeError          (CUDA / no device)
+ * dist_last_error() returns a thread-local message for the last failure.
+ * Handles are immutable after creation and safe to share across threads and
+ * streams ("fields are immutable; eval is pure").
+ */
+#ifndef DIST_B200_H
+#define DIST_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DIST_API __attribute__((visibility("default")))
+#else
+#define DIST_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DIST_OK 0
+#define DIST_ERR_CONFIG 2
+#define DIST_ERR_NUMERIC 3
+#define DIST_ERR_CUDA 4
+
+/* ray status codes, tracer.py:24 */
+#define DIST_MARCHING 0
+#define DIST_CONVERGED 1
+#define DIST_ESCAPED 2
+#define DIST_EXHAUSTED 3
+
+/* arithmetic of the decoder evaluation */
+#define DIST_PREC_FP64 0   /* SIMT fp64: the reference's own precision */
+#define DIST_PREC_FP32 1   /* SIMT fp32 */
+#define DIST_PREC_BF16X3 2 /* tcgen05 bf16 hi/lo 3-pass, fp32 accumulate in TMEM */
+
+/* warning bits in stats[3] */
+#define DIST_WARN_CAMERA_INSIDE 1   /* tracer.py:100-102 */
+
+typedef struct dist_decoder dist_decoder;
+
+/* Pinhole camera of one view: camera.py:25-61 (intrinsics) and 157-172
+ * (pose).  R is the world-to-camera rotation (row-major), origin the camera
+ * centre -R^T t.  `shape` selects the latent code (row of codes_dev). */
+typedef struct dist_camera {
+  double R[9];
+  double origin[3];
+  double fx, fy, cx, cy;
+  int32_t width, height;
+  int32_t shape;
+  int32_t reserved;
+} dist_camera;
+
+/* TraceConfig, tracer.py:27-50 (validated by the library as in :41-50). */
+typedef struct dist_trace_config {
+  double alpha, epsilon, normal_delta;
+  int32_t max_steps, k_samples, coarse_start_scale, split_interval;
+  int32_t use_dynamic_mask;
+  int32_t reserved;
+} dist_trace_config;
+
+/* Full-resolution SoA ray state, RayState of tracer.py:53-73, for V views of
+ * H x W rays, ray index = (view * H + j) * W + i.  topk_* are [n][K]. */
+typedef struct dist_ray_state {
+  double *d, *b;
+  uint8_t *status;
+  int32_t *steps;
+  double *topk_d, *topk_f, *topk_absf;
+} dist_ray_state;
+
+/* ---- library ---------------------------------------------------------- */
+DIST_API const char *dist_last_error(void);
+DIST_API int dist_device_info(int *sm_count, int *cc_major, int *cc_minor);
+/* number of kernel launches the library enqueued since load (bench audit) */
+DIST_API int64_t dist_launch_count(void);
+
+/* ---- decoder (NeuralField, fields.py:185-247) -------------------------- */
+/* W[l] is the reference's row-major W[in,out] float64 (fields.py:195-196),
+ * b[l] its bias; dims has n_layers+1 entries (dims[0] = latent_dim + 3 +
+ * 0, dims[n_layers] = 1).  skip_layer >= 0 selects the DeepSDF layout where
+ * layer `skip_layer` consumes concat(h, code, xyz);
+ * -1 is the reference's plain stack.  final_linear: 0 = tanh head, 1 =
+ * linear head (fields.py:200-201, 245-246).  Hidden activation is ReLU. */
+DIST_API int dist_decoder_create(const double *const *W, const double *const *b, int n_layers,
+                        const int32_t *dims, int latent_dim, int skip_layer,
+                        int final_linear, int precision, dist_decoder **out);
+DIST_API int dist_decoder_destroy(dist_decoder *dec);
+DIST_API int dist_decoder_precision(const dist_decoder *dec);
+
+/* Workspace needed by dist_eval / dist_eval_vjp for n points and S shapes. */
+DIST_API size_t dist_eval_workspace_size(const dist_decoder *dec, int64_t n, int n_shapes);
+
+/* NeuralField.evaluate (fields.py:233-247): f[i] = field(points[i], codes[shape[i]]).
+ * shape_dev may be NULL (all rows use code 0); codes_dev may be NULL when
+ * latent_dim == 0. */
+DIST_API int dist_eval(const dist_decoder *dec, const double *codes_dev, int n_shapes,
+              const double *points_dev, const int32_t *shape_dev, int64_t n,
+              double *f_dev, void *ws, size_t ws_bytes, void *stream);
+
+/* Taped evaluation + reverse sweep (fields.py:260-291 with
+ * autodiff.py:220-255): f, d(sum seed*f)/d code [S,D] and d/d points [n,3]
+ * (grad_points_dev may be NULL). */
+DIST_API int dist_eval_vjp(const dist_decoder *dec, const double *codes_dev, int n_shapes,
+                  const double *points_dev, const int32_t *shape_dev, int64_t n,
+                  const double *seed_dev, double *f_dev, double *grad_codes_dev,
+                  double *grad_points_dev, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- tracing (trace, tracer.py:221-252) --------------------------------- */
+DIST_API size_t dist_trace_workspace_size(const dist_decoder *dec, const dist_trace_config *cfg,
+                                 int n_views, int width, int height, int n_shapes);
+
+/* Coarse-to-fine, dynamic-mask, aggressive sphere tracing of V views that
+ * share one resolution.  Outputs: the final-level ray state, per-step query
+ * counts live_counts_dev[max_steps] (TraceResult.live_counts), and
+ * stats_dev[4] = {total_queries, nan_count, steps_done, warning bits}. */
+DIST_API int dist_trace(const dist_decoder *dec, const double *codes_dev, int n_shapes,
+               const dist_camera *cams_dev, int n_views, int width, int height,
+               const dist_trace_config *cfg, const dist_ray_state *out,
+               int64_t *live_counts_dev, int64_t *stats_dev, void *ws, size_t ws_bytes,
+               void *stream);
+
+/* ---- maps (shading.py:48-113) ------------------------------------------ */
+/* depth_map (+inf background), hard_mask, soft_silhouette for all V views,
+ * images [V,H,W].  Any output pointer may be NULL. */
+DIST_API int dist_maps(const dist_camera *cams_dev, int n_views, int width, int height,
+              const dist_trace_config *cfg, const dist_ray_state *st, double *depth_dev,
+              uint8_t *mask_dev, double *silhouette_dev, void *stream);
+
+/* normal_map (shading.py:73-94): six-probe central differences at every
+ * converged pixel, zero elsewhere; normals_dev [V,H,W,3]. */
+DIST_API size_t dist_normals_workspace_size(const dist_decoder *dec, int n_views, int width,
+                                   int height, int n_shapes);
+DIST_API int dist_normals(const dist_decoder *dec, const double *codes_dev, int n_shapes,
+                 const dist_camera *cams_dev, int n_views, int width, int height,
+                 const dist_trace_config *cfg, const dist_ray_state *st, double *normals_dev,
+                 void *ws, size_t ws_bytes, void *stream);
+
+/* ---- one latent-optimisation iterate (completion_objective,
+ *      optimize.py:102-138; HeadBundle shading.py:156-281; losses.py:54-117) */
+typedef struct dist_objective_io {
+  const double *obs_depth;       /* [V*H*W] observed camera z, +inf background; NULL = no depth term */
+  const uint8_t *obs_depth_mask; /* [V*H*W] trusted pixels or NULL (Observation.mask, losses.py:38-42) */
+  const double *obs_sil;         /* [V*H*W] binary silhouette target; NULL = no silhouette term */
+  double w_depth, w_sil, w_latent; /* LossWeights, losses.py:45-51 */
+  double *grad;                  /* out [S*D]: d total / d code (device) */
+  double *view_terms;            /* out [V*4]: depth loss, silhouette loss, n_px, n_converged */
+  double *shape_terms;           /* out [S*2]: total objective, |z|^2 */
+} dist_objective_io;
+
+DIST_API size_t dist_objective_workspace_size(const dist_decoder *dec, int n_views, int width,
+                                              int height, int k_samples, int n_shapes);
+/* After dist_trace: frozen-sample heads, loss seeds, the fused taped forward
+ * -> seed -> reverse sweep per tile of samples, and the code gradient with the
+ * latent regulariser added once per shape.  Views contribute their own
+ * per-view-normalised depth term, as Sum_v completion_objective(view v). */
+DIST_API int dist_objective(const dist_decoder *dec, const double *codes_dev, int n_shapes,
+                            const dist_camera *cams_dev, int n_views, int width, int height,
+                            const dist_trace_config *cfg, const dist_ray_state *st,
+                            const dist_objective_io *io, void *ws, size_t ws_bytes, void *stream);
+
+/* ---- Adam (AdamState/adam_step, optimize.py:35-63) ------------------------ */
+typedef struct dist_adam_config {
+  double lr, beta1, beta2, eps;
+} dist_adam_config;
+/* One bias-corrected step per shape; a shape whose gradient has a non-finite
+ * entry is skipped and counted.  With shape_terms/best_*: records the loss
+ * history hist[iter*S + s] and keeps the best-loss iterate (optimize.py:170-176)
+ * before updating. */
+DIST_API int dist_adam_step(int n_shapes, int dim, double *params_dev, const double *grad_dev,
+                            double *m_dev, double *v_dev, int32_t *t_dev, int32_t *skipped_dev,
+                            const double *shape_terms_dev, double *best_loss_dev,
+                            double *best_params_dev, int32_t *best_iter_dev, int iter,
+                            double *hist_dev, const dist_adam_config *cfg, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

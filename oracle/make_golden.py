@@ -1,0 +1,168 @@
+"""Generate tests/golden/*.npz by running the UNMODIFIED reference.
+
+TEST INFRASTRUCTURE ONLY.  Run in the build container, where the reference
+package is importable from /root/reference/pkg/src (it does not exist on the
+GPU box, so its outputs are committed as small fixtures):
+
+    python oracle/make_golden.py
+
+Each fixture records the inputs needed to rebuild the case without the
+reference (decoder recipe + seed or explicit small weights, code, camera,
+config) and the reference's outputs for the hot path: ray state, per-step
+live counts, maps, head values, loss terms and the latent gradient.
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+import warnings
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, "/root/reference/pkg/src")
+sys.path.insert(0, HERE)
+
+import sdftrace as st  # noqa: E402  (the reference, read-only)
+from sdftrace.optimize import completion_objective  # noqa: E402
+from sdftrace import shading as rsh  # noqa: E402
+
+import sdf_oracle as orc  # noqa: E402
+
+OUT = os.path.join(HERE, "..", "tests", "golden")
+
+
+def _state(res, prefix="") -> dict:
+    s = res.state
+    return {prefix + "status": s.status, prefix + "steps": s.steps, prefix + "d": s.d,
+            prefix + "b": s.b, prefix + "topk_d": s.topk_d, prefix + "topk_f": s.topk_f,
+            prefix + "topk_absf": s.topk_absf,
+            prefix + "live_counts": np.asarray(res.live_counts, np.int64),
+            prefix + "total_queries": np.int64(res.total_queries),
+            prefix + "nan_count": np.int64(res.nan_count)}
+
+
+def _cfg_arr(cfg) -> np.ndarray:
+    return np.array([cfg.alpha, cfg.epsilon, cfg.max_steps, cfg.k_samples,
+                     cfg.coarse_start_scale, cfg.split_interval, cfg.normal_delta,
+                     float(cfg.use_dynamic_mask)])
+
+
+def _pack_weights(ws) -> dict:
+    out = {"n_layers": np.int64(len(ws))}
+    for i, (W, b) in enumerate(ws):
+        out[f"W{i}"] = np.asarray(W)
+        out[f"b{i}"] = np.asarray(b)
+    return out
+
+
+def ladder():
+    """Table-1 strategy ladder at 128^2 (bench.py:59-101; test_output.txt:24)."""
+    field, pose = st.benchmark_field()
+    intr = st.Intrinsics(width=128, height=128)
+    out = _pack_weights(field.weights)
+    counts = []
+    for name, cfg in st.strategy_ladder(50):
+        res = st.trace(field, None, intr, pose, cfg)
+        counts.append(res.total_queries)
+        if name == "+coarse":
+            out.update(_state(res))
+            out["depth"] = st.depth_map(res)
+            out["silhouette"] = st.soft_silhouette(res)
+            out["normal"] = st.normal_map(res, field, None)
+    out["ladder"] = np.asarray(counts, np.int64)
+    out["omega"], out["t"] = pose.omega, pose.t
+    out["res"] = np.int64(128)
+    np.savez_compressed(os.path.join(OUT, "ladder128.npz"), **out)
+    print("ladder", counts)
+
+
+def tiny():
+    """C1: tiny_net recipe (conftest.py:33-39) at 64^2, one completion iterate."""
+    rng = np.random.default_rng(7)
+    net = st.NeuralField.init(latent_dim=2, hidden=(16, 16), rng=rng)
+    code = rng.normal(0.0, 0.3, 2)
+    intr = st.Intrinsics(width=64, height=64)
+    pose = st.look_at((0.0, 0.0, -2.0))
+    cfg = st.TraceConfig(k_samples=3)
+    out = _pack_weights(net.weights)
+    out.update(code=code, omega=pose.omega, t=pose.t, res=np.int64(64), cfg=_cfg_arr(cfg))
+    res = st.trace(net, code, intr, pose, cfg)
+    out.update(_state(res))
+    out["depth"] = st.depth_map(res)
+    out["silhouette"] = st.soft_silhouette(res)
+    out["normal"] = st.normal_map(res, net, code)
+    heads = st.diff_heads(res, net, code, want_normals=True)
+    out.update(h_ray_index=heads.ray_index, h_sample_d=heads.sample_d,
+               h_sample_f=heads.sample_f, h_best=heads.best_sample,
+               h_depth_z=heads.depth_z, h_normal=heads.normal_value)
+    rs = np.random.default_rng(3)
+    wd = rs.standard_normal(heads.sample_d.size)
+    ws = rs.standard_normal(heads.pixels.shape[0])
+    wn = rs.standard_normal((heads.pixels.shape[0], 3))
+    g = heads.backward(depth_seed=wd, sil_seed=ws, normal_seed=wn)
+    out.update(bw_depth_seed=wd, bw_sil_seed=ws, bw_normal_seed=wn, bw_code=g["code"],
+               bw_points=g["sample_point_grads"], bw_surface=g["surface_point_grads"])
+    # completion objective against depth + silhouette + normals of code + 0.05
+    z_obs = code + 0.05
+    ores = st.trace(net, z_obs, intr, pose, cfg)
+    obs = [st.Observation("depth", st.depth_map(ores)),
+           st.Observation("silhouette", st.hard_mask(ores).astype(np.float64)),
+           st.Observation("normal", st.normal_map(ores, net, z_obs))]
+    wts = st.LossWeights()
+    total, terms, gc, n_conv, q = completion_objective(net, code, obs, intr, pose, cfg, wts)
+    out.update(obs_depth=obs[0].image, obs_sil=obs[1].image, obs_normal=obs[2].image,
+               obj_total=total, obj_depth=terms["depth"], obj_sil=terms["silhouette"],
+               obj_normal=terms["normal"], obj_latent=terms["latent"], obj_grad=gc,
+               obj_nconv=np.int64(n_conv), obj_queries=np.int64(q))
+    # depth-only objective (the C3 form) and a short complete_shape run
+    total_d, terms_d, g_d, _, _ = completion_objective(net, code, obs[:1], intr, pose,
+                                                          cfg, wts)
+    out.update(objd_total=total_d, objd_grad=g_d)
+    best, rep = st.complete_shape(net, obs[:1], intr, pose, code0=np.zeros(2), iters=4, cfg=cfg)
+    out.update(cs_best=best, cs_losses=np.asarray(rep.losses), cs_best_iter=np.int64(rep.best_iter))
+    np.savez_compressed(os.path.join(OUT, "tiny64.npz"), **out)
+    print("tiny", res.total_queries, total)
+
+
+def geo(res_px=64, seed=0, name="geo64", normals=True):
+    """The standard 8x512 geometric-init decoder at a small view."""
+    ws = orc.geometric_init(256, (512,) * 8, seed)
+    net = st.NeuralField(ws, latent_dim=256)
+    z_true = np.random.default_rng(1).normal(0.0, 0.1, 256)
+    code = np.random.default_rng(2).normal(0.0, 0.1, 256)
+    intr = st.Intrinsics(width=res_px, height=res_px)
+    pose = st.look_at(orc.ring_eye(1, 8))
+    cfg = st.TraceConfig(k_samples=3)
+    out = {"seed": np.int64(seed), "code": code, "z_true": z_true, "omega": pose.omega,
+           "t": pose.t, "res": np.int64(res_px), "cfg": _cfg_arr(cfg)}
+    res = st.trace(net, code, intr, pose, cfg)
+    out.update(_state(res))
+    out["depth"] = st.depth_map(res)
+    out["silhouette"] = st.soft_silhouette(res)
+    if normals:
+        out["normal"] = st.normal_map(res, net, code)
+    heads = st.diff_heads(res, net, code)
+    out.update(h_sample_f=heads.sample_f, h_depth_z=heads.depth_z)
+    ores = st.trace(net, z_true, intr, pose, cfg)
+    obs = [st.Observation("depth", st.depth_map(ores))]
+    total, terms, g, n_conv, q = completion_objective(net, code, obs, intr, pose, cfg,
+                                                         st.LossWeights())
+    out.update(obs_depth=obs[0].image, obj_total=total, obj_depth=terms["depth"],
+               obj_grad=g, obj_nconv=np.int64(n_conv), obj_queries=np.int64(q))
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **out)
+    print(name, res.total_queries, int((res.state.status == 1).sum()), total)
+
+
+def main():
+    os.makedirs(OUT, exist_ok=True)
+    warnings.simplefilter("ignore")
+    ladder()
+    tiny()
+    geo(64, 0, "geo64")
+    geo(32, 1, "geo32s1")
+
+
+if __name__ == "__main__":
+    main()

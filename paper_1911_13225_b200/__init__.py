@@ -1,0 +1,21 @@
+"""B200-native DIST differentiable sphere tracing (arXiv 1911.13225).
+
+Drop-in for the hot path of the reference package `sdftrace`: the same public
+names for tracing, maps, heads, losses and the latent-code optimiser, backed
+by libdist_b200.so (hand-written sm_100a kernels behind a C ABI,
+include/dist.h).  There is no CPU fallback.
+"""
+
+from .camera import Intrinsics, Pose, RayBundle, generate_rays, log_rotation, look_at, \
+    rotation_matrix
+from .fields import NeuralField, eval_field
+from .losses import LossWeights, Observation, depth_loss, latent_reg, normal_loss, \
+    silhouette_loss
+from .optimize import AdamState, LatentOptimizer, OptimizationError, OptimizeReport, adam_step, \
+    complete_shape, completion_objective
+from .shading import HeadBundle, RenderMaps, depth_map, diff_heads, hard_mask, normal_map, \
+    ray_distance, render, soft_silhouette, surface_points
+from .tracer import CONVERGED, ESCAPED, EXHAUSTED, MARCHING, DeviceTrace, RayState, TraceConfig, \
+    TraceResult, trace, trace_views
+
+__version__ = "0.1.0"

@@ -1,0 +1,397 @@
+// heads.cu -- the memory-light backward of one latent-optimisation iterate,
+// fully on the device (optimize.py:102-138 with shading.py:156-281 and
+// losses.py:54-117), plus the bias-corrected Adam step (optimize.py:47-63).
+//
+// Pipeline per iterate, all stream-ordered, no host synchronisation:
+//   1. sample list over the frozen record: recorded rays (finite
+//      topk_absf[:,0]) and every finite top-K slot, both in ascending order
+//      exactly as np.nonzero/np.repeat build them (shading.py:171-183);
+//   2. per-view loss preparation: n_px (converged & observed), n_conv, the
+//      silhouette hinge loss and its per-pixel gradient (losses.py:78-91);
+//   3. ONE fused kernel per tile of samples: taped decoder forward at the
+//      frozen points c + d_k v, the depth seed w*sign(r)*scale computed from
+//      the tile's own f (losses.py:70-75) plus the silhouette seed on slot 0,
+//      then the reverse sweep -- activations and ReLU masks never leave
+//      shared memory; per-CTA column sums of the layer-0 gradient are the
+//      only output besides f;
+//   4. per-view depth loss from f, a fixed-order reduction of the column
+//      sums into d/dz, the latent regulariser added once per shape.
+#include <cmath>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "march.cuh"
+#include "mlp_eval.cuh"
+#include "scan.cuh"
+
+namespace dist {
+
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t *a, int64_t n, int64_t key) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)a[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+struct HeadsDev {
+  int32_t *rec, *samp, *samp_pix, *best, *view_rec, *view_samp, *counts;
+  double *f;
+};
+
+__global__ void k_heads_index(HeadsDev h, int K, int V, int64_t WH) {
+  const int64_t nrec = h.counts[0], nsamp = h.counts[1];
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nsamp;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t flat = h.samp[i];
+    const int64_t g = flat / K;
+    const int64_t r = lower_bound_i32(h.rec, nrec, g);
+    h.samp_pix[i] = (int32_t)r;
+    if (flat - g * K == 0) h.best[r] = (int32_t)i;
+  }
+  if (blockIdx.x == 0)
+    for (int v = threadIdx.x; v <= V; v += blockDim.x) {
+      h.view_rec[v] = (int32_t)lower_bound_i32(h.rec, nrec, (int64_t)v * WH);
+      h.view_samp[v] = (int32_t)lower_bound_i32(h.samp, nsamp, (int64_t)v * WH * K);
+    }
+}
+
+__device__ __forceinline__ double block_sum(double v, double *red) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+  return s;  // valid in thread 0
+}
+
+struct ObjIn {
+  const double *obs_depth;
+  const uint8_t *obs_mask;
+  const double *obs_sil;
+  double w_depth, w_sil, w_lat;
+};
+
+__device__ __forceinline__ bool depth_valid(const ObjIn &in, int64_t g) {
+  if (!in.obs_depth) return false;
+  const double z = in.obs_depth[g];
+  bool ok = isfinite(z);
+  if (in.obs_mask) ok = ok && in.obs_mask[g];
+  return ok;
+}
+
+// one block per view: n_px, n_conv, silhouette loss + per-pixel seed
+__global__ void k_view_prep(const dist_camera *__restrict__ cams, LevelState ls, int K, double eps,
+                            ObjIn in, int32_t *npx, double *terms, double *sil_seed) {
+  __shared__ double red[32];
+  const int v = blockIdx.x;
+  const int64_t WH = (int64_t)ls.lw * ls.lh;
+  const int64_t g0 = v * WH;
+  double n_px = 0, n_conv = 0, sl = 0;
+  const double inv_n = 1.0 / (double)WH;
+  for (int64_t q = threadIdx.x; q < WH; q += blockDim.x) {
+    const int64_t g = g0 + q;
+    const bool conv = ls.status[g] == DIST_CONVERGED;
+    const bool rec = isfinite(ls.tk_a[g * K]);
+    n_conv += (conv && rec) ? 1.0 : 0.0;
+    if (conv && rec && depth_valid(in, g)) n_px += 1.0;
+    if (in.obs_sil) {
+      double s;
+      if (rec) {
+        s = ls.tk_a[g * K] - eps;
+      } else {
+        const int j = (int)(q / ls.lw), i = (int)(q - (int64_t)j * ls.lw);
+        double dir[3];
+        pixel_ray(cams[v], i, j, 1, dir, nullptr);
+        const double *o = cams[v].origin;
+        const double m = dir[0] * o[0] + dir[1] * o[1] + dir[2] * o[2];
+        const double c2 = o[0] * o[0] + o[1] * o[1] + o[2] * o[2];
+        s = sqrt(fmax(c2 - m * m, 0.0)) - 1.0;
+      }
+      const double t = in.obs_sil[g];
+      sl += t * fmax(s, 0.0) + (1.0 - t) * fmax(-s, 0.0);
+      const double gr = (t * (s > 0.0 ? 1.0 : 0.0) - (1.0 - t) * (s < 0.0 ? 1.0 : 0.0)) * inv_n;
+      sil_seed[g] = in.w_sil * gr;
+    }
+  }
+  const double a = block_sum(n_px, red);
+  const double b = block_sum(n_conv, red);
+  const double c = block_sum(sl, red);
+  if (threadIdx.x == 0) {
+    npx[v] = (int32_t)a;
+    terms[v * 4 + 0] = 0.0;
+    terms[v * 4 + 1] = in.obs_sil ? c / (double)WH : 0.0;
+    terms[v * 4 + 2] = a;
+    terms[v * 4 + 3] = b;
+  }
+}
+
+// Generator for the fused forward -> seed -> backward over head samples.
+struct ObjGen {
+  const dist_camera *cams;
+  LevelState ls;
+  int K;
+  int64_t WH;
+  HeadsDev h;
+  ObjIn in;
+  const int32_t *npx;
+  const double *sil_seed;
+  __device__ int64_t count() const { return h.counts[1]; }
+  __device__ bool point(int64_t i, double p[3], int &s) const {
+    const int64_t flat = h.samp[i];
+    const int64_t g = flat / K;
+    const int v = (int)(g / WH);
+    const int64_t q = g - v * WH;
+    const int j = (int)(q / ls.lw), ii = (int)(q - (int64_t)j * ls.lw);
+    double dir[3];
+    pixel_ray(cams[v], ii, j, 1, dir, nullptr);
+    const double dk = ls.tk_d[flat];
+    for (int a = 0; a < 3; ++a) p[a] = __dadd_rn(cams[v].origin[a], __dmul_rn(dk, dir[a]));
+    s = cams[v].shape;
+    return true;
+  }
+  __device__ double seed(int64_t i, double f) const {
+    const int64_t flat = h.samp[i];
+    const int64_t g = flat / K;
+    const int v = (int)(g / WH);
+    double sd = 0.0;
+    if (in.obs_depth && ls.status[g] == DIST_CONVERGED && depth_valid(in, g) && npx[v] > 0) {
+      int cnt = 0;
+      for (int k = 0; k < K; ++k) cnt += isfinite(ls.tk_a[g * K + k]) ? 1 : 0;
+      const int64_t q = g - v * WH;
+      const int j = (int)(q / ls.lw), ii = (int)(q - (int64_t)j * ls.lw);
+      double dir[3], scale;
+      pixel_ray(cams[v], ii, j, 1, dir, &scale);
+      const double w = (1.0 / cnt) / (double)npx[v];
+      const double r = __dmul_rn(__dadd_rn(ls.tk_d[flat], f), scale) - in.obs_depth[g];
+      const double sg = r > 0.0 ? 1.0 : (r < 0.0 ? -1.0 : 0.0);
+      sd = in.w_depth * __dmul_rn(__dmul_rn(w, sg), scale);
+    }
+    if (sil_seed && flat - g * K == 0) sd = __dadd_rn(sd, sil_seed[g]);
+    return sd;
+  }
+  __device__ void store(int64_t i, double v) const { h.f[i] = v; }
+};
+
+// one block per view: depth loss = sum_i w_i |r_i| over the view's samples
+__global__ void k_view_depth_loss(const dist_camera *__restrict__ cams, LevelState ls, int K,
+                                  HeadsDev h, ObjIn in, const int32_t *npx, double *terms) {
+  __shared__ double red[32];
+  const int v = blockIdx.x;
+  const int64_t WH = (int64_t)ls.lw * ls.lh;
+  const int64_t s0 = h.view_samp[v], s1 = h.view_samp[v + 1];
+  double acc = 0.0;
+  if (in.obs_depth && npx[v] > 0) {
+    for (int64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
+      const int64_t flat = h.samp[i];
+      const int64_t g = flat / K;
+      if (ls.status[g] != DIST_CONVERGED || !depth_valid(in, g)) continue;
+      int cnt = 0;
+      for (int k = 0; k < K; ++k) cnt += isfinite(ls.tk_a[g * K + k]) ? 1 : 0;
+      const int64_t q = g - v * WH;
+      const int j = (int)(q / ls.lw), ii = (int)(q - (int64_t)j * ls.lw);
+      double dir[3], scale;
+      pixel_ray(cams[v], ii, j, 1, dir, &scale);
+      const double w = (1.0 / cnt) / (double)npx[v];
+      const double r = __dmul_rn(__dadd_rn(ls.tk_d[flat], h.f[i]), scale) - in.obs_depth[g];
+      acc += w * fabs(r);
+    }
+  }
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) terms[v * 4 + 0] = s;
+}
+
+// per shape: grad += w_lat * 2 z; total = sum_views(w_d L_d + w_s L_s) + w_lat |z|^2
+__global__ void k_shape_finish(const dist_camera *__restrict__ cams, int V, int S, int D,
+                               const double *__restrict__ codes, const double *__restrict__ terms,
+                               ObjIn in, double *grad, double *shape_terms) {
+  __shared__ double red[32];
+  const int s = blockIdx.x;
+  double zz = 0.0;
+  for (int k = threadIdx.x; k < D; k += blockDim.x) {
+    const double z = codes[(size_t)s * D + k];
+    zz += z * z;
+    grad[(size_t)s * D + k] += in.w_lat * (2.0 * z);
+  }
+  const double reg = block_sum(zz, red);
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int v = 0; v < V; ++v)
+      if (cams[v].shape == s)
+        tot += in.w_depth * terms[v * 4 + 0] + in.w_sil * terms[v * 4 + 1];
+    shape_terms[s * 2 + 0] = tot + in.w_lat * reg;
+    shape_terms[s * 2 + 1] = reg;
+  }
+}
+
+// Adam (optimize.py:47-63) per shape, with the best-iterate bookkeeping of
+// complete_shape (optimize.py:170-176) and the loss history.
+__global__ void k_adam(int S, int D, double *params, const double *grad, double *m, double *v,
+                       int32_t *t, int32_t *skipped, const double *shape_terms, double *best_loss,
+                       double *best_params, int32_t *best_iter, int iter, double *hist,
+                       dist_adam_config cfg) {
+  __shared__ int s_bad;
+  __shared__ int s_best;
+  const int s = blockIdx.x;
+  if (threadIdx.x == 0) {
+    s_bad = 0;
+    s_best = 0;
+    if (shape_terms) {
+      const double tot = shape_terms[s * 2];
+      if (hist) hist[(size_t)iter * S + s] = tot;
+      if (best_loss && tot < best_loss[s]) {
+        best_loss[s] = tot;
+        best_iter[s] = iter;
+        s_best = 1;
+      }
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < D; k += blockDim.x) {
+    if (s_best) best_params[(size_t)s * D + k] = params[(size_t)s * D + k];
+    if (!isfinite(grad[(size_t)s * D + k])) atomicOr(&s_bad, 1);
+  }
+  __syncthreads();
+  if (s_bad) {
+    if (threadIdx.x == 0) skipped[s] += 1;
+    return;
+  }
+  const int tt = t[s] + 1;
+  const double c1 = 1.0 - pow(cfg.beta1, (double)tt), c2 = 1.0 - pow(cfg.beta2, (double)tt);
+  for (int k = threadIdx.x; k < D; k += blockDim.x) {
+    const size_t i = (size_t)s * D + k;
+    const double g = grad[i];
+    const double mm = cfg.beta1 * m[i] + (1.0 - cfg.beta1) * g;
+    const double vv = cfg.beta2 * v[i] + (1.0 - cfg.beta2) * g * g;
+    m[i] = mm;
+    v[i] = vv;
+    params[i] = params[i] - cfg.lr * (mm / c1) / (sqrt(vv / c2) + cfg.eps);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) t[s] = tt;
+}
+
+struct ObjLayout {
+  HeadsDev h;
+  double *c0, *cs, *part0, *parts, *col0, *cols, *sil_seed;
+  int32_t *npx, *bcount;
+  size_t bytes;
+};
+
+static ObjLayout obj_layout(const DecView &dv, int V, int W, int H, int K, int S, char *ws,
+                            size_t cap) {
+  ObjLayout L{};
+  Carve cv{ws, 0, cap};
+  const int64_t n = (int64_t)V * W * H;
+  const int s1 = std::max(S, 1);
+  L.h.rec = cv.take<int32_t>(n);
+  L.h.best = cv.take<int32_t>(n);
+  L.h.samp = cv.take<int32_t>(n * K);
+  L.h.samp_pix = cv.take<int32_t>(n * K);
+  L.h.f = cv.take<double>(n * K);
+  L.h.view_rec = cv.take<int32_t>(V + 1);
+  L.h.view_samp = cv.take<int32_t>(V + 1);
+  L.h.counts = cv.take<int32_t>(4);
+  L.sil_seed = cv.take<double>(n);
+  L.npx = cv.take<int32_t>(V);
+  L.bcount = cv.take<int32_t>(ceil_div(n * K, kScanBlock) + 1);
+  L.c0 = cv.take<double>((size_t)s1 * dv.np[0]);
+  L.cs = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
+  const int G = vjp_grid_cap(dv.prec);
+  L.part0 = cv.take<double>((size_t)G * s1 * dv.np[0]);
+  L.parts = cv.take<double>((size_t)G * s1 * std::max(dv.nskip, 1));
+  L.col0 = cv.take<double>((size_t)s1 * dv.np[0]);
+  L.cols = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
+  L.bytes = cv.off + 256;
+  return L;
+}
+
+}  // namespace dist
+
+using namespace dist;
+
+extern "C" {
+
+size_t dist_objective_workspace_size(const dist_decoder *dec, int V, int W, int H, int K, int S) {
+  if (!dec) return 0;
+  return obj_layout(dec->view, V, W, H, K, S, nullptr, ~size_t(0)).bytes;
+}
+
+int dist_objective(const dist_decoder *dec, const double *codes, int S, const dist_camera *cams,
+                   int V, int W, int H, const dist_trace_config *cfg, const dist_ray_state *st,
+                   const dist_objective_io *io, void *ws, size_t ws_bytes, void *stream) {
+  if (!dec || !cams || !cfg || !st || !io || !io->grad || !io->view_terms || !io->shape_terms)
+    return fail(DIST_ERR_CONFIG, "null argument");
+  const DecView &dv = dec->view;
+  if (dv.latent_dim > 0 && (!codes || S < 1)) return fail(DIST_ERR_CONFIG, "field expects a latent code");
+  cudaStream_t sm = (cudaStream_t)stream;
+  const int K = cfg->k_samples;
+  const int s1 = std::max(S, 1);
+  ObjLayout L = obj_layout(dv, V, W, H, K, S, (char *)ws, ws_bytes);
+  if (L.bytes > ws_bytes) return fail(DIST_ERR_CONFIG, "objective workspace too small");
+  const int64_t n = (int64_t)V * W * H, WH = (int64_t)W * H;
+  LevelState ls{st->d, st->b, st->status, st->steps, st->topk_d, st->topk_f, st->topk_absf, W, H, 1, n};
+  ObjIn in{io->obs_depth, io->obs_depth_mask, io->obs_sil, io->w_depth, io->w_sil, io->w_latent};
+
+  // 1. sample list
+  const double *ta = st->topk_absf;
+  const int Kc = K;
+  int rc = compact([ta, Kc] __device__(int64_t g) { return (bool)isfinite(ta[g * Kc]); }, n, L.h.rec,
+                   L.h.counts + 0, L.bcount, sm);
+  if (rc) return rc;
+  rc = compact([ta] __device__(int64_t q) { return (bool)isfinite(ta[q]); }, n * K, L.h.samp,
+               L.h.counts + 1, L.bcount, sm);
+  if (rc) return rc;
+  const int gi = (int)std::min<int64_t>(ceil_div(n * K, 256), (int64_t)sm_count() * 8);
+  k_heads_index<<<std::max(gi, 1), 256, 0, sm>>>(L.h, K, V, WH);
+  DIST_CHECK_LAUNCH("k_heads_index");
+  // 2. per-view loss preparation
+  k_view_prep<<<V, 1024, 0, sm>>>(cams, ls, K, cfg->epsilon, in, L.npx, io->view_terms, L.sil_seed);
+  DIST_CHECK_LAUNCH("k_view_prep");
+  // 3. fused forward -> seed -> backward
+  rc = launch_code_bias(dv, dv.latent_dim > 0 ? codes : nullptr, s1, L.c0, L.cs, sm);
+  if (rc) return rc;
+  const int G = vjp_grid_cap(dv.prec);
+  cudaError_t e = cudaMemsetAsync(L.part0, 0, sizeof(double) * G * s1 * dv.np[0], sm);
+  if (e == cudaSuccess && dv.nskip) e = cudaMemsetAsync(L.parts, 0, sizeof(double) * G * s1 * dv.nskip, sm);
+  if (e == cudaSuccess) e = cudaMemsetAsync(io->grad, 0, sizeof(double) * s1 * std::max(dv.latent_dim, 1), sm);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(objective)");
+  ObjGen gen{cams, ls, K, WH, L.h, in, L.npx, io->obs_sil ? L.sil_seed : nullptr};
+  int grid = 0;
+  if (dv.prec == DIST_PREC_FP64)
+    rc = launch_vjp_gen<double>(dv, L.c0, L.cs, gen, n * K, s1, L.part0, L.parts, nullptr, G, &grid, sm);
+  else
+    rc = launch_vjp_gen<float>(dv, L.c0, L.cs, gen, n * K, s1, L.part0, L.parts, nullptr, G, &grid, sm);
+  if (rc) return rc;
+  // 4. losses, code gradient, regulariser
+  k_view_depth_loss<<<V, 1024, 0, sm>>>(cams, ls, K, L.h, in, L.npx, io->view_terms);
+  DIST_CHECK_LAUNCH("k_view_depth_loss");
+  if (dv.latent_dim > 0) {
+    rc = reduce_code_grad(dv, s1, grid, L.part0, L.parts, L.col0, L.cols, io->grad, sm);
+    if (rc) return rc;
+  }
+  k_shape_finish<<<s1, 256, 0, sm>>>(cams, V, s1, dv.latent_dim, codes, io->view_terms, in, io->grad,
+                                      io->shape_terms);
+  DIST_CHECK_LAUNCH("k_shape_finish");
+  return DIST_OK;
+}
+
+int dist_adam_step(int S, int D, double *params, const double *grad, double *m, double *v,
+                   int32_t *t, int32_t *skipped, const double *shape_terms, double *best_loss,
+                   double *best_params, int32_t *best_iter, int iter, double *hist,
+                   const dist_adam_config *cfg, void *stream) {
+  if (!params || !grad || !m || !v || !t || !skipped || !cfg) return fail(DIST_ERR_CONFIG, "null argument");
+  if (S < 1 || D < 0) return fail(DIST_ERR_CONFIG, "bad Adam shape");
+  if (D == 0) return DIST_OK;
+  k_adam<<<S, 256, 0, (cudaStream_t)stream>>>(S, D, params, grad, m, v, t, skipped, shape_terms,
+                                              best_loss, best_params, best_iter, iter, hist, *cfg);
+  DIST_CHECK_LAUNCH("k_adam");
+  return DIST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,35 @@
+// kernels.cuh -- cross-translation-unit entry points inside libdist_b200.
+#pragma once
+#include <functional>
+
+#include "common.cuh"
+
+namespace dist {
+
+int sm_count();
+int launch_code_bias(const DecView &dv, const double *codes, int S, double *c0, double *cskip,
+                     cudaStream_t st);
+int eval_points(const DecView &dv, const double *c0, const double *cskip, const double *pts,
+                const int32_t *shape, int64_t n, double *f, cudaStream_t st);
+int vjp_points(const DecView &dv, const double *c0, const double *cskip, const double *pts,
+               const int32_t *shape, int64_t n, const double *seed, int S, double *f,
+               double *part0, double *parts, double *gpts, int grid_cap, int *grid_out,
+               cudaStream_t st);
+int reduce_code_grad(const DecView &dv, int S, int G, const double *part0, const double *parts,
+                     double *colsum0, double *colsums, double *grad, cudaStream_t st);
+int vjp_grid_cap(int prec);
+size_t eval_ws(const DecView &dv, int64_t n, int S, bool vjp);
+
+// tensor-core (tcgen05) split-precision decoder, tc_mlp.cu
+int tc_eval_points(const DecView &dv, const double *c0, const double *cskip, const double *pts,
+                   const int32_t *shape, int64_t n, double *f, cudaStream_t st);
+void tc_pack_sizes(const DecView &dv, const std::function<void(int, size_t, size_t)> &put);
+void tc_pack_fill(const DecView &dv, const double *const *W, const double *const *b,
+                  const int32_t *dims, const std::function<void *(int)> &wdst,
+                  const std::function<float *(int)> &bdst);
+bool tc_supported(const DecView &dv);
+
+// stable device-wide compaction of flags -> ascending indices (scan.cu)
+size_t compact_ws_bytes(int64_t n);
+
+}  // namespace dist

@@ -1,0 +1,130 @@
+// march.cuh -- ray state, the march update (tracer.py:132-193) and the
+// step-slot bookkeeping shared by the SIMT and tcgen05 step kernels.
+#pragma once
+#include "common.cuh"
+
+namespace dist {
+
+struct LevelState {
+  double *d, *b;
+  uint8_t *status;
+  int32_t *steps;
+  double *tk_d, *tk_f, *tk_a;
+  int lw, lh, level;
+  int64_t n;  // V * lw * lh
+};
+
+struct Ctl {
+  int32_t cnt[2];
+  int32_t cur;
+  uint32_t done;
+  int32_t steps_done;
+  int32_t pad[3];
+};
+
+struct MarchArgs {
+  double alpha, eps;
+  int K, max_steps, dynamic, V;
+};
+
+__device__ __forceinline__ void ray_of(const dist_camera *__restrict__ cams, const LevelState &ls,
+                                       int64_t g, double dir[3], const dist_camera **cam) {
+  const int64_t per = (int64_t)ls.lw * ls.lh;
+  const int v = (int)(g / per);
+  const int64_t pix = g - (int64_t)v * per;
+  const int j = (int)(pix / ls.lw), i = (int)(pix - (int64_t)j * ls.lw);
+  *cam = cams + v;
+  pixel_ray(**cam, i, j, ls.level, dir, nullptr);
+}
+
+// warp-aggregated append of `value` when keep; every lane of the warp must call.
+__device__ __forceinline__ void warp_append(bool keep, int32_t value, int32_t *list, int32_t *cnt) {
+  const unsigned m = __ballot_sync(0xffffffffu, keep);
+  if (!m) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(cnt, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (keep) list[base + __popc(m & ((1u << lane) - 1u))] = value;
+}
+
+// --- the march update for one queried ray (tracer.py:170-192) -----------------
+// Returns true if the ray is still marching.  Arithmetic is kept
+// uncontracted so that d' = d + alpha*f rounds exactly like numpy.
+__device__ __forceinline__ bool march_update(const LevelState &ls, const MarchArgs &a, int64_t g,
+                                             const double dir[3], const double *o, double f,
+                                             int *nan_count) {
+  if (!isfinite(f)) {
+    ls.status[g] = DIST_EXHAUSTED;
+    ls.b[g] = __longlong_as_double(0x7ff8000000000000ll);
+    ls.steps[g] += 1;
+    ++*nan_count;
+    return false;
+  }
+  const double dk = ls.d[g];
+  const double av = fabs(f);
+  const int K = a.K;
+  double *ta = ls.tk_a + g * K, *tf = ls.tk_f + g * K, *td = ls.tk_d + g * K;
+  if (av < ta[K - 1]) {  // strict: the earliest query wins ties (tracer.py:133-134)
+    int pos = K - 1;
+    while (pos > 0 && ta[pos - 1] > av) {
+      ta[pos] = ta[pos - 1];
+      tf[pos] = tf[pos - 1];
+      td[pos] = td[pos - 1];
+      --pos;
+    }
+    ta[pos] = av;
+    tf[pos] = f;
+    td[pos] = dk;
+  }
+  ls.steps[g] += 1;
+  ls.b[g] = f;
+  const double dn = __dadd_rn(dk, __dmul_rn(a.alpha, f));
+  ls.d[g] = dn;
+  if (av < a.eps) {
+    ls.status[g] = DIST_CONVERGED;
+    return false;
+  }
+  double p[3];
+  for (int i = 0; i < 3; ++i) p[i] = __dadd_rn(o[i], __dmul_rn(dn, dir[i]));
+  const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(p[0], p[0]), __dmul_rn(p[1], p[1])), __dmul_rn(p[2], p[2]));
+  const double vp = __dadd_rn(__dadd_rn(__dmul_rn(dir[0], p[0]), __dmul_rn(dir[1], p[1])), __dmul_rn(dir[2], p[2]));
+  if (r2 > 1.0 && f > 0.0 && vp > 0.0) {
+    ls.status[g] = DIST_ESCAPED;
+    return false;
+  }
+  return true;
+}
+
+// Last CTA of a step slot records the query count and flips the live lists.
+__device__ __forceinline__ void step_epilogue(Ctl *ctl, int cur, int64_t queried, int nan_block,
+                                              int64_t *live_counts, int64_t *stats) {
+  __shared__ bool s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (nan_block) atomicAdd((unsigned long long *)&stats[1], (unsigned long long)nan_block);
+    __threadfence();
+    const unsigned prev = atomicAdd(&ctl->done, 1u);
+    s_last = (prev == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    const int sd = ctl->steps_done;
+    live_counts[sd] = queried;
+    stats[0] += queried;
+    stats[2] = sd + 1;
+    ctl->steps_done = sd + 1;
+    ctl->cnt[cur] = 0;
+    ctl->cur = cur ^ 1;
+    ctl->done = 0;
+    __threadfence();
+  }
+}
+
+int tc_run_steps(const DecView &dv, const double *c0, const double *cskip,
+                 const dist_camera *cams, const LevelState &ls, Ctl *ctl, int32_t *l0, int32_t *l1,
+                 const MarchArgs &a, int slots, int64_t *live, int64_t *stats, cudaStream_t st);
+
+}  // namespace dist

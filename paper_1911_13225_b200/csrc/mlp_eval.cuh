@@ -1,0 +1,180 @@
+// mlp_eval.cuh -- persistent point-evaluation kernels over a point generator.
+//
+// A generator `Gen` supplies, on the device:
+//   int64_t count() const                  rows to evaluate (may read a device counter)
+//   bool point(int64_t i, double p[3], int &shape) const
+//   double seed(int64_t i, double f) const (vjp only: the seed of row i given f)
+//   void store(int64_t i, double f) const  (where the value goes)
+// so the same tile code serves NeuralField.evaluate (explicit points), the
+// normal probes of shading.py:84-87 and the frozen head samples of
+// shading.py:185-206 without materialising point arrays in HBM.
+#pragma once
+#include "common.cuh"
+#include "mlp_simt.cuh"
+
+namespace dist {
+
+template <typename T, class Gen>
+__global__ void __launch_bounds__(SimtTile<T>::NT)
+    k_eval_gen(DecView dv, const double *__restrict__ c0, const double *__restrict__ cskip, Gen gen) {
+  extern __shared__ __align__(16) char smem[];
+  using Tile = SimtTile<T>;
+  Tile tile(smem);
+  const int64_t n = gen.count();
+  const int64_t ntiles = ceil_div(n, Tile::TM);
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t base = t * Tile::TM;
+    if (threadIdx.x < Tile::TM) {
+      const int64_t i = base + threadIdx.x;
+      double p[3] = {0.0, 0.0, 0.0};
+      int s = -1;
+      if (i < n && !gen.point(i, p, s)) s = -1;
+      tile.shape[threadIdx.x] = s;
+      for (int a = 0; a < 3; ++a) tile.pts[threadIdx.x * 3 + a] = p[a];
+    }
+    __syncthreads();
+    tile.forward(dv, c0, cskip, false);
+    if (threadIdx.x < Tile::TM && base + threadIdx.x < n) gen.store(base + threadIdx.x, tile.f[threadIdx.x]);
+    __syncthreads();
+  }
+}
+
+// Taped forward + reverse sweep per tile.  Column sums of the layer-0 / skip
+// pre-activation gradients accumulate into part0[cta][S][np0] /
+// parts[cta][S][nskip] (plain +=; each CTA owns its slice, so the final
+// fixed-order reduction is deterministic).  gpts[i][3] receives seed * df/dp.
+template <typename T, class Gen>
+__global__ void __launch_bounds__(SimtTile<T>::NT)
+    k_vjp_gen(DecView dv, const double *__restrict__ c0, const double *__restrict__ cskip, Gen gen,
+              int S, double *__restrict__ part0, double *__restrict__ parts,
+              double *__restrict__ gpts) {
+  extern __shared__ __align__(16) char smem[];
+  using Tile = SimtTile<T>;
+  Tile tile(smem);
+  __shared__ double s_seed[Tile::TM];
+  __shared__ double s_seedm[Tile::TM];
+  __shared__ double s_gp[Tile::TM * 3];
+  __shared__ double s_sum0[kMaxWidth];
+  __shared__ double s_sums[kMaxWidth];
+  __shared__ int s_shapes[Tile::TM];
+  __shared__ int s_nsh;
+  const int n0 = dv.np[0];
+  const int ns = dv.nskip;
+  const int64_t n = gen.count();
+  const int64_t ntiles = ceil_div(n, Tile::TM);
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t base = t * Tile::TM;
+    if (threadIdx.x < Tile::TM) {
+      const int64_t i = base + threadIdx.x;
+      double p[3] = {0.0, 0.0, 0.0};
+      int s = -1;
+      if (i < n && !gen.point(i, p, s)) s = -1;
+      tile.shape[threadIdx.x] = s;
+      for (int a = 0; a < 3; ++a) tile.pts[threadIdx.x * 3 + a] = p[a];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int cnt = 0;
+      for (int r = 0; r < Tile::TM; ++r) {
+        const int s = tile.shape[r];
+        if (s < 0) continue;
+        bool seen = false;
+        for (int q = 0; q < cnt; ++q) seen |= (s_shapes[q] == s);
+        if (!seen) s_shapes[cnt++] = s;
+      }
+      s_nsh = cnt;
+    }
+    tile.forward(dv, c0, cskip, true);
+    if (threadIdx.x < Tile::TM) {
+      const int64_t i = base + threadIdx.x;
+      const bool ok = i < n && tile.shape[threadIdx.x] >= 0;
+      const double fv = tile.f[threadIdx.x];
+      s_seed[threadIdx.x] = ok ? gen.seed(i, fv) : 0.0;
+      if (i < n) gen.store(i, fv);
+    }
+    __syncthreads();
+    const int nsh = s_nsh;
+    for (int q = 0; q < nsh; ++q) {
+      const int s = s_shapes[q];
+      if (threadIdx.x < Tile::TM) {
+        s_seedm[threadIdx.x] = (tile.shape[threadIdx.x] == s) ? s_seed[threadIdx.x] : 0.0;
+        for (int a = 0; a < 3; ++a) s_gp[threadIdx.x * 3 + a] = 0.0;
+      }
+      for (int j = threadIdx.x; j < kMaxWidth; j += blockDim.x) s_sum0[j] = s_sums[j] = 0.0;
+      __syncthreads();
+      tile.backward(dv, s_seedm, s_sum0, s_sums, s_gp);
+      double *p0 = part0 + ((size_t)blockIdx.x * S + s) * n0;
+      for (int j = threadIdx.x; j < n0; j += blockDim.x) p0[j] += s_sum0[j];
+      if (ns) {
+        double *ps = parts + ((size_t)blockIdx.x * S + s) * ns;
+        for (int j = threadIdx.x; j < ns; j += blockDim.x) ps[j] += s_sums[j];
+      }
+      if (gpts && threadIdx.x < Tile::TM && base + threadIdx.x < n && tile.shape[threadIdx.x] == s)
+        for (int a = 0; a < 3; ++a) gpts[(base + threadIdx.x) * 3 + a] = s_gp[threadIdx.x * 3 + a];
+      __syncthreads();
+    }
+  }
+}
+
+// explicit arrays (NeuralField.evaluate / HeadBundle.backward with seeds)
+struct ArrayGen {
+  const double *pts;
+  const int32_t *shape;
+  const double *seeds;
+  double *f;
+  int64_t n;
+  __device__ int64_t count() const { return n; }
+  __device__ bool point(int64_t i, double p[3], int &s) const {
+    p[0] = pts[i * 3];
+    p[1] = pts[i * 3 + 1];
+    p[2] = pts[i * 3 + 2];
+    s = shape ? shape[i] : 0;
+    return true;
+  }
+  __device__ double seed(int64_t i, double) const { return seeds[i]; }
+  __device__ void store(int64_t i, double v) const {
+    if (f) f[i] = v;
+  }
+};
+
+int sm_count();
+
+template <typename T, class Gen>
+int launch_eval_gen(const DecView &dv, const double *c0, const double *cskip, const Gen &gen,
+                    int64_t n_bound, cudaStream_t st) {
+  using Tile = SimtTile<T>;
+  const void *fn = (const void *)k_eval_gen<T, Gen>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)Tile::fwd_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(eval)");
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, Tile::NT, Tile::fwd_bytes);
+  const int64_t tiles = std::max<int64_t>(1, ceil_div(n_bound, Tile::TM));
+  const int grid = (int)std::min<int64_t>(tiles, (int64_t)std::max(per_sm, 1) * sm_count());
+  k_eval_gen<T, Gen><<<grid, Tile::NT, Tile::fwd_bytes, st>>>(dv, c0, cskip, gen);
+  DIST_CHECK_LAUNCH("k_eval_gen");
+  return DIST_OK;
+}
+
+template <typename T, class Gen>
+int launch_vjp_gen(const DecView &dv, const double *c0, const double *cskip, const Gen &gen,
+                   int64_t n_bound, int S, double *part0, double *parts, double *gpts,
+                   int grid_cap, int *grid_out, cudaStream_t st) {
+  using Tile = SimtTile<T>;
+  const void *fn = (const void *)k_vjp_gen<T, Gen>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)Tile::vjp_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(vjp)");
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, Tile::NT, Tile::vjp_bytes);
+  const int64_t tiles = std::max<int64_t>(1, ceil_div(n_bound, Tile::TM));
+  int grid = (int)std::min<int64_t>(tiles, (int64_t)std::max(per_sm, 1) * sm_count());
+  grid = std::min(grid, grid_cap);
+  *grid_out = grid;
+  k_vjp_gen<T, Gen><<<grid, Tile::NT, Tile::vjp_bytes, st>>>(dv, c0, cskip, gen, S, part0, parts,
+                                                             gpts);
+  DIST_CHECK_LAUNCH("k_vjp_gen");
+  return DIST_OK;
+}
+
+}  // namespace dist

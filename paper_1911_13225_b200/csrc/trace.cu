@@ -1,0 +1,449 @@
+// trace.cu -- device-resident sphere tracing (tracer.py:88-252) and the maps
+// of shading.py:48-113.
+//
+// The march runs as a fixed schedule of launches that the host enqueues up
+// front (no host synchronisation per step): init, split_interval step slots
+// per coarse level, a split, and max_steps slots at full resolution.  Each
+// slot is one persistent kernel that reads the live count and the global step
+// budget from a device controller and exits immediately when the reference
+// loop would have broken (tracer.py:242-245: budget spent or nothing live), so
+// the executed steps equal the reference's exactly.  Inside a slot every CTA
+// takes TM-row tiles of the current live list, evaluates the decoder, applies
+// the march update (NaN -> EXHAUSTED, top-K record, d += alpha f, converge /
+// escape tests) in the tile epilogue, and appends surviving rays to the next
+// live list with warp-aggregated atomics; the last CTA to finish records the
+// step's query count (TraceResult.live_counts) and flips the lists.
+#include <cmath>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.cuh"
+#include "mlp_eval.cuh"
+#include "scan.cuh"
+#include "march.cuh"
+
+namespace dist {
+
+// --- init (tracer.py:88-119) ----------------------------------------------
+__global__ void k_init(const dist_camera *__restrict__ cams, LevelState ls, int K,
+                       int32_t *__restrict__ list, Ctl *ctl, int64_t *stats) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ls.n; base += stride) {
+    const int64_t g = base + threadIdx.x;
+    bool live = false;
+    if (g < ls.n) {
+      double v[3];
+      const dist_camera *c;
+      ray_of(cams, ls, g, v, &c);
+      const double *o = c->origin;
+      const double c2 = __dadd_rn(__dadd_rn(__dmul_rn(o[0], o[0]), __dmul_rn(o[1], o[1])),
+                                  __dmul_rn(o[2], o[2]));
+      double d0 = 0.0;
+      uint8_t stt = DIST_MARCHING;
+      if (c2 <= 1.0) {
+        if (g == 0 || (g % ((int64_t)ls.lw * ls.lh)) == 0) atomicOr((unsigned long long *)&stats[3], (unsigned long long)DIST_WARN_CAMERA_INSIDE);
+      } else {
+        const double m = __dadd_rn(__dadd_rn(__dmul_rn(v[0], o[0]), __dmul_rn(v[1], o[1])),
+                                   __dmul_rn(v[2], o[2]));
+        const double disc = __dsub_rn(__dmul_rn(m, m), __dsub_rn(c2, 1.0));
+        if (disc >= 0.0 && m < 0.0) d0 = __dsub_rn(-m, sqrt(disc));
+        else stt = DIST_ESCAPED;
+      }
+      ls.d[g] = d0;
+      ls.b[g] = __longlong_as_double(0x7ff8000000000000ll);
+      ls.status[g] = stt;
+      ls.steps[g] = 0;
+      for (int k = 0; k < K; ++k) {
+        ls.tk_d[g * K + k] = 0.0;
+        ls.tk_f[g * K + k] = 0.0;
+        ls.tk_a[g * K + k] = __longlong_as_double(0x7ff0000000000000ll);
+      }
+      live = stt == DIST_MARCHING;
+    }
+    warp_append(live, (int32_t)g, list, &ctl->cnt[0]);
+  }
+}
+
+// --- 4-way split (tracer.py:196-218) ---------------------------------------
+__global__ void k_split(LevelState par, LevelState ch, int K, int32_t *__restrict__ list, Ctl *ctl) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t per_c = (int64_t)ch.lw * ch.lh, per_p = (int64_t)par.lw * par.lh;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ch.n; base += stride) {
+    const int64_t g = base + threadIdx.x;
+    bool live = false;
+    if (g < ch.n) {
+      const int64_t v = g / per_c, pix = g - v * per_c;
+      const int j = (int)(pix / ch.lw), i = (int)(pix - (int64_t)j * ch.lw);
+      const int64_t p = v * per_p + (int64_t)(j / 2) * par.lw + (i / 2);
+      uint8_t s = par.status[p];
+      if (s == DIST_CONVERGED) s = DIST_MARCHING;
+      ch.status[g] = s;
+      ch.d[g] = par.d[p];
+      ch.b[g] = par.b[p];
+      ch.steps[g] = par.steps[p];
+      for (int k = 0; k < K; ++k) {
+        ch.tk_d[g * K + k] = par.tk_d[p * K + k];
+        ch.tk_f[g * K + k] = par.tk_f[p * K + k];
+        ch.tk_a[g * K + k] = par.tk_a[p * K + k];
+      }
+      live = s == DIST_MARCHING;
+    }
+    warp_append(live, (int32_t)g, list, &ctl->cnt[0]);
+  }
+}
+
+__global__ void k_finalize(LevelState ls) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ls.n;
+       g += (int64_t)gridDim.x * blockDim.x)
+    if (ls.status[g] == DIST_MARCHING) ls.status[g] = DIST_EXHAUSTED;
+}
+
+// --- one step slot, SIMT decoder --------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(SimtTile<T>::NT)
+    k_step(DecView dv, const double *__restrict__ c0, const double *__restrict__ cskip,
+           const dist_camera *__restrict__ cams, LevelState ls, Ctl *ctl, int32_t *list0,
+           int32_t *list1, MarchArgs a, int64_t *live_counts, int64_t *stats) {
+  extern __shared__ __align__(16) char smem[];
+  using Tile = SimtTile<T>;
+  Tile tile(smem);
+  __shared__ int s_cur, s_cnt, s_go, s_nan;
+  if (threadIdx.x == 0) {
+    s_cur = ctl->cur;
+    s_cnt = ctl->cnt[s_cur];
+    s_go = (ctl->steps_done < a.max_steps) && (s_cnt > 0);
+    s_nan = 0;
+  }
+  __syncthreads();
+  if (!s_go) return;
+  const int cur = s_cur;
+  const int32_t *in = cur ? list1 : list0;
+  int32_t *out = cur ? list0 : list1;
+  int32_t *out_cnt = &ctl->cnt[cur ^ 1];
+  const int64_t rows = a.dynamic ? (int64_t)s_cnt : ls.n;
+  const int64_t ntiles = ceil_div(rows, Tile::TM);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int64_t g = -1;
+    double dir[3] = {0, 0, 0};
+    const dist_camera *cam = cams;
+    if (threadIdx.x < Tile::TM) {
+      const int64_t idx = t * Tile::TM + threadIdx.x;
+      double p[3] = {0, 0, 0};
+      int s = -1;
+      if (idx < rows) {
+        g = a.dynamic ? in[idx] : idx;
+        ray_of(cams, ls, g, dir, &cam);
+        const double dg = ls.d[g];
+        for (int i = 0; i < 3; ++i) p[i] = __dadd_rn(cam->origin[i], __dmul_rn(dg, dir[i]));
+        s = cam->shape;
+      }
+      tile.shape[threadIdx.x] = s;
+      for (int i = 0; i < 3; ++i) tile.pts[threadIdx.x * 3 + i] = p[i];
+    }
+    __syncthreads();
+    tile.forward(dv, c0, cskip, false);
+    if (warp == 0) {
+      bool keep = false;
+      if (threadIdx.x < Tile::TM && g >= 0 && ls.status[g] == DIST_MARCHING) {
+        int nn = 0;
+        keep = march_update(ls, a, g, dir, cam->origin, tile.f[threadIdx.x], &nn);
+        if (nn) atomicAdd(&s_nan, nn);
+      }
+      warp_append(keep, (int32_t)g, out, out_cnt);
+    }
+    (void)lane;
+    __syncthreads();
+  }
+  step_epilogue(ctl, cur, rows, s_nan, live_counts, stats);
+}
+
+// --- maps (shading.py:48-61, 97-113) ------------------------------------------
+__global__ void k_maps(const dist_camera *__restrict__ cams, LevelState ls, double alpha, double eps,
+                       int K, double *depth, uint8_t *mask, double *sil) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ls.n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const uint8_t s = ls.status[g];
+    const bool conv = s == DIST_CONVERGED;
+    double dir[3], scale;
+    const int64_t per = (int64_t)ls.lw * ls.lh;
+    const int v = (int)(g / per);
+    const int64_t pix = g - (int64_t)v * per;
+    const int j = (int)(pix / ls.lw), i = (int)(pix - (int64_t)j * ls.lw);
+    pixel_ray(cams[v], i, j, 1, dir, &scale);
+    if (depth) {
+      const double ds = __dadd_rn(ls.d[g], __dmul_rn(1.0 - alpha, ls.b[g]));
+      depth[g] = conv ? __dmul_rn(ds, scale) : __longlong_as_double(0x7ff0000000000000ll);
+    }
+    if (mask) mask[g] = conv ? 1 : 0;
+    if (sil) {
+      const double a0 = ls.tk_a[g * K];
+      if (isfinite(a0)) {
+        sil[g] = a0 - eps;
+      } else {
+        const double *o = cams[v].origin;
+        const double m = dir[0] * o[0] + dir[1] * o[1] + dir[2] * o[2];
+        const double c2 = o[0] * o[0] + o[1] * o[1] + o[2] * o[2];
+        sil[g] = sqrt(fmax(c2 - m * m, 0.0)) - 1.0;
+      }
+    }
+  }
+}
+
+// --- normals (shading.py:73-94) ----------------------------------------------
+struct ProbeGen {
+  const dist_camera *cams;
+  LevelState ls;
+  const int32_t *conv;   // converged ray ids
+  const int32_t *cnt_ptr;  // device count
+  double alpha, delta;
+  double *f;
+  __device__ int64_t count() const { return (int64_t)*cnt_ptr * 6; }
+  __device__ bool point(int64_t i, double p[3], int &s) const {
+    const int64_t r = i / 6;
+    const int a = (int)(i - r * 6);
+    const int64_t g = conv[r];
+    double dir[3];
+    const int64_t per = (int64_t)ls.lw * ls.lh;
+    const int v = (int)(g / per);
+    const int64_t pix = g - (int64_t)v * per;
+    const int j = (int)(pix / ls.lw), ii = (int)(pix - (int64_t)j * ls.lw);
+    pixel_ray(cams[v], ii, j, 1, dir, nullptr);
+    const double ds = __dadd_rn(ls.d[g], __dmul_rn(1.0 - alpha, ls.b[g]));
+    for (int q = 0; q < 3; ++q) p[q] = __dadd_rn(cams[v].origin[q], __dmul_rn(ds, dir[q]));
+    const int axis = a % 3;
+    p[axis] = __dadd_rn(p[axis], a < 3 ? delta : -delta);
+    s = cams[v].shape;
+    return true;
+  }
+  __device__ double seed(int64_t, double) const { return 0.0; }
+  __device__ void store(int64_t i, double v) const { f[i] = v; }
+};
+
+__global__ void k_normals_assemble(LevelState ls, const int32_t *__restrict__ conv,
+                                   const int32_t *__restrict__ count, const double *__restrict__ f,
+                                   double delta, double *__restrict__ normals) {
+  const int64_t n = *count;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = conv[r];
+    double raw[3];
+    for (int a = 0; a < 3; ++a) raw[a] = (f[r * 6 + a] - f[r * 6 + 3 + a]) / (2.0 * delta);
+    const double nrm = sqrt(raw[0] * raw[0] + raw[1] * raw[1] + raw[2] * raw[2]);
+    for (int a = 0; a < 3; ++a) normals[g * 3 + a] = nrm > 0.0 ? raw[a] / nrm : 0.0;
+  }
+}
+
+// --- host side --------------------------------------------------------------
+static int check_cfg(const dist_trace_config *c, int width, int height, int V) {
+  if (!c) return fail(DIST_ERR_CONFIG, "null config");
+  if (!(c->alpha > 0.0 && c->alpha < 2.0)) return fail(DIST_ERR_CONFIG, "alpha must be in (0, 2)");
+  if (!(c->epsilon > 0.0)) return fail(DIST_ERR_CONFIG, "epsilon must be positive");
+  if (c->max_steps < 1) return fail(DIST_ERR_CONFIG, "max_steps must be at least 1");
+  if (c->k_samples < 1 || c->k_samples > 16) return fail(DIST_ERR_CONFIG, "k_samples must be in [1, 16]");
+  if (c->coarse_start_scale != 1 && c->coarse_start_scale != 2 && c->coarse_start_scale != 4)
+    return fail(DIST_ERR_CONFIG, "coarse_start_scale must be 1, 2, or 4");
+  if (c->split_interval < 1) return fail(DIST_ERR_CONFIG, "split_interval must be at least 1");
+  if (width <= 0 || height <= 0 || V <= 0) return fail(DIST_ERR_CONFIG, "resolution must be positive");
+  if (width % c->coarse_start_scale || height % c->coarse_start_scale)
+    return fail(DIST_ERR_CONFIG, "resolution not divisible by coarse_start_scale");
+  if ((int64_t)V * width * height >= (int64_t)1 << 31)
+    return fail(DIST_ERR_CONFIG, "too many rays for one trace call");
+  return DIST_OK;
+}
+
+struct TraceLayout {
+  double *c0, *cskip;
+  LevelState lv[3];
+  int n_levels;
+  int32_t *list0, *list1, *bcount;
+  Ctl *ctl;
+  size_t bytes;
+};
+
+static TraceLayout layout(const DecView &dv, const dist_trace_config *cfg, int V, int W, int H,
+                          int S, char *ws, size_t cap, const dist_ray_state *out) {
+  TraceLayout L{};
+  Carve cv{ws, 0, cap};
+  const int s1 = std::max(S, 1);
+  L.c0 = cv.take<double>((size_t)s1 * dv.np[0]);
+  L.cskip = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
+  int levels[3], nl = 0;
+  for (int s = cfg->coarse_start_scale; s >= 1; s /= 2) levels[nl++] = s;
+  L.n_levels = nl;
+  const int K = cfg->k_samples;
+  for (int li = 0; li < nl; ++li) {
+    LevelState &ls = L.lv[li];
+    ls.level = levels[li];
+    ls.lw = W / ls.level;
+    ls.lh = H / ls.level;
+    ls.n = (int64_t)V * ls.lw * ls.lh;
+    if (ls.level == 1) {
+      if (out) {
+        ls.d = out->d; ls.b = out->b; ls.status = out->status; ls.steps = out->steps;
+        ls.tk_d = out->topk_d; ls.tk_f = out->topk_f; ls.tk_a = out->topk_absf;
+      }
+    } else {
+      ls.d = cv.take<double>(ls.n);
+      ls.b = cv.take<double>(ls.n);
+      ls.status = cv.take<uint8_t>(ls.n);
+      ls.steps = cv.take<int32_t>(ls.n);
+      ls.tk_d = cv.take<double>(ls.n * K);
+      ls.tk_f = cv.take<double>(ls.n * K);
+      ls.tk_a = cv.take<double>(ls.n * K);
+    }
+  }
+  const int64_t nmax = (int64_t)V * W * H;
+  L.list0 = cv.take<int32_t>(nmax);
+  L.list1 = cv.take<int32_t>(nmax);
+  L.bcount = cv.take<int32_t>(ceil_div(nmax * 6, kScanBlock) + 1);
+  L.ctl = cv.take<Ctl>(1);
+  L.bytes = cv.off + 256;
+  return L;
+}
+
+template <typename T>
+static int run_steps(const DecView &dv, const double *c0, const double *cskip,
+                     const dist_camera *cams, const LevelState &ls, Ctl *ctl, int32_t *l0,
+                     int32_t *l1, const MarchArgs &a, int slots, int64_t *live, int64_t *stats,
+                     cudaStream_t st) {
+  using Tile = SimtTile<T>;
+  const void *fn = (const void *)k_step<T>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)Tile::fwd_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(step)");
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, Tile::NT, Tile::fwd_bytes);
+  const int64_t tiles = ceil_div(ls.n, Tile::TM);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)std::max(per_sm, 1) * sm_count()));
+  for (int s = 0; s < slots; ++s) {
+    k_step<T><<<grid, Tile::NT, Tile::fwd_bytes, st>>>(dv, c0, cskip, cams, ls, ctl, l0, l1, a, live,
+                                                      stats);
+    DIST_CHECK_LAUNCH("k_step");
+  }
+  return DIST_OK;
+}
+
+static int grid_for(int64_t n, int threads) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), (int64_t)sm_count() * 16));
+}
+
+}  // namespace dist
+
+using namespace dist;
+
+extern "C" {
+
+size_t dist_trace_workspace_size(const dist_decoder *dec, const dist_trace_config *cfg, int V,
+                                 int W, int H, int S) {
+  if (!dec || !cfg || cfg->coarse_start_scale < 1) return 0;
+  return layout(dec->view, cfg, V, W, H, S, nullptr, ~size_t(0), nullptr).bytes;
+}
+
+int dist_trace(const dist_decoder *dec, const double *codes, int S, const dist_camera *cams,
+               int V, int W, int H, const dist_trace_config *cfg, const dist_ray_state *out,
+               int64_t *live, int64_t *stats, void *ws, size_t ws_bytes, void *stream) {
+  if (!dec || !out || !cams || !live || !stats) return fail(DIST_ERR_CONFIG, "null argument");
+  int rc = check_cfg(cfg, W, H, V);
+  if (rc) return rc;
+  const DecView &dv = dec->view;
+  if (dv.latent_dim > 0 && (!codes || S < 1)) return fail(DIST_ERR_CONFIG, "field expects a latent code");
+  cudaStream_t st = (cudaStream_t)stream;
+  TraceLayout L = layout(dv, cfg, V, W, H, S, (char *)ws, ws_bytes, out);
+  if (L.bytes > ws_bytes) return fail(DIST_ERR_CONFIG, "trace workspace too small");
+  cudaError_t e = cudaMemsetAsync(L.ctl, 0, sizeof(Ctl), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(stats, 0, 4 * sizeof(int64_t), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(live, 0, cfg->max_steps * sizeof(int64_t), st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(trace)");
+  rc = launch_code_bias(dv, dv.latent_dim > 0 ? codes : nullptr, std::max(S, 1), L.c0, L.cskip, st);
+  if (rc) return rc;
+  MarchArgs a{cfg->alpha, cfg->epsilon, cfg->k_samples, cfg->max_steps,
+              cfg->use_dynamic_mask ? 1 : 0, V};
+  const int K = cfg->k_samples;
+  k_init<<<grid_for(L.lv[0].n, 256), 256, 0, st>>>(cams, L.lv[0], K, L.list0, L.ctl, stats);
+  DIST_CHECK_LAUNCH("k_init");
+  for (int li = 0; li < L.n_levels; ++li) {
+    const LevelState &ls = L.lv[li];
+    if (li > 0) {
+      // fresh lists for the new level; steps_done (offset 16) persists
+      e = cudaMemsetAsync(L.ctl, 0, 16, st);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(ctl)");
+      k_split<<<grid_for(ls.n, 256), 256, 0, st>>>(L.lv[li - 1], ls, K, L.list0, L.ctl);
+      DIST_CHECK_LAUNCH("k_split");
+    }
+    const int slots = std::min(ls.level > 1 ? cfg->split_interval : cfg->max_steps, cfg->max_steps);
+    if (dv.prec == DIST_PREC_FP64)
+      rc = run_steps<double>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, live, stats, st);
+    else if (dv.prec == DIST_PREC_BF16X3 && tc_supported(dv))
+      rc = tc_run_steps(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, live, stats, st);
+    else
+      rc = run_steps<float>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, live, stats, st);
+    if (rc) return rc;
+  }
+  const LevelState &fin = L.lv[L.n_levels - 1];
+  k_finalize<<<grid_for(fin.n, 256), 256, 0, st>>>(fin);
+  DIST_CHECK_LAUNCH("k_finalize");
+  return DIST_OK;
+}
+
+int dist_maps(const dist_camera *cams, int V, int W, int H, const dist_trace_config *cfg,
+              const dist_ray_state *stt, double *depth, uint8_t *mask, double *sil, void *stream) {
+  if (!cams || !cfg || !stt) return fail(DIST_ERR_CONFIG, "null argument");
+  LevelState ls{stt->d, stt->b, stt->status, stt->steps, stt->topk_d, stt->topk_f, stt->topk_absf,
+                W, H, 1, (int64_t)V * W * H};
+  k_maps<<<grid_for(ls.n, 256), 256, 0, (cudaStream_t)stream>>>(cams, ls, cfg->alpha, cfg->epsilon,
+                                                                 cfg->k_samples, depth, mask, sil);
+  DIST_CHECK_LAUNCH("k_maps");
+  return DIST_OK;
+}
+
+size_t dist_normals_workspace_size(const dist_decoder *dec, int V, int W, int H, int S) {
+  if (!dec) return 0;
+  const int64_t n = (int64_t)V * W * H;
+  Carve cv{nullptr, 0, ~size_t(0)};
+  const int s1 = std::max(S, 1);
+  cv.take<double>((size_t)s1 * dec->view.np[0]);
+  cv.take<double>((size_t)s1 * std::max(dec->view.nskip, 1));
+  cv.take<int32_t>(n);
+  cv.take<int32_t>(4);
+  cv.take<int32_t>(ceil_div(n, kScanBlock) + 1);
+  cv.take<double>(n * 6);
+  return cv.off + 256;
+}
+
+int dist_normals(const dist_decoder *dec, const double *codes, int S, const dist_camera *cams,
+                 int V, int W, int H, const dist_trace_config *cfg, const dist_ray_state *stt,
+                 double *normals, void *ws, size_t ws_bytes, void *stream) {
+  if (!dec || !cams || !cfg || !stt || !normals) return fail(DIST_ERR_CONFIG, "null argument");
+  const DecView &dv = dec->view;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t n = (int64_t)V * W * H;
+  const int s1 = std::max(S, 1);
+  Carve cv{(char *)ws, 0, ws_bytes};
+  double *c0 = cv.take<double>((size_t)s1 * dv.np[0]);
+  double *cs = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
+  int32_t *conv = cv.take<int32_t>(n);
+  int32_t *count = cv.take<int32_t>(4);
+  int32_t *bcount = cv.take<int32_t>(ceil_div(n, kScanBlock) + 1);
+  double *f = cv.take<double>(n * 6);
+  if (!cv.ok) return fail(DIST_ERR_CONFIG, "normals workspace too small");
+  cudaError_t e = cudaMemsetAsync(normals, 0, sizeof(double) * 3 * n, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(normals)");
+  int rc = launch_code_bias(dv, dv.latent_dim > 0 ? codes : nullptr, s1, c0, cs, st);
+  if (rc) return rc;
+  const uint8_t *status = stt->status;
+  rc = compact([status] __device__(int64_t i) { return status[i] == DIST_CONVERGED; }, n, conv,
+               count, bcount, st);
+  if (rc) return rc;
+  LevelState ls{stt->d, stt->b, stt->status, stt->steps, stt->topk_d, stt->topk_f, stt->topk_absf,
+                W, H, 1, n};
+  ProbeGen gen{cams, ls, conv, count, cfg->alpha, cfg->normal_delta, f};
+  if (dv.prec == DIST_PREC_FP64) rc = launch_eval_gen<double>(dv, c0, cs, gen, n * 6, st);
+  else rc = launch_eval_gen<float>(dv, c0, cs, gen, n * 6, st);
+  if (rc) return rc;
+  k_normals_assemble<<<grid_for(n, 256), 256, 0, st>>>(ls, conv, count, f, cfg->normal_delta, normals);
+  DIST_CHECK_LAUNCH("k_normals_assemble");
+  return DIST_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,196 @@
+"""Sphere tracing on the B200 -- drop-in for the reference tracer.py.
+
+`trace(field, code, intr, pose, cfg)` has the reference signature and returns
+a `TraceResult` whose `state` is a `RayState` of numpy arrays
+(tracer.py:53-82), so the reference's own map, loss and test code can read it.
+Underneath, `trace_views` runs the whole coarse-to-fine march of V views on
+the device in one C-ABI call (dist_trace) with no host synchronisation per
+step, and keeps the state resident in HBM (`DeviceTrace`) for the heads,
+losses and optimiser that follow.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import warnings
+from dataclasses import dataclass, field as dfield
+
+import numpy as np
+
+from . import _lib
+from .camera import Intrinsics, Pose, RayBundle, camera_struct, generate_rays
+
+MARCHING, CONVERGED, ESCAPED, EXHAUSTED = 0, 1, 2, 3
+
+
+@dataclass
+class TraceConfig:
+    """tracer.py:27-50 (same defaults and validation)."""
+    alpha: float = 1.5
+    epsilon: float = 5e-5
+    max_steps: int = 100
+    k_samples: int = 1
+    coarse_start_scale: int = 4
+    split_interval: int = 3
+    normal_delta: float = 1e-3
+    use_dynamic_mask: bool = True
+
+    def __post_init__(self):
+        if not (0.0 < self.alpha < 2.0):
+            raise ValueError("alpha must be in (0, 2)")
+        if self.epsilon <= 0:
+            raise ValueError("epsilon must be positive")
+        if self.max_steps < 1:
+            raise ValueError("max_steps must be at least 1")
+        if self.k_samples < 1:
+            raise ValueError("k_samples must be at least 1")
+        if self.coarse_start_scale not in (1, 2, 4):
+            raise ValueError("coarse_start_scale must be 1, 2, or 4")
+        if self.split_interval < 1:
+            raise ValueError("split_interval must be at least 1")
+
+
+@dataclass
+class RayState:
+    """Host view of one view's final-level state (tracer.py:53-73)."""
+    bundle: RayBundle
+    d: np.ndarray
+    b: np.ndarray
+    status: np.ndarray
+    steps: np.ndarray
+    topk_d: np.ndarray
+    topk_f: np.ndarray
+    topk_absf: np.ndarray
+
+    @property
+    def n(self) -> int:
+        return self.d.shape[0]
+
+    def live(self) -> np.ndarray:
+        return self.status == MARCHING
+
+
+class DeviceTrace:
+    """Device-resident result of tracing V views (all tensors on cuda)."""
+
+    def __init__(self, field, codes, cams, intrs, poses, cfg: TraceConfig, W: int, H: int):
+        import torch
+        self.field, self.codes, self.cfg = field, codes, cfg
+        self.cams, self.intrs, self.poses = cams, intrs, poses
+        self.V, self.W, self.H = len(intrs), W, H
+        n = self.V * W * H
+        K = cfg.k_samples
+        dev = "cuda"
+        self.d = torch.empty(n, dtype=torch.float64, device=dev)
+        self.b = torch.empty(n, dtype=torch.float64, device=dev)
+        self.status = torch.empty(n, dtype=torch.uint8, device=dev)
+        self.steps = torch.empty(n, dtype=torch.int32, device=dev)
+        self.topk_d = torch.empty((n, K), dtype=torch.float64, device=dev)
+        self.topk_f = torch.empty((n, K), dtype=torch.float64, device=dev)
+        self.topk_absf = torch.empty((n, K), dtype=torch.float64, device=dev)
+        self.live_counts_dev = torch.zeros(cfg.max_steps, dtype=torch.int64, device=dev)
+        self.stats_dev = torch.zeros(4, dtype=torch.int64, device=dev)
+
+    def state_struct(self) -> _lib.dist_ray_state:
+        return _lib.dist_ray_state(self.d.data_ptr(), self.b.data_ptr(), self.status.data_ptr(),
+                                   self.steps.data_ptr(), self.topk_d.data_ptr(),
+                                   self.topk_f.data_ptr(), self.topk_absf.data_ptr())
+
+    def stats(self) -> dict:
+        s = self.stats_dev.cpu().numpy()
+        lc = self.live_counts_dev[: int(s[2])].cpu().numpy()
+        return {"total_queries": int(s[0]), "nan_count": int(s[1]), "steps": int(s[2]),
+                "warnings": int(s[3]), "live_counts": [int(x) for x in lc]}
+
+
+def _code_tensor(field, codes):
+    import torch
+    if field.latent_dim == 0:
+        return None, 1
+    if codes is None:
+        raise ValueError("field expects a latent code")
+    if isinstance(codes, torch.Tensor):
+        z = codes.to(device="cuda", dtype=torch.float64)
+    else:
+        z = torch.from_numpy(np.asarray(codes, dtype=np.float64).copy()).cuda()
+    z = z.reshape(-1, field.latent_dim).contiguous()
+    return z, z.shape[0]
+
+
+def trace_views(field, codes, views, cfg: TraceConfig | None = None,
+                shape_of_view=None) -> DeviceTrace:
+    """Trace V views (list of (Intrinsics, Pose)) of one resolution in one call.
+
+    codes: [D] or [S, D]; shape_of_view[v] picks the code row of view v.
+    """
+    import torch
+    cfg = cfg or TraceConfig()
+    _lib.require_device()
+    intrs = [v[0] for v in views]
+    poses = [v[1] for v in views]
+    W, H = intrs[0].width, intrs[0].height
+    if any(i.width != W or i.height != H for i in intrs):
+        raise ValueError("all views of one trace call must share a resolution")
+    if W % cfg.coarse_start_scale or H % cfg.coarse_start_scale:
+        raise ValueError(f"resolution {W}x{H} not divisible by coarse_start_scale "
+                         f"{cfg.coarse_start_scale}")
+    h = field.handle()
+    z, S = _code_tensor(field, codes)
+    sv = [0] * len(views) if shape_of_view is None else [int(s) for s in shape_of_view]
+    cams = _lib.cameras_to_device([camera_struct(i, p, s) for i, p, s in zip(intrs, poses, sv)])
+    dt = DeviceTrace(field, z, cams, intrs, poses, cfg, W, H)
+    lib = _lib.lib()
+    c = _lib.config_struct(cfg)
+    nbytes = lib.dist_trace_workspace_size(h, C.byref(c), len(views), W, H, S)
+    ws = _lib.workspace(nbytes)
+    st = dt.state_struct()
+    _lib.check(lib.dist_trace(h, _lib.ptr(z), S, cams.data_ptr(), len(views), W, H, C.byref(c),
+                              C.byref(st), dt.live_counts_dev.data_ptr(), dt.stats_dev.data_ptr(),
+                              ws.data_ptr(), ws.numel(), _lib.stream_ptr()))
+    dt._ws_keep = ws
+    return dt
+
+
+@dataclass
+class TraceResult:
+    """tracer.py:76-82, plus `device` (the resident DeviceTrace)."""
+    state: RayState
+    config: TraceConfig
+    intrinsics: Intrinsics
+    pose: Pose
+    live_counts: list = dfield(default_factory=list)
+    total_queries: int = 0
+    nan_count: int = 0
+    device: DeviceTrace | None = None
+    view: int = 0
+
+
+def host_result(dt: DeviceTrace, view: int = 0) -> TraceResult:
+    """Copy one view's state to numpy in the reference's RayState layout."""
+    n = dt.W * dt.H
+    sl = slice(view * n, (view + 1) * n)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        bundle = generate_rays(dt.intrs[view], dt.poses[view], 1)
+    st = RayState(bundle=bundle, d=dt.d[sl].cpu().numpy(), b=dt.b[sl].cpu().numpy(),
+                  status=dt.status[sl].cpu().numpy(),
+                  steps=dt.steps[sl].cpu().numpy().astype(np.int64),
+                  topk_d=dt.topk_d[sl].cpu().numpy(), topk_f=dt.topk_f[sl].cpu().numpy(),
+                  topk_absf=dt.topk_absf[sl].cpu().numpy())
+    s = dt.stats()
+    return TraceResult(state=st, config=dt.cfg, intrinsics=dt.intrs[view], pose=dt.poses[view],
+                       live_counts=s["live_counts"], total_queries=s["total_queries"],
+                       nan_count=s["nan_count"], device=dt, view=view)
+
+
+def trace(field, code, intr: Intrinsics, pose: Pose, cfg: TraceConfig | None = None) -> TraceResult:
+    """Full render-tracing pass (tracer.py:221-252) on the GPU."""
+    cfg = cfg or TraceConfig()
+    if intr.width % cfg.coarse_start_scale or intr.height % cfg.coarse_start_scale:
+        raise ValueError(f"resolution {intr.width}x{intr.height} not divisible by "
+                         f"coarse_start_scale {cfg.coarse_start_scale}")
+    dt = trace_views(field, code, [(intr, pose)], cfg)
+    res = host_result(dt, 0)
+    if dt.stats()["warnings"] & 1:
+        warnings.warn("camera center inside the unit sphere; rays start at d=0", RuntimeWarning)
+    return res

@@ -1,0 +1,102 @@
+"""GPU parity of heads, losses, the fused objective and Adam vs the reference goldens."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import cfg_from, golden_weights, load_golden
+
+pytestmark = pytest.mark.gpu
+
+import sdf_oracle as orc  # noqa: E402  (checker only)
+
+
+@pytest.fixture(scope="module")
+def st():
+    import paper_1911_13225_b200 as st
+    return st
+
+
+def _setup_tiny(st):
+    g = load_golden("tiny64.npz")
+    net = st.NeuralField(golden_weights(g), latent_dim=2, precision="fp64")
+    res = int(g["res"])
+    intr, pose = st.Intrinsics(width=res, height=res), st.Pose(g["omega"], g["t"])
+    cfg = st.TraceConfig(**cfg_from(g["cfg"]))
+    return g, net, intr, pose, cfg
+
+
+def test_tiny_heads_values_and_backward(st):
+    g, net, intr, pose, cfg = _setup_tiny(st)
+    r = st.trace(net, g["code"], intr, pose, cfg)
+    h = st.diff_heads(r, net, g["code"], want_normals=True)
+    assert np.array_equal(h.ray_index, g["h_ray_index"])
+    assert np.array_equal(h.best_sample, g["h_best"])
+    np.testing.assert_allclose(h.sample_d, g["h_sample_d"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(h.sample_f, g["h_sample_f"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(h.normal_value, g["h_normal"], rtol=0, atol=1e-8)
+    out = h.backward(depth_seed=g["bw_depth_seed"], sil_seed=g["bw_sil_seed"],
+                     normal_seed=g["bw_normal_seed"])
+    np.testing.assert_allclose(out["code"], g["bw_code"], rtol=1e-8, atol=1e-10)
+    np.testing.assert_allclose(out["sample_point_grads"], g["bw_points"], rtol=1e-8, atol=1e-10)
+    np.testing.assert_allclose(out["surface_point_grads"], g["bw_surface"], rtol=1e-6, atol=1e-8)
+
+
+def test_tiny_completion_objective_all_terms(st):
+    g, net, intr, pose, cfg = _setup_tiny(st)
+    obs = [st.Observation("depth", g["obs_depth"]), st.Observation("silhouette", g["obs_sil"]),
+           st.Observation("normal", g["obs_normal"])]
+    tot, terms, grad, n_conv, q = st.completion_objective(net, g["code"], obs, intr, pose, cfg,
+                                                          st.LossWeights())
+    assert n_conv == int(g["obj_nconv"]) and q == int(g["obj_queries"])
+    assert abs(tot - float(g["obj_total"])) < 1e-9
+    np.testing.assert_allclose(grad, g["obj_grad"], rtol=1e-7, atol=1e-9)
+
+
+def test_tiny_fused_objective_depth_only(st):
+    g, net, intr, pose, cfg = _setup_tiny(st)
+    obs = [st.Observation("depth", g["obs_depth"])]
+    tot, terms, grad, n_conv, q = st.completion_objective(net, g["code"], obs, intr, pose, cfg,
+                                                          st.LossWeights())
+    assert abs(tot - float(g["objd_total"])) < 1e-10
+    np.testing.assert_allclose(grad, g["objd_grad"], rtol=1e-9, atol=1e-12)
+
+
+def test_tiny_fused_objective_depth_and_silhouette(st):
+    g, net, intr, pose, cfg = _setup_tiny(st)
+    dec = orc.Decoder(golden_weights(g), 2)
+    cam = orc.Cam(64, 64, g["omega"], g["t"])
+    ocfg = orc.Cfg(k_samples=3)
+    tot_o, terms_o, g_o, n_o, q_o, _ = orc.objective(dec, g["code"], cam, ocfg, orc.Weights(),
+                                                     depth=g["obs_depth"], silhouette=g["obs_sil"])
+    obs = [st.Observation("depth", g["obs_depth"]), st.Observation("silhouette", g["obs_sil"])]
+    tot, terms, grad, n_conv, q = st.completion_objective(net, g["code"], obs, intr, pose, cfg,
+                                                          st.LossWeights())
+    assert n_conv == n_o and q == q_o
+    assert abs(terms["silhouette"] - terms_o["silhouette"]) < 1e-12
+    assert abs(tot - tot_o) < 1e-10
+    np.testing.assert_allclose(grad, g_o, rtol=1e-9, atol=1e-12)
+
+
+def test_tiny_complete_shape_matches_reference(st):
+    g, net, intr, pose, cfg = _setup_tiny(st)
+    obs = [st.Observation("depth", g["obs_depth"])]
+    best, rep = st.complete_shape(net, obs, intr, pose, code0=np.zeros(2), iters=4, cfg=cfg)
+    np.testing.assert_allclose(rep.losses, g["cs_losses"], rtol=1e-9, atol=1e-12)
+    assert rep.best_iter == int(g["cs_best_iter"])
+    np.testing.assert_allclose(best, g["cs_best"], rtol=1e-9, atol=1e-12)
+
+
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("fp32", 1e-3)])
+def test_geo64_objective(st, prec, tol):
+    g = load_golden("geo64.npz")
+    net = st.NeuralField.geometric(256, (512,) * 8, int(g["seed"]), precision=prec)
+    res = int(g["res"])
+    intr, pose = st.Intrinsics(width=res, height=res), st.Pose(g["omega"], g["t"])
+    cfg = st.TraceConfig(**cfg_from(g["cfg"]))
+    obs = [st.Observation("depth", g["obs_depth"])]
+    tot, terms, grad, n_conv, q = st.completion_objective(net, g["code"], obs, intr, pose, cfg,
+                                                          st.LossWeights())
+    ref = g["obj_grad"]
+    assert abs(tot - float(g["obj_total"])) <= tol * abs(float(g["obj_total"]))
+    assert np.linalg.norm(grad - ref) / np.linalg.norm(ref) < tol
