@@ -1,0 +1,298 @@
+"""Benchmark: multi-view latent optimisation (BASELINE config 3) on B200.
+
+One step = one full latent-optimisation iterate over this rank's 8 views of
+512x512: coarse-to-fine aggressive sphere tracing of the 8x512 DeepSDF decoder
+(latent 256), the K=3 frozen-sample heads, the fused forward -> seed ->
+backward, the latent all-reduce across ranks (N>1) and the Adam step.
+Metric: rays/s sphere-traced fwd+bwd = full-resolution pixels x views per
+step / step time (whole job), plus ms per latent-opt iterate.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  (N>1: torchrun --nproc-per-node N ... bench.py --gpus N)
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle port of the pure-numpy reference, oracle/sdf_oracle.py) on the host
+cores, on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "rays/sec sphere-traced fwd+bwd (DeepSDF 8x512, 512² views); ms/latent-opt iter"
+UNIT = "rays/s"
+VIEWS_PER_RANK = 8
+RES = 512
+F_Q = 3_674_112      # algorithmic FLOP per decoder query (layer 0 folded, no skip), SURVEY 8d
+F_B = 3_671_040      # algorithmic FLOP per differentiated sample (dgrad, no wgrad), SURVEY 8d
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p, "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        try:
+            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            rows = []
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if len(r) > 2 + i and "Active" in r[2 + i] and "Not" not in r[2 + i]})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": float(rows[0][1]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_reference_sample(seconds_hint=True):
+    """Time the CPU restatement of the reference (oracle) on a bounded sample:
+    one full completion_objective of a 128x128 crop-equivalent view (1/16 of
+    one 512^2 view) of the same decoder and scene.  Returns (rays/s, info)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import sdf_oracle as orc
+    from paper_1911_13225_b200.workloads import ring_eye, target_code
+    res = 128
+    dec = orc.Decoder(orc.geometric_init(256, (512,) * 8, 0), 256)
+    z_true = target_code(1)
+    cam = orc.cam_look_at(ring_eye(0, VIEWS_PER_RANK), res, res)
+    cfg = orc.Cfg(k_samples=3)
+    T = orc.trace(lambda p: dec(p, z_true), cam, cfg)
+    obs = orc.depth_map(T, cfg)
+    t0 = time.perf_counter()
+    tot, terms, g, n_conv, q, _ = orc.objective(dec, np.zeros(256), cam, cfg, orc.Weights(),
+                                                depth=obs)
+    dt = time.perf_counter() - t0
+    cores = len(os.sched_getaffinity(0))
+    return res * res / dt, {"cores": cores, "seconds": dt, "queries": q,
+                            "sample": f"one {res}x{res} view (1/16 of a 512^2 view), full "
+                                      f"completion_objective (trace+heads+backward) of the 8x512 "
+                                      f"decoder in numpy fp64 with {cores}-thread BLAS"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    for _ in range(args.warmup):
+        cpu_reference_sample()
+    vals, infos = [], []
+    for _ in range(args.steps):
+        v, info = cpu_reference_sample()
+        vals.append(v)
+        infos.append(info)
+    val = float(np.mean(vals))
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": float(np.mean([i["seconds"] for i in infos]) * 1e3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": _config(args),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": infos[0]["cores"], "kind": "port",
+                             "sample": infos[0]["sample"]},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def _config(args):
+    return {"workload": f"C3: {VIEWS_PER_RANK} views/GPU x {RES}x{RES} depth-supervised latent "
+                        f"optimisation, 8x512 DeepSDF decoder (latent 256, geometric init seed 0), "
+                        f"K=3, alpha 1.5, coarse 4, 100 steps",
+            "views_per_gpu": VIEWS_PER_RANK, "resolution": RES, "precision": args.precision,
+            "parallelism": f"views sharded over {args.gpus} GPU(s), latent all-reduce",
+            "l2": "working set > L2 (ray state ~320 MB per step)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--precision", default=os.environ.get("DIST_BENCH_PRECISION", "fp32"))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_1911_13225_b200 as st
+    from paper_1911_13225_b200 import _lib
+    from paper_1911_13225_b200.workloads import render_depth_observations, ring_views, target_code
+
+    field = st.NeuralField.geometric(256, (512,) * 8, 0, precision=args.precision)
+    total_views = VIEWS_PER_RANK * world
+    views = ring_views(VIEWS_PER_RANK, RES, first=rank * VIEWS_PER_RANK, total=total_views)
+    cfg = st.TraceConfig(k_samples=3)
+    obs = render_depth_observations(field, target_code(1), views, cfg)
+    weights = st.LossWeights(latent=1.0 if rank == 0 else 0.0)   # regulariser added once
+    iters = args.warmup + args.steps
+    opt = st.LatentOptimizer(field, views, {"depth": obs}, np.zeros((1, 256)), cfg, weights,
+                             max_iters=2 * iters + 2)
+
+    def allreduce(grad, shape_terms):
+        if world > 1:
+            dist.all_reduce(grad)
+            dist.all_reduce(shape_terms)
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        opt.step(allreduce)
+    torch.cuda.synchronize()
+
+    # ---- timed region: device-resident iterates -----------------------------
+    q0 = torch.zeros(1, dtype=torch.int64, device="cuda")
+    tr_ev = []
+    n0 = _lib.lib().dist_launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            dt = st.trace_views(field, opt.code, views, cfg, reuse=opt.last_trace)
+            b.record(stream)
+            opt.last_trace = dt
+            q0 += dt.stats_dev[0]
+            tr_ev.append((a, b))
+            # the rest of the iterate (heads + fused backward + reduce + Adam) on the same trace
+            opt._objective_after_trace(dt)
+            allreduce(opt.grad, opt.shape_terms)
+            opt._adam()
+        e1.record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.lib().dist_launch_count() - n0
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    trace_ms = float(np.mean([a.elapsed_time(b) for a, b in tr_ev]))
+    queries = int(q0.item()) / args.steps
+    rays_per_step = VIEWS_PER_RANK * RES * RES * world
+    value = rays_per_step / (ms * 1e-3)
+
+    # ---- e2e: host observations in, loss out, every step ----------------------
+    obs_host = obs.cpu().pin_memory()
+    loss_host = torch.empty(opt.shape_terms.shape, dtype=torch.float64).pin_memory()
+    code_host = torch.empty(opt.code.shape, dtype=torch.float64).pin_memory()
+    h2d = obs_host.numel() * obs_host.element_size()
+    d2h = loss_host.numel() * 8 + code_host.numel() * 8
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        opt.obs_depth.copy_(obs_host.reshape(-1), non_blocking=True)
+        opt.step(allreduce)
+        loss_host.copy_(opt.shape_terms, non_blocking=True)
+        code_host.copy_(opt.code, non_blocking=True)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1) / args.steps
+    t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+
+    peaks, peak_kind = _peaks()
+    # roofline of the dominant kernel family: the decoder step kernels of the march
+    flops_trace = queries * F_Q
+    achieved = flops_trace / (trace_ms * 1e-3) / 1e12
+    if args.precision == "bf16x3":
+        peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        bound = "tensor"
+    else:
+        peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+        bound = "tensor"
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": {"fp32": "f32", "fp64": "f64", "bf16x3": "bf16x3"}[args.precision],
+        "data": "synthetic (geometric-init 8x512 DeepSDF, ring views, depth rendered from z*)",
+        "config": _config(args),
+        "e2e": {"value": rays_per_step / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "kernel": "march step kernels (decoder + update), whole trace phase",
+                     "peak_source": f"{peak_kind} bf16 sustained (MEASURED_PEAKS.json)",
+                     "algorithmic_flop_per_query": F_Q, "queries_per_step": queries,
+                     "trace_ms_per_step": trace_ms},
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        v, info = cpu_reference_sample()
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": "port",
+                                "sample": info["sample"]}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

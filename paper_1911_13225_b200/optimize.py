@@ -140,6 +140,12 @@ class LatentOptimizer:
         def put(key, dtype):
             if key not in observations or observations[key] is None:
                 return None
+            if isinstance(observations[key], torch.Tensor):
+                tdt = torch.float64 if dtype == np.float64 else torch.uint8
+                a = observations[key].to(device=dev, dtype=tdt).reshape(-1).contiguous()
+                if a.numel() != n:
+                    raise ValueError(f"observation {key!r} must be [V,H,W]")
+                return a
             a = np.asarray(observations[key]).reshape(-1)
             if a.size != n:
                 raise ValueError(f"observation {key!r} must be [V,H,W]")
@@ -154,7 +160,13 @@ class LatentOptimizer:
 
     def objective(self):
         """Trace + heads + fused backward at the current code (no Adam)."""
-        dt = trace_views(self.field, self.code, self.views, self.cfg, self.shape_of_view)
+        dt = trace_views(self.field, self.code, self.views, self.cfg, self.shape_of_view,
+                         reuse=self.last_trace)
+        self.last_trace = dt
+        self._objective_after_trace(dt)
+        return dt
+
+    def _objective_after_trace(self, dt):
         lib = _lib.lib()
         h = self.field.handle()
         K = self.cfg.k_samples
@@ -169,14 +181,10 @@ class LatentOptimizer:
         _lib.check(lib.dist_objective(h, self.code.data_ptr(), self.S, dt.cams.data_ptr(), self.V,
                                       self.W, self.H, C.byref(c), C.byref(st), C.byref(io),
                                       ws.data_ptr(), ws.numel(), _lib.stream_ptr()))
-        self.last_trace = dt
-        return dt
 
-    def step(self):
-        """One full iterate: objective at the current code, then Adam."""
+    def _adam(self):
         if self.iter >= self.max_iters:
             raise ValueError("max_iters exceeded")
-        self.objective()
         _lib.check(_lib.lib().dist_adam_step(
             self.S, self.D, self.code.data_ptr(), self.grad.data_ptr(), self.m.data_ptr(),
             self.v.data_ptr(), self.t.data_ptr(), self.skipped.data_ptr(),
@@ -184,6 +192,18 @@ class LatentOptimizer:
             self.best_iter.data_ptr(), self.iter, self.hist.data_ptr(), C.byref(self.adam_cfg),
             _lib.stream_ptr()))
         self.iter += 1
+
+    def step(self, reduce_fn=None):
+        """One full iterate: objective at the current code, then Adam.
+
+        reduce_fn(grad, shape_terms) runs between the backward and Adam -- the
+        cross-GPU gradient all-reduce when views are sharded over ranks."""
+        if self.iter >= self.max_iters:
+            raise ValueError("max_iters exceeded")
+        self.objective()
+        if reduce_fn is not None:
+            reduce_fn(self.grad, self.shape_terms)
+        self._adam()
 
     def losses(self) -> np.ndarray:
         return self.hist[: self.iter].cpu().numpy()

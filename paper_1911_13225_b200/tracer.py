@@ -118,10 +118,12 @@ def _code_tensor(field, codes):
 
 
 def trace_views(field, codes, views, cfg: TraceConfig | None = None,
-                shape_of_view=None) -> DeviceTrace:
+                shape_of_view=None, reuse: DeviceTrace | None = None) -> DeviceTrace:
     """Trace V views (list of (Intrinsics, Pose)) of one resolution in one call.
 
     codes: [D] or [S, D]; shape_of_view[v] picks the code row of view v.
+    reuse: a DeviceTrace of the same views/config whose buffers (and uploaded
+    cameras) are overwritten in place -- the optimisation loop's fast path.
     """
     import torch
     cfg = cfg or TraceConfig()
@@ -136,9 +138,14 @@ def trace_views(field, codes, views, cfg: TraceConfig | None = None,
                          f"{cfg.coarse_start_scale}")
     h = field.handle()
     z, S = _code_tensor(field, codes)
-    sv = [0] * len(views) if shape_of_view is None else [int(s) for s in shape_of_view]
-    cams = _lib.cameras_to_device([camera_struct(i, p, s) for i, p, s in zip(intrs, poses, sv)])
-    dt = DeviceTrace(field, z, cams, intrs, poses, cfg, W, H)
+    if reuse is not None:
+        dt = reuse
+        dt.codes = z
+    else:
+        sv = [0] * len(views) if shape_of_view is None else [int(s) for s in shape_of_view]
+        cams = _lib.cameras_to_device([camera_struct(i, p, s) for i, p, s in zip(intrs, poses, sv)])
+        dt = DeviceTrace(field, z, cams, intrs, poses, cfg, W, H)
+    cams = dt.cams
     lib = _lib.lib()
     c = _lib.config_struct(cfg)
     nbytes = lib.dist_trace_workspace_size(h, C.byref(c), len(views), W, H, S)
