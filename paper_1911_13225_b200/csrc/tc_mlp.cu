@@ -1,28 +1,602 @@
-// tc_mlp.cu -- tcgen05/TMEM split-precision decoder (placeholder until the
-// tensor-core kernel lands; BF16X3 decoders run the fp32 SIMT tiles).
+// tc_mlp.cu -- tcgen05/TMEM/TMA split-precision decoder for sm_100a.
+//
+// The fused 8x512 DeepSDF decoder (NeuralField._forward, fields.py:239-247)
+// as one persistent kernel per CTA pair (cluster of 2, tcgen05 cta_group::2):
+//
+//   * A pair owns a tile of 128 query rows (64 per CTA).  Activations stay
+//     in shared memory for all layers as a bf16 hi/lo split (A = A_hi + A_lo,
+//     |A_lo| <= 2^-9 |A|), K-major, 128-byte swizzled: 2 x 64 KB per CTA.
+//   * Each hidden layer is D[128 x 512] = A_hi W_hi + A_hi W_lo + A_lo W_hi
+//     accumulated in fp32 in TMEM (bf16x3).  The leader CTA's
+//     single MMA thread issues tcgen05.mma.cta_group::2 M=128 N=256 K=16;
+//     each CTA supplies its 64 rows of A and half of N of the weights.
+//   * Weights (W^T, bf16 hi and lo) stream from L2 through TMA
+//     (cp.async.bulk.tensor, SWIZZLE_128B, cta_group::2 completion on the
+//     leader's mbarrier) in 3 stages of 32 KB per CTA.
+//   * The epilogue warps read D with tcgen05.ld, add bias, apply ReLU, split
+//     into hi/lo and write the next layer's A in place; on the last hidden
+//     layer they fold the 512 -> 1 head (fp32 dot) and tanh directly from the
+//     fp32 accumulator.  Layer 0 (latent part folded into a per-shape bias,
+//     SURVEY 0 finding 8) runs on the epilogue warps in fp64.
+//   * In march mode the tile epilogue applies the update of tracer.py:170-192
+//     and appends survivors to the next live list (march.cuh).
+#include <cuda.h>
+#include <cuda_bf16.h>
+
+#include <cstring>
+#include <mutex>
+#include <type_traits>
+
 #include "common.cuh"
 #include "kernels.cuh"
 #include "march.cuh"
 #include "mlp_eval.cuh"
 
 namespace dist {
+namespace tc {
 
-bool tc_supported(const DecView &) { return false; }
+constexpr int ROWS = 64;                     // rows per CTA (128 per pair)
+constexpr int KDIM = 512;
+constexpr int NKB = KDIM / 64;               // 64-element K blocks (128 B swizzle rows)
+constexpr int A_PART = NKB * ROWS * 128;     // 64 KB per hi / lo
+constexpr int B_TILE = 128 * 128;            // 128 n-rows x 64 k bf16 = 16 KB
+constexpr int STAGE_BYTES = 2 * B_TILE;      // hi + lo
+constexpr int STAGES = 3;
+constexpr int OFF_AHI = 0;
+constexpr int OFF_ALO = A_PART;
+constexpr int OFF_B = 2 * A_PART;
+constexpr int OFF_MISC = OFF_B + STAGES * STAGE_BYTES;   // 229376
+constexpr int N_EPI_WARPS = 8;
+constexpr int THREADS = (2 + N_EPI_WARPS) * 32;          // producer, MMA, 8 epilogue warps
+constexpr int TMEM_COLS = 256;
+
+struct Misc {
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t dfull[2];
+  uint64_t aready;
+  uint32_t tmem_base;
+  int32_t go, cur, cnt, nan;
+  int32_t ray[ROWS];
+  int32_t shape[ROWS];
+  float part[4][ROWS];
+};
+constexpr int SMEM_BYTES = OFF_MISC + (int)sizeof(Misc) + 1024;  // + alignment slack
+static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+
+// ---- PTX helpers -----------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  const uint32_t a = smem_u32(b);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+      "@!p bra LAB_WAIT;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx)
+               : "memory");
+}
+// arrive on the barrier at the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t *b, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(b)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void epi_sync() {  // named barrier over the epilogue warps
+  asm volatile("bar.sync 1, %0;" ::"n"(N_EPI_WARPS * 32) : "memory");
+}
+__device__ __forceinline__ void tma_load_2sm(uint32_t dst, const CUtensorMap *map, uint64_t *bar,
+                                             int x, int y) {
+  const uint32_t mb = smem_u32(bar) & 0xFEFFFFFFu;  // leader CTA's barrier
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mb), "r"(x), "r"(y)
+      : "memory");
+}
+// K-major, 128B-swizzled UMMA shared-memory descriptor (SBO = 1024 B).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO: 8-row core-matrix groups 1024 B apart
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+// kind::f16 instruction descriptor: BF16 x BF16 -> F32, K-major A/B, M=128, N=256.
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+
+__device__ __forceinline__ void mma_2sm(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+}
+__device__ __forceinline__ void commit_2sm(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
+          "r"(smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// byte offset of A[row][k] (bf16) inside one 64 KB hi/lo part
+__device__ __forceinline__ uint32_t a_off(int row, int k) {
+  const int kb = k >> 6, kk = k & 63;
+  const int chunk = (kk >> 3) ^ (row & 7);
+  return (uint32_t)(kb * (ROWS * 128) + row * 128 + chunk * 16 + (kk & 7) * 2);
+}
+
+// write 8 consecutive activations (k0..k0+7, k0 % 8 == 0) of `row` as hi/lo bf16
+__device__ __forceinline__ void put8(char *smem, int row, int k0, const float (&x)[8]) {
+  uint32_t hi[4], lo[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __nv_bfloat16 h0 = __float2bfloat16_rn(x[2 * i]);
+    const __nv_bfloat16 h1 = __float2bfloat16_rn(x[2 * i + 1]);
+    const __nv_bfloat16 l0 = __float2bfloat16_rn(x[2 * i] - __bfloat162float(h0));
+    const __nv_bfloat16 l1 = __float2bfloat16_rn(x[2 * i + 1] - __bfloat162float(h1));
+    hi[i] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
+    lo[i] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+  }
+  const uint32_t off = a_off(row, k0);
+  *reinterpret_cast<uint4 *>(smem + OFF_AHI + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+  *reinterpret_cast<uint4 *>(smem + OFF_ALO + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+}
+
+struct Params {
+  DecView dv;
+  const double *c0;       // [S][512] folded layer-0 bias (fp64)
+  const float *bias;      // [L-2][512] hidden biases 1..L-2 (fp32)
+  const float *w_out;     // [512]
+  int n_gemm;             // hidden GEMM layers (L-2)
+};
+
+// ---------------------------------------------------------------------------
+// Row sources.  EvalRows: explicit points -> f.  MarchRows: a step slot.
+struct EvalRows {
+  const double *pts;
+  const int32_t *shape;
+  double *f;
+  int64_t n;
+  __device__ bool begin(Misc &) { return n > 0; }
+  __device__ int64_t rows(const Misc &) const { return n; }
+  __device__ int load(int64_t i, double p[3], int &s) const {
+    p[0] = pts[i * 3];
+    p[1] = pts[i * 3 + 1];
+    p[2] = pts[i * 3 + 2];
+    s = shape ? shape[i] : 0;
+    return (int)i;
+  }
+  // called by the 64 row threads (2 full warps) with the tile's f
+  __device__ void finish(Misc &, int64_t i, int, bool valid, double fv) const {
+    if (valid) f[i] = fv;
+  }
+  __device__ void end(Misc &) {}
+};
+
+struct MarchRows {
+  const dist_camera *cams;
+  LevelState ls;
+  Ctl *ctl;
+  int32_t *l0, *l1;
+  MarchArgs a;
+  int64_t *live, *stats;
+  __device__ bool begin(Misc &m) {
+    if (threadIdx.x == 0) {
+      m.cur = ctl->cur;
+      m.cnt = ctl->cnt[m.cur];
+      m.go = (ctl->steps_done < a.max_steps) && (m.cnt > 0);
+      m.nan = 0;
+    }
+    __syncthreads();
+    return m.go;
+  }
+  __device__ int64_t rows(const Misc &m) const { return a.dynamic ? (int64_t)m.cnt : ls.n; }
+  __device__ int load_m(const Misc &m, int64_t i, double p[3], int &s) const {
+    const int32_t *in = m.cur ? l1 : l0;
+    const int64_t g = a.dynamic ? in[i] : i;
+    double dir[3];
+    const dist_camera *cam;
+    ray_of(cams, ls, g, dir, &cam);
+    const double dg = ls.d[g];
+    for (int q = 0; q < 3; ++q) p[q] = __dadd_rn(cam->origin[q], __dmul_rn(dg, dir[q]));
+    s = cam->shape;
+    return (int)g;
+  }
+  __device__ void finish(Misc &m, int64_t, int g, bool valid, double fv) const {
+    bool keep = false;
+    if (valid && ls.status[g] == DIST_MARCHING) {
+      double dir[3];
+      const dist_camera *cam;
+      ray_of(cams, ls, g, dir, &cam);
+      int nn = 0;
+      keep = march_update(ls, a, g, dir, cam->origin, fv, &nn);
+      if (nn) atomicAdd(&m.nan, nn);
+    }
+    int32_t *out = m.cur ? l0 : l1;
+    warp_append(keep, g, out, &ctl->cnt[m.cur ^ 1]);
+  }
+  __device__ void end(Misc &m) { step_epilogue(ctl, m.cur, rows(m), m.nan, live, stats); }
+};
+
+template <class Rows>
+__device__ __forceinline__ int load_row(const Rows &r, const Misc &m, int64_t i, double p[3], int &s) {
+  if constexpr (std::is_same<Rows, MarchRows>::value) return r.load_m(m, i, p, s);
+  else return r.load(i, p, s);
+}
+
+// ---------------------------------------------------------------------------
+template <class Rows>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_tc_mlp(const __grid_constant__ CUtensorMap wmap, Params P, Rows R) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Misc &m = *reinterpret_cast<Misc *>(smem + OFF_MISC);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+
+  if (!R.begin(m)) return;  // uniform across the grid (all CTAs read the same controller)
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&m.full[s], 1);
+      mbar_init(&m.empty[s], 1);
+    }
+    mbar_init(&m.dfull[0], 1);
+    mbar_init(&m.dfull[1], 1);
+    mbar_init(&m.aready, 2);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&m.tmem_base)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = m.tmem_base;
+
+  const int64_t nrows = R.rows(m);
+  const int64_t ntiles = ceil_div(nrows, 2 * ROWS);
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int G = P.n_gemm;
+
+  if (warp == 0) {
+    // ===== TMA producer (both CTAs) =====
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t t = cluster; t < ntiles; t += nclusters)
+        for (int l = 0; l < G; ++l)
+          for (int nh = 0; nh < 2; ++nh)
+            for (int kc = 0; kc < NKB; ++kc, ++it) {
+              const int s = it % STAGES;
+              mbar_wait(&m.empty[s], ((it / STAGES) & 1) ^ 1);
+              if (rank == 0) mbar_arrive_expect_tx(&m.full[s], 2 * STAGE_BYTES);
+              const uint32_t dst = smem_u32(smem + OFF_B + s * STAGE_BYTES);
+              const int y = nh * 256 + (int)rank * 128;
+              tma_load_2sm(dst, &wmap, &m.full[s], kc * 64, (l * 2 + 0) * KDIM + y);
+              tma_load_2sm(dst + B_TILE, &wmap, &m.full[s], kc * 64, (l * 2 + 1) * KDIM + y);
+            }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader CTA, one thread) =====
+    if (rank == 0 && lane == 0) {
+      uint32_t it = 0, layer = 0;
+      const uint32_t a_hi = smem_u32(smem + OFF_AHI), a_lo = smem_u32(smem + OFF_ALO);
+      for (int64_t t = cluster; t < ntiles; t += nclusters)
+        for (int l = 0; l < G; ++l, ++layer) {
+          mbar_wait(&m.aready, layer & 1);
+          tc_fence_after();
+          for (int nh = 0; nh < 2; ++nh) {
+            const uint32_t d = tmem + nh * 128;
+            for (int kc = 0; kc < NKB; ++kc, ++it) {
+              const int s = it % STAGES;
+              mbar_wait(&m.full[s], (it / STAGES) & 1);
+              tc_fence_after();
+              const uint32_t b_hi = smem_u32(smem + OFF_B + s * STAGE_BYTES), b_lo = b_hi + B_TILE;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t ak = kc * (ROWS * 128) + q * 32;
+                const uint64_t dah = sdesc(a_hi + ak), dal = sdesc(a_lo + ak);
+                const uint64_t dbh = sdesc(b_hi + q * 32), dbl = sdesc(b_lo + q * 32);
+                mma_2sm(d, dah, dbh, (kc | q) ? 1u : 0u);
+                mma_2sm(d, dah, dbl, 1u);
+                mma_2sm(d, dal, dbh, 1u);
+              }
+              commit_2sm(&m.empty[s]);
+            }
+            commit_2sm(&m.dfull[nh]);
+          }
+        }
+    }
+  } else {
+    // ===== epilogue warps (both CTAs) =====
+    const int q = warp & 3;                 // TMEM lane quarter of this warp
+    const int sub = (warp - 2) >> 2;        // which 64 of the quarter's 128 columns
+    const int row = (q & 1) * 32 + lane;    // tile row owned in TMEM
+    const int half = q >> 1;                // which 128-column half of each N-half
+    const bool row_thread = (sub == 0 && half == 0);   // warps 4, 5: one thread per row
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+    uint32_t layer = 0;
+    for (int64_t t = cluster; t < ntiles; t += nclusters) {
+      const int64_t base = t * (2 * ROWS) + (int64_t)rank * ROWS;
+      // ---- rows and layer 0 (fp64, latent folded into c0) ----
+      double p[3] = {0, 0, 0};
+      int s = -1, id = -1;
+      const int64_t gi = base + row;
+      if (gi < nrows) id = load_row(R, m, gi, p, s);
+      if (row_thread) {
+        m.shape[row] = s;
+        m.ray[row] = id;
+      }
+      const int n0 = P.dv.np[0];
+      const double *c0 = P.c0 + (size_t)(s < 0 ? 0 : s) * n0;
+      for (int nh = 0; nh < 2; ++nh) {
+        const int cb = nh * 256 + half * 128 + sub * 64;
+#pragma unroll 1
+        for (int j = 0; j < 64; j += 8) {
+          float x[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const int col = cb + j + e;
+            double v = 0.0;
+            if (s >= 0) {
+              v = c0[col];
+              v = fma(p[0], P.dv.W0p[col], v);
+              v = fma(p[1], P.dv.W0p[n0 + col], v);
+              v = fma(p[2], P.dv.W0p[2 * n0 + col], v);
+            }
+            x[e] = (float)(v > 0.0 ? v : 0.0);
+          }
+          put8(smem, row, cb + j, x);
+        }
+      }
+      fence_proxy_async();
+      epi_sync();
+      if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+      // ---- hidden layers ----
+      float head = 0.f;
+      for (int l = 0; l < G; ++l, ++layer) {
+        mbar_wait(&m.dfull[1], layer & 1);
+        mbar_wait(&m.dfull[0], layer & 1);
+        tc_fence_after();
+        const bool last = (l == G - 1);
+        const float *bias = P.bias + (size_t)l * KDIM;
+        for (int nh = 0; nh < 2; ++nh) {
+          const int cb = nh * 256 + half * 128 + sub * 64;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            float v[32];
+            tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
+#pragma unroll
+            for (int g8 = 0; g8 < 4; ++g8) {
+              float x[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int col = cb + c * 32 + g8 * 8 + e;
+                const float y = v[g8 * 8 + e] + __ldg(bias + col);
+                x[e] = y > 0.f ? y : 0.f;
+              }
+              if (last) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                  head = fmaf(x[e], __ldg(P.w_out + cb + c * 32 + g8 * 8 + e), head);
+              } else {
+                put8(smem, row, cb + c * 32 + g8 * 8, x);
+              }
+            }
+          }
+        }
+        tc_fence_before();
+        if (!last) {
+          fence_proxy_async();
+          epi_sync();
+          if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+        }
+      }
+      // ---- head: combine the four partial dot products of each row ----
+      m.part[half * 2 + sub][row] = head;
+      epi_sync();
+      if (row_thread) {
+        const double sum = (double)m.part[0][row] + (double)m.part[1][row] +
+                           (double)m.part[2][row] + (double)m.part[3][row] + P.dv.b_out;
+        const double fv = P.dv.final_linear ? sum : tanh(sum);
+        R.finish(m, gi, m.ray[row], gi < nrows && m.shape[row] >= 0, fv);
+      }
+      epi_sync();
+      if (G == 0) {  // no hidden GEMM layers: never happens for tc_supported decoders
+        if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+      }
+    }
+  }
+  // ---- teardown ----
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+  R.end(m);
+}
+
+// ---------------------------------------------------------------------------
+// host side: weight packing, tensor map, launch
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+}  // namespace tc
+
+bool tc_supported(const DecView &dv) {
+  if (dv.skip >= 0 || dv.n_layers < 3) return false;
+  for (int l = 0; l <= dv.n_layers - 2; ++l)
+    if (dv.np[l] != tc::KDIM) return false;
+  return dv.tc_w[0] != nullptr;
+}
+
+// tc_w[0]: [G][2][512 n][512 k] bf16 (W^T hi, lo); tc_bias[0]: [G][512] + w_out [512] fp32
+void tc_pack_sizes(const DecView &dv, const std::function<void(int, size_t, size_t)> &put) {
+  for (int l = 0; l <= dv.n_layers - 2; ++l)
+    if (dv.np[l] != tc::KDIM) return;
+  if (dv.skip >= 0 || dv.n_layers < 3) return;
+  const int G = dv.n_layers - 2;
+  put(0, (size_t)G * 2 * tc::KDIM * tc::KDIM * 2, (size_t)(G + 1) * tc::KDIM * sizeof(float));
+}
+
+void tc_pack_fill(const DecView &dv, const double *const *W, const double *const *b,
+                  const int32_t *dims, const std::function<void *(int)> &wdst,
+                  const std::function<float *(int)> &bdst) {
+  for (int l = 0; l <= dv.n_layers - 2; ++l)
+    if (dv.np[l] != tc::KDIM) return;
+  if (dv.skip >= 0 || dv.n_layers < 3) return;
+  const int G = dv.n_layers - 2, K = tc::KDIM;
+  uint16_t *w = reinterpret_cast<uint16_t *>(wdst(0));
+  float *bb = bdst(0);
+  auto bf16 = [](float x) -> uint16_t {  // round-to-nearest-even
+    uint32_t u;
+    memcpy(&u, &x, 4);
+    const uint32_t r = 0x7FFFu + ((u >> 16) & 1u);
+    return (uint16_t)((u + r) >> 16);
+  };
+  auto unbf = [](uint16_t h) -> float {
+    uint32_t u = (uint32_t)h << 16;
+    float x;
+    memcpy(&x, &u, 4);
+    return x;
+  };
+  for (int g = 0; g < G; ++g) {
+    const int l = g + 1;
+    const int kin = dims[l], nout = dims[l + 1];
+    for (int n = 0; n < K; ++n)
+      for (int k = 0; k < K; ++k) {
+        const float x = (k < kin && n < nout) ? (float)W[l][(size_t)k * nout + n] : 0.f;
+        const uint16_t h = bf16(x);
+        const uint16_t lo = bf16(x - unbf(h));
+        w[(((size_t)g * 2 + 0) * K + n) * K + k] = h;
+        w[(((size_t)g * 2 + 1) * K + n) * K + k] = lo;
+      }
+    for (int n = 0; n < K; ++n) bb[(size_t)g * K + n] = n < nout ? (float)b[l][n] : 0.f;
+  }
+  const int L = dv.n_layers;
+  for (int k = 0; k < K; ++k) bb[(size_t)G * K + k] = k < dims[L - 1] ? (float)W[L - 1][k] : 0.f;
+}
+
+static int make_wmap(const DecView &dv, CUtensorMap *map) {
+  tc::EncodeTiledFn enc = tc::encode_fn();
+  if (!enc) return fail(DIST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int G = dv.n_layers - 2;
+  cuuint64_t gdim[2] = {(cuuint64_t)tc::KDIM, (cuuint64_t)G * 2 * tc::KDIM};
+  cuuint64_t gstride[1] = {(cuuint64_t)tc::KDIM * 2};
+  cuuint32_t box[2] = {64, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(dv.tc_w[0]), gdim,
+                   gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(DIST_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+  return DIST_OK;
+}
+
+template <class Rows>
+static int launch_tc(const DecView &dv, const double *c0, const Rows &rows, int64_t tiles_bound,
+                     cudaStream_t st) {
+  CUtensorMap map;
+  int rc = make_wmap(dv, &map);
+  if (rc) return rc;
+  tc::Params P;
+  P.dv = dv;
+  P.c0 = c0;
+  P.bias = dv.tc_bias[0];
+  P.w_out = dv.tc_bias[0] + (size_t)(dv.n_layers - 2) * tc::KDIM;
+  P.n_gemm = dv.n_layers - 2;
+  const void *fn = (const void *)tc::k_tc_mlp<Rows>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc)");
+  const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_bound, sm_count() / 2));
+  tc::k_tc_mlp<Rows><<<2 * pairs, tc::THREADS, tc::SMEM_BYTES, st>>>(map, P, rows);
+  DIST_CHECK_LAUNCH("k_tc_mlp");
+  return DIST_OK;
+}
 
 int tc_eval_points(const DecView &dv, const double *c0, const double *cskip, const double *pts,
                    const int32_t *shape, int64_t n, double *f, cudaStream_t st) {
-  ArrayGen g{pts, shape, nullptr, f, n};
-  return launch_eval_gen<float>(dv, c0, cskip, g, n, st);
+  if (!tc_supported(dv)) {
+    ArrayGen g{pts, shape, nullptr, f, n};
+    return launch_eval_gen<float>(dv, c0, cskip, g, n, st);
+  }
+  tc::EvalRows rows{pts, shape, f, n};
+  return launch_tc(dv, c0, rows, ceil_div(n, 128), st);
 }
 
-void tc_pack_sizes(const DecView &, const std::function<void(int, size_t, size_t)> &) {}
-void tc_pack_fill(const DecView &, const double *const *, const double *const *, const int32_t *,
-                  const std::function<void *(int)> &, const std::function<float *(int)> &) {}
-
-int tc_run_steps(const DecView &, const double *, const double *, const dist_camera *,
-                 const LevelState &, Ctl *, int32_t *, int32_t *, const MarchArgs &, int, int64_t *,
-                 int64_t *, cudaStream_t) {
-  return fail(DIST_ERR_CONFIG, "tcgen05 step kernel not built");
+int tc_run_steps(const DecView &dv, const double *c0, const double *cskip, const dist_camera *cams,
+                 const LevelState &ls, Ctl *ctl, int32_t *l0, int32_t *l1, const MarchArgs &a,
+                 int slots, int64_t *live, int64_t *stats, cudaStream_t st) {
+  (void)cskip;
+  tc::MarchRows rows{cams, ls, ctl, l0, l1, a, live, stats};
+  for (int s = 0; s < slots; ++s) {
+    int rc = launch_tc(dv, c0, rows, ceil_div(ls.n, 128), st);
+    if (rc) return rc;
+  }
+  return DIST_OK;
 }
 
 }  // namespace dist
