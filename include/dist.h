@@ -47,6 +47,7 @@ extern "C" {
 #define DIST_PREC_FP64 0   /* SIMT fp64: the reference's own precision */
 #define DIST_PREC_FP32 1   /* SIMT fp32 */
 #define DIST_PREC_BF16X3 2 /* tcgen05 bf16 hi/lo 3-pass, fp32 accumulate in TMEM */
+#define DIST_PREC_FP16X3 3 /* tcgen05 fp16 hi/lo 3-pass with power-of-2 row/layer scaling */
 
 /* warning bits in stats[3] */
 #define DIST_WARN_CAMERA_INSIDE 1   /* tracer.py:100-102 */

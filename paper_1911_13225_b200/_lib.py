@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libdist_b200.so")
 
 DIST_OK, DIST_ERR_CONFIG, DIST_ERR_NUMERIC, DIST_ERR_CUDA = 0, 2, 3, 4
-PREC = {"fp64": 0, "fp32": 1, "bf16x3": 2}
+PREC = {"fp64": 0, "fp32": 1, "bf16x3": 2, "fp16x3": 3}
 
 
 class dist_camera(C.Structure):

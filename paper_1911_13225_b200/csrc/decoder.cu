@@ -112,7 +112,7 @@ int eval_points(const DecView &dv, const double *c0, const double *cskip, const 
   if (n <= 0) return DIST_OK;
   ArrayGen g{pts, shape, nullptr, f, n};
   if (dv.prec == DIST_PREC_FP64) return launch_eval_gen<double>(dv, c0, cskip, g, n, st);
-  if (dv.prec == DIST_PREC_BF16X3) return tc_eval_points(dv, c0, cskip, pts, shape, n, f, st);
+  if (dv.prec >= DIST_PREC_BF16X3) return tc_eval_points(dv, c0, cskip, pts, shape, n, f, st);
   return launch_eval_gen<float>(dv, c0, cskip, g, n, st);
 }
 
@@ -181,7 +181,7 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
   *out = nullptr;
   if (L < 2 || L > kMaxLayers) return fail(DIST_ERR_CONFIG, "n_layers must be in [2, 16]");
   if (D < 0) return fail(DIST_ERR_CONFIG, "latent_dim must be >= 0");
-  if (prec < DIST_PREC_FP64 || prec > DIST_PREC_BF16X3)
+  if (prec < DIST_PREC_FP64 || prec > DIST_PREC_FP16X3)
     return fail(DIST_ERR_CONFIG, "unknown precision");
   if (dims[L] != 1) return fail(DIST_ERR_CONFIG, "final layer must map to one output");
   if (skip < 0) skip = -1;
@@ -279,7 +279,7 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
 
   // tensor-core packs (bf16 hi/lo) for the split-precision path
   size_t o_tc[kMaxLayers] = {}, o_tcb[kMaxLayers] = {};
-  if (prec == DIST_PREC_BF16X3) tc_pack_sizes(v, [&](int l, size_t wbytes, size_t bbytes) {
+  if (prec >= DIST_PREC_BF16X3) tc_pack_sizes(v, [&](int l, size_t wbytes, size_t bbytes) {
       o_tc[l] = put(wbytes);
       o_tcb[l] = put(bbytes);
     });
@@ -287,7 +287,7 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
   void *blob = nullptr;
   cudaError_t e = cudaMalloc(&blob, host.size());
   if (e != cudaSuccess) return cuda_fail(e, "cudaMalloc(decoder)");
-  if (prec == DIST_PREC_BF16X3)
+  if (prec >= DIST_PREC_BF16X3)
     tc_pack_fill(v, W, b, dims, [&](int l) { return (void *)(host.data() + o_tc[l]); },
                  [&](int l) { return (float *)(host.data() + o_tcb[l]); });
   e = cudaMemcpy(blob, host.data(), host.size(), cudaMemcpyHostToDevice);
@@ -309,7 +309,7 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
   v.Wsp = skip > 0 ? (const double *)(base + o_Wsp) : nullptr;
   v.w_out[0] = base + o_wo[0];
   v.w_out[1] = base + o_wo[1];
-  if (prec == DIST_PREC_BF16X3)
+  if (prec >= DIST_PREC_BF16X3)
     for (int l = 0; l < kMaxLayers; ++l)
       if (o_tc[l]) {
         v.tc_w[l] = base + o_tc[l];

@@ -22,7 +22,10 @@
 //     and appends survivors to the next live list (march.cuh).
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
+#include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <type_traits>
@@ -48,7 +51,7 @@ constexpr int OFF_B = 2 * A_PART;
 constexpr int OFF_MISC = OFF_B + STAGES * STAGE_BYTES;   // 229376
 constexpr int N_EPI_WARPS = 8;
 constexpr int THREADS = (2 + N_EPI_WARPS) * 32;          // producer, MMA, 8 epilogue warps
-constexpr int TMEM_COLS = 256;
+constexpr int TMEM_COLS = 512;
 
 struct Misc {
   uint64_t full[STAGES];
@@ -59,7 +62,7 @@ struct Misc {
   int32_t go, cur, cnt, nan;
   int32_t ray[ROWS];
   int32_t shape[ROWS];
-  float part[4][ROWS];
+  float xch[4][ROWS];   // per-row exchange: row max (scaling), then head partial sums
 };
 constexpr int SMEM_BYTES = OFF_MISC + (int)sizeof(Misc) + 1024;  // + alignment slack
 static_assert(SMEM_BYTES <= 232448, "shared memory budget");
@@ -130,15 +133,19 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
   d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
   return d;
 }
-// kind::f16 instruction descriptor: BF16 x BF16 -> F32, K-major A/B, M=128, N=256.
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+// kind::f16 instruction descriptors: {BF16|F16} x {BF16|F16} -> F32, K-major A/B,
+// M=128 (cta_group::2), N=256.
+constexpr uint32_t IDESC_BF16 =
+    (1u << 4) | (1u << 7) | (1u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr uint32_t IDESC_F16 = (1u << 4) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
 
+template <bool F16>
 __device__ __forceinline__ void mma_2sm(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
-      "l"(a), "l"(b), "r"(IDESC), "r"(acc));
+      "l"(a), "l"(b), "n"(F16 ? IDESC_F16 : IDESC_BF16), "r"(acc));
 }
 __device__ __forceinline__ void commit_2sm(uint64_t *bar) {
   asm volatile(
@@ -170,17 +177,31 @@ __device__ __forceinline__ uint32_t a_off(int row, int k) {
   return (uint32_t)(kb * (ROWS * 128) + row * 128 + chunk * 16 + (kk & 7) * 2);
 }
 
-// write 8 consecutive activations (k0..k0+7, k0 % 8 == 0) of `row` as hi/lo bf16
+// split x into hi + lo of the MMA element type (x - hi is exact in fp32)
+template <bool F16>
+__device__ __forceinline__ void split2(float x, uint16_t &h, uint16_t &l) {
+  if constexpr (F16) {
+    const __half hh = __float2half_rn(x);
+    h = __half_as_ushort(hh);
+    l = __half_as_ushort(__float2half_rn(x - __half2float(hh)));
+  } else {
+    const __nv_bfloat16 hh = __float2bfloat16_rn(x);
+    h = __bfloat16_as_ushort(hh);
+    l = __bfloat16_as_ushort(__float2bfloat16_rn(x - __bfloat162float(hh)));
+  }
+}
+
+// write 8 consecutive activations (k0..k0+7, k0 % 8 == 0) of `row` as hi/lo
+template <bool F16>
 __device__ __forceinline__ void put8(char *smem, int row, int k0, const float (&x)[8]) {
   uint32_t hi[4], lo[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    const __nv_bfloat16 h0 = __float2bfloat16_rn(x[2 * i]);
-    const __nv_bfloat16 h1 = __float2bfloat16_rn(x[2 * i + 1]);
-    const __nv_bfloat16 l0 = __float2bfloat16_rn(x[2 * i] - __bfloat162float(h0));
-    const __nv_bfloat16 l1 = __float2bfloat16_rn(x[2 * i + 1] - __bfloat162float(h1));
-    hi[i] = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
-    lo[i] = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
+    uint16_t h0, h1, l0, l1;
+    split2<F16>(x[2 * i], h0, l0);
+    split2<F16>(x[2 * i + 1], h1, l1);
+    hi[i] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+    lo[i] = (uint32_t)l0 | ((uint32_t)l1 << 16);
   }
   const uint32_t off = a_off(row, k0);
   *reinterpret_cast<uint4 *>(smem + OFF_AHI + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
@@ -192,7 +213,9 @@ struct Params {
   const double *c0;       // [S][512] folded layer-0 bias (fp64)
   const float *bias;      // [L-2][512] hidden biases 1..L-2 (fp32)
   const float *w_out;     // [512]
+  const float *winv;      // [L-2] inverse power-of-2 weight scales (fp16x3), 1 for bf16x3
   int n_gemm;             // hidden GEMM layers (L-2)
+  int acc_mode;           // 0: one accumulator; 1: two (even/odd K blocks); 2: hi*hi | corrections
 };
 
 // ---------------------------------------------------------------------------
@@ -270,10 +293,10 @@ __device__ __forceinline__ int load_row(const Rows &r, const Misc &m, int64_t i,
 }
 
 // ---------------------------------------------------------------------------
-template <class Rows>
+template <bool F16, class Rows>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     k_tc_mlp(const __grid_constant__ CUtensorMap wmap, Params P, Rows R) {
-  extern __shared__ __align__(1024) char smem_raw[];
+  extern __shared__ __align__(16) char smem_raw[];
   char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   Misc &m = *reinterpret_cast<Misc *>(smem + OFF_MISC);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -346,9 +369,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 const uint32_t ak = kc * (ROWS * 128) + q * 32;
                 const uint64_t dah = sdesc(a_hi + ak), dal = sdesc(a_lo + ak);
                 const uint64_t dbh = sdesc(b_hi + q * 32), dbl = sdesc(b_lo + q * 32);
-                mma_2sm(d, dah, dbh, (kc | q) ? 1u : 0u);
-                mma_2sm(d, dah, dbl, 1u);
-                mma_2sm(d, dal, dbh, 1u);
+                if (P.acc_mode == 0) {
+                  mma_2sm<F16>(d, dah, dbh, (kc | q) ? 1u : 0u);
+                  mma_2sm<F16>(d, dah, dbl, 1u);
+                  mma_2sm<F16>(d, dal, dbh, 1u);
+                } else if (P.acc_mode == 1) {
+                  const uint32_t dd = d + ((kc & 1) ? 256u : 0u);
+                  mma_2sm<F16>(dd, dah, dbh, (kc >> 1 | q) ? 1u : 0u);
+                  mma_2sm<F16>(dd, dah, dbl, 1u);
+                  mma_2sm<F16>(dd, dal, dbh, 1u);
+                } else {
+                  mma_2sm<F16>(d, dah, dbh, (kc | q) ? 1u : 0u);
+                  mma_2sm<F16>(d + 256u, dah, dbl, (kc | q) ? 1u : 0u);
+                  mma_2sm<F16>(d + 256u, dal, dbh, 1u);
+                }
               }
               commit_2sm(&m.empty[s]);
             }
@@ -364,6 +398,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int half = q >> 1;                // which 128-column half of each N-half
     const bool row_thread = (sub == 0 && half == 0);   // warps 4, 5: one thread per row
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+    // D columns [col, col+32) of this thread's lane (+ the correction accumulator)
+    auto load_d = [&](int col, float (&v)[32]) {
+      tmem_ld32(tq + col, v);
+      if (P.acc_mode) {
+        float w2[32];
+        tmem_ld32(tq + 256 + col, w2);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) v[e] += w2[e];
+      }
+    };
     uint32_t layer = 0;
     for (int64_t t = cluster; t < ntiles; t += nclusters) {
       const int64_t base = t * (2 * ROWS) + (int64_t)rank * ROWS;
@@ -378,24 +422,50 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
       const int n0 = P.dv.np[0];
       const double *c0 = P.c0 + (size_t)(s < 0 ? 0 : s) * n0;
+      // layer-0 activation of column `col` (fp64 fold, rounded to fp32)
+      auto h0 = [&](int col) -> float {
+        double v = 0.0;
+        if (s >= 0) {
+          v = c0[col];
+          v = fma(p[0], P.dv.W0p[col], v);
+          v = fma(p[1], P.dv.W0p[n0 + col], v);
+          v = fma(p[2], P.dv.W0p[2 * n0 + col], v);
+        }
+        return (float)(v > 0.0 ? v : 0.0);
+      };
+      // Row scale of the fp16 split: a power of two that puts the row max in
+      // [2^14, 2^15) so hi and lo both stay normal (exact to undo).  bf16 has
+      // fp32's exponent range and needs none.
+      auto row_scale = [&](float tmax, float &sc, float &inv) {
+        if constexpr (F16) {
+          m.xch[half * 2 + sub][row] = tmax;
+          epi_sync();
+          const float mx = fmaxf(fmaxf(m.xch[0][row], m.xch[1][row]),
+                                 fmaxf(m.xch[2][row], m.xch[3][row]));
+          const int e = mx > 0.f ? min(max(14 - ilogbf(mx), -100), 100) : 0;
+          sc = ldexpf(1.f, e);
+          inv = ldexpf(1.f, -e);
+        } else {
+          (void)tmax;
+          sc = inv = 1.f;
+        }
+      };
+      float sc = 1.f, rinv = 1.f;
+      if constexpr (F16) {
+        float tmax = 0.f;
+        for (int nh = 0; nh < 2; ++nh)
+#pragma unroll 4
+          for (int j = 0; j < 64; ++j) tmax = fmaxf(tmax, h0(nh * 256 + half * 128 + sub * 64 + j));
+        row_scale(tmax, sc, rinv);
+      }
       for (int nh = 0; nh < 2; ++nh) {
         const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll 1
         for (int j = 0; j < 64; j += 8) {
           float x[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const int col = cb + j + e;
-            double v = 0.0;
-            if (s >= 0) {
-              v = c0[col];
-              v = fma(p[0], P.dv.W0p[col], v);
-              v = fma(p[1], P.dv.W0p[n0 + col], v);
-              v = fma(p[2], P.dv.W0p[2 * n0 + col], v);
-            }
-            x[e] = (float)(v > 0.0 ? v : 0.0);
-          }
-          put8(smem, row, cb + j, x);
+          for (int e = 0; e < 8; ++e) x[e] = h0(cb + j + e) * sc;
+          put8<F16>(smem, row, cb + j, x);
         }
       }
       fence_proxy_async();
@@ -409,30 +479,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         tc_fence_after();
         const bool last = (l == G - 1);
         const float *bias = P.bias + (size_t)l * KDIM;
-        for (int nh = 0; nh < 2; ++nh) {
-          const int cb = nh * 256 + half * 128 + sub * 64;
+        const float unscale = rinv * P.winv[l];   // exact: both are powers of two
+        // fp16: pass 1 finds the row max for the next scale (and the head on the
+        // last layer); bf16 needs no scale, so one pass reads D and writes A.
+        float tmax = 0.f;
+        if (F16 || last) {
+          for (int nh = 0; nh < 2; ++nh) {
+            const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            float v[32];
-            tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
+            for (int c = 0; c < 2; ++c) {
+              float v[32];
+              load_d(nh * 128 + sub * 64 + c * 32, v);
 #pragma unroll
-            for (int g8 = 0; g8 < 4; ++g8) {
-              float x[8];
-#pragma unroll
-              for (int e = 0; e < 8; ++e) {
-                const int col = cb + c * 32 + g8 * 8 + e;
-                const float y = v[g8 * 8 + e] + __ldg(bias + col);
-                x[e] = y > 0.f ? y : 0.f;
-              }
-              if (last) {
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                  head = fmaf(x[e], __ldg(P.w_out + cb + c * 32 + g8 * 8 + e), head);
-              } else {
-                put8(smem, row, cb + c * 32 + g8 * 8, x);
+              for (int e = 0; e < 32; ++e) {
+                const int col = cb + c * 32 + e;
+                float y = fmaf(v[e], unscale, __ldg(bias + col));
+                y = y > 0.f ? y : 0.f;
+                if (last) head = fmaf(y, __ldg(P.w_out + col), head);
+                else tmax = fmaxf(tmax, y);
               }
             }
           }
+        }
+        if (!last) {
+          float inv;
+          row_scale(tmax, sc, inv);
+          for (int nh = 0; nh < 2; ++nh) {
+            const int cb = nh * 256 + half * 128 + sub * 64;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              float v[32];
+              load_d(nh * 128 + sub * 64 + c * 32, v);
+#pragma unroll
+              for (int g8 = 0; g8 < 4; ++g8) {
+                float x[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  const int col = cb + c * 32 + g8 * 8 + e;
+                  float y = fmaf(v[g8 * 8 + e], unscale, __ldg(bias + col));
+                  x[e] = (y > 0.f ? y : 0.f) * sc;
+                }
+                put8<F16>(smem, row, cb + c * 32 + g8 * 8, x);
+              }
+            }
+          }
+          rinv = inv;
         }
         tc_fence_before();
         if (!last) {
@@ -442,11 +533,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
       }
       // ---- head: combine the four partial dot products of each row ----
-      m.part[half * 2 + sub][row] = head;
+      m.xch[half * 2 + sub][row] = head;
       epi_sync();
       if (row_thread) {
-        const double sum = (double)m.part[0][row] + (double)m.part[1][row] +
-                           (double)m.part[2][row] + (double)m.part[3][row] + P.dv.b_out;
+        const double sum = (double)m.xch[0][row] + (double)m.xch[1][row] +
+                           (double)m.xch[2][row] + (double)m.xch[3][row] + P.dv.b_out;
         const double fv = P.dv.final_linear ? sum : tanh(sum);
         R.finish(m, gi, m.ray[row], gi < nrows && m.shape[row] >= 0, fv);
       }
@@ -491,16 +582,18 @@ bool tc_supported(const DecView &dv) {
   if (dv.skip >= 0 || dv.n_layers < 3) return false;
   for (int l = 0; l <= dv.n_layers - 2; ++l)
     if (dv.np[l] != tc::KDIM) return false;
-  return dv.tc_w[0] != nullptr;
+  return (dv.prec == DIST_PREC_BF16X3 || dv.prec == DIST_PREC_FP16X3) && dv.tc_w[0] != nullptr;
 }
 
-// tc_w[0]: [G][2][512 n][512 k] bf16 (W^T hi, lo); tc_bias[0]: [G][512] + w_out [512] fp32
+// tc_w[0]: [G][2][512 n][512 k] (W^T hi, lo as bf16 or fp16);
+// tc_bias[0]: [G][512] hidden biases, [512] w_out, [G] inverse weight scales (fp32)
 void tc_pack_sizes(const DecView &dv, const std::function<void(int, size_t, size_t)> &put) {
   for (int l = 0; l <= dv.n_layers - 2; ++l)
     if (dv.np[l] != tc::KDIM) return;
   if (dv.skip >= 0 || dv.n_layers < 3) return;
   const int G = dv.n_layers - 2;
-  put(0, (size_t)G * 2 * tc::KDIM * tc::KDIM * 2, (size_t)(G + 1) * tc::KDIM * sizeof(float));
+  put(0, (size_t)G * 2 * tc::KDIM * tc::KDIM * 2,
+      ((size_t)(G + 1) * tc::KDIM + G) * sizeof(float));
 }
 
 void tc_pack_fill(const DecView &dv, const double *const *W, const double *const *b,
@@ -509,29 +602,36 @@ void tc_pack_fill(const DecView &dv, const double *const *W, const double *const
   for (int l = 0; l <= dv.n_layers - 2; ++l)
     if (dv.np[l] != tc::KDIM) return;
   if (dv.skip >= 0 || dv.n_layers < 3) return;
+  const bool f16 = dv.prec == DIST_PREC_FP16X3;
   const int G = dv.n_layers - 2, K = tc::KDIM;
   uint16_t *w = reinterpret_cast<uint16_t *>(wdst(0));
   float *bb = bdst(0);
-  auto bf16 = [](float x) -> uint16_t {  // round-to-nearest-even
-    uint32_t u;
-    memcpy(&u, &x, 4);
-    const uint32_t r = 0x7FFFu + ((u >> 16) & 1u);
-    return (uint16_t)((u + r) >> 16);
+  float *winv = bb + (size_t)(G + 1) * K;
+  auto to16 = [f16](float x) -> uint16_t {
+    return f16 ? __half_as_ushort(__float2half_rn(x)) : __bfloat16_as_ushort(__float2bfloat16_rn(x));
   };
-  auto unbf = [](uint16_t h) -> float {
-    uint32_t u = (uint32_t)h << 16;
-    float x;
-    memcpy(&x, &u, 4);
-    return x;
+  auto from16 = [f16](uint16_t h) -> float {
+    return f16 ? __half2float(__ushort_as_half(h)) : __bfloat162float(__ushort_as_bfloat16(h));
   };
   for (int g = 0; g < G; ++g) {
     const int l = g + 1;
     const int kin = dims[l], nout = dims[l + 1];
+    // fp16: scale the layer by a power of two so max|W| lands in [2^14, 2^15)
+    float sc = 1.f;
+    if (f16) {
+      double mx = 0.0;
+      for (size_t i = 0; i < (size_t)kin * nout; ++i) mx = std::max(mx, std::fabs(W[l][i]));
+      const int e = mx > 0.0 ? 14 - std::ilogb(mx) : 0;
+      sc = std::ldexp(1.f, e);
+      winv[g] = std::ldexp(1.f, -e);
+    } else {
+      winv[g] = 1.f;
+    }
     for (int n = 0; n < K; ++n)
       for (int k = 0; k < K; ++k) {
-        const float x = (k < kin && n < nout) ? (float)W[l][(size_t)k * nout + n] : 0.f;
-        const uint16_t h = bf16(x);
-        const uint16_t lo = bf16(x - unbf(h));
+        const float x = (k < kin && n < nout) ? (float)W[l][(size_t)k * nout + n] * sc : 0.f;
+        const uint16_t h = to16(x);
+        const uint16_t lo = to16(x - from16(h));
         w[(((size_t)g * 2 + 0) * K + n) * K + k] = h;
         w[(((size_t)g * 2 + 1) * K + n) * K + k] = lo;
       }
@@ -549,16 +649,18 @@ static int make_wmap(const DecView &dv, CUtensorMap *map) {
   cuuint64_t gstride[1] = {(cuuint64_t)tc::KDIM * 2};
   cuuint32_t box[2] = {64, 128};
   cuuint32_t estr[2] = {1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(dv.tc_w[0]), gdim,
+  const CUtensorMapDataType dt = dv.prec == DIST_PREC_FP16X3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
+                                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  CUresult r = enc(map, dt, 2, const_cast<void *>(dv.tc_w[0]), gdim,
                    gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return fail(DIST_ERR_CUDA, "cuTensorMapEncodeTiled failed");
   return DIST_OK;
 }
 
-template <class Rows>
-static int launch_tc(const DecView &dv, const double *c0, const Rows &rows, int64_t tiles_bound,
-                     cudaStream_t st) {
+template <bool F16, class Rows>
+static int launch_tc_t(const DecView &dv, const double *c0, const Rows &rows, int64_t tiles_bound,
+                       cudaStream_t st) {
   CUtensorMap map;
   int rc = make_wmap(dv, &map);
   if (rc) return rc;
@@ -568,13 +670,25 @@ static int launch_tc(const DecView &dv, const double *c0, const Rows &rows, int6
   P.bias = dv.tc_bias[0];
   P.w_out = dv.tc_bias[0] + (size_t)(dv.n_layers - 2) * tc::KDIM;
   P.n_gemm = dv.n_layers - 2;
-  const void *fn = (const void *)tc::k_tc_mlp<Rows>;
+  P.winv = P.w_out + tc::KDIM;
+  {
+    const char *am = getenv("DIST_TC_ACC");
+    P.acc_mode = am ? atoi(am) : 2;
+  }
+  const void *fn = (const void *)tc::k_tc_mlp<F16, Rows>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc)");
   const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_bound, sm_count() / 2));
-  tc::k_tc_mlp<Rows><<<2 * pairs, tc::THREADS, tc::SMEM_BYTES, st>>>(map, P, rows);
+  tc::k_tc_mlp<F16, Rows><<<2 * pairs, tc::THREADS, tc::SMEM_BYTES, st>>>(map, P, rows);
   DIST_CHECK_LAUNCH("k_tc_mlp");
   return DIST_OK;
+}
+
+template <class Rows>
+static int launch_tc(const DecView &dv, const double *c0, const Rows &rows, int64_t tiles_bound,
+                     cudaStream_t st) {
+  if (dv.prec == DIST_PREC_FP16X3) return launch_tc_t<true>(dv, c0, rows, tiles_bound, st);
+  return launch_tc_t<false>(dv, c0, rows, tiles_bound, st);
 }
 
 int tc_eval_points(const DecView &dv, const double *c0, const double *cskip, const double *pts,

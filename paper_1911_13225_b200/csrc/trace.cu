@@ -374,7 +374,7 @@ int dist_trace(const dist_decoder *dec, const double *codes, int S, const dist_c
     const int slots = std::min(ls.level > 1 ? cfg->split_interval : cfg->max_steps, cfg->max_steps);
     if (dv.prec == DIST_PREC_FP64)
       rc = run_steps<double>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, live, stats, st);
-    else if (dv.prec == DIST_PREC_BF16X3 && tc_supported(dv))
+    else if (tc_supported(dv))
       rc = tc_run_steps(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, live, stats, st);
     else
       rc = run_steps<float>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, live, stats, st);

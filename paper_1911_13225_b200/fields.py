@@ -18,7 +18,7 @@ import numpy as np
 
 from . import _lib
 
-PRECISIONS = ("fp64", "fp32", "bf16x3")
+PRECISIONS = ("fp64", "fp32", "bf16x3", "fp16x3")
 
 
 def _pts(points) -> np.ndarray:
