@@ -23,23 +23,9 @@
 #include "march.cuh"
 #include "mlp_eval.cuh"
 #include "scan.cuh"
+#include "heads.cuh"
 
 namespace dist {
-
-__device__ __forceinline__ int64_t lower_bound_i32(const int32_t *a, int64_t n, int64_t key) {
-  int64_t lo = 0, hi = n;
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if ((int64_t)a[mid] < key) lo = mid + 1;
-    else hi = mid;
-  }
-  return lo;
-}
-
-struct HeadsDev {
-  int32_t *rec, *samp, *samp_pix, *best, *view_rec, *view_samp, *counts;
-  double *f;
-};
 
 __global__ void k_heads_index(HeadsDev h, int K, int V, int64_t WH) {
   const int64_t nrec = h.counts[0], nsamp = h.counts[1];
@@ -68,21 +54,6 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
   if (threadIdx.x == 0)
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
   return s;  // valid in thread 0
-}
-
-struct ObjIn {
-  const double *obs_depth;
-  const uint8_t *obs_mask;
-  const double *obs_sil;
-  double w_depth, w_sil, w_lat;
-};
-
-__device__ __forceinline__ bool depth_valid(const ObjIn &in, int64_t g) {
-  if (!in.obs_depth) return false;
-  const double z = in.obs_depth[g];
-  bool ok = isfinite(z);
-  if (in.obs_mask) ok = ok && in.obs_mask[g];
-  return ok;
 }
 
 // one block per view: n_px, n_conv, silhouette loss + per-pixel seed
@@ -130,53 +101,6 @@ __global__ void k_view_prep(const dist_camera *__restrict__ cams, LevelState ls,
     terms[v * 4 + 3] = b;
   }
 }
-
-// Generator for the fused forward -> seed -> backward over head samples.
-struct ObjGen {
-  const dist_camera *cams;
-  LevelState ls;
-  int K;
-  int64_t WH;
-  HeadsDev h;
-  ObjIn in;
-  const int32_t *npx;
-  const double *sil_seed;
-  __device__ int64_t count() const { return h.counts[1]; }
-  __device__ bool point(int64_t i, double p[3], int &s) const {
-    const int64_t flat = h.samp[i];
-    const int64_t g = flat / K;
-    const int v = (int)(g / WH);
-    const int64_t q = g - v * WH;
-    const int j = (int)(q / ls.lw), ii = (int)(q - (int64_t)j * ls.lw);
-    double dir[3];
-    pixel_ray(cams[v], ii, j, 1, dir, nullptr);
-    const double dk = ls.tk_d[flat];
-    for (int a = 0; a < 3; ++a) p[a] = __dadd_rn(cams[v].origin[a], __dmul_rn(dk, dir[a]));
-    s = cams[v].shape;
-    return true;
-  }
-  __device__ double seed(int64_t i, double f) const {
-    const int64_t flat = h.samp[i];
-    const int64_t g = flat / K;
-    const int v = (int)(g / WH);
-    double sd = 0.0;
-    if (in.obs_depth && ls.status[g] == DIST_CONVERGED && depth_valid(in, g) && npx[v] > 0) {
-      int cnt = 0;
-      for (int k = 0; k < K; ++k) cnt += isfinite(ls.tk_a[g * K + k]) ? 1 : 0;
-      const int64_t q = g - v * WH;
-      const int j = (int)(q / ls.lw), ii = (int)(q - (int64_t)j * ls.lw);
-      double dir[3], scale;
-      pixel_ray(cams[v], ii, j, 1, dir, &scale);
-      const double w = (1.0 / cnt) / (double)npx[v];
-      const double r = __dmul_rn(__dadd_rn(ls.tk_d[flat], f), scale) - in.obs_depth[g];
-      const double sg = r > 0.0 ? 1.0 : (r < 0.0 ? -1.0 : 0.0);
-      sd = in.w_depth * __dmul_rn(__dmul_rn(w, sg), scale);
-    }
-    if (sil_seed && flat - g * K == 0) sd = __dadd_rn(sd, sil_seed[g]);
-    return sd;
-  }
-  __device__ void store(int64_t i, double v) const { h.f[i] = v; }
-};
 
 // one block per view: depth loss = sum_i w_i |r_i| over the view's samples
 __global__ void k_view_depth_loss(const dist_camera *__restrict__ cams, LevelState ls, int K,
@@ -363,7 +287,9 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(objective)");
   ObjGen gen{cams, ls, K, WH, L.h, in, L.npx, io->obs_sil ? L.sil_seed : nullptr};
   int grid = 0;
-  if (dv.prec == DIST_PREC_FP64)
+  if (tc_heads_supported(dv))
+    rc = launch_tc_heads<ObjGen>(dv, L.c0, gen, n * K, s1, L.part0, G, &grid, sm);
+  else if (dv.prec == DIST_PREC_FP64)
     rc = launch_vjp_gen<double>(dv, L.c0, L.cs, gen, n * K, s1, L.part0, L.parts, nullptr, G, &grid, sm);
   else
     rc = launch_vjp_gen<float>(dv, L.c0, L.cs, gen, n * K, s1, L.part0, L.parts, nullptr, G, &grid, sm);

@@ -1,0 +1,87 @@
+// heads.cuh -- frozen-sample head list and the per-sample seed generator of
+// the fused objective (shading.py:166-206, losses.py:54-91), shared by the
+// SIMT (mlp_eval.cuh) and tcgen05 (tc_heads.cu) backward kernels.
+#pragma once
+#include "common.cuh"
+#include "march.cuh"
+
+namespace dist {
+
+__device__ __forceinline__ int64_t lower_bound_i32(const int32_t *a, int64_t n, int64_t key) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if ((int64_t)a[mid] < key) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+struct HeadsDev {
+  int32_t *rec, *samp, *samp_pix, *best, *view_rec, *view_samp, *counts;
+  double *f;
+};
+
+struct ObjIn {
+  const double *obs_depth;
+  const uint8_t *obs_mask;
+  const double *obs_sil;
+  double w_depth, w_sil, w_lat;
+};
+
+__device__ __forceinline__ bool depth_valid(const ObjIn &in, int64_t g) {
+  if (!in.obs_depth) return false;
+  const double z = in.obs_depth[g];
+  bool ok = isfinite(z);
+  if (in.obs_mask) ok = ok && in.obs_mask[g];
+  return ok;
+}
+
+// Generator for the fused forward -> seed -> backward over head samples.
+struct ObjGen {
+  const dist_camera *cams;
+  LevelState ls;
+  int K;
+  int64_t WH;
+  HeadsDev h;
+  ObjIn in;
+  const int32_t *npx;
+  const double *sil_seed;
+  __device__ int64_t count() const { return h.counts[1]; }
+  __device__ bool point(int64_t i, double p[3], int &s) const {
+    const int64_t flat = h.samp[i];
+    const int64_t g = flat / K;
+    const int v = (int)(g / WH);
+    const int64_t q = g - v * WH;
+    const int j = (int)(q / ls.lw), ii = (int)(q - (int64_t)j * ls.lw);
+    double dir[3];
+    pixel_ray(cams[v], ii, j, 1, dir, nullptr);
+    const double dk = ls.tk_d[flat];
+    for (int a = 0; a < 3; ++a) p[a] = __dadd_rn(cams[v].origin[a], __dmul_rn(dk, dir[a]));
+    s = cams[v].shape;
+    return true;
+  }
+  __device__ double seed(int64_t i, double f) const {
+    const int64_t flat = h.samp[i];
+    const int64_t g = flat / K;
+    const int v = (int)(g / WH);
+    double sd = 0.0;
+    if (in.obs_depth && ls.status[g] == DIST_CONVERGED && depth_valid(in, g) && npx[v] > 0) {
+      int cnt = 0;
+      for (int k = 0; k < K; ++k) cnt += isfinite(ls.tk_a[g * K + k]) ? 1 : 0;
+      const int64_t q = g - v * WH;
+      const int j = (int)(q / ls.lw), ii = (int)(q - (int64_t)j * ls.lw);
+      double dir[3], scale;
+      pixel_ray(cams[v], ii, j, 1, dir, &scale);
+      const double w = (1.0 / cnt) / (double)npx[v];
+      const double r = __dmul_rn(__dadd_rn(ls.tk_d[flat], f), scale) - in.obs_depth[g];
+      const double sg = r > 0.0 ? 1.0 : (r < 0.0 ? -1.0 : 0.0);
+      sd = in.w_depth * __dmul_rn(__dmul_rn(w, sg), scale);
+    }
+    if (sil_seed && flat - g * K == 0) sd = __dadd_rn(sd, sil_seed[g]);
+    return sd;
+  }
+  __device__ void store(int64_t i, double v) const { h.f[i] = v; }
+};
+
+}  // namespace dist

@@ -28,6 +28,14 @@ void tc_pack_fill(const DecView &dv, const double *const *W, const double *const
                   const int32_t *dims, const std::function<void *(int)> &wdst,
                   const std::function<float *(int)> &bdst);
 bool tc_supported(const DecView &dv);
+bool tc_heads_supported(const DecView &dv);
+}  // namespace dist
+#include <cuda.h>
+namespace dist {
+int tc_make_map(const DecView &dv, int slot, CUtensorMap *map);
+template <class Gen>
+int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
+                    double *part0, int grid_cap, int *grid_out, cudaStream_t st);
 
 // stable device-wide compaction of flags -> ascending indices (scan.cu)
 size_t compact_ws_bytes(int64_t n);

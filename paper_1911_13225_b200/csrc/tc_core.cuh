@@ -1,0 +1,185 @@
+// tc_core.cuh -- tcgen05 / TMEM / TMA building blocks shared by the
+// split-precision decoder kernels (tc_mlp.cu forward, tc_heads.cu fused
+// forward + backward).  See tc_mlp.cu for the design.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+
+namespace dist {
+namespace tc {
+
+constexpr int ROWS = 64;                     // rows per CTA (128 per pair)
+constexpr int KDIM = 512;
+constexpr int NKB = KDIM / 64;               // 64-element K blocks (128 B swizzle rows)
+constexpr int A_PART = NKB * ROWS * 128;     // 64 KB per hi / lo
+constexpr int B_TILE = 128 * 128;            // 128 n-rows x 64 k bf16 = 16 KB
+constexpr int STAGE_BYTES = 2 * B_TILE;      // hi + lo
+constexpr int STAGES = 3;
+constexpr int OFF_AHI = 0;
+constexpr int OFF_ALO = A_PART;
+constexpr int OFF_B = 2 * A_PART;
+constexpr int OFF_MISC = OFF_B + STAGES * STAGE_BYTES;   // 229376
+constexpr int N_EPI_WARPS = 8;
+constexpr int THREADS = (2 + N_EPI_WARPS) * 32;          // producer, MMA, 8 epilogue warps
+constexpr int TMEM_COLS = 512;
+
+struct Misc {
+  uint64_t full[STAGES];
+  uint64_t empty[STAGES];
+  uint64_t dfull[2];
+  uint64_t aready;
+  uint32_t tmem_base;
+  int32_t go, cur, cnt, nan;
+  int32_t ray[ROWS];
+  int32_t shape[ROWS];
+  float xch[4][ROWS];   // per-row exchange: row max (scaling), then head partial sums
+};
+constexpr int SMEM_BYTES = OFF_MISC + (int)sizeof(Misc) + 1024;  // + alignment slack
+static_assert(SMEM_BYTES <= 232448, "shared memory budget");
+
+// ---- PTX helpers -----------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void mbar_init(uint64_t *b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
+  const uint32_t a = smem_u32(b);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 10000000;\n\t"
+      "@!p bra LAB_WAIT;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx)
+               : "memory");
+}
+// arrive on the barrier at the same offset in CTA `rank` of the cluster
+__device__ __forceinline__ void mbar_arrive_cluster(uint64_t *b, uint32_t rank) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(b)), "r"(rank));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void epi_sync() {  // named barrier over the epilogue warps
+  asm volatile("bar.sync 1, %0;" ::"n"(N_EPI_WARPS * 32) : "memory");
+}
+__device__ __forceinline__ void tma_load_2sm(uint32_t dst, const CUtensorMap *map, uint64_t *bar,
+                                             int x, int y) {
+  const uint32_t mb = smem_u32(bar) & 0xFEFFFFFFu;  // leader CTA's barrier
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(mb), "r"(x), "r"(y)
+      : "memory");
+}
+// K-major, 128B-swizzled UMMA shared-memory descriptor (SBO = 1024 B).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)1 << 16;                 // LBO (unused for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;       // SBO: 8-row core-matrix groups 1024 B apart
+  d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+  d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+  return d;
+}
+// kind::f16 instruction descriptors: {BF16|F16} x {BF16|F16} -> F32, K-major A/B,
+// M=128 (cta_group::2), N=256.
+constexpr uint32_t IDESC_BF16 =
+    (1u << 4) | (1u << 7) | (1u << 10) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+constexpr uint32_t IDESC_F16 = (1u << 4) | ((256u >> 3) << 17) | ((128u >> 4) << 24);
+
+template <bool F16>
+__device__ __forceinline__ void mma_2sm(uint32_t dtmem, uint64_t a, uint64_t b, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dtmem),
+      "l"(a), "l"(b), "n"(F16 ? IDESC_F16 : IDESC_BF16), "r"(acc));
+}
+__device__ __forceinline__ void commit_2sm(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::
+          "r"(smem_u32(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// byte offset of A[row][k] (bf16) inside one 64 KB hi/lo part
+__device__ __forceinline__ uint32_t a_off(int row, int k) {
+  const int kb = k >> 6, kk = k & 63;
+  const int chunk = (kk >> 3) ^ (row & 7);
+  return (uint32_t)(kb * (ROWS * 128) + row * 128 + chunk * 16 + (kk & 7) * 2);
+}
+
+// split x into hi + lo of the MMA element type (x - hi is exact in fp32)
+template <bool F16>
+__device__ __forceinline__ void split2(float x, uint16_t &h, uint16_t &l) {
+  if constexpr (F16) {
+    const __half hh = __float2half_rn(x);
+    h = __half_as_ushort(hh);
+    l = __half_as_ushort(__float2half_rn(x - __half2float(hh)));
+  } else {
+    const __nv_bfloat16 hh = __float2bfloat16_rn(x);
+    h = __bfloat16_as_ushort(hh);
+    l = __bfloat16_as_ushort(__float2bfloat16_rn(x - __bfloat162float(hh)));
+  }
+}
+
+// write 8 consecutive activations (k0..k0+7, k0 % 8 == 0) of `row` as hi/lo
+template <bool F16>
+__device__ __forceinline__ void put8(char *smem, int row, int k0, const float (&x)[8]) {
+  uint32_t hi[4], lo[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    uint16_t h0, h1, l0, l1;
+    split2<F16>(x[2 * i], h0, l0);
+    split2<F16>(x[2 * i + 1], h1, l1);
+    hi[i] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+    lo[i] = (uint32_t)l0 | ((uint32_t)l1 << 16);
+  }
+  const uint32_t off = a_off(row, k0);
+  *reinterpret_cast<uint4 *>(smem + OFF_AHI + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+  *reinterpret_cast<uint4 *>(smem + OFF_ALO + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+}
+
+}  // namespace tc
+}  // namespace dist

@@ -1,0 +1,409 @@
+// tc_heads.cu -- the memory-light backward on tensor cores: ONE fused
+// tcgen05 kernel per tile of 128 frozen head samples (64 per CTA of a pair)
+// that runs the taped decoder forward (shading.py:185-206), forms each
+// sample's loss seed from its own f (losses.py:54-91, via the generator of
+// heads.cuh) and sweeps the gradient back through the hidden layers
+// (autodiff.py:220-255) down to the layer-0 pre-activation, whose per-column
+// row sums are the only gradient output (the code gradient is their product
+// with W0[:D], done once per shape in k_reduce_code_grad).
+//
+//   * forward phases: as tc_mlp.cu (bf16x3, W^T streamed by TMA), plus the
+//     ReLU mask bits of every layer kept in TMEM (columns 256..319) -- the
+//     activations themselves are never stored;
+//   * backward phases: A = the bf16 hi/lo split of g (overwriting the
+//     activation buffer), B = W (untransposed) streamed by a second TMA map,
+//     D = g W^T in TMEM, epilogue multiplies by the stored masks;
+//   * the last backward epilogue reduces g over the CTA's 64 rows with a
+//     warp butterfly (62 shuffles per thread) and adds the column sums into
+//     this CTA's slice of part0 (deterministic: one owner per slice).
+#include <cmath>
+#include <cstring>
+
+#include "common.cuh"
+#include "heads.cuh"
+#include "kernels.cuh"
+#include "tc_core.cuh"
+
+namespace dist {
+namespace tc {
+
+struct HParams {
+  DecView dv;
+  const double *c0;
+  const float *bias;   // [G][512]
+  const float *w_out;  // [512]
+  int n_gemm;
+  int S;
+  double *part0;       // [grid][S][512]
+};
+
+__device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&r)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3])
+               : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Sum v[0..63] over the 32 lanes of the warp; afterwards lane l holds the
+// column sums of columns 2l and 2l+1 in v[0], v[1].
+__device__ __forceinline__ void warp_colsum64(float (&v)[64]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16, n = 32; o >= 1; o >>= 1, n >>= 1) {
+    const bool upper = lane & o;
+#pragma unroll
+    for (int j = 0; j < n; ++j) {
+      const float send = upper ? v[j] : v[j + n];
+      const float keep = upper ? v[j + n] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+}
+
+template <class Gen>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    k_tc_heads(const __grid_constant__ CUtensorMap wfwd, const __grid_constant__ CUtensorMap wbwd,
+               HParams P, Gen gen) {
+  extern __shared__ __align__(16) char smem_raw[];
+  char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  Misc &m = *reinterpret_cast<Misc *>(smem + OFF_MISC);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cta_rank();
+  const int64_t nrows = gen.count();
+  if (nrows <= 0) return;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&m.full[s], 1);
+      mbar_init(&m.empty[s], 1);
+    }
+    mbar_init(&m.dfull[0], 1);
+    mbar_init(&m.dfull[1], 1);
+    mbar_init(&m.aready, 2);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&m.tmem_base)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = m.tmem_base;
+
+  const int64_t ntiles = ceil_div(nrows, 2 * ROWS);
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int G = P.n_gemm;
+  const int NPH = 2 * G;  // forward GEMM phases, then backward phases
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      uint32_t it = 0;
+      for (int64_t t = cluster; t < ntiles; t += nclusters)
+        for (int ph = 0; ph < NPH; ++ph) {
+          const bool fwd = ph < G;
+          const int l = fwd ? ph : 2 * G - 1 - ph;
+          const CUtensorMap *map = fwd ? &wfwd : &wbwd;
+          for (int nh = 0; nh < 2; ++nh)
+            for (int kc = 0; kc < NKB; ++kc, ++it) {
+              const int s = it % STAGES;
+              mbar_wait(&m.empty[s], ((it / STAGES) & 1) ^ 1);
+              if (rank == 0) mbar_arrive_expect_tx(&m.full[s], 2 * STAGE_BYTES);
+              const uint32_t dst = smem_u32(smem + OFF_B + s * STAGE_BYTES);
+              const int y = nh * 256 + (int)rank * 128;
+              tma_load_2sm(dst, map, &m.full[s], kc * 64, (l * 2 + 0) * KDIM + y);
+              tma_load_2sm(dst + B_TILE, map, &m.full[s], kc * 64, (l * 2 + 1) * KDIM + y);
+            }
+        }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer (leader CTA) =====
+    if (rank == 0 && lane == 0) {
+      uint32_t it = 0, phase = 0;
+      const uint32_t a_hi = smem_u32(smem + OFF_AHI), a_lo = smem_u32(smem + OFF_ALO);
+      for (int64_t t = cluster; t < ntiles; t += nclusters)
+        for (int ph = 0; ph < NPH; ++ph, ++phase) {
+          mbar_wait(&m.aready, phase & 1);
+          tc_fence_after();
+          for (int nh = 0; nh < 2; ++nh) {
+            const uint32_t d = tmem + nh * 128;
+            for (int kc = 0; kc < NKB; ++kc, ++it) {
+              const int s = it % STAGES;
+              mbar_wait(&m.full[s], (it / STAGES) & 1);
+              tc_fence_after();
+              const uint32_t b_hi = smem_u32(smem + OFF_B + s * STAGE_BYTES), b_lo = b_hi + B_TILE;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t ak = kc * (ROWS * 128) + q * 32;
+                const uint64_t dah = sdesc(a_hi + ak), dal = sdesc(a_lo + ak);
+                const uint64_t dbh = sdesc(b_hi + q * 32), dbl = sdesc(b_lo + q * 32);
+                mma_2sm<false>(d, dah, dbh, (kc | q) ? 1u : 0u);
+                mma_2sm<false>(d, dah, dbl, 1u);
+                mma_2sm<false>(d, dal, dbh, 1u);
+              }
+              commit_2sm(&m.empty[s]);
+            }
+            commit_2sm(&m.dfull[nh]);
+          }
+        }
+    }
+  } else {
+    // ===== epilogue warps =====
+    const int q = warp & 3;
+    const int sub = (warp - 2) >> 2;
+    const int row = (q & 1) * 32 + lane;
+    const int half = q >> 1;
+    const bool row_thread = (sub == 0 && half == 0);
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+    // mask bits of layer output ml, this thread's 2 x 64 columns: TMEM cols 256 + 8 ml + 4 sub
+    auto mask_addr = [&](int ml) { return tq + 256 + ml * 8 + sub * 4; };
+    const int n0 = P.dv.np[0];
+    uint32_t phase = 0;
+    float *gout = reinterpret_cast<float *>(&m.xch[0][0]);   // [64] per-row head gradient
+    for (int64_t t = cluster; t < ntiles; t += nclusters) {
+      const int64_t gi = t * (2 * ROWS) + (int64_t)rank * ROWS + row;
+      double p[3] = {0, 0, 0};
+      int s = -1;
+      if (gi < nrows && !gen.point(gi, p, s)) s = -1;
+      if (row_thread) m.shape[row] = s;
+      // ---- layer 0 (fp64 fold) + mask 0 ----
+      {
+        const double *c0 = P.c0 + (size_t)(s < 0 ? 0 : s) * n0;
+        uint32_t mk[4] = {0, 0, 0, 0};
+        for (int nh = 0; nh < 2; ++nh) {
+          const int cb = nh * 256 + half * 128 + sub * 64;
+#pragma unroll 1
+          for (int j = 0; j < 64; j += 8) {
+            float x[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int col = cb + j + e;
+              double v = 0.0;
+              if (s >= 0) {
+                v = c0[col];
+                v = fma(p[0], P.dv.W0p[col], v);
+                v = fma(p[1], P.dv.W0p[n0 + col], v);
+                v = fma(p[2], P.dv.W0p[2 * n0 + col], v);
+              }
+              x[e] = (float)(v > 0.0 ? v : 0.0);
+              if (v > 0.0) mk[nh * 2 + ((j + e) >> 5)] |= 1u << ((j + e) & 31);
+            }
+            put8<false>(smem, row, cb + j, x);
+          }
+        }
+        tmem_st4(mask_addr(0), mk);
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      epi_sync();
+      if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+      // ---- forward hidden layers ----
+      float head = 0.f;
+      for (int l = 0; l < G; ++l, ++phase) {
+        mbar_wait(&m.dfull[1], phase & 1);
+        mbar_wait(&m.dfull[0], phase & 1);
+        tc_fence_after();
+        const bool last = (l == G - 1);
+        const float *bias = P.bias + (size_t)l * KDIM;
+        uint32_t mk[4] = {0, 0, 0, 0};
+        for (int nh = 0; nh < 2; ++nh) {
+          const int cb = nh * 256 + half * 128 + sub * 64;
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            float v[32];
+            tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
+            uint32_t bits = 0;
+#pragma unroll
+            for (int g8 = 0; g8 < 4; ++g8) {
+              float x[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const int col = cb + c * 32 + g8 * 8 + e;
+                const float y = v[g8 * 8 + e] + __ldg(bias + col);
+                x[e] = y > 0.f ? y : 0.f;
+                bits |= (y > 0.f ? 1u : 0u) << (g8 * 8 + e);
+                if (last) head = fmaf(x[e], __ldg(P.w_out + col), head);
+              }
+              if (!last) put8<false>(smem, row, cb + c * 32 + g8 * 8, x);
+            }
+            mk[nh * 2 + c] = bits;
+          }
+        }
+        tmem_st4(mask_addr(l + 1), mk);
+        tc_fence_before();
+        if (!last) {
+          fence_proxy_async();
+          epi_sync();
+          if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+        }
+      }
+      // ---- head, seed, d loss / d h_G ----
+      m.xch[half * 2 + sub][row] = head;
+      epi_sync();
+      double go = 0.0;
+      if (row_thread) {
+        const double sum = (double)m.xch[0][row] + (double)m.xch[1][row] +
+                           (double)m.xch[2][row] + (double)m.xch[3][row] + P.dv.b_out;
+        const double fv = P.dv.final_linear ? sum : tanh(sum);
+        if (gi < nrows && s >= 0) {
+          gen.store(gi, fv);
+          const double sd = gen.seed(gi, fv);
+          go = P.dv.final_linear ? sd : sd * (1.0 - fv * fv);
+        }
+      }
+      epi_sync();
+      if (row_thread) gout[row] = (float)go;
+      epi_sync();
+      {
+        const float gr = gout[row];
+        uint32_t mk[4];
+        tmem_ld4(mask_addr(G), mk);
+        for (int nh = 0; nh < 2; ++nh) {
+          const int cb = nh * 256 + half * 128 + sub * 64;
+#pragma unroll 1
+          for (int j = 0; j < 64; j += 8) {
+            float x[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const int jj = j + e;
+              const bool on = (mk[nh * 2 + (jj >> 5)] >> (jj & 31)) & 1u;
+              x[e] = on ? gr * __ldg(P.w_out + cb + jj) : 0.f;
+            }
+            put8<false>(smem, row, cb + j, x);
+          }
+        }
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      epi_sync();
+      if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+      // ---- backward through GEMM layers G-1 .. 0 ----
+      for (int gl = G - 1; gl >= 0; --gl, ++phase) {
+        mbar_wait(&m.dfull[1], phase & 1);
+        mbar_wait(&m.dfull[0], phase & 1);
+        tc_fence_after();
+        uint32_t mk[4];
+        tmem_ld4(mask_addr(gl), mk);
+        if (gl > 0) {
+          for (int nh = 0; nh < 2; ++nh) {
+            const int cb = nh * 256 + half * 128 + sub * 64;
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              float v[32];
+              tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
+              const uint32_t bits = mk[nh * 2 + c];
+#pragma unroll
+              for (int g8 = 0; g8 < 4; ++g8) {
+                float x[8];
+#pragma unroll
+                for (int e = 0; e < 8; ++e) x[e] = ((bits >> (g8 * 8 + e)) & 1u) ? v[g8 * 8 + e] : 0.f;
+                put8<false>(smem, row, cb + c * 32 + g8 * 8, x);
+              }
+            }
+          }
+          tc_fence_before();
+          fence_proxy_async();
+          epi_sync();
+          if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+        } else {
+          // g_pre0 = D * mask0; column sums over the CTA's rows, per shape
+          float gv[2][64];
+          for (int nh = 0; nh < 2; ++nh)
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+              float v[32];
+              tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
+              const uint32_t bits = mk[nh * 2 + c];
+#pragma unroll
+              for (int e = 0; e < 32; ++e) gv[nh][c * 32 + e] = ((bits >> e) & 1u) ? v[e] : 0.f;
+            }
+          tc_fence_before();
+          epi_sync();   // every row's shape is in m.shape; all TMEM reads of this tile done
+          // distinct shapes of this CTA's rows (usually one)
+          float *red = reinterpret_cast<float *>(smem + OFF_AHI);  // A is free now: [2][512] floats
+          int shapes_done = 0;
+          for (int guard = 0; guard < ROWS; ++guard) {
+            // next shape = smallest shape id > previous (uniform across threads)
+            int next = 0x7fffffff;
+            for (int r = 0; r < ROWS; ++r) {
+              const int sr = m.shape[r];
+              if (sr >= 0 && sr >= shapes_done && sr < next) next = sr;
+            }
+            if (next == 0x7fffffff) break;
+            const bool mine = (s == next);
+            for (int nh = 0; nh < 2; ++nh) {
+              float w[64];
+#pragma unroll
+              for (int e = 0; e < 64; ++e) w[e] = mine ? gv[nh][e] : 0.f;
+              warp_colsum64(w);
+              const int cb = nh * 256 + half * 128 + sub * 64;
+              // the two row-warps (q&1 = 0, 1) of this column block combine in smem
+              red[(q & 1) * 512 + cb + 2 * lane] = w[0];
+              red[(q & 1) * 512 + cb + 2 * lane + 1] = w[1];
+            }
+            epi_sync();
+            double *dst = P.part0 + ((size_t)blockIdx.x * P.S + next) * n0;
+            for (int col = threadIdx.x - 64; col < KDIM; col += N_EPI_WARPS * 32)
+              dst[col] += (double)red[col] + (double)red[512 + col];
+            epi_sync();
+            shapes_done = next + 1;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+}
+
+}  // namespace tc
+
+// ---------------------------------------------------------------------------
+bool tc_heads_supported(const DecView &dv) {
+  return dv.prec == DIST_PREC_BF16X3 && tc_supported(dv) && dv.tc_w[1] != nullptr;
+}
+
+
+template <class Gen>
+int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
+                    double *part0, int grid_cap, int *grid_out, cudaStream_t st) {
+  CUtensorMap mf, mb;
+  int rc = tc_make_map(dv, 0, &mf);
+  if (!rc) rc = tc_make_map(dv, 1, &mb);
+  if (rc) return rc;
+  tc::HParams P;
+  P.dv = dv;
+  P.c0 = c0;
+  P.bias = dv.tc_bias[0];
+  P.w_out = dv.tc_bias[0] + (size_t)(dv.n_layers - 2) * tc::KDIM;
+  P.n_gemm = dv.n_layers - 2;
+  P.S = S;
+  P.part0 = part0;
+  const void *fn = (const void *)tc::k_tc_heads<Gen>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc heads)");
+  int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_bound, 128), sm_count() / 2));
+  pairs = std::min(pairs, grid_cap / 2);
+  *grid_out = 2 * pairs;
+  tc::k_tc_heads<Gen><<<2 * pairs, tc::THREADS, tc::SMEM_BYTES, st>>>(mf, mb, P, gen);
+  DIST_CHECK_LAUNCH("k_tc_heads");
+  return DIST_OK;
+}
+
+template int launch_tc_heads<ObjGen>(const DecView &, const double *, const ObjGen &, int64_t, int,
+                                     double *, int, int *, cudaStream_t);
+
+}  // namespace dist

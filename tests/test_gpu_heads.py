@@ -87,7 +87,7 @@ def test_tiny_complete_shape_matches_reference(st):
     np.testing.assert_allclose(best, g["cs_best"], rtol=1e-9, atol=1e-12)
 
 
-@pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("fp32", 1e-3)])
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("fp32", 1e-3), ("bf16x3", 1e-3), ("fp16x3", 1e-3)])
 def test_geo64_objective(st, prec, tol):
     g = load_golden("geo64.npz")
     net = st.NeuralField.geometric(256, (512,) * 8, int(g["seed"]), precision=prec)
