@@ -154,7 +154,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--precision", default=os.environ.get("DIST_BENCH_PRECISION", "fp32"))
+    ap.add_argument("--precision", default=os.environ.get("DIST_BENCH_PRECISION", "bf16x3"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -257,27 +257,28 @@ def main():
     e2e_ms = float(t.item())
 
     peaks, peak_kind = _peaks()
-    # roofline of the dominant kernel family: the decoder step kernels of the march
+    # Roofline of the dominant kernel family: the decoder step kernels of the
+    # march (k_tc_mlp in march mode for bf16x3).  achieved = algorithmic FLOP
+    # (F_Q per query) / device time of the trace phase; executed MMA
+    # FLOP are 3x for the split-precision scheme.
     flops_trace = queries * F_Q
     achieved = flops_trace / (trace_ms * 1e-3) / 1e12
-    if args.precision == "bf16x3":
-        peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-        bound = "tensor"
-    else:
-        peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-        bound = "tensor"
+    peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
+    split = 3.0 if args.precision in ("bf16x3", "fp16x3") else 1.0
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": {"fp32": "f32", "fp64": "f64", "bf16x3": "bf16x3"}[args.precision],
+        "vs_baseline": None, "dtype": {"fp32": "f32", "fp64": "f64", "bf16x3": "bf16x3", "fp16x3": "fp16x3"}[args.precision],
         "data": "synthetic (geometric-init 8x512 DeepSDF, ring views, depth rendered from z*)",
         "config": _config(args),
         "e2e": {"value": rays_per_step / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
-        "roofline": {"bound": bound, "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": None,
+                     "executed_mma_tflops": achieved * split,
+                     "executed_frac": achieved * split / peak,
                      "kernel": "march step kernels (decoder + update), whole trace phase",
                      "peak_source": f"{peak_kind} bf16 sustained (MEASURED_PEAKS.json)",
                      "algorithmic_flop_per_query": F_Q, "queries_per_step": queries,
