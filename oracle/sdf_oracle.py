@@ -258,6 +258,8 @@ class Trace:
     tk_f: np.ndarray
     tk_a: np.ndarray
     band: np.ndarray
+    margin_f: np.ndarray = None     # min over own+inherited queries of ||b| - eps|
+    margin_esc: np.ndarray = None   # min over escape tests of min(|p|^2-1|, |v.p|, |b|)
     live_counts: list = dfield(default_factory=list)
     total_queries: int = 0
     nan_count: int = 0
@@ -282,7 +284,7 @@ def _init(rays: Rays, K: int) -> Trace:
         st[~hit] = ESCAPED
     return Trace(rays, d, np.full(n, np.nan), st, np.zeros(n, np.int64),
                  np.zeros((n, K)), np.zeros((n, K)), np.full((n, K), np.inf),
-                 np.zeros(n, bool))
+                 np.zeros(n, bool), np.full(n, np.inf), np.full(n, np.inf))
 
 
 def _step(T: Trace, fn, cfg: Cfg, band_f=BAND_F, band_esc=BAND_ESC):
@@ -315,6 +317,7 @@ def _step(T: Trace, fn, cfg: Cfg, band_f=BAND_F, band_esc=BAND_ESC):
     T.d[rows] = dk + cfg.alpha * f
     conv = a < cfg.epsilon
     T.band[rows] |= np.abs(a - cfg.epsilon) < band_f
+    T.margin_f[rows] = np.minimum(T.margin_f[rows], np.abs(a - cfg.epsilon))
     T.status[rows[conv]] = CONVERGED
     mv = rows[~conv]
     if mv.size:
@@ -324,6 +327,8 @@ def _step(T: Trace, fn, cfg: Cfg, band_f=BAND_F, band_esc=BAND_ESC):
         fm = f[~conv]
         esc = (r2 > 0.0) & (fm > 0.0) & (vp > 0.0)
         T.band[mv] |= (np.abs(r2) < band_esc) | (np.abs(vp) < band_esc) | (np.abs(fm) < band_esc)
+        T.margin_esc[mv] = np.minimum(T.margin_esc[mv], np.minimum(np.minimum(np.abs(r2), np.abs(vp)),
+                                                                    np.abs(fm)))
         T.status[mv[esc]] = ESCAPED
     return queried, int(bad.sum())
 
@@ -335,7 +340,8 @@ def _split(T: Trace, fine: Rays) -> Trace:
     st[st == CONVERGED] = MARCHING
     return Trace(fine, T.d[par].copy(), T.b[par].copy(), st, T.steps[par].copy(),
                  T.tk_d[par].copy(), T.tk_f[par].copy(), T.tk_a[par].copy(),
-                 T.band[par].copy(), T.live_counts, T.total_queries, T.nan_count)
+                 T.band[par].copy(), T.margin_f[par].copy(), T.margin_esc[par].copy(),
+                 T.live_counts, T.total_queries, T.nan_count)
 
 
 def trace(fn, cam: Cam, cfg: Cfg, band_f=BAND_F, band_esc=BAND_ESC) -> Trace:
