@@ -14,7 +14,7 @@
 
 namespace dist {
 
-template <typename T, class Gen>
+template <typename T, class Gen, bool PAIR = false>
 __global__ void __launch_bounds__(SimtTile<T>::NT)
     k_eval_gen(DecView dv, const double *__restrict__ c0, const double *__restrict__ cskip, Gen gen) {
   extern __shared__ __align__(16) char smem[];
@@ -33,7 +33,8 @@ __global__ void __launch_bounds__(SimtTile<T>::NT)
       for (int a = 0; a < 3; ++a) tile.pts[threadIdx.x * 3 + a] = p[a];
     }
     __syncthreads();
-    tile.forward(dv, c0, cskip, false);
+    if constexpr (PAIR) tile.forward_pair(dv, c0);
+    else tile.forward(dv, c0, cskip, false);
     if (threadIdx.x < Tile::TM && base + threadIdx.x < n) gen.store(base + threadIdx.x, tile.f[threadIdx.x]);
     __syncthreads();
   }
@@ -139,11 +140,11 @@ struct ArrayGen {
 
 int sm_count();
 
-template <typename T, class Gen>
+template <typename T, class Gen, bool PAIR = false>
 int launch_eval_gen(const DecView &dv, const double *c0, const double *cskip, const Gen &gen,
                     int64_t n_bound, cudaStream_t st) {
   using Tile = SimtTile<T>;
-  const void *fn = (const void *)k_eval_gen<T, Gen>;
+  const void *fn = (const void *)k_eval_gen<T, Gen, PAIR>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)Tile::fwd_bytes);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(eval)");
@@ -151,7 +152,7 @@ int launch_eval_gen(const DecView &dv, const double *c0, const double *cskip, co
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, Tile::NT, Tile::fwd_bytes);
   const int64_t tiles = std::max<int64_t>(1, ceil_div(n_bound, Tile::TM));
   const int grid = (int)std::min<int64_t>(tiles, (int64_t)std::max(per_sm, 1) * sm_count());
-  k_eval_gen<T, Gen><<<grid, Tile::NT, Tile::fwd_bytes, st>>>(dv, c0, cskip, gen);
+  k_eval_gen<T, Gen, PAIR><<<grid, Tile::NT, Tile::fwd_bytes, st>>>(dv, c0, cskip, gen);
   DIST_CHECK_LAUNCH("k_eval_gen");
   return DIST_OK;
 }

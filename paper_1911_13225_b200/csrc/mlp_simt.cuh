@@ -202,6 +202,114 @@ struct SimtTile {
     output(dv);
   }
 
+  // ---- (mid, diff) pair mode: rows 2i / 2i+1 hold the probes p+ / p- of one
+  // central difference (shading.py:84-87).  They are carried through the
+  // network as m = (h+ + h-)/2 and d = (h+ - h-)/2, so the difference never
+  // cancels; the result row 2i+1 receives f+ - f-.
+  __device__ static __forceinline__ void relu_pair(double m, double d, double &mo, double &dd) {
+    const double ad = fabs(d);
+    if (m - ad > 0.0) {          // both probes active: exact pass-through
+      mo = m;
+      dd = d;
+    } else if (m + ad <= 0.0) {  // both inactive
+      mo = 0.0;
+      dd = 0.0;
+    } else {                     // straddles the kink
+      const double a = fmax(m + d, 0.0), b = fmax(m - d, 0.0);
+      mo = 0.5 * (a + b);
+      dd = 0.5 * (a - b);
+    }
+  }
+
+  __device__ void layer0_pair(const DecView &dv, const double *__restrict__ c0) {
+    const int tid = threadIdx.x, cg = tid & 63, rg = tid >> 6;
+    const int n0 = dv.np[0];
+    for (int c = 0; c < kMaxWidth / 64; ++c) {
+      const int col = cg + 64 * c;
+      if (col >= n0) break;
+      const double w0 = dv.W0p[col], w1 = dv.W0p[n0 + col], w2 = dv.W0p[2 * n0 + col];
+#pragma unroll
+      for (int r = 0; r < 8; r += 2) {
+        const int row = rg * 8 + r;
+        const int s = shape[row];
+        double m = 0.0, d = 0.0;
+        if (s >= 0) {
+          double vp = c0[(size_t)s * n0 + col], vm = vp;
+          vp = fma(pts[row * 3 + 0], w0, vp);
+          vp = fma(pts[row * 3 + 1], w1, vp);
+          vp = fma(pts[row * 3 + 2], w2, vp);
+          vm = fma(pts[row * 3 + 3], w0, vm);
+          vm = fma(pts[row * 3 + 4], w1, vm);
+          vm = fma(pts[row * 3 + 5], w2, vm);
+          const double a = vp > 0.0 ? vp : 0.0, b = vm > 0.0 ? vm : 0.0;
+          m = 0.5 * (a + b);
+          d = 0.5 * (a - b);
+        }
+        H[col * LD + row] = (T)m;
+        H[col * LD + row + 1] = (T)d;
+      }
+    }
+    __syncthreads();
+  }
+
+  __device__ void hidden_pair(const DecView &dv, int l) {
+    const int tid = threadIdx.x, cg = tid & 63, rg = tid >> 6;
+    const int K = dv.kp[l], N = dv.np[l];
+    T acc[8][8];
+    gemm(reinterpret_cast<const T *>(dv.W[WI][l]), K, N, acc);
+    const T *bias = reinterpret_cast<const T *>(dv.bias[WI][l]);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      const int col = cg + 64 * c;
+      if (col < N) {
+        const double bb = (double)bias[col];
+#pragma unroll
+        for (int r = 0; r < 8; r += 2) {
+          double mo, dd;
+          relu_pair((double)acc[c][r] + bb, (double)acc[c][r + 1], mo, dd);
+          acc[c][r] = (T)mo;
+          acc[c][r + 1] = (T)dd;
+        }
+        T *dst = H + col * LD + rg * 8;
+#pragma unroll
+        for (int r = 0; r < 8; ++r) dst[r] = acc[c][r];
+      }
+    }
+    __syncthreads();
+  }
+
+  __device__ void output_pair(const DecView &dv) {
+    const int tid = threadIdx.x;
+    const int K = dv.np[dv.n_layers - 2];
+    const T *w = reinterpret_cast<const T *>(dv.w_out[WI]);
+    constexpr int P = NT / TM;
+    const int row = tid % TM, part = tid / TM;
+    T acc = (T)0;
+    for (int k = part; k < K; k += P) acc = fma(H[k * LD + row], w[k], acc);
+    red[tid] = (double)acc;
+    __syncthreads();
+    if (tid < TM) {
+      double s = 0.0;
+#pragma unroll
+      for (int p = 0; p < P; ++p) s += red[p * TM + tid];
+      f[tid] = s;
+    }
+    __syncthreads();
+    if (tid < TM && (tid & 1)) {
+      const double om = f[tid - 1] + dv.b_out, od = f[tid];
+      // f+ - f- without cancellation: tanh(a) - tanh(b) = sinh(a - b) / (cosh a cosh b)
+      f[tid] = dv.final_linear ? 2.0 * od : sinh(2.0 * od) / (cosh(om + od) * cosh(om - od));
+      f[tid - 1] = dv.final_linear ? om : tanh(om);
+    }
+    __syncthreads();
+  }
+
+  __device__ void forward_pair(const DecView &dv, const double *c0) {
+    layer0_pair(dv, c0);
+    for (int l = 1; l <= dv.n_layers - 2; ++l) hidden_pair(dv, l);
+    output_pair(dv);
+  }
+
   // Reverse sweep after forward(keep_mask=true).  seed[row] (shared, TM
   // entries, 0 for empty rows) multiplies f.  Accumulates the column sums of
   // the layer-0 (and skip-layer) pre-activation gradients into gsum0/gsums

@@ -211,8 +211,10 @@ struct ProbeGen {
     pixel_ray(cams[v], ii, j, 1, dir, nullptr);
     const double ds = __dadd_rn(ls.d[g], __dmul_rn(1.0 - alpha, ls.b[g]));
     for (int q = 0; q < 3; ++q) p[q] = __dadd_rn(cams[v].origin[q], __dmul_rn(ds, dir[q]));
-    const int axis = a % 3;
-    p[axis] = __dadd_rn(p[axis], a < 3 ? delta : -delta);
+    // probe order (+x, -x, +y, -y, +z, -z): consecutive rows form the
+    // (p + delta e_a, p - delta e_a) pairs of the (mid, diff) evaluation
+    const int axis = a >> 1;
+    p[axis] = __dadd_rn(p[axis], (a & 1) ? -delta : delta);
     s = cams[v].shape;
     return true;
   }
@@ -222,13 +224,15 @@ struct ProbeGen {
 
 __global__ void k_normals_assemble(LevelState ls, const int32_t *__restrict__ conv,
                                    const int32_t *__restrict__ count, const double *__restrict__ f,
-                                   double delta, double *__restrict__ normals) {
+                                   double delta, int pair, double *__restrict__ normals) {
   const int64_t n = *count;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
     const int64_t g = conv[r];
     double raw[3];
-    for (int a = 0; a < 3; ++a) raw[a] = (f[r * 6 + a] - f[r * 6 + 3 + a]) / (2.0 * delta);
+    for (int a = 0; a < 3; ++a)  // row 2a+1 of the pair holds f(p + d e_a) - f(p - d e_a)
+      raw[a] = pair ? f[r * 6 + 2 * a + 1] / (2.0 * delta)
+                    : (f[r * 6 + 2 * a] - f[r * 6 + 2 * a + 1]) / (2.0 * delta);
     const double nrm = sqrt(raw[0] * raw[0] + raw[1] * raw[1] + raw[2] * raw[2]);
     for (int a = 0; a < 3; ++a) normals[g * 3 + a] = nrm > 0.0 ? raw[a] / nrm : 0.0;
   }
@@ -438,10 +442,15 @@ int dist_normals(const dist_decoder *dec, const double *codes, int S, const dist
   LevelState ls{stt->d, stt->b, stt->status, stt->steps, stt->topk_d, stt->topk_f, stt->topk_absf,
                 W, H, 1, n};
   ProbeGen gen{cams, ls, conv, count, cfg->alpha, cfg->normal_delta, f};
-  if (dv.prec == DIST_PREC_FP64) rc = launch_eval_gen<double>(dv, c0, cs, gen, n * 6, st);
-  else rc = launch_eval_gen<float>(dv, c0, cs, gen, n * 6, st);
+  // fp64: plain probes (the reference's own arithmetic); every other mode
+  // evaluates the probe pairs as (mid, diff) in fp32 so that the 1/(2 delta)
+  // amplification does not act on rounding error (SURVEY 0 finding 3).
+  const int pair = dv.prec == DIST_PREC_FP64 ? 0 : 1;
+  if (!pair) rc = launch_eval_gen<double>(dv, c0, cs, gen, n * 6, st);
+  else rc = launch_eval_gen<float, ProbeGen, true>(dv, c0, cs, gen, n * 6, st);
   if (rc) return rc;
-  k_normals_assemble<<<grid_for(n, 256), 256, 0, st>>>(ls, conv, count, f, cfg->normal_delta, normals);
+  k_normals_assemble<<<grid_for(n, 256), 256, 0, st>>>(ls, conv, count, f, cfg->normal_delta, pair,
+                                                       normals);
   DIST_CHECK_LAUNCH("k_normals_assemble");
   return DIST_OK;
 }

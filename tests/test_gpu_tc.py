@@ -87,4 +87,11 @@ def test_c2_render_256_depth_normals_vs_oracle(st, prec):
     rel = np.abs(maps.depth[both] - ref.depth[both]) / ref.depth[both]
     assert np.percentile(rel, 99.9) < 1e-4 and rel.max() < (1e-4 if prec == "fp32" else 5e-4)
     nd = np.linalg.norm(maps.normal - ref.normal, axis=2)[both]
-    assert np.percentile(nd, 99) < (2e-3 if prec == "fp32" else 2e-2)
+    # SURVEY 0 finding 3 metric: share of hit pixels whose normal differs by > 1e-4.
+    # Probes are (mid, diff) pairs in fp32 for both modes; in bf16x3 the traced
+    # surface point itself sits ~1e-5..1e-4 further along the ray, which moves
+    # the normal by curvature x shift.
+    if prec == "fp32":
+        assert np.percentile(nd, 99) < 1e-4 and np.mean(nd > 1e-4) < 2e-3
+    else:
+        assert np.percentile(nd, 99) < 5e-4 and np.mean(nd > 1e-3) < 2e-3
