@@ -160,6 +160,9 @@ typedef struct dist_objective_io {
   double *grad;                  /* out [S*D]: d total / d code (device) */
   double *view_terms;            /* out [V*4]: depth loss, silhouette loss, n_px, n_converged */
   double *shape_terms;           /* out [S*2]: total objective, |z|^2 */
+  int32_t grad_mode;             /* 0: the reference's frozen-sample surrogate (shading.py:9-11);
+                                    1: implicit gradient -(df/dz)/(grad f . v) at converged pixels */
+  int32_t reserved;
 } dist_objective_io;
 
 DIST_API size_t dist_objective_workspace_size(const dist_decoder *dec, int n_views, int width,

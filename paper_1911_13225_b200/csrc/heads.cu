@@ -202,8 +202,8 @@ __global__ void k_adam(int S, int D, double *params, const double *grad, double 
 
 struct ObjLayout {
   HeadsDev h;
-  double *c0, *cs, *part0, *parts, *col0, *cols, *sil_seed;
-  int32_t *npx, *bcount;
+  double *c0, *cs, *part0, *parts, *col0, *cols, *sil_seed, *gdotv, *probe_f;
+  int32_t *npx, *bcount, *conv, *conv_count;
   size_t bytes;
 };
 
@@ -222,6 +222,10 @@ static ObjLayout obj_layout(const DecView &dv, int V, int W, int H, int K, int S
   L.h.view_samp = cv.take<int32_t>(V + 1);
   L.h.counts = cv.take<int32_t>(4);
   L.sil_seed = cv.take<double>(n);
+  L.gdotv = cv.take<double>(n);
+  L.probe_f = cv.take<double>(n * 6);
+  L.conv = cv.take<int32_t>(n);
+  L.conv_count = cv.take<int32_t>(4);
   L.npx = cv.take<int32_t>(V);
   L.bcount = cv.take<int32_t>(ceil_div(n * K, kScanBlock) + 1);
   L.c0 = cv.take<double>((size_t)s1 * dv.np[0]);
@@ -285,7 +289,15 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
   if (e == cudaSuccess && dv.nskip) e = cudaMemsetAsync(L.parts, 0, sizeof(double) * G * s1 * dv.nskip, sm);
   if (e == cudaSuccess) e = cudaMemsetAsync(io->grad, 0, sizeof(double) * s1 * std::max(dv.latent_dim, 1), sm);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(objective)");
-  ObjGen gen{cams, ls, K, WH, L.h, in, L.npx, io->obs_sil ? L.sil_seed : nullptr};
+  if (io->grad_mode == 1) {
+    rc = normals_pass(dv, L.c0, L.cs, cams, ls, cfg, nullptr, L.gdotv, L.conv, L.conv_count,
+                      L.bcount, L.probe_f, sm);
+    if (rc) return rc;
+  } else if (io->grad_mode != 0) {
+    return fail(DIST_ERR_CONFIG, "grad_mode must be 0 (surrogate) or 1 (implicit)");
+  }
+  ObjGen gen{cams, ls, K, WH, L.h, in, L.npx, io->obs_sil ? L.sil_seed : nullptr,
+             io->grad_mode == 1 ? L.gdotv : nullptr};
   int grid = 0;
   if (tc_heads_supported(dv))
     rc = launch_tc_heads<ObjGen>(dv, L.c0, gen, n * K, s1, L.part0, G, &grid, sm);

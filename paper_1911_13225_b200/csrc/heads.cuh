@@ -47,6 +47,7 @@ struct ObjGen {
   ObjIn in;
   const int32_t *npx;
   const double *sil_seed;
+  const double *gdotv;   // implicit mode: grad f . v per ray (raw Eq. 3 vector), else null
   __device__ int64_t count() const { return h.counts[1]; }
   __device__ bool point(int64_t i, double p[3], int &s) const {
     const int64_t flat = h.samp[i];
@@ -77,6 +78,10 @@ struct ObjGen {
       const double r = __dmul_rn(__dadd_rn(ls.tk_d[flat], f), scale) - in.obs_depth[g];
       const double sg = r > 0.0 ? 1.0 : (r < 0.0 ? -1.0 : 0.0);
       sd = in.w_depth * __dmul_rn(__dmul_rn(w, sg), scale);
+      if (gdotv) {  // implicit gradient: scale by -1/(grad f . v), drop grazing
+        const double gv = gdotv[g];
+        sd = gv < -1e-3 ? sd * (-1.0 / gv) : 0.0;
+      }
     }
     if (sil_seed && flat - g * K == 0) sd = __dadd_rn(sd, sil_seed[g]);
     return sd;

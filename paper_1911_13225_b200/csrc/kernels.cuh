@@ -37,6 +37,11 @@ template <class Gen>
 int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
                     double *part0, int grid_cap, int *grid_out, cudaStream_t st);
 
+struct LevelState;
+int normals_pass(const DecView &dv, const double *c0, const double *cs, const dist_camera *cams,
+                 const LevelState &ls, const dist_trace_config *cfg, double *normals, double *gdotv,
+                 int32_t *conv, int32_t *count, int32_t *bcount, double *f, cudaStream_t st);
+
 // stable device-wide compaction of flags -> ascending indices (scan.cu)
 size_t compact_ws_bytes(int64_t n);
 

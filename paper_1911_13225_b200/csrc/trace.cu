@@ -190,6 +190,10 @@ __global__ void k_maps(const dist_camera *__restrict__ cams, LevelState ls, doub
   }
 }
 
+static int grid_for(int64_t n, int threads) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), (int64_t)sm_count() * 16));
+}
+
 // --- normals (shading.py:73-94) ----------------------------------------------
 struct ProbeGen {
   const dist_camera *cams;
@@ -222,9 +226,11 @@ struct ProbeGen {
   __device__ void store(int64_t i, double v) const { f[i] = v; }
 };
 
-__global__ void k_normals_assemble(LevelState ls, const int32_t *__restrict__ conv,
+__global__ void k_normals_assemble(const dist_camera *__restrict__ cams, LevelState ls,
+                                   const int32_t *__restrict__ conv,
                                    const int32_t *__restrict__ count, const double *__restrict__ f,
-                                   double delta, int pair, double *__restrict__ normals) {
+                                   double delta, int pair, double *__restrict__ normals,
+                                   double *__restrict__ gdotv) {
   const int64_t n = *count;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
@@ -234,8 +240,43 @@ __global__ void k_normals_assemble(LevelState ls, const int32_t *__restrict__ co
       raw[a] = pair ? f[r * 6 + 2 * a + 1] / (2.0 * delta)
                     : (f[r * 6 + 2 * a] - f[r * 6 + 2 * a + 1]) / (2.0 * delta);
     const double nrm = sqrt(raw[0] * raw[0] + raw[1] * raw[1] + raw[2] * raw[2]);
-    for (int a = 0; a < 3; ++a) normals[g * 3 + a] = nrm > 0.0 ? raw[a] / nrm : 0.0;
+    if (normals)
+      for (int a = 0; a < 3; ++a) normals[g * 3 + a] = nrm > 0.0 ? raw[a] / nrm : 0.0;
+    if (gdotv) {  // grad f . v with the raw Eq. 3 vector, for the implicit gradient
+      const int64_t per = (int64_t)ls.lw * ls.lh;
+      const int v = (int)(g / per);
+      const int64_t pix = g - (int64_t)v * per;
+      const int j = (int)(pix / ls.lw), i = (int)(pix - (int64_t)j * ls.lw);
+      double dir[3];
+      pixel_ray(cams[v], i, j, 1, dir, nullptr);
+      gdotv[g] = raw[0] * dir[0] + raw[1] * dir[1] + raw[2] * dir[2];
+    }
   }
+}
+
+// Normal probes at every converged ray (shading.py:73-94): compaction, probe
+// evaluation ((mid, diff) pairs except in fp64), assembly of unit normals
+// and/or grad f . v.
+int normals_pass(const DecView &dv, const double *c0, const double *cs, const dist_camera *cams,
+                 const LevelState &ls, const dist_trace_config *cfg, double *normals, double *gdotv,
+                 int32_t *conv, int32_t *count, int32_t *bcount, double *f, cudaStream_t st) {
+  const int64_t n = ls.n;
+  const uint8_t *status = ls.status;
+  int rc = compact([status] __device__(int64_t i) { return status[i] == DIST_CONVERGED; }, n, conv,
+                   count, bcount, st);
+  if (rc) return rc;
+  ProbeGen gen{cams, ls, conv, count, cfg->alpha, cfg->normal_delta, f};
+  // fp64: plain probes (the reference's own arithmetic); every other mode
+  // evaluates the probe pairs as (mid, diff) in fp32 so that the 1/(2 delta)
+  // amplification does not act on rounding error (SURVEY 0 finding 3).
+  const int pair = dv.prec == DIST_PREC_FP64 ? 0 : 1;
+  if (!pair) rc = launch_eval_gen<double>(dv, c0, cs, gen, n * 6, st);
+  else rc = launch_eval_gen<float, ProbeGen, true>(dv, c0, cs, gen, n * 6, st);
+  if (rc) return rc;
+  k_normals_assemble<<<grid_for(n, 256), 256, 0, st>>>(cams, ls, conv, count, f, cfg->normal_delta,
+                                                       pair, normals, gdotv);
+  DIST_CHECK_LAUNCH("k_normals_assemble");
+  return DIST_OK;
 }
 
 // --- host side --------------------------------------------------------------
@@ -328,9 +369,6 @@ static int run_steps(const DecView &dv, const double *c0, const double *cskip,
   return DIST_OK;
 }
 
-static int grid_for(int64_t n, int threads) {
-  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), (int64_t)sm_count() * 16));
-}
 
 }  // namespace dist
 
@@ -435,24 +473,9 @@ int dist_normals(const dist_decoder *dec, const double *codes, int S, const dist
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(normals)");
   int rc = launch_code_bias(dv, dv.latent_dim > 0 ? codes : nullptr, s1, c0, cs, st);
   if (rc) return rc;
-  const uint8_t *status = stt->status;
-  rc = compact([status] __device__(int64_t i) { return status[i] == DIST_CONVERGED; }, n, conv,
-               count, bcount, st);
-  if (rc) return rc;
   LevelState ls{stt->d, stt->b, stt->status, stt->steps, stt->topk_d, stt->topk_f, stt->topk_absf,
                 W, H, 1, n};
-  ProbeGen gen{cams, ls, conv, count, cfg->alpha, cfg->normal_delta, f};
-  // fp64: plain probes (the reference's own arithmetic); every other mode
-  // evaluates the probe pairs as (mid, diff) in fp32 so that the 1/(2 delta)
-  // amplification does not act on rounding error (SURVEY 0 finding 3).
-  const int pair = dv.prec == DIST_PREC_FP64 ? 0 : 1;
-  if (!pair) rc = launch_eval_gen<double>(dv, c0, cs, gen, n * 6, st);
-  else rc = launch_eval_gen<float, ProbeGen, true>(dv, c0, cs, gen, n * 6, st);
-  if (rc) return rc;
-  k_normals_assemble<<<grid_for(n, 256), 256, 0, st>>>(ls, conv, count, f, cfg->normal_delta, pair,
-                                                       normals);
-  DIST_CHECK_LAUNCH("k_normals_assemble");
-  return DIST_OK;
+  return normals_pass(dv, c0, cs, cams, ls, cfg, normals, nullptr, conv, count, bcount, f, st);
 }
 
 }  // extern "C"

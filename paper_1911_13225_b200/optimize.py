@@ -109,7 +109,7 @@ class LatentOptimizer:
 
     def __init__(self, field, views, observations: dict, code0, cfg: TraceConfig | None = None,
                  weights: LossWeights | None = None, lr: float = 1e-2, shape_of_view=None,
-                 max_iters: int = 1024):
+                 max_iters: int = 1024, grad_mode: str = "surrogate"):
         import torch
         _lib.require_device()
         self.field = field
@@ -153,6 +153,9 @@ class LatentOptimizer:
         self.obs_depth = put("depth", np.float64)
         self.obs_mask = put("depth_mask", np.uint8)
         self.obs_sil = put("silhouette", np.float64)
+        if grad_mode not in ("surrogate", "implicit"):
+            raise ValueError("grad_mode must be 'surrogate' or 'implicit'")
+        self.grad_mode = grad_mode
         self.adam_cfg = _lib.dist_adam_config(lr, 0.9, 0.999, 1e-8)
         self.iter = 0
         self.max_iters = max_iters
@@ -175,7 +178,8 @@ class LatentOptimizer:
                                     _lib.ptr(self.obs_sil), self.weights.depth,
                                     self.weights.silhouette, self.weights.latent,
                                     self.grad.data_ptr(), self.view_terms.data_ptr(),
-                                    self.shape_terms.data_ptr())
+                                    self.shape_terms.data_ptr(),
+                                    1 if self.grad_mode == "implicit" else 0, 0)
         c = _lib.config_struct(self.cfg)
         st = dt.state_struct()
         _lib.check(lib.dist_objective(h, self.code.data_ptr(), self.S, dt.cams.data_ptr(), self.V,
@@ -210,10 +214,15 @@ class LatentOptimizer:
 
 
 def completion_objective(field, code, observations, intr, pose, cfg: TraceConfig,
-                         weights: LossWeights):
-    """(total, terms, grad_code, n_converged, queries) of one iterate (optimize.py:102-138)."""
+                         weights: LossWeights, *, grad_mode: str = "surrogate"):
+    """(total, terms, grad_code, n_converged, queries) of one iterate (optimize.py:102-138).
+
+    grad_mode="implicit" (extension) replaces the reference's
+    frozen-sample depth surrogate gradient by -(df/dz)/(grad f . v)."""
     obs = _split_observations(observations)
     if "normal" in obs:
+        if grad_mode != "surrogate":
+            raise ValueError("implicit gradients are implemented for depth/silhouette terms")
         return _completion_objective_heads(field, code, obs, intr, pose, cfg, weights)
     H, W = intr.height, intr.width
     o = {}
@@ -224,7 +233,8 @@ def completion_objective(field, code, observations, intr, pose, cfg: TraceConfig
     if "silhouette" in obs:
         o["silhouette"] = obs["silhouette"].image
     code = np.asarray(code, dtype=np.float64)
-    opt = LatentOptimizer(field, [(intr, pose)], o, code.reshape(1, -1), cfg, weights, max_iters=1)
+    opt = LatentOptimizer(field, [(intr, pose)], o, code.reshape(1, -1), cfg, weights, max_iters=1,
+                          grad_mode=grad_mode)
     dt = opt.objective()
     vt = opt.view_terms.cpu().numpy()[0]
     stt = opt.shape_terms.cpu().numpy()[0]
