@@ -40,6 +40,7 @@ struct DecView {
   int kp[kMaxLayers + 1]; // padded input width of hidden layer l (GEMM K)
   // layer 0 in fp64: W0z [D][np0], W0p [3][np0], b0 [np0]
   const double *W0z, *W0p, *b0;
+  const float *W0pf;       // fp32 copy of W0p for the tensor-core prologue
   // hidden GEMM layers 1..L-2, [0] = fp64 copy, [1] = fp32 copy:
   // W [kp][np] (row-major, the reference's x@W layout), Wt [np][kp], bias [np]
   const void *W[2][kMaxLayers], *Wt[2][kMaxLayers], *bias[2][kMaxLayers];

@@ -216,6 +216,7 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
   const int n0 = v.np[0];
   size_t o_W0z = put(sizeof(double) * std::max(D, 1) * n0);
   size_t o_W0p = put(sizeof(double) * 3 * n0);
+  size_t o_W0pf = put(sizeof(float) * 3 * n0);
   size_t o_b0 = put(sizeof(double) * n0);
   {
     double *W0z = (double *)(host.data() + o_W0z);
@@ -225,6 +226,8 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
       for (int j = 0; j < dims[1]; ++j) W0z[(size_t)k * n0 + j] = W[0][(size_t)k * dims[1] + j];
     for (int a = 0; a < 3; ++a)
       for (int j = 0; j < dims[1]; ++j) W0p[(size_t)a * n0 + j] = W[0][(size_t)(D + a) * dims[1] + j];
+    float *W0pf = (float *)(host.data() + o_W0pf);
+    for (int i = 0; i < 3 * n0; ++i) W0pf[i] = (float)W0p[i];
     for (int j = 0; j < dims[1]; ++j) b0[j] = b[0][j];
   }
   size_t o_W[2][kMaxLayers] = {}, o_Wt[2][kMaxLayers] = {}, o_b[2][kMaxLayers] = {};
@@ -298,6 +301,7 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
   char *base = (char *)blob;
   v.W0z = (const double *)(base + o_W0z);
   v.W0p = (const double *)(base + o_W0p);
+  v.W0pf = (const float *)(base + o_W0pf);
   v.b0 = (const double *)(base + o_b0);
   for (int l = 1; l <= L - 2; ++l)
     for (int c = 0; c < 2; ++c) {

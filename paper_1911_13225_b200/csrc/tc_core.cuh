@@ -143,6 +143,44 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// Two 32-column TMEM loads in flight, one wait (the accumulator and the
+// correction accumulator of the same columns).
+__device__ __forceinline__ void tmem_ld32x2(uint32_t ta, uint32_t tb, float (&v)[32], float (&w)[32]) {
+  uint32_t r[32], s[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(ta));
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(s[0]), "=r"(s[1]), "=r"(s[2]), "=r"(s[3]), "=r"(s[4]), "=r"(s[5]), "=r"(s[6]),
+        "=r"(s[7]), "=r"(s[8]), "=r"(s[9]), "=r"(s[10]), "=r"(s[11]), "=r"(s[12]), "=r"(s[13]),
+        "=r"(s[14]), "=r"(s[15]), "=r"(s[16]), "=r"(s[17]), "=r"(s[18]), "=r"(s[19]),
+        "=r"(s[20]), "=r"(s[21]), "=r"(s[22]), "=r"(s[23]), "=r"(s[24]), "=r"(s[25]),
+        "=r"(s[26]), "=r"(s[27]), "=r"(s[28]), "=r"(s[29]), "=r"(s[30]), "=r"(s[31])
+      : "r"(tb));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    v[i] = __uint_as_float(r[i]);
+    w[i] = __uint_as_float(s[i]);
+  }
+}
+
+// 8 consecutive fp32 constants (32-byte aligned) through the read-only path
+__device__ __forceinline__ void ldg8(const float *p, float (&x)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4 *>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4 *>(p) + 1);
+  x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+  x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+}
+
 // byte offset of A[row][k] (bf16) inside one 64 KB hi/lo part
 __device__ __forceinline__ uint32_t a_off(int row, int k) {
   const int kb = k >> 6, kk = k & 63;
@@ -170,11 +208,22 @@ __device__ __forceinline__ void put8(char *smem, int row, int k0, const float (&
   uint32_t hi[4], lo[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    uint16_t h0, h1, l0, l1;
-    split2<F16>(x[2 * i], h0, l0);
-    split2<F16>(x[2 * i + 1], h1, l1);
-    hi[i] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-    lo[i] = (uint32_t)l0 | ((uint32_t)l1 << 16);
+    if constexpr (F16) {
+      uint16_t h0, h1, l0, l1;
+      split2<F16>(x[2 * i], h0, l0);
+      split2<F16>(x[2 * i + 1], h1, l1);
+      hi[i] = (uint32_t)h0 | ((uint32_t)h1 << 16);
+      lo[i] = (uint32_t)l0 | ((uint32_t)l1 << 16);
+    } else {
+      // one cvt.rn.bf16x2 per pair; bf16 -> f32 is a 16-bit shift
+      const __nv_bfloat162 h = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+      const uint32_t hu = *reinterpret_cast<const uint32_t *>(&h);
+      const float r0 = x[2 * i] - __uint_as_float(hu << 16);
+      const float r1 = x[2 * i + 1] - __uint_as_float(hu & 0xFFFF0000u);
+      const __nv_bfloat162 l = __floats2bfloat162_rn(r0, r1);
+      hi[i] = hu;
+      lo[i] = *reinterpret_cast<const uint32_t *>(&l);
+    }
   }
   const uint32_t off = a_off(row, k0);
   *reinterpret_cast<uint4 *>(smem + OFF_AHI + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);

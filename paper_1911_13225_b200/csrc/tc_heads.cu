@@ -176,28 +176,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       int s = -1;
       if (gi < nrows && !gen.point(gi, p, s)) s = -1;
       if (row_thread) m.shape[row] = s;
-      // ---- layer 0 (fp64 fold) + mask 0 ----
+      // ---- layer 0 (folded bias + p . W0p, fp32) + mask 0 ----
       {
         const double *c0 = P.c0 + (size_t)(s < 0 ? 0 : s) * n0;
+        const float px = (float)p[0], py = (float)p[1], pz = (float)p[2];
         uint32_t mk[4] = {0, 0, 0, 0};
         for (int nh = 0; nh < 2; ++nh) {
           const int cb = nh * 256 + half * 128 + sub * 64;
-#pragma unroll 1
+#pragma unroll 2
           for (int j = 0; j < 64; j += 8) {
-            float x[8];
+            float x[8], w0[8], w1[8], w2[8];
+            ldg8(P.dv.W0pf + cb + j, w0);
+            ldg8(P.dv.W0pf + n0 + cb + j, w1);
+            ldg8(P.dv.W0pf + 2 * n0 + cb + j, w2);
+            const double2 *cc = reinterpret_cast<const double2 *>(c0 + cb + j);
+            uint32_t bits = 0;
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int col = cb + j + e;
-              double v = 0.0;
-              if (s >= 0) {
-                v = c0[col];
-                v = fma(p[0], P.dv.W0p[col], v);
-                v = fma(p[1], P.dv.W0p[n0 + col], v);
-                v = fma(p[2], P.dv.W0p[2 * n0 + col], v);
-              }
-              x[e] = (float)(v > 0.0 ? v : 0.0);
-              if (v > 0.0) mk[nh * 2 + ((j + e) >> 5)] |= 1u << ((j + e) & 31);
+            for (int e = 0; e < 8; e += 2) {
+              const double2 cv = __ldg(cc + e / 2);
+              const float v0 = fmaf(pz, w2[e], fmaf(py, w1[e], fmaf(px, w0[e], (float)cv.x)));
+              const float v1 = fmaf(pz, w2[e + 1], fmaf(py, w1[e + 1], fmaf(px, w0[e + 1], (float)cv.y)));
+              const bool on0 = s >= 0 && v0 > 0.f, on1 = s >= 0 && v1 > 0.f;
+              x[e] = on0 ? v0 : 0.f;
+              x[e + 1] = on1 ? v1 : 0.f;
+              bits |= (on0 ? 1u : 0u) << e;
+              bits |= (on1 ? 1u : 0u) << (e + 1);
             }
+            mk[nh * 2 + (j >> 5)] |= bits << (j & 31);
             put8<false>(smem, row, cb + j, x);
           }
         }
@@ -225,14 +230,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             uint32_t bits = 0;
 #pragma unroll
             for (int g8 = 0; g8 < 4; ++g8) {
-              float x[8];
+              float x[8], bb[8], wo[8];
+              ldg8(bias + cb + c * 32 + g8 * 8, bb);
+              if (last) ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
-                const int col = cb + c * 32 + g8 * 8 + e;
-                const float y = v[g8 * 8 + e] + __ldg(bias + col);
+                const float y = v[g8 * 8 + e] + bb[e];
                 x[e] = y > 0.f ? y : 0.f;
                 bits |= (y > 0.f ? 1u : 0u) << (g8 * 8 + e);
-                if (last) head = fmaf(x[e], __ldg(P.w_out + col), head);
+                if (last) head = fmaf(x[e], wo[e], head);
               }
               if (!last) put8<false>(smem, row, cb + c * 32 + g8 * 8, x);
             }
@@ -270,14 +276,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         tmem_ld4(mask_addr(G), mk);
         for (int nh = 0; nh < 2; ++nh) {
           const int cb = nh * 256 + half * 128 + sub * 64;
-#pragma unroll 1
+#pragma unroll 2
           for (int j = 0; j < 64; j += 8) {
-            float x[8];
+            float x[8], wo[8];
+            ldg8(P.w_out + cb + j, wo);
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               const int jj = j + e;
               const bool on = (mk[nh * 2 + (jj >> 5)] >> (jj & 31)) & 1u;
-              x[e] = on ? gr * __ldg(P.w_out + cb + jj) : 0.f;
+              x[e] = on ? gr * wo[e] : 0.f;
             }
             put8<false>(smem, row, cb + j, x);
           }

@@ -231,12 +231,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
     // D columns [col, col+32) of this thread's lane (+ the correction accumulator)
     auto load_d = [&](int col, float (&v)[32]) {
-      tmem_ld32(tq + col, v);
       if (P.acc_mode) {
         float w2[32];
-        tmem_ld32(tq + 256 + col, w2);
+        tmem_ld32x2(tq + col, tq + 256 + col, v, w2);
 #pragma unroll
         for (int e = 0; e < 32; ++e) v[e] += w2[e];
+      } else {
+        tmem_ld32(tq + col, v);
       }
     };
     uint32_t layer = 0;
@@ -253,16 +254,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
       const int n0 = P.dv.np[0];
       const double *c0 = P.c0 + (size_t)(s < 0 ? 0 : s) * n0;
-      // layer-0 activation of column `col` (fp64 fold, rounded to fp32)
-      auto h0 = [&](int col) -> float {
-        double v = 0.0;
-        if (s >= 0) {
-          v = c0[col];
-          v = fma(p[0], P.dv.W0p[col], v);
-          v = fma(p[1], P.dv.W0p[n0 + col], v);
-          v = fma(p[2], P.dv.W0p[2 * n0 + col], v);
+      // layer-0 activations of 8 consecutive columns: folded bias c0 (fp64,
+      // rounded) + p . W0p in fp32 -- the bf16x3 split of the result carries
+      // ~17 bits, so fp32 here costs nothing and keeps the loads vectorised.
+      const float px = (float)p[0], py = (float)p[1], pz = (float)p[2];
+      auto h0x8 = [&](int col, float (&x)[8]) {
+        float w0[8], w1[8], w2[8];
+        ldg8(P.dv.W0pf + col, w0);
+        ldg8(P.dv.W0pf + n0 + col, w1);
+        ldg8(P.dv.W0pf + 2 * n0 + col, w2);
+        const double2 *cc = reinterpret_cast<const double2 *>(c0 + col);
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          const double2 cv = __ldg(cc + e / 2);
+          float v0 = fmaf(pz, w2[e], fmaf(py, w1[e], fmaf(px, w0[e], (float)cv.x)));
+          float v1 = fmaf(pz, w2[e + 1], fmaf(py, w1[e + 1], fmaf(px, w0[e + 1], (float)cv.y)));
+          x[e] = (s >= 0 && v0 > 0.f) ? v0 : 0.f;
+          x[e + 1] = (s >= 0 && v1 > 0.f) ? v1 : 0.f;
         }
-        return (float)(v > 0.0 ? v : 0.0);
       };
       // Row scale of the fp16 split: a power of two that puts the row max in
       // [2^14, 2^15) so hi and lo both stay normal (exact to undo).  bf16 has
@@ -285,17 +294,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if constexpr (F16) {
         float tmax = 0.f;
         for (int nh = 0; nh < 2; ++nh)
-#pragma unroll 4
-          for (int j = 0; j < 64; ++j) tmax = fmaxf(tmax, h0(nh * 256 + half * 128 + sub * 64 + j));
+#pragma unroll 1
+          for (int j = 0; j < 64; j += 8) {
+            float x[8];
+            h0x8(nh * 256 + half * 128 + sub * 64 + j, x);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) tmax = fmaxf(tmax, x[e]);
+          }
         row_scale(tmax, sc, rinv);
       }
       for (int nh = 0; nh < 2; ++nh) {
         const int cb = nh * 256 + half * 128 + sub * 64;
-#pragma unroll 1
+#pragma unroll 2
         for (int j = 0; j < 64; j += 8) {
           float x[8];
+          h0x8(cb + j, x);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] = h0(cb + j + e) * sc;
+          for (int e = 0; e < 8; ++e) x[e] *= sc;
           put8<F16>(smem, row, cb + j, x);
         }
       }
@@ -322,12 +337,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               float v[32];
               load_d(nh * 128 + sub * 64 + c * 32, v);
 #pragma unroll
-              for (int e = 0; e < 32; ++e) {
-                const int col = cb + c * 32 + e;
-                float y = fmaf(v[e], unscale, __ldg(bias + col));
-                y = y > 0.f ? y : 0.f;
-                if (last) head = fmaf(y, __ldg(P.w_out + col), head);
-                else tmax = fmaxf(tmax, y);
+              for (int g8 = 0; g8 < 4; ++g8) {
+                float bb[8], wo[8];
+                ldg8(bias + cb + c * 32 + g8 * 8, bb);
+                if (last) ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  float y = fmaf(v[g8 * 8 + e], unscale, bb[e]);
+                  y = y > 0.f ? y : 0.f;
+                  if (last) head = fmaf(y, wo[e], head);
+                  else tmax = fmaxf(tmax, y);
+                }
               }
             }
           }
@@ -343,11 +363,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               load_d(nh * 128 + sub * 64 + c * 32, v);
 #pragma unroll
               for (int g8 = 0; g8 < 4; ++g8) {
-                float x[8];
+                float x[8], bb[8];
+                ldg8(bias + cb + c * 32 + g8 * 8, bb);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                  const int col = cb + c * 32 + g8 * 8 + e;
-                  float y = fmaf(v[g8 * 8 + e], unscale, __ldg(bias + col));
+                  const float y = fmaf(v[g8 * 8 + e], unscale, bb[e]);
                   x[e] = (y > 0.f ? y : 0.f) * sc;
                 }
                 put8<F16>(smem, row, cb + c * 32 + g8 * 8, x);
