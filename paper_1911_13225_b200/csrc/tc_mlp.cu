@@ -47,6 +47,7 @@ struct Params {
   const float *winv;      // [L-2] inverse power-of-2 weight scales (fp16x3), 1 for bf16x3
   int n_gemm;             // hidden GEMM layers (L-2)
   int acc_mode;           // 0: one accumulator; 1: two (even/odd K blocks); 2: hi*hi | corrections
+  int debug;              // timing experiments: 1 = no epilogue math, 2 = no MMAs (results invalid)
 };
 
 // ---------------------------------------------------------------------------
@@ -195,8 +196,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               mbar_wait(&m.full[s], (it / STAGES) & 1);
               tc_fence_after();
               const uint32_t b_hi = smem_u32(smem + OFF_B + s * STAGE_BYTES), b_lo = b_hi + B_TILE;
+              if (P.acc_mode == 3 && P.debug != 2) {
+                // hi*hi of the whole stage into D, then the corrections into D2:
+                // two accumulator switches per stage instead of eight
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const uint32_t ak = kc * (ROWS * 128) + q * 32;
+                  mma_2sm<F16>(d, sdesc(a_hi + ak), sdesc(b_hi + q * 32), (kc | q) ? 1u : 0u);
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                  const uint32_t ak = kc * (ROWS * 128) + q * 32;
+                  mma_2sm<F16>(d + 256u, sdesc(a_hi + ak), sdesc(b_lo + q * 32), (kc | q) ? 1u : 0u);
+                  mma_2sm<F16>(d + 256u, sdesc(a_lo + ak), sdesc(b_hi + q * 32), 1u);
+                }
+              } else
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
+                if (P.debug == 2) break;
                 const uint32_t ak = kc * (ROWS * 128) + q * 32;
                 const uint64_t dah = sdesc(a_hi + ak), dal = sdesc(a_lo + ak);
                 const uint64_t dbh = sdesc(b_hi + q * 32), dbl = sdesc(b_lo + q * 32);
@@ -326,6 +343,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const bool last = (l == G - 1);
         const float *bias = P.bias + (size_t)l * KDIM;
         const float unscale = rinv * P.winv[l];   // exact: both are powers of two
+        if (P.debug == 1) {
+          tc_fence_before();
+          if (!last) {
+            epi_sync();
+            if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+          }
+          continue;
+        }
         // fp16: pass 1 finds the row max for the next scale (and the head on the
         // last layer); bf16 needs no scale, so one pass reads D and writes A.
         float tmax = 0.f;
@@ -540,7 +565,9 @@ static int launch_tc_t(const DecView &dv, const double *c0, const Rows &rows, in
   P.winv = P.w_out + tc::KDIM;
   {
     const char *am = getenv("DIST_TC_ACC");
-    P.acc_mode = am ? atoi(am) : 2;
+    P.acc_mode = am ? atoi(am) : 3;
+    const char *dbg = getenv("DIST_TC_DEBUG");
+    P.debug = dbg ? atoi(dbg) : 0;
   }
   const void *fn = (const void *)tc::k_tc_mlp<F16, Rows>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
