@@ -272,8 +272,22 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
   int rc = compact([ta, Kc] __device__(int64_t g) { return (bool)isfinite(ta[g * Kc]); }, n, L.h.rec,
                    L.h.counts + 0, L.bcount, sm);
   if (rc) return rc;
-  rc = compact([ta] __device__(int64_t q) { return (bool)isfinite(ta[q]); }, n * K, L.h.samp,
-               L.h.counts + 1, L.bcount, sm);
+  // Only samples that carry a seed enter the fused kernel: slot 0 of every
+  // recorded ray when a silhouette term is present, and every sample of a
+  // converged pixel with a valid depth observation (losses.py:60-75).  The
+  // others contribute neither loss nor gradient (~60% of K=3
+  // samples remain in the depth-only C3 objective).
+  const uint8_t *status = st->status;
+  const bool has_sil = io->obs_sil != nullptr;
+  const ObjIn inq = in;
+  rc = compact(
+      [ta, Kc, status, has_sil, inq] __device__(int64_t q) {
+        if (!isfinite(ta[q])) return false;
+        const int64_t g = q / Kc;
+        if (has_sil && q - g * Kc == 0) return true;
+        return status[g] == DIST_CONVERGED && depth_valid(inq, g);
+      },
+      n * K, L.h.samp, L.h.counts + 1, L.bcount, sm);
   if (rc) return rc;
   const int gi = (int)std::min<int64_t>(ceil_div(n * K, 256), (int64_t)sm_count() * 8);
   k_heads_index<<<std::max(gi, 1), 256, 0, sm>>>(L.h, K, V, WH);
