@@ -95,3 +95,25 @@ def test_c2_render_256_depth_normals_vs_oracle(st, prec):
         assert np.percentile(nd, 99) < 1e-4 and np.mean(nd > 1e-4) < 2e-3
     else:
         assert np.percentile(nd, 99) < 5e-4 and np.mean(nd > 1e-3) < 2e-3
+
+
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("bf16x3", 5e-3)])
+def test_depth_and_silhouette_objective_vs_oracle(st, prec, tol):
+    """The C4 loss (depth + silhouette hinge, losses.py:54-91) on the 8x512 decoder."""
+    g = load_golden("geo64.npz")
+    seed = int(g["seed"])
+    dec = orc.Decoder(orc.geometric_init(256, (512,) * 8, seed), 256)
+    cam = orc.Cam(64, 64, g["omega"], g["t"])
+    ocfg = orc.Cfg(k_samples=3)
+    T = orc.trace(lambda p: dec(p, g["z_true"]), cam, ocfg)
+    sil = orc.hard_mask(T).astype(np.float64)
+    tot_o, terms_o, g_o, n_o, q_o, _ = orc.objective(dec, g["code"], cam, ocfg, orc.Weights(),
+                                                     depth=g["obs_depth"], silhouette=sil)
+    net = st.NeuralField.geometric(256, (512,) * 8, seed, precision=prec)
+    obs = [st.Observation("depth", g["obs_depth"]), st.Observation("silhouette", sil)]
+    tot, terms, grad, n_conv, q = st.completion_objective(
+        net, g["code"], obs, st.Intrinsics(width=64, height=64), st.Pose(g["omega"], g["t"]),
+        st.TraceConfig(**cfg_from(g["cfg"])), st.LossWeights())
+    assert abs(terms["silhouette"] - terms_o["silhouette"]) < tol * max(abs(terms_o["silhouette"]), 1e-3)
+    assert abs(tot - tot_o) < tol * abs(tot_o)
+    assert np.linalg.norm(grad - g_o) / np.linalg.norm(g_o) < tol
