@@ -196,7 +196,8 @@ def main():
 
     # ---- timed region: device-resident iterates -----------------------------
     q0 = torch.zeros(1, dtype=torch.int64, device="cuda")
-    tr_ev = []
+    s0 = torch.zeros((), dtype=torch.int64, device="cuda")
+    tr_ev, obj_ev = [], []
     n0 = _lib.lib().dist_launch_count()
     if world > 1:
         dist.barrier()
@@ -215,7 +216,11 @@ def main():
             q0 += dt.stats_dev[0]
             tr_ev.append((a, b))
             # the rest of the iterate (heads + fused backward + reduce + Adam) on the same trace
+            c = torch.cuda.Event(enable_timing=True)
             opt._objective_after_trace(dt)
+            c.record(stream)
+            obj_ev.append((b, c))
+            s0 += opt.head_counts[1].to(torch.int64)
             allreduce(opt.grad, opt.shape_terms)
             opt._adam()
         e1.record(stream)
@@ -227,7 +232,9 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     trace_ms = float(np.mean([a.elapsed_time(b) for a, b in tr_ev]))
+    obj_ms = float(np.mean([a.elapsed_time(b) for a, b in obj_ev]))
     queries = int(q0.item()) / args.steps
+    samples = int(s0.item()) / args.steps
     rays_per_step = VIEWS_PER_RANK * RES * RES * world
     value = rays_per_step / (ms * 1e-3)
 
@@ -282,7 +289,12 @@ def main():
                      "kernel": "march step kernels (decoder + update), whole trace phase",
                      "peak_source": f"{peak_kind} bf16 sustained (MEASURED_PEAKS.json)",
                      "algorithmic_flop_per_query": F_Q, "queries_per_step": queries,
-                     "trace_ms_per_step": trace_ms},
+                     "trace_ms_per_step": trace_ms,
+                     "objective_ms_per_step": obj_ms,
+                     "head_samples_per_step": samples,
+                     "objective_achieved_tflops": samples * (F_Q + F_B) / (obj_ms * 1e-3) / 1e12,
+                     "objective_note": "heads + seeds + fused tcgen05 backward + reductions "
+                                       "(k_tc_heads dominates; its ncu capture is in profiles/)"},
     }
     if rank == 0 and not args.no_cpu_baseline:
         v, info = cpu_reference_sample()
@@ -291,6 +303,7 @@ def main():
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
+        dist.barrier()          # the other ranks wait for rank 0's CPU-baseline leg
         dist.destroy_process_group()
     return 0
 

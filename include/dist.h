@@ -163,6 +163,7 @@ typedef struct dist_objective_io {
   int32_t grad_mode;             /* 0: the reference's frozen-sample surrogate (shading.py:9-11);
                                     1: implicit gradient -(df/dz)/(grad f . v) at converged pixels */
   int32_t reserved;
+  int32_t *counts_out;           /* optional out [2]: recorded rays, seeded head samples (device) */
 } dist_objective_io;
 
 DIST_API size_t dist_objective_workspace_size(const dist_decoder *dec, int n_views, int width,

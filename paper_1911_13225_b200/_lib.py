@@ -46,7 +46,8 @@ class dist_objective_io(C.Structure):
     _fields_ = [("obs_depth", C.c_void_p), ("obs_depth_mask", C.c_void_p),
                 ("obs_sil", C.c_void_p), ("w_depth", C.c_double), ("w_sil", C.c_double),
                 ("w_latent", C.c_double), ("grad", C.c_void_p), ("view_terms", C.c_void_p),
-                ("shape_terms", C.c_void_p), ("grad_mode", C.c_int32), ("reserved", C.c_int32)]
+                ("shape_terms", C.c_void_p), ("grad_mode", C.c_int32), ("reserved", C.c_int32),
+                ("counts_out", C.c_void_p)]
 
 
 class dist_adam_config(C.Structure):

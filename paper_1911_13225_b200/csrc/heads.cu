@@ -327,6 +327,10 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
     rc = reduce_code_grad(dv, s1, grid, L.part0, L.parts, L.col0, L.cols, io->grad, sm);
     if (rc) return rc;
   }
+  if (io->counts_out) {
+    e = cudaMemcpyAsync(io->counts_out, L.h.counts, 2 * sizeof(int32_t), cudaMemcpyDeviceToDevice, sm);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemcpyAsync(counts)");
+  }
   k_shape_finish<<<s1, 256, 0, sm>>>(cams, V, s1, dv.latent_dim, codes, io->view_terms, in, io->grad,
                                       io->shape_terms);
   DIST_CHECK_LAUNCH("k_shape_finish");

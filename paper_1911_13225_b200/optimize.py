@@ -135,6 +135,7 @@ class LatentOptimizer:
         self.grad = torch.zeros_like(self.code)
         self.view_terms = torch.zeros((V, 4), dtype=torch.float64, device=dev)
         self.shape_terms = torch.zeros((self.S, 2), dtype=torch.float64, device=dev)
+        self.head_counts = torch.zeros(2, dtype=torch.int32, device=dev)  # recorded rays, seeded samples
         n = V * self.W * self.H
 
         def put(key, dtype):
@@ -179,7 +180,8 @@ class LatentOptimizer:
                                     self.weights.silhouette, self.weights.latent,
                                     self.grad.data_ptr(), self.view_terms.data_ptr(),
                                     self.shape_terms.data_ptr(),
-                                    1 if self.grad_mode == "implicit" else 0, 0)
+                                    1 if self.grad_mode == "implicit" else 0, 0,
+                                    self.head_counts.data_ptr())
         c = _lib.config_struct(self.cfg)
         st = dt.state_struct()
         _lib.check(lib.dist_objective(h, self.code.data_ptr(), self.S, dt.cams.data_ptr(), self.V,
