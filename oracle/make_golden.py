@@ -155,9 +155,35 @@ def geo(res_px=64, seed=0, name="geo64", normals=True):
     print(name, res.total_queries, int((res.state.status == 1).sum()), total)
 
 
+def pose():
+    """Pose objective + recovery (optimize.py:185-266) on the tiny net at 32^2."""
+    from sdftrace.optimize import pose_objective, recover_pose
+    rng = np.random.default_rng(7)
+    net = st.NeuralField.init(latent_dim=2, hidden=(16, 16), rng=rng)
+    code = rng.normal(0.0, 0.3, 2)
+    intr = st.Intrinsics(width=32, height=32)
+    pose = st.look_at((0.3, 0.2, -2.0))
+    cfg = st.TraceConfig(alpha=1.0, k_samples=1, coarse_start_scale=1)
+    res = st.trace(net, code, intr, pose, cfg)
+    obs = [st.Observation("depth", st.depth_map(res)),
+           st.Observation("silhouette", st.hard_mask(res).astype(np.float64))]
+    params = pose.params() + np.array([0.01, -0.02, 0.015, 0.02, -0.01, 0.03])
+    total, terms, g, q = pose_objective(net, code, obs, intr, params, cfg, st.LossWeights())
+    p0 = st.Pose.from_params(params)
+    best, rep = recover_pose(net, code, obs, intr, p0, iters=5, cfg=cfg, lr_decay_every=2)
+    out = _pack_weights(net.weights)
+    out.update(code=code, true_params=pose.params(), params=params, obs_depth=obs[0].image,
+               obs_sil=obs[1].image, total=total, grad=g, queries=np.int64(q),
+               rp_best=best.params(), rp_losses=np.asarray(rep.losses),
+               rp_best_iter=np.int64(rep.best_iter))
+    np.savez_compressed(os.path.join(OUT, "pose32.npz"), **out)
+    print("pose", total, g)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     warnings.simplefilter("ignore")
+    pose()
     ladder()
     tiny()
     geo(64, 0, "geo64")

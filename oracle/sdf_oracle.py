@@ -641,3 +641,71 @@ def min_steps(d, alpha, theta, eps):
     """Eq. 9 bound (tracer.py:258-273) -- used only by oracle self-tests."""
     r = abs(1.0 - alpha * math.sin(theta))
     return max(1, math.ceil((math.log(eps) - math.log(d)) / math.log(r)))
+
+
+# --------------------------------------------------------------------------
+# camera pose gradient and recovery (SURVEY 8f row f2; camera.py:85-103,
+# 215-278; optimize.py:185-266)
+# --------------------------------------------------------------------------
+
+def _hat(w):
+    return np.array([[0.0, -w[2], w[1]], [w[2], 0.0, -w[0]], [-w[1], w[0], 0.0]])
+
+
+def rotation_partials(omega):
+    """R and dR/d omega_i of the exponential map (camera.py:85-103)."""
+    w = np.asarray(omega, dtype=np.float64)
+    R = rodrigues(w)
+    t2 = float(w @ w)
+    if t2 < 1e-16:
+        return R, [_hat(e) for e in np.eye(3)]
+    I = np.eye(3)
+    return R, [_hat((w[i] * w + np.cross(w, (I - R) @ I[:, i])) / t2) @ R for i in range(3)]
+
+
+def pose_grad(cam: Cam, pixels, dist, grads, level=1):
+    """Chain dL/dp_m into (dL/d omega, dL/d t) with frozen distances (camera.py:255-278)."""
+    g = np.atleast_2d(np.asarray(grads, dtype=np.float64))
+    d = np.asarray(dist, dtype=np.float64).reshape(-1)
+    px = np.asarray(pixels, dtype=np.float64)
+    cx, cy = cam.width / 2.0, cam.height / 2.0
+    u = np.stack([((px[:, 0] + 0.5) * level - cx) / cam.fx,
+                  ((px[:, 1] + 0.5) * level - cy) / cam.fx, np.ones(len(px))], axis=1)
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    R, dR = rotation_partials(cam.omega)
+    gs = g.sum(axis=0)
+    gw = np.array([gs @ (-(dRi.T @ cam.t)) + np.einsum("m,mk,mk->", d, g, u @ dRi) for dRi in dR])
+    return gw, -(R @ gs)
+
+
+def pose_objective(dec: Decoder, code, cam: Cam, cfg: Cfg, w: Weights, depth=None, silhouette=None):
+    """Loss and 6-vector gradient of one pose iterate (optimize.py:185-233)."""
+    fn = lambda p: dec(p, code)  # noqa: E731
+    T = trace(fn, cam, cfg)
+    H = heads(T, fn, cfg)
+    terms, ds, ss, gimg = {}, None, None, None
+    if depth is not None:
+        l, s = depth_loss(H, depth, np.isfinite(depth))
+        terms["depth"] = l
+        ds = w.depth * s
+    if silhouette is not None:
+        l, gimg = silhouette_loss(soft_silhouette(T, cfg), silhouette)
+        terms["silhouette"] = l
+        ss = w.silhouette * gimg[H.pixels[:, 1], H.pixels[:, 0]]
+    b = heads_backward(H, dec, code, cfg, ds, ss)
+    pix, dist, pg = H.pixels[H.sample_pixel], H.sample_d, b["sample_point_grads"]
+    if gimg is not None:
+        miss = np.nonzero(~np.isfinite(T.tk_a[:, 0]))[0]
+        if miss.size:
+            sd = w.silhouette * gimg[T.rays.pixels[miss, 1], T.rays.pixels[miss, 0]]
+            dirs = T.rays.dirs[miss]
+            dstar = -(dirs @ T.rays.origin)
+            pstar = T.rays.origin + dstar[:, None] * dirs
+            nrm = np.linalg.norm(pstar, axis=1, keepdims=True)
+            gm = sd[:, None] * np.divide(pstar, nrm, out=np.zeros_like(pstar), where=nrm > 0)
+            pix = np.concatenate([pix, T.rays.pixels[miss]])
+            dist = np.concatenate([dist, dstar])
+            pg = np.concatenate([pg, gm])
+    gw, gt = pose_grad(cam, pix, dist, pg)
+    total = w.depth * terms.get("depth", 0.0) + w.silhouette * terms.get("silhouette", 0.0)
+    return total, terms, np.concatenate([gw, gt]), T.total_queries

@@ -7,12 +7,12 @@ include/dist.h).  There is no CPU fallback.
 """
 
 from .camera import Intrinsics, Pose, RayBundle, generate_rays, log_rotation, look_at, \
-    rotation_matrix
+    pose_gradient, rotation_derivatives, rotation_matrix
 from .fields import NeuralField, eval_field
 from .losses import LossWeights, Observation, depth_loss, latent_reg, normal_loss, \
     silhouette_loss
 from .optimize import AdamState, LatentOptimizer, OptimizationError, OptimizeReport, adam_step, \
-    complete_shape, completion_objective
+    complete_shape, completion_objective, pose_objective, recover_pose
 from .shading import HeadBundle, RenderMaps, depth_map, diff_heads, hard_mask, normal_map, \
     ray_distance, render, soft_silhouette, surface_points
 from .tracer import CONVERGED, ESCAPED, EXHAUSTED, MARCHING, DeviceTrace, RayState, TraceConfig, \

@@ -332,3 +332,79 @@ def complete_shape(field, observations, intr, pose, code0=None, iters: int = 100
     report.skipped_steps = int(opt.skipped[0].item())
     report.elapsed = time.perf_counter() - t0
     return opt.best_code[0].cpu().numpy(), report
+
+
+# === pose recovery (optimize.py:185-266) ======================
+
+def pose_objective(field, code, observations, intr, params, cfg: TraceConfig,
+                   weights: LossWeights):
+    """Loss and 6-vector pose gradient of one iterate with frozen distances
+    (optimize.py:185-233).  Trace and the taped backward to the sample points
+    run on the GPU; the 6-parameter chain rule is camera.pose_gradient."""
+    from .camera import Pose, pose_gradient
+    from .losses import depth_loss, silhouette_loss
+    from .shading import diff_heads, soft_silhouette
+    from .tracer import trace
+    pose = Pose.from_params(params)
+    obs = _split_observations(observations)
+    result = trace(field, code, intr, pose, cfg)
+    heads = diff_heads(result, field, code)
+    terms = {}
+    ds = ss = gimg = None
+    if "depth" in obs:
+        l, s = depth_loss(heads, obs["depth"])
+        terms["depth"] = l
+        ds = weights.depth * s
+    if "silhouette" in obs:
+        l, gimg = silhouette_loss(soft_silhouette(result), obs["silhouette"].image)
+        terms["silhouette"] = l
+        ss = weights.silhouette * gimg[heads.pixels[:, 1], heads.pixels[:, 0]]
+    grads = heads.backward(depth_seed=ds, sil_seed=ss)
+    pix, dist, pg = heads.pixels[heads.sample_pixel], heads.sample_d, grads["sample_point_grads"]
+    if gimg is not None:
+        st = result.state
+        miss = np.nonzero(~np.isfinite(st.topk_absf[:, 0]))[0]
+        if miss.size:
+            sd = weights.silhouette * gimg[st.bundle.pixels[miss, 1], st.bundle.pixels[miss, 0]]
+            dirs = st.bundle.dirs[miss]
+            c = st.bundle.origin
+            dstar = -(dirs @ c)
+            pstar = c + dstar[:, None] * dirs
+            nrm = np.linalg.norm(pstar, axis=1, keepdims=True)
+            gm = sd[:, None] * np.divide(pstar, nrm, out=np.zeros_like(pstar), where=nrm > 0)
+            pix = np.concatenate([pix, st.bundle.pixels[miss]])
+            dist = np.concatenate([dist, dstar])
+            pg = np.concatenate([pg, gm])
+    gw, gt = pose_gradient(intr, pose, pix, dist, pg)
+    total = weights.depth * terms.get("depth", 0.0) + weights.silhouette * terms.get("silhouette", 0.0)
+    return total, terms, np.concatenate([gw, gt]), result.total_queries
+
+
+def recover_pose(field, code, observations, intr, pose0, iters: int = 200,
+                 cfg: TraceConfig | None = None, weights: LossWeights | None = None,
+                 lr: float = 1e-2, lr_decay: float = 0.5, lr_decay_every: int = 50):
+    """Recover the 6 pose parameters (optimize.py:236-266): Adam on the device
+    with the stepped learning-rate decay, best-loss iterate returned."""
+    from .camera import Pose
+    cfg = cfg or TraceConfig()
+    weights = weights or LossWeights()
+    params = pose0.params()
+    report = OptimizeReport()
+    adam = AdamState(lr=lr)
+    best = params.copy()
+    t0 = time.perf_counter()
+    for it in range(iters):
+        total, terms, g, queries = pose_objective(field, code, observations, intr, params, cfg,
+                                                  weights)
+        report.total_queries += queries
+        report.record(total, terms, float(np.linalg.norm(g)))
+        if total < report.best_loss:
+            report.best_loss = total
+            report.best_iter = it
+            best = params.copy()
+        params = adam_step(adam, params, g)
+        if lr_decay_every and (it + 1) % lr_decay_every == 0:
+            adam.lr *= lr_decay
+    report.skipped_steps = adam.skipped
+    report.elapsed = time.perf_counter() - t0
+    return Pose.from_params(best), report

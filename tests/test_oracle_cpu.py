@@ -162,3 +162,16 @@ def test_neural_init_matches_reference_recipe():
     geo = st.NeuralField.geometric(256, (512,) * 8, 0)
     ref = orc.geometric_init(256, (512,) * 8, 0)
     assert all(np.array_equal(a[0], b[0]) for a, b in zip(geo.weights, ref))
+
+
+def test_oracle_pose_objective_vs_reference():
+    g = load_golden("pose32.npz")
+    dec = orc.Decoder(golden_weights(g), 2)
+    p = g["params"]
+    cam = orc.Cam(32, 32, p[:3], p[3:])
+    cfg = orc.Cfg(alpha=1.0, k_samples=1, coarse_start_scale=1)
+    tot, terms, grad, q = orc.pose_objective(dec, g["code"], cam, cfg, orc.Weights(),
+                                             depth=g["obs_depth"], silhouette=g["obs_sil"])
+    assert q == int(g["queries"])
+    assert abs(tot - float(g["total"])) < 1e-14
+    np.testing.assert_allclose(grad, g["grad"], rtol=1e-10, atol=1e-13)
