@@ -180,9 +180,24 @@ def pose():
     print("pose", total, g)
 
 
+def formats():
+    """Files written by the reference (fields.py:444-459, camera.py:284-312, imageio.py)."""
+    rng = np.random.default_rng(7)
+    net = st.NeuralField.init(latent_dim=2, hidden=(16, 16), rng=rng)
+    code = rng.normal(0.0, 0.3, 2)
+    intr = st.Intrinsics(width=32, height=24, cx=15.5, cy=12.25)
+    pose = st.look_at((0.3, 0.2, -2.0))
+    st.save_field(net, os.path.join(OUT, "ref_field.json"), codes=code[None, :])
+    st.save_camera(intr, pose, os.path.join(OUT, "ref_camera.json"))
+    res = st.trace(net, code, st.Intrinsics(width=32, height=32), pose, st.TraceConfig())
+    st.write_pfm(os.path.join(OUT, "ref_depth.pfm"), st.depth_map(res))
+    st.write_pgm(os.path.join(OUT, "ref_mask.pgm"), st.hard_mask(res))
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     warnings.simplefilter("ignore")
+    formats()
     pose()
     ladder()
     tiny()

@@ -9,6 +9,8 @@ include/dist.h).  There is no CPU fallback.
 from .camera import Intrinsics, Pose, RayBundle, generate_rays, log_rotation, look_at, \
     pose_gradient, rotation_derivatives, rotation_matrix
 from .fields import NeuralField, eval_field
+from .formats import load_camera, load_field, read_pfm, read_pgm, save_camera, save_field, \
+    write_pfm, write_pgm
 from .losses import LossWeights, Observation, depth_loss, latent_reg, normal_loss, \
     silhouette_loss
 from .optimize import AdamState, LatentOptimizer, OptimizationError, OptimizeReport, adam_step, \

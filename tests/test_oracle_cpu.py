@@ -175,3 +175,30 @@ def test_oracle_pose_objective_vs_reference():
     assert q == int(g["queries"])
     assert abs(tot - float(g["total"])) < 1e-14
     np.testing.assert_allclose(grad, g["grad"], rtol=1e-10, atol=1e-13)
+
+
+def test_formats_roundtrip_with_reference_files(tmp_path):
+    """files written by the reference load here and are re-written
+    byte-identically (field/camera JSON, PFM depth, PGM mask)."""
+    from conftest import GOLDEN
+    from paper_1911_13225_b200 import formats as fm
+    g = load_golden("tiny64.npz")
+    f, codes = fm.load_field(os.path.join(GOLDEN, "ref_field.json"))
+    for (W, b), (Wg, bg) in zip(f.weights, golden_weights(g)):
+        assert np.array_equal(W, Wg) and np.array_equal(b, bg)
+    fm.save_field(f, tmp_path / "f.json", codes=codes)
+    assert open(tmp_path / "f.json").read() == open(os.path.join(GOLDEN, "ref_field.json")).read()
+    intr, pose = fm.load_camera(os.path.join(GOLDEN, "ref_camera.json"))
+    fm.save_camera(intr, pose, tmp_path / "c.json")
+    import json
+    a = json.load(open(tmp_path / "c.json"))
+    b = json.load(open(os.path.join(GOLDEN, "ref_camera.json")))
+    assert a["resolution"] == b["resolution"] and a["principal"] == b["principal"]
+    # log/exp of the rotation round-trips to ~1e-11 in the reference as well (camera.py:135-151)
+    np.testing.assert_allclose(a["extrinsic"], b["extrinsic"], rtol=0, atol=1e-10)
+    d = fm.read_pfm(os.path.join(GOLDEN, "ref_depth.pfm"))
+    fm.write_pfm(tmp_path / "d.pfm", d)
+    assert open(tmp_path / "d.pfm", "rb").read() == open(os.path.join(GOLDEN, "ref_depth.pfm"), "rb").read()
+    m = fm.read_pgm(os.path.join(GOLDEN, "ref_mask.pgm"))
+    fm.write_pgm(tmp_path / "m.pgm", m.astype(bool))
+    assert open(tmp_path / "m.pgm", "rb").read() == open(os.path.join(GOLDEN, "ref_mask.pgm"), "rb").read()
