@@ -177,6 +177,18 @@ DIST_API int dist_objective(const dist_decoder *dec, const double *codes_dev, in
                             const dist_trace_config *cfg, const dist_ray_state *st,
                             const dist_objective_io *io, void *ws, size_t ws_bytes, void *stream);
 
+/* ---- photometric consistency (losses.py:128-222) ------- */
+/* cams_dev[0] = view i, cams_dev[1] = view j.  Images are row-major doubles
+ * (depth: +inf background).  Outputs: loss_dev[2] = {mean |r| over visible
+ * pixels, n visible}, dz_dev[H*W] = d loss / d z_i, vis_dev[H*W] = visibility
+ * of i's pixels in j (visibility_mask, losses.py:159-183). */
+DIST_API size_t dist_photometric_workspace_size(int height, int width);
+DIST_API int dist_photometric(const dist_camera *cams_dev, int height, int width, int height_j,
+                              int width_j, const double *z_i, const double *gray_i,
+                              const double *gray_j, const double *z_j, double thresh,
+                              double *loss_dev, double *dz_dev, uint8_t *vis_dev, void *ws,
+                              size_t ws_bytes, void *stream);
+
 /* ---- Adam (AdamState/adam_step, optimize.py:35-63) ------------------------ */
 typedef struct dist_adam_config {
   double lr, beta1, beta2, eps;

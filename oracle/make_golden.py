@@ -194,9 +194,45 @@ def formats():
     st.write_pgm(os.path.join(OUT, "ref_mask.pgm"), st.hard_mask(res))
 
 
+def multiview():
+    """Photometric warp + reconstruct_multiview (losses.py:120-222, optimize.py:272-358)
+    on the tiny net with textured views (test_optimize.py:25-38 pattern)."""
+    from sdftrace.losses import photometric_loss, visibility_mask
+    from sdftrace.optimize import reconstruct_multiview
+    rng = np.random.default_rng(7)
+    net = st.NeuralField.init(latent_dim=2, hidden=(16, 16), rng=rng)
+    code = rng.normal(0.0, 0.3, 2)
+    intr = st.Intrinsics(width=24, height=24)
+    cfg = st.TraceConfig(alpha=1.0, k_samples=1, coarse_start_scale=1)
+    eyes = [(2.0 * np.sin(a), 0.3 * np.cos(2 * a), -2.0 * np.cos(a)) for a in (0.0, 0.3, 0.6)]
+    poses = [st.look_at(e) for e in eyes]
+    images, depths = [], []
+    for p in poses:
+        res = st.trace(net, code, intr, p, cfg)
+        pts, idx = st.surface_points(res)
+        img = np.zeros((24, 24))
+        b = res.state.bundle
+        img[b.pixels[idx, 1], b.pixels[idx, 0]] = 0.5 + 0.25 * np.sin(7.0 * pts[:, 0]) * \
+            np.cos(6.0 * pts[:, 1]) + 0.2 * np.sin(5.0 * pts[:, 2])
+        images.append(img)
+        depths.append(st.depth_map(res))
+    l, dz = photometric_loss(depths[0], images[0], intr, poses[0], images[1], intr, poses[1],
+                             depths[1])
+    vis = visibility_mask(depths[0], intr, poses[0], depths[1], intr, poses[1])
+    best, rep = reconstruct_multiview(net, images, [(intr, p) for p in poses],
+                                      code0=code + 0.1, iters=3, views_per_iter=2, cfg=cfg, seed=1)
+    out = _pack_weights(net.weights)
+    out.update(code=code, eyes=np.asarray(eyes), images=np.stack(images), depths=np.stack(depths),
+               ph_loss=l, ph_dz=dz, ph_vis=vis, mv_best=best, mv_losses=np.asarray(rep.losses),
+               mv_best_iter=np.int64(rep.best_iter))
+    np.savez_compressed(os.path.join(OUT, "multiview24.npz"), **out)
+    print("multiview", l, int(vis.sum()), rep.losses)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     warnings.simplefilter("ignore")
+    multiview()
     formats()
     pose()
     ladder()

@@ -89,3 +89,68 @@ def latent_reg(code):
     """|z|^2 and its gradient (losses.py:114-117)."""
     z = np.asarray(code, dtype=np.float64)
     return float(z @ z), 2.0 * z
+
+
+# === photometric consistency (SURVEY 8f row f1; losses.py:120-222) ============
+
+def to_gray(img):
+    """Channel mean of a colour image (losses.py:123-125)."""
+    img = np.asarray(img, dtype=np.float64)
+    return img.mean(axis=2) if img.ndim == 3 else img
+
+
+def bilinear_sample(img, u, v):
+    """Pixel-centre bilinear sample with border clamping, plus d/du and d/dv
+    (losses.py:128-150).  Host utility; the warp itself runs on the device."""
+    h, w = img.shape
+    xs = np.clip(u - 0.5, 0.0, w - 1.0)
+    ys = np.clip(v - 0.5, 0.0, h - 1.0)
+    x0 = np.clip(np.floor(xs).astype(np.int64), 0, w - 2) if w > 1 else np.zeros_like(xs, np.int64)
+    y0 = np.clip(np.floor(ys).astype(np.int64), 0, h - 2) if h > 1 else np.zeros_like(ys, np.int64)
+    x1, y1 = np.minimum(x0 + 1, w - 1), np.minimum(y0 + 1, h - 1)
+    fx, fy = xs - x0, ys - y0
+    a, b, c, d = img[y0, x0], img[y0, x1], img[y1, x0], img[y1, x1]
+    val = (a * (1 - fx) + b * fx) * (1 - fy) + (c * (1 - fx) + d * fx) * fy
+    return val, (b - a) * (1 - fy) + (d - c) * fy, (c - a) * (1 - fx) + (d - b) * fx
+
+
+def _photometric_device(z_i, gray_i, intr_i, pose_i, gray_j, intr_j, pose_j, z_j, thresh):
+    import torch
+
+    from . import _lib
+    from .camera import camera_struct
+    _lib.require_device()
+    z_i = np.asarray(z_i, dtype=np.float64)
+    h, w = z_i.shape
+    hj, wj = np.asarray(z_j).shape
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()  # noqa: E731
+    cams = _lib.cameras_to_device([camera_struct(intr_i, pose_i), camera_struct(intr_j, pose_j)])
+    zi, gi, gj, zj = dev(z_i), dev(gray_i), dev(gray_j), dev(z_j)
+    loss = torch.zeros(2, dtype=torch.float64, device="cuda")
+    dz = torch.empty(h * w, dtype=torch.float64, device="cuda")
+    vis = torch.empty(h * w, dtype=torch.uint8, device="cuda")
+    lib = _lib.lib()
+    ws = _lib.workspace(lib.dist_photometric_workspace_size(h, w))
+    _lib.check(lib.dist_photometric(cams.data_ptr(), h, w, hj, wj, zi.data_ptr(), gi.data_ptr(),
+                                    gj.data_ptr(), zj.data_ptr(), float(thresh), loss.data_ptr(),
+                                    dz.data_ptr(), vis.data_ptr(), ws.data_ptr(), ws.numel(),
+                                    _lib.stream_ptr()))
+    lv = loss.cpu().numpy()
+    return float(lv[0]), dz.cpu().numpy().reshape(h, w), vis.cpu().numpy().reshape(h, w).astype(bool)
+
+
+def visibility_mask(z_i, intr_i, pose_i, z_j, intr_j, pose_j, thresh: float = 0.001):
+    """Pixels of view i whose surface point view j also sees (losses.py:159-183)."""
+    zeros = np.zeros_like(np.asarray(z_i, dtype=np.float64))
+    zj = np.asarray(z_j, dtype=np.float64)
+    return _photometric_device(z_i, zeros, intr_i, pose_i, np.zeros_like(zj), intr_j, pose_j,
+                               zj, thresh)[2]
+
+
+def photometric_loss(z_i, gray_i, intr_i, pose_i, gray_j, intr_j, pose_j, z_j,
+                     thresh: float = 0.001):
+    """Mean L1 between view i and view j warped through i's depth, and dL/dz_i
+    (losses.py:186-222), computed by the dist_photometric kernels."""
+    loss, dz, _ = _photometric_device(z_i, gray_i, intr_i, pose_i, gray_j, intr_j, pose_j, z_j,
+                                      thresh)
+    return loss, dz

@@ -408,3 +408,87 @@ def recover_pose(field, code, observations, intr, pose0, iters: int = 200,
     report.skipped_steps = adam.skipped
     report.elapsed = time.perf_counter() - t0
     return Pose.from_params(best), report
+
+
+# === multi-view photometric reconstruction (optimize.py:272-358) ===
+
+def _nearest_view(centers):
+    unit = centers / np.linalg.norm(centers, axis=1, keepdims=True)
+    cosine = unit @ unit.T
+    np.fill_diagonal(cosine, -np.inf)
+    return cosine.argmax(axis=1)
+
+
+def reconstruct_multiview(field, images, cameras, code0=None, iters: int = 60,
+                          views_per_iter: int = 8, cfg: TraceConfig | None = None,
+                          weights: LossWeights | None = None, lr: float = 1e-2, seed: int = 0):
+    """Recover a latent code from posed colour views by photometric warping
+    (optimize.py:272-358): each iterate traces the sampled views and their
+    nearest neighbours, warps every sampled view into its neighbour
+    (dist_photometric), seeds the best sample of each converged pixel with
+    w_photo * dL/dz * scale, and back-propagates on the GPU."""
+    import warnings as _w
+
+    from .losses import latent_reg, photometric_loss, to_gray
+    from .shading import diff_heads
+    from .tracer import trace
+    if len(images) < 2:
+        raise ValueError("multi-view reconstruction needs at least two views")
+    if len(images) != len(cameras):
+        raise ValueError("images and cameras must align")
+    cams = [tuple(c) for c in cameras]
+    cfg = cfg or TraceConfig(k_samples=1)
+    weights = weights or LossWeights()
+    rng = np.random.default_rng(seed)
+    code = rng.normal(0.0, 0.1, field.latent_dim) if code0 is None else \
+        np.asarray(code0, dtype=np.float64).copy()
+    grays = [to_gray(im) for im in images]
+    neighbor = _nearest_view(np.stack([c[1].center() for c in cams], axis=0))
+    n_views = len(images)
+    report = OptimizeReport()
+    adam = AdamState(lr=lr)
+    best_code = code.copy()
+    t0 = time.perf_counter()
+    for it in range(iters):
+        sel = rng.choice(n_views, size=min(views_per_iter, n_views), replace=False)
+        needed = sorted(set(sel) | {neighbor[i] for i in sel})
+        heads_by, z_by, queries = {}, {}, 0
+        for i in needed:
+            intr, pose = cams[i]
+            res = trace(field, code, intr, pose, cfg)
+            h = diff_heads(res, field, code)
+            heads_by[i] = h
+            z_by[i] = h.depth_image(intr.height, intr.width)
+            queries += res.total_queries
+        g = np.zeros_like(code)
+        photo = 0.0
+        for i in sel:
+            j = int(neighbor[i])
+            l, dz = photometric_loss(z_by[i], grays[i], cams[i][0], cams[i][1], grays[j],
+                                     cams[j][0], cams[j][1], z_by[j])
+            photo += l
+            h = heads_by[i]
+            rows = h._conv_rows
+            if rows.size:
+                seeds = np.zeros(h.sample_d.shape[0])
+                px = h.pixels[rows]
+                seeds[h.best_sample[rows]] = weights.photometric * dz[px[:, 1], px[:, 0]] * h.scale[rows]
+                hg = h.backward(depth_seed=seeds)
+                if "code" in hg:
+                    g += hg["code"]
+        reg, reg_grad = latent_reg(code)
+        g += weights.latent * reg_grad
+        total = weights.photometric * photo + weights.latent * reg
+        report.total_queries += queries
+        report.record(total, {"photometric": photo, "latent": reg}, float(np.linalg.norm(g)))
+        if total < report.best_loss:
+            report.best_loss = total
+            report.best_iter = it
+            best_code = code.copy()
+        code = adam_step(adam, code, g)
+    report.skipped_steps = adam.skipped
+    report.elapsed = time.perf_counter() - t0
+    if report.grad_norms and max(report.grad_norms) < 1e-10:
+        report.non_identifiable = True
+        _w.warn("photometric loss is flat; views carry no texture signal", RuntimeWarning)
+    return best_code, report

@@ -1,0 +1,44 @@
+"""photometric warp kernels and reconstruct_multiview vs the reference."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import golden_weights, load_golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def st():
+    import paper_1911_13225_b200 as st
+    return st
+
+
+def _views(st, g):
+    intr = st.Intrinsics(width=24, height=24)
+    return intr, [st.look_at(e) for e in g["eyes"]]
+
+
+def test_photometric_loss_and_visibility_vs_reference(st):
+    g = load_golden("multiview24.npz")
+    intr, poses = _views(st, g)
+    d, im = g["depths"], g["images"]
+    l, dz = st.photometric_loss(d[0], im[0], intr, poses[0], im[1], intr, poses[1], d[1])
+    assert abs(l - float(g["ph_loss"])) < 1e-12
+    np.testing.assert_allclose(dz, g["ph_dz"], rtol=1e-9, atol=1e-12)
+    vis = st.visibility_mask(d[0], intr, poses[0], d[1], intr, poses[1])
+    assert np.array_equal(vis, g["ph_vis"])
+
+
+def test_reconstruct_multiview_history_vs_reference(st):
+    g = load_golden("multiview24.npz")
+    intr, poses = _views(st, g)
+    net = st.NeuralField(golden_weights(g), latent_dim=2, precision="fp64")
+    cfg = st.TraceConfig(alpha=1.0, k_samples=1, coarse_start_scale=1)
+    best, rep = st.reconstruct_multiview(net, list(g["images"]), [(intr, p) for p in poses],
+                                         code0=g["code"] + 0.1, iters=3, views_per_iter=2,
+                                         cfg=cfg, seed=1)
+    np.testing.assert_allclose(rep.losses, g["mv_losses"], rtol=1e-9, atol=1e-12)
+    assert rep.best_iter == int(g["mv_best_iter"])
+    np.testing.assert_allclose(best, g["mv_best"], rtol=1e-9, atol=1e-12)
