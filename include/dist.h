@@ -94,8 +94,9 @@ DIST_API int64_t dist_launch_count(void);
  * b[l] its bias; dims has n_layers+1 entries (dims[0] = latent_dim + 3 +
  * 0, dims[n_layers] = 1).  skip_layer >= 0 selects the DeepSDF layout where
  * layer `skip_layer` consumes concat(h, code, xyz);
- * -1 is the reference's plain stack.  final_linear: 0 = tanh head, 1 =
- * linear head (fields.py:200-201, 245-246).  Hidden activation is ReLU. */
+ * -1 is the reference's plain stack.  final_linear selects the head: 0 = tanh,
+ * 1 = linear (fields.py:200-201, 245-246), 2 = sigmoid (AttributeField,
+ * fields.py:332-338).  Hidden activation is ReLU. */
 DIST_API int dist_decoder_create(const double *const *W, const double *const *b, int n_layers,
                         const int32_t *dims, int latent_dim, int skip_layer,
                         int final_linear, int precision, dist_decoder **out);

@@ -229,9 +229,29 @@ def multiview():
     print("multiview", l, int(vis.sum()), rep.losses)
 
 
+def attribute():
+    """AttributeField + attribute_map (fields.py:294-338, shading.py:116-126)."""
+    rng = np.random.default_rng(7)
+    net = st.NeuralField.init(latent_dim=2, hidden=(16, 16), rng=rng)
+    code = rng.normal(0.0, 0.3, 2)
+    attr = st.AttributeField.init(shape_dim=2, attr_dim=1, hidden=(16, 16), out_dim=3,
+                                  rng=np.random.default_rng(3))
+    acode = np.concatenate([code, [0.4]])
+    pts = np.random.default_rng(4).uniform(-0.7, 0.7, (50, 3))
+    intr = st.Intrinsics(width=32, height=32)
+    pose = st.look_at((0.0, 0.0, -2.0))
+    maps = st.render(net, code, intr, pose, st.TraceConfig(), attr_field=attr, attr_code=acode)
+    out = {f"A{k}": v for k, v in _pack_weights(attr.weights).items()}
+    out.update(_pack_weights(net.weights))
+    out.update(code=code, acode=acode, pts=pts, vals=attr.evaluate(pts, acode), amap=maps.attribute)
+    np.savez_compressed(os.path.join(OUT, "attr32.npz"), **out)
+    print("attribute", maps.attribute.sum())
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     warnings.simplefilter("ignore")
+    attribute()
     multiview()
     formats()
     pose()

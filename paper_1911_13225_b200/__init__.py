@@ -8,15 +8,15 @@ include/dist.h).  There is no CPU fallback.
 
 from .camera import Intrinsics, Pose, RayBundle, generate_rays, log_rotation, look_at, \
     pose_gradient, rotation_derivatives, rotation_matrix
-from .fields import NeuralField, eval_field
+from .fields import AttributeField, NeuralField, eval_field
 from .formats import load_camera, load_field, read_pfm, read_pgm, save_camera, save_field, \
     write_pfm, write_pgm
 from .losses import LossWeights, Observation, bilinear_sample, depth_loss, latent_reg, \
     normal_loss, photometric_loss, silhouette_loss, to_gray, visibility_mask
 from .optimize import AdamState, LatentOptimizer, OptimizationError, OptimizeReport, adam_step, \
     complete_shape, completion_objective, pose_objective, reconstruct_multiview, recover_pose
-from .shading import HeadBundle, RenderMaps, depth_map, diff_heads, hard_mask, normal_map, \
-    ray_distance, render, soft_silhouette, surface_points
+from .shading import HeadBundle, RenderMaps, attribute_map, depth_map, diff_heads, hard_mask, \
+    normal_map, ray_distance, render, soft_silhouette, surface_points
 from .tracer import CONVERGED, ESCAPED, EXHAUSTED, MARCHING, DeviceTrace, RayState, TraceConfig, \
     TraceResult, trace, trace_views
 

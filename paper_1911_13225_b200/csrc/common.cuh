@@ -34,7 +34,7 @@ struct DecView {
   int n_layers;           // L weight matrices
   int latent_dim;         // D
   int skip;               // -1 or skip layer index
-  int final_linear;
+  int final_act;          // head activation: 0 tanh, 1 linear, 2 sigmoid (AttributeField)
   int prec;
   int np[kMaxLayers + 1]; // padded output width of layer l (np[L-1] = 1)
   int kp[kMaxLayers + 1]; // padded input width of hidden layer l (GEMM K)
@@ -65,6 +65,15 @@ struct dist_decoder {
 };
 
 namespace dist {
+
+// Head activation and its derivative written in terms of the output f
+// (fields.py:245-246 tanh/linear; fields.py:332-338 sigmoid of AttributeField).
+__host__ __device__ inline double head_act(int act, double s) {
+  return act == 0 ? tanh(s) : (act == 1 ? s : 1.0 / (1.0 + exp(-s)));
+}
+__host__ __device__ inline double head_dact(int act, double f) {
+  return act == 0 ? 1.0 - f * f : (act == 1 ? 1.0 : f * (1.0 - f));
+}
 
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ inline int64_t round_up(int64_t a, int64_t b) { return ceil_div(a, b) * b; }

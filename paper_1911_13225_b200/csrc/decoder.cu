@@ -199,7 +199,8 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
   v.n_layers = L;
   v.latent_dim = D;
   v.skip = skip;
-  v.final_linear = final_linear ? 1 : 0;
+  if (final_linear < 0 || final_linear > 2) return fail(DIST_ERR_CONFIG, "final activation must be 0 (tanh), 1 (linear) or 2 (sigmoid)");
+  v.final_act = final_linear;
   v.prec = prec;
   for (int l = 0; l < L - 1; ++l) v.np[l] = (int)round_up(dims[l + 1], 64);
   v.np[L - 1] = 1;

@@ -189,7 +189,7 @@ struct SimtTile {
 #pragma unroll
       for (int p = 0; p < P; ++p) s += red[p * TM + tid];
       s += dv.b_out;
-      f[tid] = dv.final_linear ? s : tanh(s);
+      f[tid] = head_act(dv.final_act, s);
     }
     __syncthreads();
   }
@@ -298,8 +298,13 @@ struct SimtTile {
     if (tid < TM && (tid & 1)) {
       const double om = f[tid - 1] + dv.b_out, od = f[tid];
       // f+ - f- without cancellation: tanh(a) - tanh(b) = sinh(a - b) / (cosh a cosh b)
-      f[tid] = dv.final_linear ? 2.0 * od : sinh(2.0 * od) / (cosh(om + od) * cosh(om - od));
-      f[tid - 1] = dv.final_linear ? om : tanh(om);
+      if (dv.final_act == 0)
+        f[tid] = sinh(2.0 * od) / (cosh(om + od) * cosh(om - od));
+      else if (dv.final_act == 1)
+        f[tid] = 2.0 * od;
+      else
+        f[tid] = head_act(2, om + od) - head_act(2, om - od);
+      f[tid - 1] = head_act(dv.final_act, om);
     }
     __syncthreads();
   }
@@ -331,7 +336,7 @@ struct SimtTile {
         for (int r = 0; r < 8; ++r) {
           const int row = rg * 8 + r;
           const double fr = f[row];
-          const double gh = dv.final_linear ? seed[row] : seed[row] * (1.0 - fr * fr);
+          const double gh = seed[row] * head_dact(dv.final_act, fr);
           H[col * LD + row] = ((bits >> r) & 1u) ? (T)(gh * (double)wk) : (T)0;
         }
       }

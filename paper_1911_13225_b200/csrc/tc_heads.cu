@@ -260,11 +260,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (row_thread) {
         const double sum = (double)m.xch[0][row] + (double)m.xch[1][row] +
                            (double)m.xch[2][row] + (double)m.xch[3][row] + P.dv.b_out;
-        const double fv = P.dv.final_linear ? sum : tanh(sum);
+        const double fv = head_act(P.dv.final_act, sum);
         if (gi < nrows && s >= 0) {
           gen.store(gi, fv);
           const double sd = gen.seed(gi, fv);
-          go = P.dv.final_linear ? sd : sd * (1.0 - fv * fv);
+          go = sd * head_dact(P.dv.final_act, fv);
         }
       }
       epi_sync();

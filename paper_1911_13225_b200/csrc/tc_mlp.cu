@@ -414,7 +414,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (row_thread) {
         const double sum = (double)m.xch[0][row] + (double)m.xch[1][row] +
                            (double)m.xch[2][row] + (double)m.xch[3][row] + P.dv.b_out;
-        const double fv = P.dv.final_linear ? sum : tanh(sum);
+        const double fv = head_act(P.dv.final_act, sum);
         R.finish(m, gi, m.ray[row], gi < nrows && m.shape[row] >= 0, fv);
       }
       epi_sync();

@@ -40,7 +40,7 @@ class NeuralField:
         self.latent_dim = int(latent_dim)
         if hidden_activation not in ("relu", "tanh"):
             raise ValueError(f"unknown hidden activation {hidden_activation!r}")
-        if final_activation not in ("tanh", "linear"):
+        if final_activation not in ("tanh", "linear", "sigmoid"):
             raise ValueError(f"unknown final activation {final_activation!r}")
         if hidden_activation != "relu":
             raise ValueError("the B200 decoder implements ReLU hidden layers only")
@@ -124,7 +124,7 @@ class NeuralField:
         out = C.c_void_p()
         _lib.check(_lib.lib().dist_decoder_create(
             Wp, bp, L, dims_c, self.latent_dim, self.skip,
-            1 if self.final_activation == "linear" else 0, _lib.PREC[self.precision],
+            {"tanh": 0, "linear": 1, "sigmoid": 2}[self.final_activation], _lib.PREC[self.precision],
             C.byref(out)))
         self._handles[self.precision] = out.value
         return out.value
@@ -200,6 +200,47 @@ class NeuralField:
                                      gc.data_ptr() if self.latent_dim else None, _lib.ptr(gp),
                                      ws.data_ptr(), ws.numel(), _lib.stream_ptr()))
         return f, gc[:, :self.latent_dim], gp
+
+
+class AttributeField:
+    """MLP from concat(shape code, attribute code, p) to an m-vector in [0, 1]
+    (fields.py:294-338).  Evaluated on the device as m
+    single-output sigmoid-head decoders sharing the hidden stack."""
+
+    def __init__(self, weights, shape_dim: int = 0, attr_dim: int = 0,
+                 hidden_activation: str = "relu", precision: str = "fp64"):
+        self.weights = [(np.asarray(W, dtype=np.float64), np.asarray(b, dtype=np.float64))
+                        for W, b in weights]
+        self.shape_dim, self.attr_dim = int(shape_dim), int(attr_dim)
+        self.hidden_activation = hidden_activation
+        if self.weights[0][0].shape[0] != self.shape_dim + self.attr_dim + 3:
+            raise ValueError("first layer width must be shape_dim + attr_dim + 3")
+        self.out_dim = self.weights[-1][0].shape[1]
+        W, b = self.weights[-1]
+        self._channels = [NeuralField(self.weights[:-1] + [(W[:, c:c + 1], b[c:c + 1])],
+                                      latent_dim=self.shape_dim + self.attr_dim,
+                                      hidden_activation=hidden_activation,
+                                      final_activation="sigmoid", precision=precision)
+                          for c in range(self.out_dim)]
+
+    @classmethod
+    def init(cls, shape_dim: int = 0, attr_dim: int = 0, hidden=(32, 32, 32), out_dim: int = 3,
+             rng=None, **kw):
+        """He-normal init (fields.py:312-319), same RNG draws as the reference."""
+        rng = np.random.default_rng(rng)
+        dims = [shape_dim + attr_dim + 3, *hidden, out_dim]
+        weights = [(rng.standard_normal((p, q)) * np.sqrt(2.0 / p), np.zeros(q))
+                   for p, q in zip(dims[:-1], dims[1:])]
+        return cls(weights, shape_dim=shape_dim, attr_dim=attr_dim, **kw)
+
+    def evaluate(self, points, code=None):
+        d = self.shape_dim + self.attr_dim
+        if d:
+            code = np.asarray(code, dtype=np.float64)
+            if code.shape != (d,):
+                raise ValueError(f"attribute code shape {code.shape} != ({d},)")
+        p = _pts(points)
+        return np.stack([ch.evaluate(p, code if d else None) for ch in self._channels], axis=1)
 
 
 def eval_field(field, points, code=None):

@@ -108,6 +108,18 @@ def normal_map(result: TraceResult, field=None, code=None) -> np.ndarray:
     return device_normals(dt)[result.view].cpu().numpy()
 
 
+def attribute_map(result: TraceResult, attr_field, code=None) -> np.ndarray:
+    """Surface attributes (colour) per converged pixel, zero background
+    (shading.py:116-126)."""
+    pts, idx = surface_points(result)
+    m = getattr(attr_field, "out_dim", 3)
+    b = result.state.bundle
+    img = np.zeros((b.height, b.width, m))
+    if idx.size:
+        img[b.pixels[idx, 1], b.pixels[idx, 0]] = attr_field.evaluate(pts, code)
+    return img
+
+
 @dataclass
 class RenderMaps:
     """shading.py:129-135."""
@@ -121,12 +133,11 @@ class RenderMaps:
 def render(field, code, intr, pose, cfg=None, attr_field=None, attr_code=None,
            with_normals: bool = True) -> RenderMaps:
     """Trace and assemble every map (shading.py:138-150)."""
-    if attr_field is not None:
-        raise ValueError("attribute (colour) rendering is outside the B200 hot path")
     result = trace(field, code, intr, pose, cfg)
     normal = normal_map(result) if with_normals else np.zeros((intr.height, intr.width, 3))
+    attr = attribute_map(result, attr_field, attr_code) if attr_field is not None else None
     return RenderMaps(depth=depth_map(result), normal=normal, silhouette=soft_silhouette(result),
-                      mask=hard_mask(result))
+                      mask=hard_mask(result), attribute=attr)
 
 
 # === differentiable heads (shading.py:156-288) ================================

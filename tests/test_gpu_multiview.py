@@ -42,3 +42,15 @@ def test_reconstruct_multiview_history_vs_reference(st):
     np.testing.assert_allclose(rep.losses, g["mv_losses"], rtol=1e-9, atol=1e-12)
     assert rep.best_iter == int(g["mv_best_iter"])
     np.testing.assert_allclose(best, g["mv_best"], rtol=1e-9, atol=1e-12)
+
+
+def test_attribute_field_and_map_vs_reference(st):
+    """sigmoid-head colour MLP at hit points."""
+    g = load_golden("attr32.npz")
+    aw = [(g[f"AW{i}"], g[f"Ab{i}"]) for i in range(int(g["An_layers"]))]
+    attr = st.AttributeField(aw, shape_dim=2, attr_dim=1)
+    np.testing.assert_allclose(attr.evaluate(g["pts"], g["acode"]), g["vals"], rtol=0, atol=1e-13)
+    net = st.NeuralField(golden_weights(g), latent_dim=2)
+    maps = st.render(net, g["code"], st.Intrinsics(width=32, height=32), st.look_at((0.0, 0.0, -2.0)),
+                     st.TraceConfig(), attr_field=attr, attr_code=g["acode"])
+    np.testing.assert_allclose(maps.attribute, g["amap"], rtol=0, atol=1e-12)
