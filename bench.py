@@ -166,9 +166,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("DIST_BENCH_BACKEND", "nccl")   # gloo: CI with ranks sharing a GPU
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     import paper_1911_13225_b200 as st
     from paper_1911_13225_b200 import _lib
@@ -263,6 +268,14 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     e2e_ms = float(t.item())
 
+    consistent = True
+    if world > 1:   # replicated Adam after the all-reduce: every rank holds the same code
+        ref = opt.code.clone()
+        dist.broadcast(ref, 0)
+        diff = (opt.code - ref).abs().max().reshape(1)
+        dist.all_reduce(diff, op=dist.ReduceOp.MAX)
+        consistent = bool(diff.item() == 0.0)
+
     peaks, peak_kind = _peaks()
     # Roofline of the dominant kernel family: the decoder step kernels of the
     # march (k_tc_mlp in march mode for bf16x3).  achieved = algorithmic FLOP
@@ -281,6 +294,7 @@ def main():
         "e2e": {"value": rays_per_step / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),
+        "replicas_bit_identical": consistent,
         "clocks": clk.summary(),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": None,
