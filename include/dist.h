@@ -168,7 +168,8 @@ typedef struct dist_objective_io {
 } dist_objective_io;
 
 DIST_API size_t dist_objective_workspace_size(const dist_decoder *dec, int n_views, int width,
-                                              int height, int k_samples, int n_shapes);
+                                              int height, int k_samples, int n_shapes,
+                                              int grad_mode);
 /* After dist_trace: frozen-sample heads, loss seeds, the fused taped forward
  * -> seed -> reverse sweep per tile of samples, and the code gradient with the
  * latent regulariser added once per shape.  Views contribute their own

@@ -83,7 +83,7 @@ _SIGS = {
                                C.c_int, C.POINTER(dist_trace_config), C.POINTER(dist_ray_state),
                                C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "dist_objective_workspace_size": (C.c_size_t, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
-                                                   C.c_int]),
+                                                   C.c_int, C.c_int]),
     "dist_objective": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                  C.c_int, C.POINTER(dist_trace_config), C.POINTER(dist_ray_state),
                                  C.POINTER(dist_objective_io), C.c_void_p, C.c_size_t, C.c_void_p]),

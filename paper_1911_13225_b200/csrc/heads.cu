@@ -207,8 +207,8 @@ struct ObjLayout {
   size_t bytes;
 };
 
-static ObjLayout obj_layout(const DecView &dv, int V, int W, int H, int K, int S, char *ws,
-                            size_t cap) {
+static ObjLayout obj_layout(const DecView &dv, int V, int W, int H, int K, int S, int mode,
+                            char *ws, size_t cap) {
   ObjLayout L{};
   Carve cv{ws, 0, cap};
   const int64_t n = (int64_t)V * W * H;
@@ -222,9 +222,9 @@ static ObjLayout obj_layout(const DecView &dv, int V, int W, int H, int K, int S
   L.h.view_samp = cv.take<int32_t>(V + 1);
   L.h.counts = cv.take<int32_t>(4);
   L.sil_seed = cv.take<double>(n);
-  L.gdotv = cv.take<double>(n);
-  L.probe_f = cv.take<double>(n * 6);
-  L.conv = cv.take<int32_t>(n);
+  L.gdotv = cv.take<double>(mode == 1 ? n : 1);
+  L.probe_f = cv.take<double>(mode == 1 ? n * 6 : 1);   // implicit mode only
+  L.conv = cv.take<int32_t>(mode == 1 ? n : 1);
   L.conv_count = cv.take<int32_t>(4);
   L.npx = cv.take<int32_t>(V);
   L.bcount = cv.take<int32_t>(ceil_div(n * K, kScanBlock) + 1);
@@ -245,9 +245,10 @@ using namespace dist;
 
 extern "C" {
 
-size_t dist_objective_workspace_size(const dist_decoder *dec, int V, int W, int H, int K, int S) {
+size_t dist_objective_workspace_size(const dist_decoder *dec, int V, int W, int H, int K, int S,
+                                     int mode) {
   if (!dec) return 0;
-  return obj_layout(dec->view, V, W, H, K, S, nullptr, ~size_t(0)).bytes;
+  return obj_layout(dec->view, V, W, H, K, S, mode, nullptr, ~size_t(0)).bytes;
 }
 
 int dist_objective(const dist_decoder *dec, const double *codes, int S, const dist_camera *cams,
@@ -260,7 +261,7 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
   cudaStream_t sm = (cudaStream_t)stream;
   const int K = cfg->k_samples;
   const int s1 = std::max(S, 1);
-  ObjLayout L = obj_layout(dv, V, W, H, K, S, (char *)ws, ws_bytes);
+  ObjLayout L = obj_layout(dv, V, W, H, K, S, io->grad_mode, (char *)ws, ws_bytes);
   if (L.bytes > ws_bytes) return fail(DIST_ERR_CONFIG, "objective workspace too small");
   const int64_t n = (int64_t)V * W * H, WH = (int64_t)W * H;
   LevelState ls{st->d, st->b, st->status, st->steps, st->topk_d, st->topk_f, st->topk_absf, W, H, 1, n};

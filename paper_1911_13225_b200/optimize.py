@@ -174,7 +174,8 @@ class LatentOptimizer:
         lib = _lib.lib()
         h = self.field.handle()
         K = self.cfg.k_samples
-        ws = _lib.workspace(lib.dist_objective_workspace_size(h, self.V, self.W, self.H, K, self.S))
+        ws = _lib.workspace(lib.dist_objective_workspace_size(h, self.V, self.W, self.H, K, self.S,
+                                                              1 if self.grad_mode == "implicit" else 0))
         io = _lib.dist_objective_io(_lib.ptr(self.obs_depth), _lib.ptr(self.obs_mask),
                                     _lib.ptr(self.obs_sil), self.weights.depth,
                                     self.weights.silhouette, self.weights.latent,
