@@ -38,6 +38,9 @@ int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t
                     double *part0, int grid_cap, int *grid_out, cudaStream_t st);
 
 struct LevelState;
+struct ProbeGen;
+int tc_eval_probes(const DecView &dv, const double *c0, const ProbeGen &gen, int64_t n_bound,
+                   cudaStream_t st);
 int normals_pass(const DecView &dv, const double *c0, const double *cs, const dist_camera *cams,
                  const LevelState &ls, const dist_trace_config *cfg, double *normals, double *gdotv,
                  int32_t *conv, int32_t *count, int32_t *bcount, double *f, cudaStream_t st);

@@ -127,4 +127,38 @@ int tc_run_steps(const DecView &dv, const double *c0, const double *cskip,
                  const dist_camera *cams, const LevelState &ls, Ctl *ctl, int32_t *l0, int32_t *l1,
                  const MarchArgs &a, int slots, int64_t *live, int64_t *stats, cudaStream_t st);
 
+// Normal probes of the converged rays (shading.py:73-94): row 6r + 2a (+1)
+// is p +/- delta e_a of converged ray r, so consecutive rows form the
+// (p+, p-) pairs of the (mid, diff) evaluation.
+struct ProbeGen {
+  const dist_camera *cams;
+  LevelState ls;
+  const int32_t *conv;   // converged ray ids
+  const int32_t *cnt_ptr;  // device count
+  double alpha, delta;
+  double *f;
+  __device__ int64_t count() const { return (int64_t)*cnt_ptr * 6; }
+  __device__ bool point(int64_t i, double p[3], int &s) const {
+    const int64_t r = i / 6;
+    const int a = (int)(i - r * 6);
+    const int64_t g = conv[r];
+    double dir[3];
+    const int64_t per = (int64_t)ls.lw * ls.lh;
+    const int v = (int)(g / per);
+    const int64_t pix = g - (int64_t)v * per;
+    const int j = (int)(pix / ls.lw), ii = (int)(pix - (int64_t)j * ls.lw);
+    pixel_ray(cams[v], ii, j, 1, dir, nullptr);
+    const double ds = __dadd_rn(ls.d[g], __dmul_rn(1.0 - alpha, ls.b[g]));
+    for (int q = 0; q < 3; ++q) p[q] = __dadd_rn(cams[v].origin[q], __dmul_rn(ds, dir[q]));
+    // probe order (+x, -x, +y, -y, +z, -z): consecutive rows form the
+    // (p + delta e_a, p - delta e_a) pairs of the (mid, diff) evaluation
+    const int axis = a >> 1;
+    p[axis] = __dadd_rn(p[axis], (a & 1) ? -delta : delta);
+    s = cams[v].shape;
+    return true;
+  }
+  __device__ double seed(int64_t, double) const { return 0.0; }
+  __device__ void store(int64_t i, double v) const { f[i] = v; }
+};
+
 }  // namespace dist

@@ -124,8 +124,37 @@ __device__ __forceinline__ int load_row(const Rows &r, const Misc &m, int64_t i,
   else return r.load(i, p, s);
 }
 
+// Normal probes (march.cuh ProbeGen) in (mid, diff) pair mode.
+struct ProbeRows {
+  ProbeGen g;
+  __device__ bool begin(Misc &) { return g.count() > 0; }
+  __device__ int64_t rows(const Misc &) const { return g.count(); }
+  __device__ int load(int64_t i, double p[3], int &s) const {
+    if (!g.point(i, p, s)) s = -1;
+    return (int)i;
+  }
+  __device__ void finish(Misc &, int64_t i, int, bool valid, double fv) const {
+    if (valid) g.store(i, fv);
+  }
+  __device__ void end(Misc &) {}
+};
+
+// ReLU of a (mid, diff) pair, m = (h+ + h-)/2, d = (h+ - h-)/2 (SURVEY 7.2
+// H5; the SIMT relu_pair of mlp_simt.cuh in fp32): the even row of the pair
+// keeps the new mid, the odd row the new diff.
+__device__ __forceinline__ float relu_pair_sel(float m, float d, bool odd) {
+  const float ad = fabsf(d);
+  if (m - ad > 0.f) return odd ? d : m;
+  if (m + ad <= 0.f) return 0.f;
+  const float a = fmaxf(m + d, 0.f), b = fmaxf(m - d, 0.f);
+  return 0.5f * (odd ? a - b : a + b);
+}
+
 // ---------------------------------------------------------------------------
-template <bool F16, class Rows>
+// PAIR: rows 2i / 2i+1 are the probes p+ / p- of one central difference and
+// travel through the network as (mid, diff) -- adjacent TMEM lanes, so each
+// pair meets in one shfl.xor 1; the odd row's result is f(p+) - f(p-).
+template <bool F16, class Rows, bool PAIR = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     k_tc_mlp(const __grid_constant__ CUtensorMap wmap, Params P, Rows R) {
   extern __shared__ __align__(16) char smem_raw[];
@@ -269,14 +298,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         m.shape[row] = s;
         m.ray[row] = id;
       }
+      const bool odd = PAIR && (lane & 1);
       const int n0 = P.dv.np[0];
       const double *c0 = P.c0 + (size_t)(s < 0 ? 0 : s) * n0;
       // layer-0 activations of 8 consecutive columns: folded bias c0 (fp64,
       // rounded) + p . W0p in fp32 -- the bf16x3 split of the result carries
       // ~17 bits, so fp32 here costs nothing and keeps the loads vectorised.
-      const float px = (float)p[0], py = (float)p[1], pz = (float)p[2];
+      // pair mode: layer 0 of the pair from its midpoint and half-offset
+      // (fp64, exact), so the diff pre-activation is off . W0p, never a
+      // difference of two rounded pre-activations
+      float px = (float)p[0], py = (float)p[1], pz = (float)p[2], ox = 0.f, oy = 0.f, oz = 0.f;
+      if constexpr (PAIR) {
+        double pp[3], o[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) pp[a] = __shfl_xor_sync(0xffffffffu, p[a], 1);
+        const double *pa = odd ? pp : p, *pb = odd ? p : pp;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) o[a] = 0.5 * (pa[a] - pb[a]);
+        px = (float)(0.5 * (pa[0] + pb[0]));
+        py = (float)(0.5 * (pa[1] + pb[1]));
+        pz = (float)(0.5 * (pa[2] + pb[2]));
+        ox = (float)o[0];
+        oy = (float)o[1];
+        oz = (float)o[2];
+      }
       auto h0x8 = [&](int col, float (&x)[8]) {
-        float w0[8], w1[8], w2[8];
+        float w0[8], w1[8], w2[8], cf[8];
         ldg8(P.dv.W0pf + col, w0);
         ldg8(P.dv.W0pf + n0 + col, w1);
         ldg8(P.dv.W0pf + 2 * n0 + col, w2);
@@ -284,10 +331,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 8; e += 2) {
           const double2 cv = __ldg(cc + e / 2);
-          float v0 = fmaf(pz, w2[e], fmaf(py, w1[e], fmaf(px, w0[e], (float)cv.x)));
-          float v1 = fmaf(pz, w2[e + 1], fmaf(py, w1[e + 1], fmaf(px, w0[e + 1], (float)cv.y)));
-          x[e] = (s >= 0 && v0 > 0.f) ? v0 : 0.f;
-          x[e + 1] = (s >= 0 && v1 > 0.f) ? v1 : 0.f;
+          cf[e] = (float)cv.x;
+          cf[e + 1] = (float)cv.y;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float v = fmaf(pz, w2[e], fmaf(py, w1[e], fmaf(px, w0[e], cf[e])));
+          if constexpr (PAIR) {
+            const float dd = fmaf(oz, w2[e], fmaf(oy, w1[e], ox * w0[e]));
+            x[e] = s >= 0 ? relu_pair_sel(v, dd, odd) : 0.f;
+          } else {
+            x[e] = (s >= 0 && v > 0.f) ? v : 0.f;
+          }
         }
       };
       // Row scale of the fp16 split: a power of two that puts the row max in
@@ -316,7 +371,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             float x[8];
             h0x8(nh * 256 + half * 128 + sub * 64 + j, x);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) tmax = fmaxf(tmax, x[e]);
+            for (int e = 0; e < 8; ++e) tmax = fmaxf(tmax, fabsf(x[e]));  // pair diffs are signed
           }
         row_scale(tmax, sc, rinv);
       }
@@ -343,6 +398,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const bool last = (l == G - 1);
         const float *bias = P.bias + (size_t)l * KDIM;
         const float unscale = rinv * P.winv[l];   // exact: both are powers of two
+        // bias + ReLU (pair mode: diff rows carry no bias; ReLU of the pair)
+        auto act = [&](float v, float bb) -> float {
+          if constexpr (PAIR) {
+            const float y = fmaf(v, unscale, odd ? 0.f : bb);
+            const float yp = __shfl_xor_sync(0xffffffffu, y, 1);
+            return relu_pair_sel(odd ? yp : y, odd ? y : yp, odd);
+          } else {
+            const float y = fmaf(v, unscale, bb);
+            return y > 0.f ? y : 0.f;
+          }
+        };
         if (P.debug == 1) {
           tc_fence_before();
           if (!last) {
@@ -368,10 +434,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 if (last) ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                  float y = fmaf(v[g8 * 8 + e], unscale, bb[e]);
-                  y = y > 0.f ? y : 0.f;
+                  const float y = act(v[g8 * 8 + e], bb[e]);
                   if (last) head = fmaf(y, wo[e], head);
-                  else tmax = fmaxf(tmax, y);
+                  else tmax = fmaxf(tmax, fabsf(y));
                 }
               }
             }
@@ -392,8 +457,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 ldg8(bias + cb + c * 32 + g8 * 8, bb);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                  const float y = fmaf(v[g8 * 8 + e], unscale, bb[e]);
-                  x[e] = (y > 0.f ? y : 0.f) * sc;
+                  x[e] = act(v[g8 * 8 + e], bb[e]) * sc;
                 }
                 put8<F16>(smem, row, cb + c * 32 + g8 * 8, x);
               }
@@ -413,8 +477,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       epi_sync();
       if (row_thread) {
         const double sum = (double)m.xch[0][row] + (double)m.xch[1][row] +
-                           (double)m.xch[2][row] + (double)m.xch[3][row] + P.dv.b_out;
-        const double fv = head_act(P.dv.final_act, sum);
+                           (double)m.xch[2][row] + (double)m.xch[3][row] + (odd ? 0.0 : P.dv.b_out);
+        double fv;
+        if constexpr (PAIR) {
+          // f+ - f- without cancellation (mlp_simt.cuh output_pair)
+          const double sp = __shfl_xor_sync(0xffffffffu, sum, 1);
+          const double om = odd ? sp : sum, od = odd ? sum : sp;
+          const int fa = P.dv.final_act;
+          fv = !odd ? head_act(fa, om)
+                    : (fa == 0 ? sinh(2.0 * od) / (cosh(om + od) * cosh(om - od))
+                               : (fa == 1 ? 2.0 * od : head_act(2, om + od) - head_act(2, om - od)));
+        } else {
+          fv = head_act(P.dv.final_act, sum);
+        }
         R.finish(m, gi, m.ray[row], gi < nrows && m.shape[row] >= 0, fv);
       }
       epi_sync();
@@ -461,18 +536,30 @@ bool tc_supported(const DecView &dv) {
   return (dv.prec == DIST_PREC_BF16X3 || dv.prec == DIST_PREC_FP16X3) && dv.tc_w[0] != nullptr;
 }
 
-// tc_w[0]: [G][2][512 n][512 k] (W^T hi, lo as bf16 or fp16);
-// tc_bias[0]: [G][512] hidden biases, [512] w_out, [G] inverse weight scales (fp32)
+// Packs (slot: contents):
+//   0: the decoder's forward pack, bf16 or fp16 by precision
+//      tc_w  [G][2][512 n][512 k] (W^T hi, lo)
+//      tc_bias [G][512] hidden biases, [512] w_out, [G] inverse weight scales (fp32)
+//   1: bf16x3 only -- backward pack (W untransposed, bf16 hi/lo) for k_tc_heads
+//   2: bf16x3 only -- fp16x3 forward pack for the (mid, diff) normal probes:
+//      fp16's 11-bit halves carry the diff rows to ~1e-5 where bf16's 8-bit
+//      halves leave ~1e-4 (normals)
 void tc_pack_sizes(const DecView &dv, const std::function<void(int, size_t, size_t)> &put) {
   for (int l = 0; l <= dv.n_layers - 2; ++l)
     if (dv.np[l] != tc::KDIM) return;
   if (dv.skip >= 0 || dv.n_layers < 3) return;
   const int G = dv.n_layers - 2;
-  put(0, (size_t)G * 2 * tc::KDIM * tc::KDIM * 2,
-      ((size_t)(G + 1) * tc::KDIM + G) * sizeof(float));
-  // backward pack (W untransposed, bf16 hi/lo) for the fused head kernel
-  if (dv.prec == DIST_PREC_BF16X3) put(1, (size_t)G * 2 * tc::KDIM * tc::KDIM * 2, 16);
+  const size_t wb = (size_t)G * 2 * tc::KDIM * tc::KDIM * 2;
+  const size_t bb = ((size_t)(G + 1) * tc::KDIM + G) * sizeof(float);
+  put(0, wb, bb);
+  if (dv.prec == DIST_PREC_BF16X3) {
+    put(1, wb, 16);
+    put(2, wb, bb);
+  }
 }
+
+static void fill_fwd(const DecView &dv, const double *const *W, const double *const *b,
+                     const int32_t *dims, bool f16, uint16_t *w, float *bb);
 
 void tc_pack_fill(const DecView &dv, const double *const *W, const double *const *b,
                   const int32_t *dims, const std::function<void *(int)> &wdst,
@@ -481,9 +568,29 @@ void tc_pack_fill(const DecView &dv, const double *const *W, const double *const
     if (dv.np[l] != tc::KDIM) return;
   if (dv.skip >= 0 || dv.n_layers < 3) return;
   const bool f16 = dv.prec == DIST_PREC_FP16X3;
+  fill_fwd(dv, W, b, dims, f16, reinterpret_cast<uint16_t *>(wdst(0)), bdst(0));
+  if (f16) return;
+  fill_fwd(dv, W, b, dims, true, reinterpret_cast<uint16_t *>(wdst(2)), bdst(2));
   const int G = dv.n_layers - 2, K = tc::KDIM;
-  uint16_t *w = reinterpret_cast<uint16_t *>(wdst(0));
-  float *bb = bdst(0);
+  auto to16 = [](float x) -> uint16_t { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); };
+  auto from16 = [](uint16_t h) -> float { return __bfloat162float(__ushort_as_bfloat16(h)); };
+  uint16_t *wb = reinterpret_cast<uint16_t *>(wdst(1));
+  for (int g = 0; g < G; ++g) {
+    const int l = g + 1;
+    const int kin = dims[l], nout = dims[l + 1];
+    for (int n = 0; n < K; ++n)        // n: layer input index (dgrad output)
+      for (int k = 0; k < K; ++k) {    // k: layer output index (contracted)
+        const float x = (n < kin && k < nout) ? (float)W[l][(size_t)n * nout + k] : 0.f;
+        const uint16_t h = to16(x);
+        wb[(((size_t)g * 2 + 0) * K + n) * K + k] = h;
+        wb[(((size_t)g * 2 + 1) * K + n) * K + k] = to16(x - from16(h));
+      }
+  }
+}
+
+static void fill_fwd(const DecView &dv, const double *const *W, const double *const *b,
+                     const int32_t *dims, bool f16, uint16_t *w, float *bb) {
+  const int G = dv.n_layers - 2, K = tc::KDIM;
   float *winv = bb + (size_t)(G + 1) * K;
   auto to16 = [f16](float x) -> uint16_t {
     return f16 ? __half_as_ushort(__float2half_rn(x)) : __bfloat16_as_ushort(__float2bfloat16_rn(x));
@@ -517,20 +624,6 @@ void tc_pack_fill(const DecView &dv, const double *const *W, const double *const
   }
   const int L = dv.n_layers;
   for (int k = 0; k < K; ++k) bb[(size_t)G * K + k] = k < dims[L - 1] ? (float)W[L - 1][k] : 0.f;
-  if (!f16) {
-    uint16_t *wb = reinterpret_cast<uint16_t *>(wdst(1));
-    for (int g = 0; g < G; ++g) {
-      const int l = g + 1;
-      const int kin = dims[l], nout = dims[l + 1];
-      for (int n = 0; n < K; ++n)        // n: layer input index (dgrad output)
-        for (int k = 0; k < K; ++k) {    // k: layer output index (contracted)
-          const float x = (n < kin && k < nout) ? (float)W[l][(size_t)n * nout + k] : 0.f;
-          const uint16_t h = to16(x);
-          wb[(((size_t)g * 2 + 0) * K + n) * K + k] = h;
-          wb[(((size_t)g * 2 + 1) * K + n) * K + k] = to16(x - from16(h));
-        }
-    }
-  }
 }
 
 int tc_make_map(const DecView &dv, int slot, CUtensorMap *map) {
@@ -541,8 +634,8 @@ int tc_make_map(const DecView &dv, int slot, CUtensorMap *map) {
   cuuint64_t gstride[1] = {(cuuint64_t)tc::KDIM * 2};
   cuuint32_t box[2] = {64, 128};
   cuuint32_t estr[2] = {1, 1};
-  const CUtensorMapDataType dt = dv.prec == DIST_PREC_FP16X3 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16
-                                                              : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const bool f16 = slot == 2 || (slot == 0 && dv.prec == DIST_PREC_FP16X3);
+  const CUtensorMapDataType dt = f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   CUresult r = enc(map, dt, 2, const_cast<void *>(dv.tc_w[slot]), gdim,
                    gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -550,17 +643,17 @@ int tc_make_map(const DecView &dv, int slot, CUtensorMap *map) {
   return DIST_OK;
 }
 
-template <bool F16, class Rows>
+template <bool F16, class Rows, bool PAIR = false>
 static int launch_tc_t(const DecView &dv, const double *c0, const Rows &rows, int64_t tiles_bound,
-                       cudaStream_t st) {
+                       cudaStream_t st, int slot = 0) {
   CUtensorMap map;
-  int rc = tc_make_map(dv, 0, &map);
+  int rc = tc_make_map(dv, slot, &map);
   if (rc) return rc;
   tc::Params P;
   P.dv = dv;
   P.c0 = c0;
-  P.bias = dv.tc_bias[0];
-  P.w_out = dv.tc_bias[0] + (size_t)(dv.n_layers - 2) * tc::KDIM;
+  P.bias = dv.tc_bias[slot];
+  P.w_out = dv.tc_bias[slot] + (size_t)(dv.n_layers - 2) * tc::KDIM;
   P.n_gemm = dv.n_layers - 2;
   P.winv = P.w_out + tc::KDIM;
   {
@@ -569,20 +662,29 @@ static int launch_tc_t(const DecView &dv, const double *c0, const Rows &rows, in
     const char *dbg = getenv("DIST_TC_DEBUG");
     P.debug = dbg ? atoi(dbg) : 0;
   }
-  const void *fn = (const void *)tc::k_tc_mlp<F16, Rows>;
+  const void *fn = (const void *)tc::k_tc_mlp<F16, Rows, PAIR>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc)");
   const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_bound, sm_count() / 2));
-  tc::k_tc_mlp<F16, Rows><<<2 * pairs, tc::THREADS, tc::SMEM_BYTES, st>>>(map, P, rows);
+  tc::k_tc_mlp<F16, Rows, PAIR><<<2 * pairs, tc::THREADS, tc::SMEM_BYTES, st>>>(map, P, rows);
   DIST_CHECK_LAUNCH("k_tc_mlp");
   return DIST_OK;
 }
 
-template <class Rows>
+template <class Rows, bool PAIR = false>
 static int launch_tc(const DecView &dv, const double *c0, const Rows &rows, int64_t tiles_bound,
                      cudaStream_t st) {
-  if (dv.prec == DIST_PREC_FP16X3) return launch_tc_t<true>(dv, c0, rows, tiles_bound, st);
-  return launch_tc_t<false>(dv, c0, rows, tiles_bound, st);
+  if (dv.prec == DIST_PREC_FP16X3) return launch_tc_t<true, Rows, PAIR>(dv, c0, rows, tiles_bound, st);
+  return launch_tc_t<false, Rows, PAIR>(dv, c0, rows, tiles_bound, st);
+}
+
+int tc_eval_probes(const DecView &dv, const double *c0, const ProbeGen &gen, int64_t n_bound,
+                   cudaStream_t st) {
+  tc::ProbeRows rows{gen};
+  // always fp16x3: a bf16x3 decoder carries an fp16 probe pack in slot 2
+  const int slot = dv.prec == DIST_PREC_FP16X3 ? 0 : 2;
+  if (!dv.tc_w[slot]) return fail(DIST_ERR_CONFIG, "decoder has no fp16 probe pack");
+  return launch_tc_t<true, tc::ProbeRows, true>(dv, c0, rows, ceil_div(n_bound, 128), st, slot);
 }
 
 int tc_eval_points(const DecView &dv, const double *c0, const double *cskip, const double *pts,

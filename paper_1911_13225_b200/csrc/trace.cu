@@ -195,36 +195,6 @@ static int grid_for(int64_t n, int threads) {
 }
 
 // --- normals (shading.py:73-94) ----------------------------------------------
-struct ProbeGen {
-  const dist_camera *cams;
-  LevelState ls;
-  const int32_t *conv;   // converged ray ids
-  const int32_t *cnt_ptr;  // device count
-  double alpha, delta;
-  double *f;
-  __device__ int64_t count() const { return (int64_t)*cnt_ptr * 6; }
-  __device__ bool point(int64_t i, double p[3], int &s) const {
-    const int64_t r = i / 6;
-    const int a = (int)(i - r * 6);
-    const int64_t g = conv[r];
-    double dir[3];
-    const int64_t per = (int64_t)ls.lw * ls.lh;
-    const int v = (int)(g / per);
-    const int64_t pix = g - (int64_t)v * per;
-    const int j = (int)(pix / ls.lw), ii = (int)(pix - (int64_t)j * ls.lw);
-    pixel_ray(cams[v], ii, j, 1, dir, nullptr);
-    const double ds = __dadd_rn(ls.d[g], __dmul_rn(1.0 - alpha, ls.b[g]));
-    for (int q = 0; q < 3; ++q) p[q] = __dadd_rn(cams[v].origin[q], __dmul_rn(ds, dir[q]));
-    // probe order (+x, -x, +y, -y, +z, -z): consecutive rows form the
-    // (p + delta e_a, p - delta e_a) pairs of the (mid, diff) evaluation
-    const int axis = a >> 1;
-    p[axis] = __dadd_rn(p[axis], (a & 1) ? -delta : delta);
-    s = cams[v].shape;
-    return true;
-  }
-  __device__ double seed(int64_t, double) const { return 0.0; }
-  __device__ void store(int64_t i, double v) const { f[i] = v; }
-};
 
 __global__ void k_normals_assemble(const dist_camera *__restrict__ cams, LevelState ls,
                                    const int32_t *__restrict__ conv,
@@ -269,8 +239,10 @@ int normals_pass(const DecView &dv, const double *c0, const double *cs, const di
   // fp64: plain probes (the reference's own arithmetic); every other mode
   // evaluates the probe pairs as (mid, diff) in fp32 so that the 1/(2 delta)
   // amplification does not act on rounding error (SURVEY 0 finding 3).
+  // On tensor-core decoders the pairs run through k_tc_mlp's pair mode.
   const int pair = dv.prec == DIST_PREC_FP64 ? 0 : 1;
   if (!pair) rc = launch_eval_gen<double>(dv, c0, cs, gen, n * 6, st);
+  else if (tc_supported(dv)) rc = tc_eval_probes(dv, c0, gen, n * 6, st);
   else rc = launch_eval_gen<float, ProbeGen, true>(dv, c0, cs, gen, n * 6, st);
   if (rc) return rc;
   k_normals_assemble<<<grid_for(n, 256), 256, 0, st>>>(cams, ls, conv, count, f, cfg->normal_delta,

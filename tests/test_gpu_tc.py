@@ -97,6 +97,24 @@ def test_c2_render_256_depth_normals_vs_oracle(st, prec):
         assert np.percentile(nd, 99) < 5e-4 and np.mean(nd > 1e-3) < 2e-3
 
 
+@pytest.mark.parametrize("prec", ["bf16x3", "fp16x3"])
+def test_tc_pair_normals_same_points(st, prec):
+    """Tensor-core (mid, diff) probe pairs (always fp16x3) vs the fp64 probes at
+    the SAME traced surface points (north_star: normals within 1e-4)."""
+    from paper_1911_13225_b200.shading import device_normals
+    code = np.random.default_rng(1).normal(0.0, 0.1, 256)
+    net = st.NeuralField.geometric(256, (512,) * 8, 0, precision=prec)
+    view = [(st.Intrinsics(width=128, height=128), st.look_at((0.0, 0.0, -2.0)))]
+    dt = st.trace_views(net, code, view, st.TraceConfig())
+    n_tc = device_normals(dt).cpu().numpy().reshape(-1, 3)
+    dt.field = net.with_precision("fp64")
+    n_64 = device_normals(dt).cpu().numpy().reshape(-1, 3)
+    hit = np.linalg.norm(n_64, axis=1) > 0
+    assert hit.sum() > 1000
+    nd = np.linalg.norm(n_tc - n_64, axis=1)[hit]
+    assert np.percentile(nd, 99) < 2e-5 and nd.max() < 1e-4
+
+
 @pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("bf16x3", 5e-3)])
 def test_depth_and_silhouette_objective_vs_oracle(st, prec, tol):
     """The C4 loss (depth + silhouette hinge, losses.py:54-91) on the 8x512 decoder."""
