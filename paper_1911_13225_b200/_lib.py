@@ -16,7 +16,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdist_b200.so")
+LIB_PATH = os.environ.get("DIST_LIB_PATH") or os.path.join(_HERE, "libdist_b200.so")  # override: A/B timing only
 
 DIST_OK, DIST_ERR_CONFIG, DIST_ERR_NUMERIC, DIST_ERR_CUDA = 0, 2, 3, 4
 PREC = {"fp64": 0, "fp32": 1, "bf16x3": 2, "fp16x3": 3}

@@ -286,18 +286,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         tmem_ld32(tq + col, v);
       }
     };
+    // Tile boundaries keep the tensor core busy: the next tile's rows are
+    // fetched while the current tile's last GEMM runs, and a tile's row
+    // results (march update + survivor append) are applied only after the
+    // next tile's layer 0 is handed to the MMA warp.
+    struct RowIn {
+      double p[3];
+      int s, id;
+      int64_t gi;
+    };
+    auto fetch = [&](int64_t t, RowIn &r) {
+      r.gi = t * (2 * ROWS) + (int64_t)rank * ROWS + row;
+      r.p[0] = r.p[1] = r.p[2] = 0.0;
+      r.s = -1;
+      r.id = -1;
+      if (t < ntiles && r.gi < nrows) r.id = load_row(R, m, r.gi, r.p, r.s);
+    };
+    bool pend = false, pvalid = false;
+    int64_t pgi = 0;
+    int pid = -1;
+    double pfv = 0.0;
+    RowIn nx;
+    fetch(cluster, nx);
     uint32_t layer = 0;
     for (int64_t t = cluster; t < ntiles; t += nclusters) {
-      const int64_t base = t * (2 * ROWS) + (int64_t)rank * ROWS;
       // ---- rows and layer 0 (fp64, latent folded into c0) ----
-      double p[3] = {0, 0, 0};
-      int s = -1, id = -1;
-      const int64_t gi = base + row;
-      if (gi < nrows) id = load_row(R, m, gi, p, s);
-      if (row_thread) {
-        m.shape[row] = s;
-        m.ray[row] = id;
-      }
+      double p[3] = {nx.p[0], nx.p[1], nx.p[2]};
+      const int s = nx.s, id = nx.id;
+      const int64_t gi = nx.gi;
       const bool odd = PAIR && (lane & 1);
       const int n0 = P.dv.np[0];
       const double *c0 = P.c0 + (size_t)(s < 0 ? 0 : s) * n0;
@@ -389,9 +405,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       fence_proxy_async();
       epi_sync();
       if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+      // the previous tile's row results, while this tile's first GEMM runs
+      if (row_thread && pend) R.finish(m, pgi, pid, pvalid, pfv);
+      pend = false;
       // ---- hidden layers ----
       float head = 0.f;
       for (int l = 0; l < G; ++l, ++layer) {
+        if (l == G - 1) fetch(t + nclusters, nx);
         mbar_wait(&m.dfull[1], layer & 1);
         mbar_wait(&m.dfull[0], layer & 1);
         tc_fence_after();
@@ -478,6 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (row_thread) {
         const double sum = (double)m.xch[0][row] + (double)m.xch[1][row] +
                            (double)m.xch[2][row] + (double)m.xch[3][row] + (odd ? 0.0 : P.dv.b_out);
+        pend = true;
         double fv;
         if constexpr (PAIR) {
           // f+ - f- without cancellation (mlp_simt.cuh output_pair)
@@ -490,13 +511,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         } else {
           fv = head_act(P.dv.final_act, sum);
         }
-        R.finish(m, gi, m.ray[row], gi < nrows && m.shape[row] >= 0, fv);
+        pgi = gi;
+        pid = id;
+        pvalid = gi < nrows && s >= 0;
+        pfv = fv;
       }
       epi_sync();
       if (G == 0) {  // no hidden GEMM layers: never happens for tc_supported decoders
         if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
       }
     }
+    if (row_thread && pend) R.finish(m, pgi, pid, pvalid, pfv);
   }
   // ---- teardown ----
   tc_fence_before();
