@@ -230,5 +230,22 @@ __device__ __forceinline__ void put8(char *smem, int row, int k0, const float (&
   *reinterpret_cast<uint4 *>(smem + OFF_ALO + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
 }
 
+// write 8 consecutive values (k0 % 8 == 0) of `row` as fp16 into A_hi only
+// (the single-term fp16 activation operand of the backward GEMMs)
+__device__ __forceinline__ void put8h(char *smem, int row, int k0, const float (&x)[8]) {
+  uint32_t h[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const __half2 v = __floats2half2_rn(x[2 * i], x[2 * i + 1]);
+    h[i] = *reinterpret_cast<const uint32_t *>(&v);
+  }
+  *reinterpret_cast<uint4 *>(smem + OFF_AHI + a_off(row, k0)) = make_uint4(h[0], h[1], h[2], h[3]);
+}
+
+// power of two that puts a row maximum `mx` in [2^14, 2^15) (fp16 operands)
+__device__ __forceinline__ float pow2_scale(float mx) {
+  return mx > 0.f ? ldexpf(1.f, min(max(14 - ilogbf(mx), -126), 126)) : 1.f;
+}
+
 }  // namespace tc
 }  // namespace dist

@@ -565,7 +565,10 @@ bool tc_supported(const DecView &dv) {
 //   0: the decoder's forward pack, bf16 or fp16 by precision
 //      tc_w  [G][2][512 n][512 k] (W^T hi, lo)
 //      tc_bias [G][512] hidden biases, [512] w_out, [G] inverse weight scales (fp32)
-//   1: bf16x3 only -- backward pack (W untransposed, bf16 hi/lo) for k_tc_heads
+//   1: bf16x3 only -- backward pack for k_tc_heads: W untransposed as fp16
+//      hi/lo, each layer scaled by a power of two (max |W| in [2^14, 2^15));
+//      tc_bias[1] holds the [G] inverse scales.  The backward GEMMs are
+//      fp16x2: g (one row-scaled fp16 term) x (W_hi + W_lo), see tc_heads.cu
 //   2: bf16x3 only -- fp16x3 forward pack for the (mid, diff) normal probes:
 //      fp16's 11-bit halves carry the diff rows to ~1e-5 where bf16's 8-bit
 //      halves leave ~1e-4 (normals)
@@ -578,7 +581,7 @@ void tc_pack_sizes(const DecView &dv, const std::function<void(int, size_t, size
   const size_t bb = ((size_t)(G + 1) * tc::KDIM + G) * sizeof(float);
   put(0, wb, bb);
   if (dv.prec == DIST_PREC_BF16X3) {
-    put(1, wb, 16);
+    put(1, wb, ((size_t)G * sizeof(float) + 15) / 16 * 16);
     put(2, wb, bb);
   }
 }
@@ -597,15 +600,21 @@ void tc_pack_fill(const DecView &dv, const double *const *W, const double *const
   if (f16) return;
   fill_fwd(dv, W, b, dims, true, reinterpret_cast<uint16_t *>(wdst(2)), bdst(2));
   const int G = dv.n_layers - 2, K = tc::KDIM;
-  auto to16 = [](float x) -> uint16_t { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); };
-  auto from16 = [](uint16_t h) -> float { return __bfloat162float(__ushort_as_bfloat16(h)); };
+  auto to16 = [](float x) -> uint16_t { return __half_as_ushort(__float2half_rn(x)); };
+  auto from16 = [](uint16_t h) -> float { return __half2float(__ushort_as_half(h)); };
   uint16_t *wb = reinterpret_cast<uint16_t *>(wdst(1));
+  float *winv_b = bdst(1);
   for (int g = 0; g < G; ++g) {
     const int l = g + 1;
     const int kin = dims[l], nout = dims[l + 1];
+    double mx = 0.0;
+    for (size_t i = 0; i < (size_t)kin * nout; ++i) mx = std::max(mx, std::fabs(W[l][i]));
+    const int e = mx > 0.0 ? 14 - std::ilogb(mx) : 0;
+    const float sc = std::ldexp(1.f, e);
+    winv_b[g] = std::ldexp(1.f, -e);
     for (int n = 0; n < K; ++n)        // n: layer input index (dgrad output)
       for (int k = 0; k < K; ++k) {    // k: layer output index (contracted)
-        const float x = (n < kin && k < nout) ? (float)W[l][(size_t)n * nout + k] : 0.f;
+        const float x = (n < kin && k < nout) ? (float)W[l][(size_t)n * nout + k] * sc : 0.f;
         const uint16_t h = to16(x);
         wb[(((size_t)g * 2 + 0) * K + n) * K + k] = h;
         wb[(((size_t)g * 2 + 1) * K + n) * K + k] = to16(x - from16(h));
@@ -659,7 +668,7 @@ int tc_make_map(const DecView &dv, int slot, CUtensorMap *map) {
   cuuint64_t gstride[1] = {(cuuint64_t)tc::KDIM * 2};
   cuuint32_t box[2] = {64, 128};
   cuuint32_t estr[2] = {1, 1};
-  const bool f16 = slot == 2 || (slot == 0 && dv.prec == DIST_PREC_FP16X3);
+  const bool f16 = slot != 0 || dv.prec == DIST_PREC_FP16X3;
   const CUtensorMapDataType dt = f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   CUresult r = enc(map, dt, 2, const_cast<void *>(dv.tc_w[slot]), gdim,
                    gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
