@@ -38,6 +38,18 @@ F_Q = 3_674_112      # algorithmic FLOP per decoder query (layer 0 folded, no sk
 F_B = 3_671_040      # algorithmic FLOP per differentiated sample (dgrad, no wgrad), SURVEY 8d
 
 
+def _traffic(queries):
+    """DRAM bytes of the march kernel per trace phase: bytes/query from the
+    committed ncu --set full capture (profiles/r01_ncu_traffic.json) x this
+    run's queries per step.  None if the capture summary is absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_traffic.json")) as fh:
+            t = json.load(fh)
+        return t["bytes_per_query"] * queries, t
+    except Exception:
+        return None, None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -285,6 +297,7 @@ def main():
     achieved = flops_trace / (trace_ms * 1e-3) / 1e12
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     split = 3.0 if args.precision in ("bf16x3", "fp16x3") else 1.0
+    traffic, tsrc = _traffic(queries) if args.precision == "bf16x3" else (None, None)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
@@ -297,7 +310,11 @@ def main():
         "replicas_bit_identical": consistent,
         "clocks": clk.summary(),
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_note": None if tsrc is None else (
+                         f"DRAM bytes per trace phase = {tsrc['bytes_per_query']:.0f} B/query "
+                         f"(ncu --set full, {tsrc['capture']}) x queries; algorithmic <= "
+                         f"{tsrc['algorithmic_bytes_per_query_max']} B/query, weights stream from L2"),
                      "executed_mma_tflops": achieved * split,
                      "executed_frac": achieved * split / peak,
                      "kernel": "march step kernels (decoder + update), whole trace phase",
