@@ -39,6 +39,7 @@ struct HParams {
   const float *winv_b; // [G] inverse power-of-two scales of the backward pack
   int n_gemm;
   int S;
+  int timeline;        // DIST_TC_TIMELINE: CTA 0 / thread 64 records %globaltimer marks
   double *part0;       // [grid][S][512]
 };
 
@@ -53,6 +54,18 @@ __device__ __forceinline__ void tmem_ld4(uint32_t taddr, uint32_t (&r)[4]) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Mask words indexed by a run-time nh: selects keep the array in registers
+// (a dynamic subscript would put it in local memory).
+__device__ __forceinline__ uint32_t get4(const uint32_t (&a)[4], int i) {
+  return i == 0 ? a[0] : (i == 1 ? a[1] : (i == 2 ? a[2] : a[3]));
+}
+__device__ __forceinline__ void set4(uint32_t (&a)[4], int i, uint32_t v) {
+  a[0] = i == 0 ? v : a[0];
+  a[1] = i == 1 ? v : a[1];
+  a[2] = i == 2 ? v : a[2];
+  a[3] = i == 3 ? v : a[3];
 }
 
 // Sum v[0..63] over the 32 lanes of the warp; afterwards lane l holds the
@@ -70,6 +83,18 @@ __device__ __forceinline__ void warp_colsum64(float (&v)[64]) {
     }
   }
 }
+
+// debug timeline (DIST_TC_TIMELINE=1): (mark id, %globaltimer) pairs of CTA 0's
+// first epilogue thread; read with dist_debug_heads_timeline
+static __device__ unsigned long long g_heads_tl[4096];
+#define TL(id)                                                                        \
+  do {                                                                                \
+    if (tl_on && tl_i < 4096) {                                                       \
+      unsigned long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      g_heads_tl[tl_i++] = ((unsigned long long)(id) << 56) | (t_ & 0xFFFFFFFFFFFFFFull); \
+    }                                                                                 \
+  } while (0)
 
 template <class Gen>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
@@ -173,6 +198,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
   } else {
     // ===== epilogue warps =====
+    const bool tl_on = P.timeline && blockIdx.x == 0 && threadIdx.x == 64;
+    int tl_i = 0;
     const int q = warp & 3;
     const int sub = (warp - 2) >> 2;
     const int row = (q & 1) * 32 + lane;
@@ -185,6 +212,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     uint32_t phase = 0;
     float *gout = reinterpret_cast<float *>(&m.xch[0][0]);   // [64] per-row head gradient
     for (int64_t t = cluster; t < ntiles; t += nclusters) {
+      TL(1);
       const int64_t gi = t * (2 * ROWS) + (int64_t)rank * ROWS + row;
       double p[3] = {0, 0, 0};
       int s = -1;
@@ -216,7 +244,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               bits |= (on0 ? 1u : 0u) << e;
               bits |= (on1 ? 1u : 0u) << (e + 1);
             }
-            mk[nh * 2 + (j >> 5)] |= bits << (j & 31);
+            set4(mk, nh * 2 + (j >> 5), get4(mk, nh * 2 + (j >> 5)) | (bits << (j & 31)));
             put8<false>(smem, row, cb + j, x);
           }
         }
@@ -226,10 +254,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       tc_fence_before();
       epi_sync();
       if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+      TL(2);
       // ---- forward hidden layers ----
       float head = 0.f;
       for (int l = 0; l < G; ++l, ++phase) {
         mbar_wait(&m.dfull[1], phase & 1);
+        TL(3);
         mbar_wait(&m.dfull[0], phase & 1);
         tc_fence_after();
         const bool last = (l == G - 1);
@@ -256,7 +286,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               }
               if (!last) put8<false>(smem, row, cb + c * 32 + g8 * 8, x);
             }
-            mk[nh * 2 + c] = bits;
+            set4(mk, nh * 2 + c, bits);
           }
         }
         tmem_st4(mask_addr(l + 1), mk);
@@ -265,6 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           fence_proxy_async();
           epi_sync();
           if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+          TL(4);
         }
       }
       // ---- head, seed, d loss / d h_G ----
@@ -284,6 +315,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       epi_sync();
       if (row_thread) gout[row] = (float)go;
       epi_sync();
+      TL(5);
       // Row scale exchange for the fp16 backward operand: every epilogue warp
       // posts its part max, the row's scale is a power of two of the total.
       auto row_max = [&](float part) -> float {
@@ -304,15 +336,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int j = 0; j < 64; j += 8) {
             float wo[8];
             ldg8(P.w_out + cb + j, wo);
+            const uint32_t wb = get4(mk, nh * 2 + (j >> 5)) >> (j & 31);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int jj = j + e;
-              const bool on = (mk[nh * 2 + (jj >> 5)] >> (jj & 31)) & 1u;
-              part = fmaxf(part, on ? fabsf(gr * wo[e]) : 0.f);
-            }
+            for (int e = 0; e < 8; ++e) part = fmaxf(part, ((wb >> e) & 1u) ? fabsf(wo[e]) : 0.f);
           }
         }
-        const float sc = pow2_scale(row_max(part));
+        const float sc = pow2_scale(row_max(part * fabsf(gr)));
         rinv = 1.f / sc;
         for (int nh = 0; nh < 2; ++nh) {
           const int cb = nh * 256 + half * 128 + sub * 64;
@@ -320,12 +349,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int j = 0; j < 64; j += 8) {
             float x[8], wo[8];
             ldg8(P.w_out + cb + j, wo);
+            const uint32_t wb = get4(mk, nh * 2 + (j >> 5)) >> (j & 31);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              const int jj = j + e;
-              const bool on = (mk[nh * 2 + (jj >> 5)] >> (jj & 31)) & 1u;
-              x[e] = on ? (gr * sc) * wo[e] : 0.f;
-            }
+            for (int e = 0; e < 8; ++e) x[e] = ((wb >> e) & 1u) ? (gr * sc) * wo[e] : 0.f;
             put8h(smem, row, cb + j, x);
           }
         }
@@ -334,9 +360,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       tc_fence_before();
       epi_sync();
       if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+      TL(6);
       // ---- backward through GEMM layers G-1 .. 0 ----
       for (int gl = G - 1; gl >= 0; --gl, ++phase) {
         mbar_wait(&m.dfull[1], phase & 1);
+        TL(7);
         mbar_wait(&m.dfull[0], phase & 1);
         tc_fence_after();
         uint32_t mk[4];
@@ -350,7 +378,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             for (int c = 0; c < 2; ++c) {
               float v[32];
               tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
-              const uint32_t bits = mk[nh * 2 + c];
+              const uint32_t bits = get4(mk, nh * 2 + c);
 #pragma unroll
               for (int e = 0; e < 32; ++e) part = fmaxf(part, ((bits >> e) & 1u) ? fabsf(v[e]) : 0.f);
             }
@@ -363,7 +391,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             for (int c = 0; c < 2; ++c) {
               float v[32];
               tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
-              const uint32_t bits = mk[nh * 2 + c];
+              const uint32_t bits = get4(mk, nh * 2 + c);
 #pragma unroll
               for (int g8 = 0; g8 < 4; ++g8) {
                 float x[8];
@@ -378,21 +406,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           fence_proxy_async();
           epi_sync();
           if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+          TL(8);
         } else {
-          // g_pre0 = D * mask0; column sums over the CTA's rows, per shape
-          float gv[2][64];
-          for (int nh = 0; nh < 2; ++nh)
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              float v[32];
-              tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
-              const uint32_t bits = mk[nh * 2 + c];
-#pragma unroll
-              for (int e = 0; e < 32; ++e) gv[nh][c * 32 + e] = ((bits >> e) & 1u) ? v[e] * unscale : 0.f;
-            }
-          tc_fence_before();
-          epi_sync();   // every row's shape is in m.shape; all TMEM reads of this tile done
-          // distinct shapes of this CTA's rows (usually one)
+          // g_pre0 = D * mask0 * unscale; column sums over the CTA's rows, per
+          // shape.  TMEM is read inside the shape loop (usually one pass), so no
+          // per-thread copy of the 128 values is kept (it lived in local memory).
           float *red = reinterpret_cast<float *>(smem + OFF_AHI);  // A is free now: [2][512] floats
           int shapes_done = 0;
           for (int guard = 0; guard < ROWS; ++guard) {
@@ -407,19 +425,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             for (int nh = 0; nh < 2; ++nh) {
               float w[64];
 #pragma unroll
-              for (int e = 0; e < 64; ++e) w[e] = mine ? gv[nh][e] : 0.f;
+              for (int c = 0; c < 2; ++c) {
+                float v[32];
+                tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
+                const uint32_t bits = mine ? get4(mk, nh * 2 + c) : 0u;
+#pragma unroll
+                for (int e = 0; e < 32; ++e) w[c * 32 + e] = ((bits >> e) & 1u) ? v[e] * unscale : 0.f;
+              }
               warp_colsum64(w);
               const int cb = nh * 256 + half * 128 + sub * 64;
               // the two row-warps (q&1 = 0, 1) of this column block combine in smem
               red[(q & 1) * 512 + cb + 2 * lane] = w[0];
               red[(q & 1) * 512 + cb + 2 * lane + 1] = w[1];
             }
+            tc_fence_before();
             epi_sync();
             double *dst = P.part0 + ((size_t)blockIdx.x * P.S + next) * n0;
             for (int col = threadIdx.x - 64; col < KDIM; col += N_EPI_WARPS * 32)
               dst[col] += (double)red[col] + (double)red[512 + col];
             epi_sync();
             shapes_done = next + 1;
+            TL(9);
           }
         }
       }
@@ -455,6 +481,10 @@ int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t
   P.winv_b = dv.tc_bias[1];
   P.n_gemm = dv.n_layers - 2;
   P.S = S;
+  {
+    const char *tl = getenv("DIST_TC_TIMELINE");
+    P.timeline = tl ? atoi(tl) : 0;
+  }
   P.part0 = part0;
   const void *fn = (const void *)tc::k_tc_heads<Gen>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
@@ -465,6 +495,11 @@ int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t
   tc::k_tc_heads<Gen><<<2 * pairs, tc::THREADS, tc::SMEM_BYTES, st>>>(mf, mb, P, gen);
   DIST_CHECK_LAUNCH("k_tc_heads");
   return DIST_OK;
+}
+
+extern "C" DIST_API int dist_debug_heads_timeline(unsigned long long *out, int n) {
+  return cudaMemcpyFromSymbol(out, tc::g_heads_tl, sizeof(unsigned long long) * (size_t)std::min(n, 4096)) ==
+                 cudaSuccess ? 0 : -1;
 }
 
 template int launch_tc_heads<ObjGen>(const DecView &, const double *, const ObjGen &, int64_t, int,
