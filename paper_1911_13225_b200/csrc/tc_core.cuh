@@ -181,6 +181,26 @@ __device__ __forceinline__ void ldg8(const float *p, float (&x)[8]) {
   x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
 }
 
+// 32 consecutive fp32 constants (128-byte aligned), issued ahead of a TMEM load
+__device__ __forceinline__ void ldg32(const float *p, float (&x)[32]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float4 a = __ldg(reinterpret_cast<const float4 *>(p) + i);
+    x[4 * i] = a.x; x[4 * i + 1] = a.y; x[4 * i + 2] = a.z; x[4 * i + 3] = a.w;
+  }
+}
+
+// Debug phase timeline (DIST_TC_TIMELINE=1): CTA 0's first epilogue thread
+// appends (mark id << 56 | %globaltimer) to a per-kernel device buffer.
+#define DIST_TL_MARK(buf, id)                                                          \
+  do {                                                                                \
+    if (tl_on && tl_i < 4096) {                                                       \
+      unsigned long long t_;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
+      buf[tl_i++] = ((unsigned long long)(id) << 56) | (t_ & 0xFFFFFFFFFFFFFFull);    \
+    }                                                                                 \
+  } while (0)
+
 // byte offset of A[row][k] (bf16) inside one 64 KB hi/lo part
 __device__ __forceinline__ uint32_t a_off(int row, int k) {
   const int kb = k >> 6, kk = k & 63;

@@ -87,14 +87,7 @@ __device__ __forceinline__ void warp_colsum64(float (&v)[64]) {
 // debug timeline (DIST_TC_TIMELINE=1): (mark id, %globaltimer) pairs of CTA 0's
 // first epilogue thread; read with dist_debug_heads_timeline
 static __device__ unsigned long long g_heads_tl[4096];
-#define TL(id)                                                                        \
-  do {                                                                                \
-    if (tl_on && tl_i < 4096) {                                                       \
-      unsigned long long t_;                                                          \
-      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                          \
-      g_heads_tl[tl_i++] = ((unsigned long long)(id) << 56) | (t_ & 0xFFFFFFFFFFFFFFull); \
-    }                                                                                 \
-  } while (0)
+#define TL(id) DIST_TL_MARK(g_heads_tl, id)
 
 template <class Gen>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
@@ -269,13 +262,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            float v[32];
+            float v[32], bbc[32];
+            ldg32(bias + cb + c * 32, bbc);   // in flight across the TMEM load
             tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
             uint32_t bits = 0;
 #pragma unroll
             for (int g8 = 0; g8 < 4; ++g8) {
-              float x[8], bb[8], wo[8];
-              ldg8(bias + cb + c * 32 + g8 * 8, bb);
+              float x[8], wo[8];
+              const float *bb = bbc + g8 * 8;
               if (last) ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
 #pragma unroll
               for (int e = 0; e < 8; ++e) {

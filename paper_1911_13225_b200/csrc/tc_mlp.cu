@@ -47,6 +47,7 @@ struct Params {
   const float *winv;      // [L-2] inverse power-of-2 weight scales (fp16x3), 1 for bf16x3
   int n_gemm;             // hidden GEMM layers (L-2)
   int acc_mode;           // 0: one accumulator; 1: two (even/odd K blocks); 2: hi*hi | corrections
+  int timeline;           // DIST_TC_TIMELINE: phase marks of CTA 0 (debug)
   int debug;              // timing experiments: 1 = no epilogue math, 2 = no MMAs (results invalid)
 };
 
@@ -149,6 +150,9 @@ __device__ __forceinline__ float relu_pair_sel(float m, float d, bool odd) {
   const float a = fmaxf(m + d, 0.f), b = fmaxf(m - d, 0.f);
   return 0.5f * (odd ? a - b : a + b);
 }
+
+static __device__ unsigned long long g_mlp_tl[4096];
+#define TL(id) DIST_TL_MARK(g_mlp_tl, id)
 
 // ---------------------------------------------------------------------------
 // PAIR: rows 2i / 2i+1 are the probes p+ / p- of one central difference and
@@ -269,6 +273,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
   } else {
     // ===== epilogue warps (both CTAs) =====
+    const bool tl_on = P.timeline && blockIdx.x == 0 && threadIdx.x == 64;
+    int tl_i = 0;
     const int q = warp & 3;                 // TMEM lane quarter of this warp
     const int sub = (warp - 2) >> 2;        // which 64 of the quarter's 128 columns
     const int row = (q & 1) * 32 + lane;    // tile row owned in TMEM
@@ -310,6 +316,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     fetch(cluster, nx);
     uint32_t layer = 0;
     for (int64_t t = cluster; t < ntiles; t += nclusters) {
+      TL(1);
       // ---- rows and layer 0 (fp64, latent folded into c0) ----
       double p[3] = {nx.p[0], nx.p[1], nx.p[2]};
       const int s = nx.s, id = nx.id;
@@ -405,14 +412,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       fence_proxy_async();
       epi_sync();
       if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+      TL(2);
       // the previous tile's row results, while this tile's first GEMM runs
       if (row_thread && pend) R.finish(m, pgi, pid, pvalid, pfv);
       pend = false;
+      TL(10);
       // ---- hidden layers ----
       float head = 0.f;
       for (int l = 0; l < G; ++l, ++layer) {
         if (l == G - 1) fetch(t + nclusters, nx);
         mbar_wait(&m.dfull[1], layer & 1);
+        TL(3);
         mbar_wait(&m.dfull[0], layer & 1);
         tc_fence_after();
         const bool last = (l == G - 1);
@@ -490,6 +500,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           fence_proxy_async();
           epi_sync();
           if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+          TL(4);
         }
       }
       // ---- head: combine the four partial dot products of each row ----
@@ -517,6 +528,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         pfv = fv;
       }
       epi_sync();
+      TL(9);
       if (G == 0) {  // no hidden GEMM layers: never happens for tc_supported decoders
         if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
       }
@@ -695,6 +707,8 @@ static int launch_tc_t(const DecView &dv, const double *c0, const Rows &rows, in
     P.acc_mode = am ? atoi(am) : 3;
     const char *dbg = getenv("DIST_TC_DEBUG");
     P.debug = dbg ? atoi(dbg) : 0;
+    const char *tl = getenv("DIST_TC_TIMELINE");
+    P.timeline = tl ? atoi(tl) : 0;
   }
   const void *fn = (const void *)tc::k_tc_mlp<F16, Rows, PAIR>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
@@ -710,6 +724,11 @@ static int launch_tc(const DecView &dv, const double *c0, const Rows &rows, int6
                      cudaStream_t st) {
   if (dv.prec == DIST_PREC_FP16X3) return launch_tc_t<true, Rows, PAIR>(dv, c0, rows, tiles_bound, st);
   return launch_tc_t<false, Rows, PAIR>(dv, c0, rows, tiles_bound, st);
+}
+
+extern "C" DIST_API int dist_debug_mlp_timeline(unsigned long long *out, int n) {
+  return cudaMemcpyFromSymbol(out, tc::g_mlp_tl, sizeof(unsigned long long) * (size_t)std::min(n, 4096)) ==
+                 cudaSuccess ? 0 : -1;
 }
 
 int tc_eval_probes(const DecView &dv, const double *c0, const ProbeGen &gen, int64_t n_bound,
