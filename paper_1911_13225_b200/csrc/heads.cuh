@@ -87,6 +87,50 @@ struct ObjGen {
     return sd;
   }
   __device__ void store(int64_t i, double v) const { h.f[i] = v; }
+
+  // seed(i, f) split in two for the tensor-core head kernel: prep() does every
+  // load at tile start (overlapping the forward GEMMs), apply() needs only f.
+  // Bit-identical to seed(): the +-1 sign factor commutes exactly with the
+  // roundings it is moved across.
+  struct Prep {
+    double d, scale, obs, c1, ginv, sil;   // c1 = w_depth * (w * scale); 0 if no depth term
+  };
+  __device__ Prep prep(int64_t i) const {
+    Prep r{0.0, 0.0, 0.0, 0.0, 1.0, 0.0};
+    const int64_t flat = h.samp[i];
+    const int64_t g = flat / K;
+    const int v = (int)(g / WH);
+    if (in.obs_depth && ls.status[g] == DIST_CONVERGED && depth_valid(in, g) && npx[v] > 0) {
+      int cnt = 0;
+      for (int k = 0; k < K; ++k) cnt += isfinite(ls.tk_a[g * K + k]) ? 1 : 0;
+      const int64_t q = g - v * WH;
+      const int j = (int)(q / ls.lw), ii = (int)(q - (int64_t)j * ls.lw);
+      double dir[3], scale;
+      pixel_ray(cams[v], ii, j, 1, dir, &scale);
+      const double w = (1.0 / cnt) / (double)npx[v];
+      r.d = ls.tk_d[flat];
+      r.scale = scale;
+      r.obs = in.obs_depth[g];
+      r.c1 = in.w_depth * __dmul_rn(w, scale);
+      if (gdotv) {
+        const double gv = gdotv[g];
+        r.ginv = gv < -1e-3 ? (-1.0 / gv) : 0.0;
+      }
+    }
+    if (sil_seed && flat - g * K == 0) r.sil = sil_seed[g];
+    return r;
+  }
+  __device__ double apply(const Prep &p, double f) const {
+    double sd = 0.0;
+    if (p.c1 != 0.0) {
+      const double r = __dmul_rn(__dadd_rn(p.d, f), p.scale) - p.obs;
+      const double sg = r > 0.0 ? 1.0 : (r < 0.0 ? -1.0 : 0.0);
+      sd = sg * p.c1;
+      if (gdotv) sd = sd * p.ginv;
+    }
+    if (sil_seed) sd = __dadd_rn(sd, p.sil);
+    return sd;
+  }
 };
 
 }  // namespace dist

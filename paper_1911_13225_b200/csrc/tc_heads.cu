@@ -210,6 +210,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       double p[3] = {0, 0, 0};
       int s = -1;
       if (gi < nrows && !gen.point(gi, p, s)) s = -1;
+
       if (row_thread) m.shape[row] = s;
       // ---- layer 0 (folded bias + p . W0p, fp32) + mask 0 ----
       {
@@ -248,6 +249,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       epi_sync();
       if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
       TL(2);
+      // the seed's loads, issued once layer 0 is handed to the MMA warp so
+      // they land during the forward GEMMs
+      typename Gen::Prep sp{};
+      if (row_thread && gi < nrows && s >= 0) sp = gen.prep(gi);
       // ---- forward hidden layers ----
       float head = 0.f;
       for (int l = 0; l < G; ++l, ++phase) {
@@ -302,7 +307,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const double fv = head_act(P.dv.final_act, sum);
         if (gi < nrows && s >= 0) {
           gen.store(gi, fv);
-          const double sd = gen.seed(gi, fv);
+          const double sd = gen.apply(sp, fv);
           go = sd * head_dact(P.dv.final_act, fv);
         }
       }
