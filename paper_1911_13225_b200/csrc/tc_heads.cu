@@ -204,12 +204,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int n0 = P.dv.np[0];
     uint32_t phase = 0;
     float *gout = reinterpret_cast<float *>(&m.xch[0][0]);   // [64] per-row head gradient
+    // the next tile's sample point is fetched during the current tile's last
+    // backward GEMM (a dependent chain of global loads)
+    auto fetch = [&](int64_t tt, double (&q)[3], int &ss) {
+      const int64_t g2 = tt * (2 * ROWS) + (int64_t)rank * ROWS + row;
+      q[0] = q[1] = q[2] = 0.0;
+      ss = -1;
+      if (tt < ntiles && g2 < nrows && !gen.point(g2, q, ss)) ss = -1;
+    };
+    double nxp[3];
+    int nxs;
+    fetch(cluster, nxp, nxs);
     for (int64_t t = cluster; t < ntiles; t += nclusters) {
       TL(1);
       const int64_t gi = t * (2 * ROWS) + (int64_t)rank * ROWS + row;
-      double p[3] = {0, 0, 0};
-      int s = -1;
-      if (gi < nrows && !gen.point(gi, p, s)) s = -1;
+      double p[3] = {nxp[0], nxp[1], nxp[2]};
+      const int s = nxs;
 
       if (row_thread) m.shape[row] = s;
       // ---- layer 0 (folded bias + p . W0p, fp32) + mask 0 ----
@@ -362,6 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       TL(6);
       // ---- backward through GEMM layers G-1 .. 0 ----
       for (int gl = G - 1; gl >= 0; --gl, ++phase) {
+        if (gl == 0) fetch(t + nclusters, nxp, nxs);
         mbar_wait(&m.dfull[1], phase & 1);
         TL(7);
         mbar_wait(&m.dfull[0], phase & 1);
