@@ -87,6 +87,13 @@ __device__ __forceinline__ void tc_fence_after() {
 __device__ __forceinline__ void epi_sync() {  // named barrier over the epilogue warps
   asm volatile("bar.sync 1, %0;" ::"n"(N_EPI_WARPS * 32) : "memory");
 }
+// producer / consumer named barriers (count = arriving + syncing threads)
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(count) : "memory");
+}
 __device__ __forceinline__ void tma_load_2sm(uint32_t dst, const CUtensorMap *map, uint64_t *bar,
                                              int x, int y) {
   const uint32_t mb = smem_u32(bar) & 0xFEFFFFFFu;  // leader CTA's barrier

@@ -37,6 +37,7 @@ struct HParams {
   const float *bias;   // [G][512]
   const float *w_out;  // [512]
   const float *winv_b; // [G] inverse power-of-two scales of the backward pack
+  const float *nrm_b;  // [G] max row l1 norm of each backward W: |g W^T| <= max|g| * nrm
   int n_gemm;
   int S;
   int timeline;        // DIST_TC_TIMELINE: CTA 0 / thread 64 records %globaltimer marks
@@ -334,6 +335,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         return fmaxf(fmaxf(m.xch[0][row], m.xch[1][row]), fmaxf(m.xch[2][row], m.xch[3][row]));
       };
       float rinv;   // 1 / (this row's scale of the A operand now in smem)
+      float amax;   // max |g| of this row's A operand (true units)
       {
         const float gr = gout[row];
         uint32_t mk[4];
@@ -350,7 +352,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             for (int e = 0; e < 8; ++e) part = fmaxf(part, ((wb >> e) & 1u) ? fabsf(wo[e]) : 0.f);
           }
         }
-        const float sc = pow2_scale(row_max(part * fabsf(gr)));
+        amax = row_max(part * fabsf(gr));
+        const float sc = pow2_scale(amax);
         rinv = 1.f / sc;
         for (int nh = 0; nh < 2; ++nh) {
           const int cb = nh * 256 + half * 128 + sub * 64;
@@ -382,19 +385,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         // D = (g / rinv) (W / winv_b): true dgrad = D * unscale
         const float unscale = rinv * P.winv_b[gl];
         if (gl > 0) {
-          float part = 0.f;   // pass 1: row max of |masked D|
-          for (int nh = 0; nh < 2; ++nh)
-#pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              float v[32];
-              tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
-              const uint32_t bits = get4(mk, nh * 2 + c);
-#pragma unroll
-              for (int e = 0; e < 32; ++e) part = fmaxf(part, ((bits >> e) & 1u) ? fabsf(v[e]) : 0.f);
-            }
-          const float sc = pow2_scale(row_max(part) * unscale);
+          // One pass: the scale comes from a rigorous bound, |g_next| <= amax *
+          // nrm_b[gl], so the fp16 operand cannot overflow; the true row max
+          // of what is written becomes the next phase's amax.
+          const float sc = pow2_scale(amax * P.nrm_b[gl]);
           const float f = unscale * sc;   // exact: powers of two
           rinv = 1.f / sc;
+          float part = 0.f;
           for (int nh = 0; nh < 2; ++nh) {
             const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll
@@ -406,15 +403,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               for (int g8 = 0; g8 < 4; ++g8) {
                 float x[8];
 #pragma unroll
-                for (int e = 0; e < 8; ++e)
+                for (int e = 0; e < 8; ++e) {
                   x[e] = ((bits >> (g8 * 8 + e)) & 1u) ? v[g8 * 8 + e] * f : 0.f;
+                  part = fmaxf(part, fabsf(x[e]));
+                }
                 put8h(smem, row, cb + c * 32 + g8 * 8, x);
               }
             }
           }
+          // post this warp's part max; barrier 2 orders it after every warp's
+          // read of the previous phase's maxima (bar.arrive there, below)
+          if (gl < G - 1) named_sync(2, 2 * N_EPI_WARPS * 32);
+          m.xch[half * 2 + sub][row] = part * rinv;
           tc_fence_before();
           fence_proxy_async();
           epi_sync();
+          amax = fmaxf(fmaxf(m.xch[0][row], m.xch[1][row]), fmaxf(m.xch[2][row], m.xch[3][row]));
+          if (gl >= 2) named_arrive(2, 2 * N_EPI_WARPS * 32);
           if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
           TL(8);
         } else {
@@ -489,6 +494,7 @@ int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t
   P.bias = dv.tc_bias[0];
   P.w_out = dv.tc_bias[0] + (size_t)(dv.n_layers - 2) * tc::KDIM;
   P.winv_b = dv.tc_bias[1];
+  P.nrm_b = dv.tc_bias[1] + (dv.n_layers - 2);
   P.n_gemm = dv.n_layers - 2;
   P.S = S;
   {
