@@ -41,6 +41,7 @@ __global__ void k_code_bias(DecView dv, const double *__restrict__ codes, int S,
     double v = dv.b0[j];
     for (int k = 0; k < D; ++k) v = fma(codes[(size_t)s * D + k], dv.W0z[(size_t)k * n0 + j], v);
     c0[idx] = v;
+    reinterpret_cast<float *>(c0 + total)[idx] = (float)v;   // fp32 copy (kernels.cuh c0_f32)
   }
   if (dv.skip > 0) {
     const int ns = dv.nskip;
@@ -107,12 +108,12 @@ int vjp_grid_cap(int prec) {
   return 4 * sm_count();
 }
 
-int eval_points(const DecView &dv, const double *c0, const double *cskip, const double *pts,
+int eval_points(const DecView &dv, const double *c0, const double *cskip, int S, const double *pts,
                 const int32_t *shape, int64_t n, double *f, cudaStream_t st) {
   if (n <= 0) return DIST_OK;
   ArrayGen g{pts, shape, nullptr, f, n};
   if (dv.prec == DIST_PREC_FP64) return launch_eval_gen<double>(dv, c0, cskip, g, n, st);
-  if (dv.prec >= DIST_PREC_BF16X3) return tc_eval_points(dv, c0, cskip, pts, shape, n, f, st);
+  if (dv.prec >= DIST_PREC_BF16X3) return tc_eval_points(dv, c0, cskip, S, pts, shape, n, f, st);
   return launch_eval_gen<float>(dv, c0, cskip, g, n, st);
 }
 
@@ -139,7 +140,7 @@ int reduce_code_grad(const DecView &dv, int S, int G, const double *part0, const
 size_t eval_ws(const DecView &dv, int64_t n, int S, bool vjp) {
   Carve cv{nullptr, 0, ~size_t(0)};
   const int s1 = std::max(S, 1);
-  cv.take<double>((size_t)s1 * dv.np[0]);
+  cv.take<double>(c0_doubles(s1, dv.np[0]));
   cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
   if (vjp) {
     const int G = vjp_grid_cap(dv.prec);
@@ -351,7 +352,7 @@ int dist_eval(const dist_decoder *dec, const double *codes, int S, const double 
   cudaStream_t st = (cudaStream_t)stream;
   Carve cv{(char *)ws, 0, ws_bytes};
   const int s1 = std::max(S, 1);
-  double *c0 = cv.take<double>((size_t)s1 * dv.np[0]);
+  double *c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
   double *cs = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
   if (!cv.ok) return fail(DIST_ERR_CONFIG, "workspace too small");
   int rc;
@@ -361,7 +362,7 @@ int dist_eval(const dist_decoder *dec, const double *codes, int S, const double 
     rc = launch_code_bias(dv, nullptr, 1, c0, cs, st);
   }
   if (rc) return rc;
-  return eval_points(dv, c0, cs, pts, shape, n, f, st);
+  return eval_points(dv, c0, cs, s1, pts, shape, n, f, st);
 }
 
 int dist_eval_vjp(const dist_decoder *dec, const double *codes, int S, const double *pts,
@@ -373,7 +374,7 @@ int dist_eval_vjp(const dist_decoder *dec, const double *codes, int S, const dou
   cudaStream_t st = (cudaStream_t)stream;
   const int s1 = std::max(S, 1);
   Carve cv{(char *)ws, 0, ws_bytes};
-  double *c0 = cv.take<double>((size_t)s1 * dv.np[0]);
+  double *c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
   double *cs = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
   const int G = vjp_grid_cap(dv.prec);
   double *part0 = cv.take<double>((size_t)G * s1 * dv.np[0]);

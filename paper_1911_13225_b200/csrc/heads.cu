@@ -228,7 +228,7 @@ static ObjLayout obj_layout(const DecView &dv, int V, int W, int H, int K, int S
   L.conv_count = cv.take<int32_t>(4);
   L.npx = cv.take<int32_t>(V);
   L.bcount = cv.take<int32_t>(ceil_div(n * K, kScanBlock) + 1);
-  L.c0 = cv.take<double>((size_t)s1 * dv.np[0]);
+  L.c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
   L.cs = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
   const int G = vjp_grid_cap(dv.prec);
   L.part0 = cv.take<double>((size_t)G * s1 * dv.np[0]);
@@ -305,7 +305,7 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
   if (e == cudaSuccess) e = cudaMemsetAsync(io->grad, 0, sizeof(double) * s1 * std::max(dv.latent_dim, 1), sm);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(objective)");
   if (io->grad_mode == 1) {
-    rc = normals_pass(dv, L.c0, L.cs, cams, ls, cfg, nullptr, L.gdotv, L.conv, L.conv_count,
+    rc = normals_pass(dv, L.c0, L.cs, s1, cams, ls, cfg, nullptr, L.gdotv, L.conv, L.conv_count,
                       L.bcount, L.probe_f, sm);
     if (rc) return rc;
   } else if (io->grad_mode != 0) {

@@ -7,9 +7,18 @@
 namespace dist {
 
 int sm_count();
+// c0 buffers hold [s1][np0] fp64 followed by the same values in fp32 (read by
+// the tensor-core prologues, which would otherwise convert per row and column)
+inline size_t c0_doubles(int s1, int np0) {
+  const size_t n = (size_t)s1 * np0;
+  return n + (n + 1) / 2;
+}
+inline const float *c0_f32(const double *c0, int s1, int np0) {
+  return reinterpret_cast<const float *>(c0 + (size_t)s1 * np0);
+}
 int launch_code_bias(const DecView &dv, const double *codes, int S, double *c0, double *cskip,
                      cudaStream_t st);
-int eval_points(const DecView &dv, const double *c0, const double *cskip, const double *pts,
+int eval_points(const DecView &dv, const double *c0, const double *cskip, int S, const double *pts,
                 const int32_t *shape, int64_t n, double *f, cudaStream_t st);
 int vjp_points(const DecView &dv, const double *c0, const double *cskip, const double *pts,
                const int32_t *shape, int64_t n, const double *seed, int S, double *f,
@@ -21,7 +30,7 @@ int vjp_grid_cap(int prec);
 size_t eval_ws(const DecView &dv, int64_t n, int S, bool vjp);
 
 // tensor-core (tcgen05) split-precision decoder, tc_mlp.cu
-int tc_eval_points(const DecView &dv, const double *c0, const double *cskip, const double *pts,
+int tc_eval_points(const DecView &dv, const double *c0, const double *cskip, int S, const double *pts,
                    const int32_t *shape, int64_t n, double *f, cudaStream_t st);
 void tc_pack_sizes(const DecView &dv, const std::function<void(int, size_t, size_t)> &put);
 void tc_pack_fill(const DecView &dv, const double *const *W, const double *const *b,
@@ -39,9 +48,9 @@ int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t
 
 struct LevelState;
 struct ProbeGen;
-int tc_eval_probes(const DecView &dv, const double *c0, const ProbeGen &gen, int64_t n_bound,
+int tc_eval_probes(const DecView &dv, const double *c0, int S, const ProbeGen &gen, int64_t n_bound,
                    cudaStream_t st);
-int normals_pass(const DecView &dv, const double *c0, const double *cs, const dist_camera *cams,
+int normals_pass(const DecView &dv, const double *c0, const double *cs, int S, const dist_camera *cams,
                  const LevelState &ls, const dist_trace_config *cfg, double *normals, double *gdotv,
                  int32_t *conv, int32_t *count, int32_t *bcount, double *f, cudaStream_t st);
 

@@ -123,7 +123,7 @@ __device__ __forceinline__ void step_epilogue(Ctl *ctl, int cur, int64_t queried
   }
 }
 
-int tc_run_steps(const DecView &dv, const double *c0, const double *cskip,
+int tc_run_steps(const DecView &dv, const double *c0, const double *cskip, int S,
                  const dist_camera *cams, const LevelState &ls, Ctl *ctl, int32_t *l0, int32_t *l1,
                  const MarchArgs &a, int slots, int64_t *live, int64_t *stats, cudaStream_t st);
 

@@ -34,6 +34,7 @@ namespace tc {
 struct HParams {
   DecView dv;
   const double *c0;
+  const float *c0f;    // fp32 copy of c0 (kernels.cuh c0_f32)
   const float *bias;   // [G][512]
   const float *w_out;  // [512]
   const float *winv_b; // [G] inverse power-of-two scales of the backward pack
@@ -225,29 +226,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (row_thread) m.shape[row] = s;
       // ---- layer 0 (folded bias + p . W0p, fp32) + mask 0 ----
       {
-        const double *c0 = P.c0 + (size_t)(s < 0 ? 0 : s) * n0;
+        const float *c0f = P.c0f + (size_t)(s < 0 ? 0 : s) * n0;
         const float px = (float)p[0], py = (float)p[1], pz = (float)p[2];
         uint32_t mk[4] = {0, 0, 0, 0};
         for (int nh = 0; nh < 2; ++nh) {
           const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll 2
           for (int j = 0; j < 64; j += 8) {
-            float x[8], w0[8], w1[8], w2[8];
+            float x[8], w0[8], w1[8], w2[8], cf[8];
             ldg8(P.dv.W0pf + cb + j, w0);
             ldg8(P.dv.W0pf + n0 + cb + j, w1);
             ldg8(P.dv.W0pf + 2 * n0 + cb + j, w2);
-            const double2 *cc = reinterpret_cast<const double2 *>(c0 + cb + j);
+            ldg8(c0f + cb + j, cf);
             uint32_t bits = 0;
 #pragma unroll
-            for (int e = 0; e < 8; e += 2) {
-              const double2 cv = __ldg(cc + e / 2);
-              const float v0 = fmaf(pz, w2[e], fmaf(py, w1[e], fmaf(px, w0[e], (float)cv.x)));
-              const float v1 = fmaf(pz, w2[e + 1], fmaf(py, w1[e + 1], fmaf(px, w0[e + 1], (float)cv.y)));
-              const bool on0 = s >= 0 && v0 > 0.f, on1 = s >= 0 && v1 > 0.f;
-              x[e] = on0 ? v0 : 0.f;
-              x[e + 1] = on1 ? v1 : 0.f;
-              bits |= (on0 ? 1u : 0u) << e;
-              bits |= (on1 ? 1u : 0u) << (e + 1);
+            for (int e = 0; e < 8; ++e) {
+              const float v = fmaf(pz, w2[e], fmaf(py, w1[e], fmaf(px, w0[e], cf[e])));
+              const bool on = s >= 0 && v > 0.f;
+              x[e] = on ? v : 0.f;
+              bits |= (on ? 1u : 0u) << e;
             }
             set4(mk, nh * 2 + (j >> 5), get4(mk, nh * 2 + (j >> 5)) | (bits << (j & 31)));
             put8<false>(smem, row, cb + j, x);
@@ -491,6 +488,7 @@ int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t
   tc::HParams P;
   P.dv = dv;
   P.c0 = c0;
+  P.c0f = c0_f32(c0, S, dv.np[0]);
   P.bias = dv.tc_bias[0];
   P.w_out = dv.tc_bias[0] + (size_t)(dv.n_layers - 2) * tc::KDIM;
   P.winv_b = dv.tc_bias[1];

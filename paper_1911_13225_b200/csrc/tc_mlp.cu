@@ -42,6 +42,7 @@ namespace tc {
 struct Params {
   DecView dv;
   const double *c0;       // [S][512] folded layer-0 bias (fp64)
+  const float *c0f;       // the same in fp32 (kernels.cuh c0_f32)
   const float *bias;      // [L-2][512] hidden biases 1..L-2 (fp32)
   const float *w_out;     // [512]
   const float *winv;      // [L-2] inverse power-of-2 weight scales (fp16x3), 1 for bf16x3
@@ -323,7 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const int64_t gi = nx.gi;
       const bool odd = PAIR && (lane & 1);
       const int n0 = P.dv.np[0];
-      const double *c0 = P.c0 + (size_t)(s < 0 ? 0 : s) * n0;
+      const float *c0f = P.c0f + (size_t)(s < 0 ? 0 : s) * n0;
       // layer-0 activations of 8 consecutive columns: folded bias c0 (fp64,
       // rounded) + p . W0p in fp32 -- the bf16x3 split of the result carries
       // ~17 bits, so fp32 here costs nothing and keeps the loads vectorised.
@@ -350,13 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         ldg8(P.dv.W0pf + col, w0);
         ldg8(P.dv.W0pf + n0 + col, w1);
         ldg8(P.dv.W0pf + 2 * n0 + col, w2);
-        const double2 *cc = reinterpret_cast<const double2 *>(c0 + col);
-#pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-          const double2 cv = __ldg(cc + e / 2);
-          cf[e] = (float)cv.x;
-          cf[e + 1] = (float)cv.y;
-        }
+        ldg8(c0f + col, cf);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const float v = fmaf(pz, w2[e], fmaf(py, w1[e], fmaf(px, w0[e], cf[e])));
@@ -698,14 +693,15 @@ int tc_make_map(const DecView &dv, int slot, CUtensorMap *map) {
 }
 
 template <bool F16, class Rows, bool PAIR = false>
-static int launch_tc_t(const DecView &dv, const double *c0, const Rows &rows, int64_t tiles_bound,
-                       cudaStream_t st, int slot = 0) {
+static int launch_tc_t(const DecView &dv, const double *c0, int S, const Rows &rows,
+                       int64_t tiles_bound, cudaStream_t st, int slot = 0) {
   CUtensorMap map;
   int rc = tc_make_map(dv, slot, &map);
   if (rc) return rc;
   tc::Params P;
   P.dv = dv;
   P.c0 = c0;
+  P.c0f = c0_f32(c0, S, dv.np[0]);
   P.bias = dv.tc_bias[slot];
   P.w_out = dv.tc_bias[slot] + (size_t)(dv.n_layers - 2) * tc::KDIM;
   P.n_gemm = dv.n_layers - 2;
@@ -728,10 +724,10 @@ static int launch_tc_t(const DecView &dv, const double *c0, const Rows &rows, in
 }
 
 template <class Rows, bool PAIR = false>
-static int launch_tc(const DecView &dv, const double *c0, const Rows &rows, int64_t tiles_bound,
-                     cudaStream_t st) {
-  if (dv.prec == DIST_PREC_FP16X3) return launch_tc_t<true, Rows, PAIR>(dv, c0, rows, tiles_bound, st);
-  return launch_tc_t<false, Rows, PAIR>(dv, c0, rows, tiles_bound, st);
+static int launch_tc(const DecView &dv, const double *c0, int S, const Rows &rows,
+                     int64_t tiles_bound, cudaStream_t st) {
+  if (dv.prec == DIST_PREC_FP16X3) return launch_tc_t<true, Rows, PAIR>(dv, c0, S, rows, tiles_bound, st);
+  return launch_tc_t<false, Rows, PAIR>(dv, c0, S, rows, tiles_bound, st);
 }
 
 extern "C" DIST_API int dist_debug_mlp_timeline(unsigned long long *out, int n) {
@@ -739,32 +735,32 @@ extern "C" DIST_API int dist_debug_mlp_timeline(unsigned long long *out, int n) 
                  cudaSuccess ? 0 : -1;
 }
 
-int tc_eval_probes(const DecView &dv, const double *c0, const ProbeGen &gen, int64_t n_bound,
+int tc_eval_probes(const DecView &dv, const double *c0, int S, const ProbeGen &gen, int64_t n_bound,
                    cudaStream_t st) {
   tc::ProbeRows rows{gen};
   // always fp16x3: a bf16x3 decoder carries an fp16 probe pack in slot 2
   const int slot = dv.prec == DIST_PREC_FP16X3 ? 0 : 2;
   if (!dv.tc_w[slot]) return fail(DIST_ERR_CONFIG, "decoder has no fp16 probe pack");
-  return launch_tc_t<true, tc::ProbeRows, true>(dv, c0, rows, ceil_div(n_bound, 128), st, slot);
+  return launch_tc_t<true, tc::ProbeRows, true>(dv, c0, S, rows, ceil_div(n_bound, 128), st, slot);
 }
 
-int tc_eval_points(const DecView &dv, const double *c0, const double *cskip, const double *pts,
+int tc_eval_points(const DecView &dv, const double *c0, const double *cskip, int S, const double *pts,
                    const int32_t *shape, int64_t n, double *f, cudaStream_t st) {
   if (!tc_supported(dv)) {
     ArrayGen g{pts, shape, nullptr, f, n};
     return launch_eval_gen<float>(dv, c0, cskip, g, n, st);
   }
   tc::EvalRows rows{pts, shape, f, n};
-  return launch_tc(dv, c0, rows, ceil_div(n, 128), st);
+  return launch_tc(dv, c0, S, rows, ceil_div(n, 128), st);
 }
 
-int tc_run_steps(const DecView &dv, const double *c0, const double *cskip, const dist_camera *cams,
+int tc_run_steps(const DecView &dv, const double *c0, const double *cskip, int S, const dist_camera *cams,
                  const LevelState &ls, Ctl *ctl, int32_t *l0, int32_t *l1, const MarchArgs &a,
                  int slots, int64_t *live, int64_t *stats, cudaStream_t st) {
   (void)cskip;
   tc::MarchRows rows{cams, ls, ctl, l0, l1, a, live, stats};
   for (int s = 0; s < slots; ++s) {
-    int rc = launch_tc(dv, c0, rows, ceil_div(ls.n, 128), st);
+    int rc = launch_tc(dv, c0, S, rows, ceil_div(ls.n, 128), st);
     if (rc) return rc;
   }
   return DIST_OK;

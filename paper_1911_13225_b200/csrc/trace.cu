@@ -227,7 +227,7 @@ __global__ void k_normals_assemble(const dist_camera *__restrict__ cams, LevelSt
 // Normal probes at every converged ray (shading.py:73-94): compaction, probe
 // evaluation ((mid, diff) pairs except in fp64), assembly of unit normals
 // and/or grad f . v.
-int normals_pass(const DecView &dv, const double *c0, const double *cs, const dist_camera *cams,
+int normals_pass(const DecView &dv, const double *c0, const double *cs, int S, const dist_camera *cams,
                  const LevelState &ls, const dist_trace_config *cfg, double *normals, double *gdotv,
                  int32_t *conv, int32_t *count, int32_t *bcount, double *f, cudaStream_t st) {
   const int64_t n = ls.n;
@@ -242,7 +242,7 @@ int normals_pass(const DecView &dv, const double *c0, const double *cs, const di
   // On tensor-core decoders the pairs run through k_tc_mlp's pair mode.
   const int pair = dv.prec == DIST_PREC_FP64 ? 0 : 1;
   if (!pair) rc = launch_eval_gen<double>(dv, c0, cs, gen, n * 6, st);
-  else if (tc_supported(dv)) rc = tc_eval_probes(dv, c0, gen, n * 6, st);
+  else if (tc_supported(dv)) rc = tc_eval_probes(dv, c0, S, gen, n * 6, st);
   else rc = launch_eval_gen<float, ProbeGen, true>(dv, c0, cs, gen, n * 6, st);
   if (rc) return rc;
   k_normals_assemble<<<grid_for(n, 256), 256, 0, st>>>(cams, ls, conv, count, f, cfg->normal_delta,
@@ -283,7 +283,7 @@ static TraceLayout layout(const DecView &dv, const dist_trace_config *cfg, int V
   TraceLayout L{};
   Carve cv{ws, 0, cap};
   const int s1 = std::max(S, 1);
-  L.c0 = cv.take<double>((size_t)s1 * dv.np[0]);
+  L.c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
   L.cskip = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
   int levels[3], nl = 0;
   for (int s = cfg->coarse_start_scale; s >= 1; s /= 2) levels[nl++] = s;
@@ -389,7 +389,7 @@ int dist_trace(const dist_decoder *dec, const double *codes, int S, const dist_c
     if (dv.prec == DIST_PREC_FP64)
       rc = run_steps<double>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, live, stats, st);
     else if (tc_supported(dv))
-      rc = tc_run_steps(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, live, stats, st);
+      rc = tc_run_steps(dv, L.c0, L.cskip, std::max(S, 1), cams, ls, L.ctl, L.list0, L.list1, a, slots, live, stats, st);
     else
       rc = run_steps<float>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, live, stats, st);
     if (rc) return rc;
@@ -416,7 +416,7 @@ size_t dist_normals_workspace_size(const dist_decoder *dec, int V, int W, int H,
   const int64_t n = (int64_t)V * W * H;
   Carve cv{nullptr, 0, ~size_t(0)};
   const int s1 = std::max(S, 1);
-  cv.take<double>((size_t)s1 * dec->view.np[0]);
+  cv.take<double>(c0_doubles(s1, dec->view.np[0]));
   cv.take<double>((size_t)s1 * std::max(dec->view.nskip, 1));
   cv.take<int32_t>(n);
   cv.take<int32_t>(4);
@@ -434,7 +434,7 @@ int dist_normals(const dist_decoder *dec, const double *codes, int S, const dist
   const int64_t n = (int64_t)V * W * H;
   const int s1 = std::max(S, 1);
   Carve cv{(char *)ws, 0, ws_bytes};
-  double *c0 = cv.take<double>((size_t)s1 * dv.np[0]);
+  double *c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
   double *cs = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
   int32_t *conv = cv.take<int32_t>(n);
   int32_t *count = cv.take<int32_t>(4);
@@ -447,7 +447,7 @@ int dist_normals(const dist_decoder *dec, const double *codes, int S, const dist
   if (rc) return rc;
   LevelState ls{stt->d, stt->b, stt->status, stt->steps, stt->topk_d, stt->topk_f, stt->topk_absf,
                 W, H, 1, n};
-  return normals_pass(dv, c0, cs, cams, ls, cfg, normals, nullptr, conv, count, bcount, f, st);
+  return normals_pass(dv, c0, cs, s1, cams, ls, cfg, normals, nullptr, conv, count, bcount, f, st);
 }
 
 }  // extern "C"
