@@ -194,6 +194,20 @@ def formats():
     st.write_pgm(os.path.join(OUT, "ref_mask.pgm"), st.hard_mask(res))
 
 
+def report():
+    """An sdftrace-report/1 file written by the reference CLI's own writer
+    (cli.py:55-70) from a 3-iteration complete_shape on the tiny net."""
+    from sdftrace import cli
+    rng = np.random.default_rng(7)
+    net = st.NeuralField.init(latent_dim=2, hidden=(16, 16), rng=rng)
+    code = rng.normal(0.0, 0.3, 2)
+    intr, pose = st.Intrinsics(width=32, height=32), st.look_at((0.0, 0.0, -2.0))
+    res = st.trace(net, code + 0.05, intr, pose, st.TraceConfig())
+    obs = [st.Observation("depth", st.depth_map(res))]
+    _, rep = st.complete_shape(net, obs, intr, pose, iters=3)
+    cli._write_report(os.path.join(OUT, "ref_report.json"), "complete-depth", cli._report_payload(rep))
+
+
 def multiview():
     """Photometric warp + reconstruct_multiview (losses.py:120-222, optimize.py:272-358)
     on the tiny net with textured views (test_optimize.py:25-38 pattern)."""
@@ -251,6 +265,12 @@ def attribute():
 def main():
     os.makedirs(OUT, exist_ok=True)
     warnings.simplefilter("ignore")
+    only = sys.argv[1:]
+    if only:   # regenerate selected sets, e.g. `python oracle/make_golden.py report`
+        for name in only:
+            globals()[name]()
+        return
+    report()
     attribute()
     multiview()
     formats()

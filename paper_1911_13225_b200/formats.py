@@ -7,6 +7,8 @@ and maps move between the two implementations bit-exactly:
   written with repr, so a load/save/load cycle is bit-exact;
 * ``sdftrace-camera/1`` JSON (camera.py:284-312): focal/sensor in mm,
   resolution, principal point and the 3x4 world-to-camera extrinsic;
+* ``sdftrace-report/1`` JSON for optimisation reports (cli.py:29, 55-70):
+  the command name plus the ``OptimizeReport`` fields the reference writes;
 * grayscale PFM for depth (float32, bottom-up rows, little-endian scale -1,
   +inf background stored as 0) and 8-bit binary PGM for masks
   (imageio.py:17-78).
@@ -25,6 +27,9 @@ from .fields import NeuralField
 
 FIELD_FORMAT = "sdftrace-field/1"
 CAMERA_FORMAT = "sdftrace-camera/1"
+REPORT_FORMAT = "sdftrace-report/1"
+_REPORT_KEYS = ("losses", "grad_norms", "best_iter", "best_loss", "total_queries", "elapsed",
+                "skipped_steps", "non_identifiable")
 
 
 def save_field(field: NeuralField, path, codes=None) -> None:
@@ -75,6 +80,40 @@ def load_camera(path):
         raise ValueError("extrinsic must be 3x4")
     return Intrinsics(doc["focal_mm"], doc["sensor_mm"], w, h, cx=cx, cy=cy), \
         Pose(log_rotation(ext[:, :3]), ext[:, 3])
+
+
+def save_report(report, path, command: str) -> None:
+    """cli.py:55-70: {"format", "command", losses, grad_norms, best_iter, best_loss,
+    total_queries, elapsed, skipped_steps, non_identifiable}, indent 2, trailing newline."""
+    payload = {}
+    for k in _REPORT_KEYS:
+        v = getattr(report, k)
+        if isinstance(v, (list, tuple)):
+            v = [float(x) for x in v]
+        elif isinstance(v, (bool, np.bool_)):
+            v = bool(v)
+        elif isinstance(v, (int, np.integer)):
+            v = int(v)
+        elif isinstance(v, (float, np.floating)):
+            v = float(v)
+        payload[k] = v
+    doc = {"format": REPORT_FORMAT, "command": command, **payload}
+    with open(path, "w") as fh:
+        fh.write(json.dumps(doc, indent=2) + "\n")
+
+
+def load_report(path):
+    """Returns (command, OptimizeReport) from an sdftrace-report/1 file."""
+    from .optimize import OptimizeReport
+    with open(path) as fh:
+        doc = json.load(fh)
+    if doc.get("format") != REPORT_FORMAT:
+        raise ValueError(f"not a report file: format={doc.get('format')!r}")
+    rep = OptimizeReport()
+    for k in _REPORT_KEYS:
+        if k in doc:
+            setattr(rep, k, doc[k])
+    return doc.get("command"), rep
 
 
 def write_pfm(path, img) -> None:

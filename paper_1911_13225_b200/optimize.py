@@ -313,8 +313,16 @@ def complete_shape(field, observations, intr, pose, code0=None, iters: int = 100
     opt = LatentOptimizer(field, [(intr, pose)], o, code.reshape(1, -1), cfg, weights, lr=lr,
                           max_iters=iters)
     queries = 0
+    import torch
+    # per-iterate terms and |g| (optimize.py:160-166), kept on the device:
+    # [depth, silhouette, latent, |g|]
+    rec = torch.zeros((iters, 4), dtype=torch.float64, device=opt.grad.device)
     for it in range(iters):
-        opt.step()
+        opt.objective()
+        rec[it, 0:2] = opt.view_terms[0, 0:2]
+        rec[it, 2] = opt.shape_terms[0, 1]
+        rec[it, 3] = torch.linalg.vector_norm(opt.grad[0])
+        opt._adam()
         if it == 0:
             n_conv = int(opt.view_terms[0, 3].item())
             if n_conv == 0:
@@ -325,8 +333,15 @@ def complete_shape(field, observations, intr, pose, code0=None, iters: int = 100
                 report.silhouette_only_start = True
         queries += opt.last_trace.stats_dev[0]
     hist = opt.losses()[:, 0]
+    rec = rec.cpu().numpy()
     for it, loss in enumerate(hist):
-        report.record(float(loss), {}, float("nan"))
+        terms = {}
+        if "depth" in obs:
+            terms["depth"] = float(rec[it, 0])
+        if "silhouette" in obs:
+            terms["silhouette"] = float(rec[it, 1])
+        terms["latent"] = float(rec[it, 2])
+        report.record(float(loss), terms, float(rec[it, 3]))
     report.total_queries = int(queries.item()) if hasattr(queries, "item") else int(queries)
     report.best_iter = int(opt.best_iter[0].item())
     report.best_loss = float(opt.best_loss[0].item())

@@ -1,6 +1,8 @@
 """GPU parity of heads, losses, the fused objective and Adam vs the reference goldens."""
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -122,3 +124,30 @@ def test_implicit_gradient_mode_vs_oracle(st, prec, tol):
     assert np.linalg.norm(grad - g_o) / np.linalg.norm(g_o) < tol
     # the implicit and surrogate gradients differ (SURVEY 0 finding 4)
     assert np.linalg.norm(g_o - g["obj_grad"]) / np.linalg.norm(g["obj_grad"]) > 1e-2
+
+
+@pytest.mark.gpu
+def test_complete_shape_report_matches_reference_file(st, tmp_path):
+    """The reference CLI's report of a 3-iteration complete_shape (tiny net, 32^2,
+    tests/golden/ref_report.json) is reproduced in fp64: losses, best iterate and
+    query count; the written report carries the same fields."""
+    import json
+    from conftest import GOLDEN
+    from paper_1911_13225_b200 import formats as fm
+    rng = np.random.default_rng(7)
+    net = st.NeuralField.init(latent_dim=2, hidden=(16, 16), rng=rng, precision="fp64")
+    code = rng.normal(0.0, 0.3, 2)
+    intr, pose = st.Intrinsics(width=32, height=32), st.look_at((0.0, 0.0, -2.0))
+    res = st.trace(net, code + 0.05, intr, pose, st.TraceConfig())
+    obs = [st.Observation("depth", st.depth_map(res))]
+    _, rep = st.complete_shape(net, obs, intr, pose, iters=3)
+    ref = json.load(open(os.path.join(GOLDEN, "ref_report.json")))
+    np.testing.assert_allclose(rep.losses, ref["losses"], rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(rep.grad_norms, ref["grad_norms"], rtol=1e-8)
+    assert rep.best_iter == ref["best_iter"] and rep.total_queries == ref["total_queries"]
+    fm.save_report(rep, tmp_path / "r.json", "complete-depth")
+    mine = json.load(open(tmp_path / "r.json"))
+    assert set(mine) == set(ref) and mine["format"] == "sdftrace-report/1"
+    # per-iterate loss terms as the reference records them
+    assert set(rep.terms[0]) == {"depth", "latent"}
+    assert abs(rep.terms[0]["depth"] * 10.0 + rep.terms[0]["latent"] - rep.losses[0]) < 1e-12

@@ -202,3 +202,17 @@ def test_formats_roundtrip_with_reference_files(tmp_path):
     m = fm.read_pgm(os.path.join(GOLDEN, "ref_mask.pgm"))
     fm.write_pgm(tmp_path / "m.pgm", m.astype(bool))
     assert open(tmp_path / "m.pgm", "rb").read() == open(os.path.join(GOLDEN, "ref_mask.pgm"), "rb").read()
+
+
+def test_report_roundtrip_with_reference_file(tmp_path):
+    """an sdftrace-report/1 file written by the reference CLI
+    (cli.py:55-70) loads here and is re-written byte-identically."""
+    from conftest import GOLDEN
+    from paper_1911_13225_b200 import formats as fm
+    src = os.path.join(GOLDEN, "ref_report.json")
+    cmd, rep = fm.load_report(src)
+    assert cmd == "complete-depth" and rep.best_iter == 2 and len(rep.losses) == 3
+    fm.save_report(rep, tmp_path / "r.json", cmd)
+    assert open(tmp_path / "r.json").read() == open(src).read()
+    with pytest.raises(ValueError):
+        fm.load_report(os.path.join(GOLDEN, "ref_camera.json"))
