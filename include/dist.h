@@ -89,6 +89,12 @@ DIST_API int dist_device_info(int *sm_count, int *cc_major, int *cc_minor);
 /* number of kernel launches the library enqueued since load (bench audit) */
 DIST_API int64_t dist_launch_count(void);
 
+/* Debug: per-phase timeline of the last k_tc_mlp / k_tc_heads launch, recorded
+ * when DIST_TC_TIMELINE=1 (entries: mark id << 56 | %globaltimer ns of CTA 0's
+ * first epilogue thread; scripts/tile_timeline.py). Copies up to n entries. */
+DIST_API int dist_debug_mlp_timeline(unsigned long long *out, int n);
+DIST_API int dist_debug_heads_timeline(unsigned long long *out, int n);
+
 /* ---- decoder (NeuralField, fields.py:185-247) -------------------------- */
 /* W[l] is the reference's row-major W[in,out] float64 (fields.py:195-196),
  * b[l] its bias; dims has n_layers+1 entries (dims[0] = latent_dim + 3 +

@@ -1,0 +1,70 @@
+"""Per-phase timeline of one tile of the tensor-core kernels on a B200.
+
+With DIST_TC_TIMELINE=1 the first epilogue thread of CTA 0 appends
+(mark id << 56 | %globaltimer) pairs to a device buffer per kernel
+(csrc/tc_core.cuh DIST_TL_MARK); this script runs
+  * k_tc_mlp on a 1M-point evaluation (same tile loop as a march step) and
+  * k_tc_heads in one C3 latent-optimisation iterate (8 views x 512^2),
+and prints the phase durations of two tiles of each.
+
+  python scripts/tile_timeline.py
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import sys
+
+os.environ["DIST_TC_TIMELINE"] = "1"
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1911_13225_b200 as st  # noqa: E402
+from paper_1911_13225_b200 import _lib  # noqa: E402
+from paper_1911_13225_b200.workloads import render_depth_observations, ring_views, target_code  # noqa: E402
+
+MLP = {1: "tile start", 2: "layer0 A ready", 10: "prev tile rows done", 3: "D ready", 4: "A ready",
+       9: "head done"}
+HEADS = {1: "tile start", 2: "layer0 A ready", 3: "fwd D ready", 4: "fwd A ready", 5: "seed done",
+         6: "bwd A0 ready", 7: "bwd D ready", 8: "bwd A ready", 9: "colsum done"}
+
+
+def show(fn, names, label):
+    buf = (ctypes.c_ulonglong * 4096)()
+    fn(buf, 4096)
+    a = np.array(buf[:], dtype=np.uint64)
+    ids = (a >> np.uint64(56)).astype(int)
+    t = (a & np.uint64((1 << 56) - 1)).astype(np.int64)
+    n = int(np.argmax(ids == 0)) if (ids == 0).any() else len(ids)
+    ids, t = ids[:n], t[:n]
+    starts = np.nonzero(ids == 1)[0]
+    for k in range(1, min(3, len(starts) - 1)):
+        s, e = starts[k], starts[k + 1]
+        print(f"--- {label} tile {k}: {(t[e] - t[s]) / 1e3:.1f} us")
+        for i in range(s, e):
+            dt = (t[i] - t[i - 1]) / 1e3 if i > s else 0.0
+            print(f"  {names[ids[i]]:20s} +{(t[i] - t[s]) / 1e3:7.2f} us  (dt {dt:6.2f})")
+
+
+def main():
+    lib = _lib.lib()
+    field = st.NeuralField.geometric(256, (512,) * 8, 0, precision="bf16x3")
+    code = np.random.default_rng(2).normal(0, 0.1, 256)
+    pts = torch.from_numpy(np.random.default_rng(0).uniform(-0.8, 0.8, (1 << 20, 3))).cuda()
+    field.evaluate_device(pts, code)
+    torch.cuda.synchronize()
+    show(lib.dist_debug_mlp_timeline, MLP, "k_tc_mlp")
+    views = ring_views(8, 512)
+    cfg = st.TraceConfig(k_samples=3)
+    obs = render_depth_observations(field, target_code(1), views, cfg)
+    opt = st.LatentOptimizer(field, views, {"depth": obs}, np.zeros((1, 256)), cfg, max_iters=4)
+    opt.step()
+    opt.step()
+    torch.cuda.synchronize()
+    show(lib.dist_debug_heads_timeline, HEADS, "k_tc_heads")
+
+
+if __name__ == "__main__":
+    main()
