@@ -156,7 +156,7 @@ def _config(args):
                         f"optimisation, 8x512 DeepSDF decoder (latent 256, geometric init seed 0), "
                         f"K=3, alpha 1.5, coarse 4, 100 steps",
             "views_per_gpu": VIEWS_PER_RANK, "resolution": RES, "precision": args.precision,
-            "parallelism": f"views sharded over {args.gpus} GPU(s), latent all-reduce",
+            "parallelism": f"views sharded over {args.gpus} GPU(s) (ring interleaved), latent all-reduce",
             "l2": "working set > L2 (ray state ~320 MB per step)"}
 
 
@@ -193,7 +193,9 @@ def main():
 
     field = st.NeuralField.geometric(256, (512,) * 8, 0, precision=args.precision)
     total_views = VIEWS_PER_RANK * world
-    views = ring_views(VIEWS_PER_RANK, RES, first=rank * VIEWS_PER_RANK, total=total_views)
+    # rank r traces ring views r, r+N, ..., r+7N of an 8N-view ring: every rank
+    # covers the whole ring, so per-rank cost stays balanced as N grows
+    views = ring_views(VIEWS_PER_RANK, RES, first=rank, total=total_views, stride=world)
     cfg = st.TraceConfig(k_samples=3)
     obs = render_depth_observations(field, target_code(1), views, cfg)
     weights = st.LossWeights(latent=1.0 if rank == 0 else 0.0)   # regulariser added once

@@ -19,11 +19,13 @@ def ring_eye(k: int, n: int, radius: float = 2.0) -> np.ndarray:
     return eye * (radius / np.linalg.norm(eye))
 
 
-def ring_views(n_views: int, res: int, first: int = 0, total: int | None = None):
-    """Views first..first+n_views-1 of a `total`-view ring at res x res."""
-    total = total or n_views
+def ring_views(n_views: int, res: int, first: int = 0, total: int | None = None, stride: int = 1):
+    """Views first, first+stride, ... (n_views of them) of a `total`-view ring at
+    res x res.  stride = world size interleaves the ring over ranks, so every
+    rank sees the whole ring (balanced per-rank cost)."""
+    total = total or n_views * stride
     intr = Intrinsics(width=res, height=res)
-    return [(intr, look_at(ring_eye(k, total))) for k in range(first, first + n_views)]
+    return [(intr, look_at(ring_eye(first + j * stride, total))) for j in range(n_views)]
 
 
 def target_code(seed: int = 1, dim: int = 256) -> np.ndarray:
