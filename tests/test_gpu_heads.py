@@ -151,3 +151,24 @@ def test_complete_shape_report_matches_reference_file(st, tmp_path):
     # per-iterate loss terms as the reference records them
     assert set(rep.terms[0]) == {"depth", "latent"}
     assert abs(rep.terms[0]["depth"] * 10.0 + rep.terms[0]["latent"] - rep.losses[0]) < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("k", [-40, -12, 12, 40])
+def test_backward_exactly_linear_in_power_of_two_weight(st, k):
+    """Size-independent property of the fused fp16x2 backward: the power-of-two
+    row scales absorb a 2^k loss weight exactly, so the latent gradient scales
+    bit-exactly (no fp16 overflow or underflow at |k| = 40)."""
+    from paper_1911_13225_b200.workloads import render_depth_observations, ring_views, target_code
+    field = st.NeuralField.geometric(256, (512,) * 8, 0, precision="bf16x3")
+    views = ring_views(2, 128)
+    cfg = st.TraceConfig(k_samples=3)
+    obs = render_depth_observations(field, target_code(1), views, cfg)
+    grads = []
+    for w in (10.0, 10.0 * 2.0 ** k):
+        opt = st.LatentOptimizer(field, views, {"depth": obs}, np.full((1, 256), 0.01), cfg,
+                                 st.LossWeights(depth=w, latent=0.0), max_iters=1)
+        opt.objective()
+        grads.append(opt.grad.cpu().numpy()[0])
+    assert np.all(np.isfinite(grads[1])) and np.linalg.norm(grads[0]) > 0
+    assert np.array_equal(grads[1], grads[0] * 2.0 ** k)
