@@ -329,14 +329,14 @@ def main():
                      "objective_note": "heads + seeds + fused tcgen05 backward + reductions "
                                        "(k_tc_heads dominates; its ncu capture is in profiles/)"},
     }
-    if rank == 0 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:   # the contract: rank 0 at N=1 only
         v, info = cpu_reference_sample()
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": "port",
                                 "sample": info["sample"]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
-        dist.barrier()          # the other ranks wait for rank 0's CPU-baseline leg
+        dist.barrier()
         dist.destroy_process_group()
     return 0
 
