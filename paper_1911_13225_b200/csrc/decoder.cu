@@ -126,6 +126,9 @@ int vjp_points(const DecView &dv, const double *c0, const double *cskip, const d
   ArrayGen g{pts, shape, seed, f, n};
   if (dv.prec == DIST_PREC_FP64)
     return launch_vjp_gen<double>(dv, c0, cskip, g, n, S, part0, parts, gpts, grid_cap, grid_out, st);
+  // bf16x3: the fused tensor-core head kernel (forward, given seeds, fp16x2 dgrad)
+  if (tc_heads_supported(dv))
+    return launch_tc_heads<ArrayGen>(dv, c0, g, n, S, part0, grid_cap, grid_out, st, gpts);
   return launch_vjp_gen<float>(dv, c0, cskip, g, n, S, part0, parts, gpts, grid_cap, grid_out, st);
 }
 

@@ -44,7 +44,8 @@ namespace dist {
 int tc_make_map(const DecView &dv, int slot, CUtensorMap *map);
 template <class Gen>
 int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
-                    double *part0, int grid_cap, int *grid_out, cudaStream_t st);
+                    double *part0, int grid_cap, int *grid_out, cudaStream_t st,
+                    double *gpts = nullptr);
 
 struct LevelState;
 struct ProbeGen;

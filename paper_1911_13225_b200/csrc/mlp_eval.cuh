@@ -136,6 +136,13 @@ struct ArrayGen {
   __device__ void store(int64_t i, double v) const {
     if (f) f[i] = v;
   }
+  // the tensor-core head kernel's seed interface (heads.cuh ObjGen): the seed
+  // is given, so prep() loads it and apply() ignores f
+  struct Prep {
+    double seed;
+  };
+  __device__ Prep prep(int64_t i) const { return Prep{seeds ? seeds[i] : 0.0}; }
+  __device__ double apply(const Prep &p, double) const { return p.seed; }
 };
 
 int sm_count();

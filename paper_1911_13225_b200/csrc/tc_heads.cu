@@ -26,6 +26,7 @@
 #include "common.cuh"
 #include "heads.cuh"
 #include "kernels.cuh"
+#include "mlp_eval.cuh"
 #include "tc_core.cuh"
 
 namespace dist {
@@ -43,6 +44,7 @@ struct HParams {
   int S;
   int timeline;        // DIST_TC_TIMELINE: CTA 0 / thread 64 records %globaltimer marks
   double *part0;       // [grid][S][512]
+  double *gpts;        // [n][3] seed * df/dp per row, or null
 };
 
 __device__ __forceinline__ void tmem_st4(uint32_t taddr, const uint32_t (&r)[4]) {
@@ -424,6 +426,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           // shape.  TMEM is read inside the shape loop (usually one pass), so no
           // per-thread copy of the 128 values is kept (it lived in local memory).
           float *red = reinterpret_cast<float *>(smem + OFF_AHI);  // A is free now: [2][512] floats
+          if (P.gpts) {
+            // d loss / d p = g_pre0 . W0p^T per row: this thread's 128 columns,
+            // then the row's four part sums through smem (after `red`)
+            float *gp = red + 2 * KDIM;   // [3][4][64]
+            float acc[3] = {0.f, 0.f, 0.f};
+            for (int nh = 0; nh < 2; ++nh) {
+              const int cb = nh * 256 + half * 128 + sub * 64;
+#pragma unroll 1
+              for (int c = 0; c < 2; ++c) {
+                float v[32];
+                tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
+                const uint32_t bits = get4(mk, nh * 2 + c);
+#pragma unroll
+                for (int g8 = 0; g8 < 4; ++g8) {
+                  float w0[8], w1[8], w2[8];
+                  const int col = cb + c * 32 + g8 * 8;
+                  ldg8(P.dv.W0pf + col, w0);
+                  ldg8(P.dv.W0pf + n0 + col, w1);
+                  ldg8(P.dv.W0pf + 2 * n0 + col, w2);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) {
+                    const float g = ((bits >> (g8 * 8 + e)) & 1u) ? v[g8 * 8 + e] * unscale : 0.f;
+                    acc[0] = fmaf(g, w0[e], acc[0]);
+                    acc[1] = fmaf(g, w1[e], acc[1]);
+                    acc[2] = fmaf(g, w2[e], acc[2]);
+                  }
+                }
+              }
+            }
+#pragma unroll
+            for (int a = 0; a < 3; ++a) gp[(a * 4 + half * 2 + sub) * ROWS + row] = acc[a];
+            tc_fence_before();
+            epi_sync();
+            if (row_thread && gi < nrows && s >= 0)
+#pragma unroll
+              for (int a = 0; a < 3; ++a)
+                P.gpts[gi * 3 + a] = (double)gp[(a * 4) * ROWS + row] + (double)gp[(a * 4 + 1) * ROWS + row] +
+                                     (double)gp[(a * 4 + 2) * ROWS + row] + (double)gp[(a * 4 + 3) * ROWS + row];
+          }
           int shapes_done = 0;
           for (int guard = 0; guard < ROWS; ++guard) {
             // next shape = smallest shape id > previous (uniform across threads)
@@ -480,7 +521,7 @@ bool tc_heads_supported(const DecView &dv) {
 
 template <class Gen>
 int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
-                    double *part0, int grid_cap, int *grid_out, cudaStream_t st) {
+                    double *part0, int grid_cap, int *grid_out, cudaStream_t st, double *gpts) {
   CUtensorMap mf, mb;
   int rc = tc_make_map(dv, 0, &mf);
   if (!rc) rc = tc_make_map(dv, 1, &mb);
@@ -500,6 +541,7 @@ int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t
     P.timeline = tl ? atoi(tl) : 0;
   }
   P.part0 = part0;
+  P.gpts = gpts;
   const void *fn = (const void *)tc::k_tc_heads<Gen>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc heads)");
@@ -517,6 +559,8 @@ extern "C" DIST_API int dist_debug_heads_timeline(unsigned long long *out, int n
 }
 
 template int launch_tc_heads<ObjGen>(const DecView &, const double *, const ObjGen &, int64_t, int,
-                                     double *, int, int *, cudaStream_t);
+                                     double *, int, int *, cudaStream_t, double *);
+template int launch_tc_heads<ArrayGen>(const DecView &, const double *, const ArrayGen &, int64_t, int,
+                                       double *, int, int *, cudaStream_t, double *);
 
 }  // namespace dist

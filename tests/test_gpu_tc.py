@@ -135,3 +135,35 @@ def test_depth_and_silhouette_objective_vs_oracle(st, prec, tol):
     assert abs(terms["silhouette"] - terms_o["silhouette"]) < tol * max(abs(terms_o["silhouette"]), 1e-3)
     assert abs(tot - tot_o) < tol * abs(tot_o)
     assert np.linalg.norm(grad - g_o) / np.linalg.norm(g_o) < tol
+
+
+@pytest.mark.parametrize("S,kind", [(1, "coherent"), (3, "coherent"), (1, "random")])
+def test_tc_vjp_matches_fp64(st, S, kind):
+    """dist_eval_vjp on a bf16x3 decoder runs the fused tensor-core head kernel
+    (given seeds, fp16x2 dgrad, per-point xyz gradient); f, the code gradient
+    and d(seed.f)/dp agree with the fp64 SIMT path.  Coherent seeds (the sign
+    of f, as a depth loss gives) are the real use; random-sign seeds cancel in
+    the code gradient and amplify relative error for every reduced-precision
+    mode (fp32 SIMT: 1.3e-3), so they get a looser bar."""
+    import torch
+    rng = np.random.default_rng(5)
+    n = 5000
+    p = rng.normal(size=(n, 3))
+    p *= rng.uniform(0.3, 0.9, (n, 1)) / np.linalg.norm(p, axis=1, keepdims=True)
+    codes = rng.normal(0.0, 0.1, (S, 256))
+    sid = torch.from_numpy(rng.integers(0, S, n).astype(np.int32))
+    P = torch.from_numpy(p)
+    nets = {prec: st.NeuralField.geometric(256, (512,) * 8, 0, precision=prec) for prec in ("fp64", "bf16x3")}
+    f_ref = nets["fp64"].evaluate_device(P, torch.from_numpy(codes), sid).cpu().numpy() \
+        if S > 1 else nets["fp64"].evaluate(p, codes[0])
+    sign = rng.choice([-1.0, 1.0], n) if kind == "random" else np.sign(f_ref)
+    sd = torch.from_numpy(sign * rng.uniform(0.5, 1.0, n) / n)
+    out = {}
+    for prec, net in nets.items():
+        f, gc, gp = net.vjp_device(P, torch.from_numpy(codes), sd, shape_ids=sid)
+        out[prec] = (f.cpu().numpy(), gc.cpu().numpy(), gp.cpu().numpy())
+    (f64, g64, p64), (f16, g16, p16) = out["fp64"], out["bf16x3"]
+    assert np.max(np.abs(f16 - f64)) < 2e-5
+    tol_g, tol_p = (1e-3, 2e-3) if kind == "coherent" else (1e-2, 5e-3)
+    assert np.linalg.norm(g16 - g64) < tol_g * np.linalg.norm(g64)
+    assert np.linalg.norm(p16 - p64) < tol_p * np.linalg.norm(p64)
