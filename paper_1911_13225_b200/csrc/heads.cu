@@ -102,13 +102,17 @@ __global__ void k_view_prep(const dist_camera *__restrict__ cams, LevelState ls,
   }
 }
 
-// one block per view: depth loss = sum_i w_i |r_i| over the view's samples
+// depth loss = sum_i w_i |r_i| over each view's samples: gridDim.y blocks per
+// view sum fixed chunks into part[v][b]; k_view_loss_finish adds them in order
+constexpr int kLossBlocks = 64;
 __global__ void k_view_depth_loss(const dist_camera *__restrict__ cams, LevelState ls, int K,
-                                  HeadsDev h, ObjIn in, const int32_t *npx, double *terms) {
+                                  HeadsDev h, ObjIn in, const int32_t *npx, double *part) {
   __shared__ double red[32];
-  const int v = blockIdx.x;
+  const int v = blockIdx.x, b = blockIdx.y, nb = gridDim.y;
   const int64_t WH = (int64_t)ls.lw * ls.lh;
-  const int64_t s0 = h.view_samp[v], s1 = h.view_samp[v + 1];
+  const int64_t v0 = h.view_samp[v], v1 = h.view_samp[v + 1];
+  const int64_t chunk = (v1 - v0 + nb - 1) / nb;
+  const int64_t s0 = v0 + b * chunk, s1 = min(v1, s0 + chunk);
   double acc = 0.0;
   if (in.obs_depth && npx[v] > 0) {
     for (int64_t i = s0 + threadIdx.x; i < s1; i += blockDim.x) {
@@ -127,7 +131,15 @@ __global__ void k_view_depth_loss(const dist_camera *__restrict__ cams, LevelSta
     }
   }
   const double s = block_sum(acc, red);
-  if (threadIdx.x == 0) terms[v * 4 + 0] = s;
+  if (threadIdx.x == 0) part[(size_t)v * nb + b] = s;
+}
+
+__global__ void k_view_loss_finish(int V, int nb, const double *__restrict__ part, double *terms) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[(size_t)v * nb + b];
+    terms[v * 4 + 0] = s;
+  }
 }
 
 // per shape: grad += w_lat * 2 z; total = sum_views(w_d L_d + w_s L_s) + w_lat |z|^2
@@ -202,7 +214,7 @@ __global__ void k_adam(int S, int D, double *params, const double *grad, double 
 
 struct ObjLayout {
   HeadsDev h;
-  double *c0, *cs, *part0, *parts, *col0, *cols, *sil_seed, *gdotv, *probe_f;
+  double *c0, *cs, *part0, *parts, *col0, *cols, *sil_seed, *gdotv, *probe_f, *loss_part;
   int32_t *npx, *bcount, *conv, *conv_count;
   size_t bytes;
 };
@@ -227,6 +239,7 @@ static ObjLayout obj_layout(const DecView &dv, int V, int W, int H, int K, int S
   L.conv = cv.take<int32_t>(mode == 1 ? n : 1);
   L.conv_count = cv.take<int32_t>(4);
   L.npx = cv.take<int32_t>(V);
+  L.loss_part = cv.take<double>((size_t)V * kLossBlocks);
   L.bcount = cv.take<int32_t>(ceil_div(n * K, kScanBlock) + 1);
   L.c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
   L.cs = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
@@ -322,8 +335,10 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
     rc = launch_vjp_gen<float>(dv, L.c0, L.cs, gen, n * K, s1, L.part0, L.parts, nullptr, G, &grid, sm);
   if (rc) return rc;
   // 4. losses, code gradient, regulariser
-  k_view_depth_loss<<<V, 1024, 0, sm>>>(cams, ls, K, L.h, in, L.npx, io->view_terms);
+  k_view_depth_loss<<<dim3(V, kLossBlocks), 256, 0, sm>>>(cams, ls, K, L.h, in, L.npx, L.loss_part);
   DIST_CHECK_LAUNCH("k_view_depth_loss");
+  k_view_loss_finish<<<(int)ceil_div(V, 128), 128, 0, sm>>>(V, kLossBlocks, L.loss_part, io->view_terms);
+  DIST_CHECK_LAUNCH("k_view_loss_finish");
   if (dv.latent_dim > 0) {
     rc = reduce_code_grad(dv, s1, grid, L.part0, L.parts, L.col0, L.cols, io->grad, sm);
     if (rc) return rc;
