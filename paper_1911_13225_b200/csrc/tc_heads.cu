@@ -40,6 +40,7 @@ struct HParams {
   const float *w_out;  // [512]
   const float *winv_b; // [G] inverse power-of-two scales of the backward pack
   const float *nrm_b;  // [G] max row l1 norm of each backward W: |g W^T| <= max|g| * nrm
+  // nrm_b[G] = max |w_out|: |first backward operand| <= |gout| * max |w_out|
   int n_gemm;
   int S;
   int timeline;        // DIST_TC_TIMELINE: CTA 0 / thread 64 records %globaltimer marks
@@ -207,7 +208,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     auto mask_addr = [&](int ml) { return tq + 256 + ml * 8 + sub * 4; };
     const int n0 = P.dv.np[0];
     uint32_t phase = 0;
-    float *gout = reinterpret_cast<float *>(&m.xch[0][0]);   // [64] per-row head gradient
+    // [64] per-row head gradient; m.ray is unused by this kernel, so gout does
+    // not alias the m.xch row exchange
+    float *gout = reinterpret_cast<float *>(&m.ray[0]);
     // the next tile's sample point is fetched during the current tile's last
     // backward GEMM (a dependent chain of global loads)
     auto fetch = [&](int64_t tt, double (&q)[3], int &ss) {
@@ -325,35 +328,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (row_thread) gout[row] = (float)go;
       epi_sync();
       TL(5);
-      // Row scale exchange for the fp16 backward operand: every epilogue warp
-      // posts its part max, the row's scale is a power of two of the total.
-      auto row_max = [&](float part) -> float {
-        epi_sync();   // previous readers of m.xch (gout, earlier maxima) are done
-        m.xch[half * 2 + sub][row] = part;
-        epi_sync();
-        return fmaxf(fmaxf(m.xch[0][row], m.xch[1][row]), fmaxf(m.xch[2][row], m.xch[3][row]));
-      };
       float rinv;   // 1 / (this row's scale of the A operand now in smem)
       float amax;   // max |g| of this row's A operand (true units)
       {
+        // one pass: the scale comes from the bound |gout| * max|w_out|; the true
+        // row max of what is written feeds the first backward phase's bound
         const float gr = gout[row];
         uint32_t mk[4];
         tmem_ld4(mask_addr(G), mk);
-        float part = 0.f;
-        for (int nh = 0; nh < 2; ++nh) {
-          const int cb = nh * 256 + half * 128 + sub * 64;
-#pragma unroll 2
-          for (int j = 0; j < 64; j += 8) {
-            float wo[8];
-            ldg8(P.w_out + cb + j, wo);
-            const uint32_t wb = get4(mk, nh * 2 + (j >> 5)) >> (j & 31);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) part = fmaxf(part, ((wb >> e) & 1u) ? fabsf(wo[e]) : 0.f);
-          }
-        }
-        amax = row_max(part * fabsf(gr));
-        const float sc = pow2_scale(amax);
+        const float sc = pow2_scale(fabsf(gr) * P.nrm_b[G]);
         rinv = 1.f / sc;
+        float part = 0.f;
         for (int nh = 0; nh < 2; ++nh) {
           const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll 2
@@ -362,14 +347,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             ldg8(P.w_out + cb + j, wo);
             const uint32_t wb = get4(mk, nh * 2 + (j >> 5)) >> (j & 31);
 #pragma unroll
-            for (int e = 0; e < 8; ++e) x[e] = ((wb >> e) & 1u) ? (gr * sc) * wo[e] : 0.f;
+            for (int e = 0; e < 8; ++e) {
+              x[e] = ((wb >> e) & 1u) ? (gr * sc) * wo[e] : 0.f;
+              part = fmaxf(part, fabsf(x[e]));
+            }
             put8h(smem, row, cb + j, x);
           }
         }
+        m.xch[half * 2 + sub][row] = part * rinv;
       }
       fence_proxy_async();
       tc_fence_before();
       epi_sync();
+      amax = fmaxf(fmaxf(m.xch[0][row], m.xch[1][row]), fmaxf(m.xch[2][row], m.xch[3][row]));
+      named_arrive(2, 2 * N_EPI_WARPS * 32);   // this read happens before phase G-1 posts its maxima
       if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
       TL(6);
       // ---- backward through GEMM layers G-1 .. 0 ----
@@ -412,7 +403,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           }
           // post this warp's part max; barrier 2 orders it after every warp's
           // read of the previous phase's maxima (bar.arrive there, below)
-          if (gl < G - 1) named_sync(2, 2 * N_EPI_WARPS * 32);
+          named_sync(2, 2 * N_EPI_WARPS * 32);
           m.xch[half * 2 + sub][row] = part * rinv;
           tc_fence_before();
           fence_proxy_async();
@@ -534,6 +525,7 @@ int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t
   P.w_out = dv.tc_bias[0] + (size_t)(dv.n_layers - 2) * tc::KDIM;
   P.winv_b = dv.tc_bias[1];
   P.nrm_b = dv.tc_bias[1] + (dv.n_layers - 2);
+
   P.n_gemm = dv.n_layers - 2;
   P.S = S;
   {

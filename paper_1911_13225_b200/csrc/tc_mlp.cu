@@ -575,7 +575,8 @@ bool tc_supported(const DecView &dv) {
 //   1: bf16x3 only -- backward pack for k_tc_heads: W untransposed as fp16
 //      hi/lo, each layer scaled by a power of two (max |W| in [2^14, 2^15));
 //      tc_bias[1] holds the [G] inverse scales, then the [G] row l1 norms
-//      max_n sum_k |W[n][k]| that bound the dgrad growth.  The backward GEMMs are
+//      max_n sum_k |W[n][k]| that bound the dgrad growth, then max |w_out|.
+//      The backward GEMMs are
 //      fp16x2: g (one row-scaled fp16 term) x (W_hi + W_lo), see tc_heads.cu
 //   2: bf16x3 only -- fp16x3 forward pack for the (mid, diff) normal probes:
 //      fp16's 11-bit halves carry the diff rows to ~1e-5 where bf16's 8-bit
@@ -589,7 +590,7 @@ void tc_pack_sizes(const DecView &dv, const std::function<void(int, size_t, size
   const size_t bb = ((size_t)(G + 1) * tc::KDIM + G) * sizeof(float);
   put(0, wb, bb);
   if (dv.prec == DIST_PREC_BF16X3) {
-    put(1, wb, ((size_t)2 * G * sizeof(float) + 15) / 16 * 16);
+    put(1, wb, ((size_t)(2 * G + 1) * sizeof(float) + 15) / 16 * 16);
     put(2, wb, bb);
   }
 }
@@ -627,6 +628,11 @@ void tc_pack_fill(const DecView &dv, const double *const *W, const double *const
       nrm = std::max(nrm, r);
     }
     winv_b[G + g] = (float)(nrm * (1.0 + 1e-6));   // rounded up: a bound
+    if (g == G - 1) {   // [2G]: max |w_out|, bounds the first backward operand
+      double wm = 0.0;
+      for (int k = 0; k < dims[dv.n_layers - 1]; ++k) wm = std::max(wm, std::fabs(W[dv.n_layers - 1][k]));
+      winv_b[2 * G] = (float)(wm * (1.0 + 1e-6));
+    }
     for (int n = 0; n < K; ++n)        // n: layer input index (dgrad output)
       for (int k = 0; k < K; ++k) {    // k: layer output index (contracted)
         const float x = (n < kin && k < nout) ? (float)W[l][(size_t)n * nout + k] * sc : 0.f;
