@@ -324,8 +324,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           go = sd * head_dact(P.dv.final_act, fv);
         }
       }
-      epi_sync();
-      if (row_thread) gout[row] = (float)go;
+      if (row_thread) gout[row] = (float)go;   // gout does not alias m.xch: no barrier before
       epi_sync();
       TL(5);
       float rinv;   // 1 / (this row's scale of the A operand now in smem)
