@@ -143,7 +143,7 @@ def run_reference(args):
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": float(np.mean([i["seconds"] for i in infos]) * 1e3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": _config(args),
+            "data": "synthetic", "config": dict(_config(args), precision="fp64 (numpy port of the reference)"),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": infos[0]["cores"], "kind": "port",
                              "sample": infos[0]["sample"]},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
