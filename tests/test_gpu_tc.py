@@ -167,3 +167,25 @@ def test_tc_vjp_matches_fp64(st, S, kind):
     tol_g, tol_p = (1e-3, 2e-3) if kind == "coherent" else (1e-2, 5e-3)
     assert np.linalg.norm(g16 - g64) < tol_g * np.linalg.norm(g64)
     assert np.linalg.norm(p16 - p64) < tol_p * np.linalg.norm(p64)
+
+
+def test_c3_full_size_bf16x3_vs_fp32(st):
+    """BASELINE config 3 at full size (8 ring views x 512^2, the bench workload):
+    one latent-optimisation iterate on the tensor cores (bf16x3) against the
+    fp32 SIMT path on the same inputs -- queries, loss and latent gradient."""
+    from paper_1911_13225_b200.workloads import render_depth_observations, ring_views, target_code
+    views = ring_views(8, 512)
+    cfg = st.TraceConfig(k_samples=3)
+    ref_field = st.NeuralField.geometric(256, (512,) * 8, 0, precision="fp32")
+    obs = render_depth_observations(ref_field, target_code(1), views, cfg)
+    out = {}
+    for prec in ("fp32", "bf16x3"):
+        field = ref_field if prec == "fp32" else ref_field.with_precision(prec)
+        opt = st.LatentOptimizer(field, views, {"depth": obs}, np.zeros((1, 256)), cfg, max_iters=1)
+        dt = opt.objective()
+        out[prec] = (dt.stats()["total_queries"], float(opt.shape_terms[0, 0].item()),
+                     opt.grad.cpu().numpy()[0])
+    (q32, l32, g32), (q16, l16, g16) = out["fp32"], out["bf16x3"]
+    assert abs(q16 - q32) <= 1e-3 * q32
+    assert abs(l16 - l32) <= 3e-4 * abs(l32)   # measured 8.4e-5
+    assert np.linalg.norm(g16 - g32) <= 1e-3 * np.linalg.norm(g32)
