@@ -178,6 +178,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     mbar_init(&m.dfull[0], 1);
     mbar_init(&m.dfull[1], 1);
     mbar_init(&m.aready, 2);
+    mbar_init(&m.aready2, 2);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -226,6 +227,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int nh = 0; nh < 2; ++nh) {
             const uint32_t d = tmem + nh * 128;
             for (int kc = 0; kc < NKB; ++kc, ++it) {
+              if (nh == 0 && kc == NKB / 2) {   // second half of A: written after the first
+                mbar_wait(&m.aready2, layer & 1);
+                tc_fence_after();
+              }
               const int s = it % STAGES;
               mbar_wait(&m.full[s], (it / STAGES) & 1);
               tc_fence_after();
@@ -282,6 +287,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int half = q >> 1;                // which 128-column half of each N-half
     const bool row_thread = (sub == 0 && half == 0);   // warps 4, 5: one thread per row
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+    // the next layer's A is announced in two halves (K blocks 0..3, 4..7) so
+    // the MMA warp can start the next GEMM's first N half on the first
+    auto a_ready_lo = [&] { if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0); };
+    auto a_ready_hi = [&] { if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready2, 0); };
+    auto a_ready_all = [&] { a_ready_lo(); a_ready_hi(); };
     // D columns [col, col+32) of this thread's lane (+ the correction accumulator)
     auto load_d = [&](int col, float (&v)[32]) {
       if (P.acc_mode) {
@@ -406,7 +416,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       }
       fence_proxy_async();
       epi_sync();
-      if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+      a_ready_all();
       TL(2);
       // the previous tile's row results, while this tile's first GEMM runs
       if (row_thread && pend) R.finish(m, pgi, pid, pvalid, pfv);
@@ -438,7 +448,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           tc_fence_before();
           if (!last) {
             epi_sync();
-            if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+            a_ready_all();
           }
           continue;
         }
@@ -471,6 +481,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           float inv;
           row_scale(tmax, sc, inv);
           for (int nh = 0; nh < 2; ++nh) {
+            if (!F16 && nh == 1) {   // columns 0..255 of every row are in A: announce them
+              fence_proxy_async();
+              tc_fence_before();
+              epi_sync();
+              a_ready_lo();
+            }
             const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
@@ -494,7 +510,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (!last) {
           fence_proxy_async();
           epi_sync();
-          if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+          if (F16) a_ready_all();
+          else a_ready_hi();
           TL(4);
         }
       }
@@ -525,7 +542,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       epi_sync();
       TL(9);
       if (G == 0) {  // no hidden GEMM layers: never happens for tc_supported decoders
-        if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+        a_ready_all();
       }
     }
     if (row_thread && pend) R.finish(m, pgi, pid, pvalid, pfv);
