@@ -114,6 +114,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     mbar_init(&m.dfull[0], 1);
     mbar_init(&m.dfull[1], 1);
     mbar_init(&m.aready, 2);
+    mbar_init(&m.aready2, 2);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -166,6 +167,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int nh = 0; nh < 2; ++nh) {
             const uint32_t d = tmem + nh * 128;
             for (int kc = 0; kc < NKB; ++kc, ++it) {
+              if (nh == 0 && kc == NKB / 2) {   // second half of A: written after the first
+                mbar_wait(&m.aready2, phase & 1);
+                tc_fence_after();
+              }
               const int s = it % STAGES;
               mbar_wait(&m.full[s], (it / STAGES) & 1);
               tc_fence_after();
@@ -204,6 +209,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int half = q >> 1;
     const bool row_thread = (sub == 0 && half == 0);
     const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16);
+    // the next GEMM's A is announced in two halves (K blocks 0..3, 4..7): the MMA
+    // warp starts its first N half while the epilogue writes the second
+    auto a_ready_lo = [&] { if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0); };
+    auto a_ready_hi = [&] { if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready2, 0); };
+    auto a_ready_all = [&] { a_ready_lo(); a_ready_hi(); };
+    auto announce_lo = [&] {
+      fence_proxy_async();
+      tc_fence_before();
+      epi_sync();
+      a_ready_lo();
+    };
     // mask bits of layer output ml, this thread's 2 x 64 columns: TMEM cols 256 + 8 ml + 4 sub
     auto mask_addr = [&](int ml) { return tq + 256 + ml * 8 + sub * 4; };
     const int n0 = P.dv.np[0];
@@ -260,7 +276,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       fence_proxy_async();
       tc_fence_before();
       epi_sync();
-      if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+      a_ready_all();
       TL(2);
       // the seed's loads, issued once layer 0 is handed to the MMA warp so
       // they land during the forward GEMMs
@@ -277,6 +293,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         const float *bias = P.bias + (size_t)l * KDIM;
         uint32_t mk[4] = {0, 0, 0, 0};
         for (int nh = 0; nh < 2; ++nh) {
+          if (nh == 1 && !last) announce_lo();
           const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
@@ -306,7 +323,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (!last) {
           fence_proxy_async();
           epi_sync();
-          if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+          a_ready_hi();
           TL(4);
         }
       }
@@ -360,7 +377,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       epi_sync();
       amax = fmaxf(fmaxf(m.xch[0][row], m.xch[1][row]), fmaxf(m.xch[2][row], m.xch[3][row]));
       named_arrive(2, 2 * N_EPI_WARPS * 32);   // this read happens before phase G-1 posts its maxima
-      if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+      a_ready_all();
       TL(6);
       // ---- backward through GEMM layers G-1 .. 0 ----
       for (int gl = G - 1; gl >= 0; --gl, ++phase) {
@@ -382,6 +399,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           rinv = 1.f / sc;
           float part = 0.f;
           for (int nh = 0; nh < 2; ++nh) {
+            if (nh == 1) announce_lo();
             const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
@@ -409,7 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           epi_sync();
           amax = fmaxf(fmaxf(m.xch[0][row], m.xch[1][row]), fmaxf(m.xch[2][row], m.xch[3][row]));
           if (gl >= 2) named_arrive(2, 2 * N_EPI_WARPS * 32);
-          if (warp == 2 && lane == 0) mbar_arrive_cluster(&m.aready, 0);
+          a_ready_hi();
           TL(8);
         } else {
           // g_pre0 = D * mask0 * unscale; column sums over the CTA's rows, per
