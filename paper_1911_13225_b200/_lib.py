@@ -176,15 +176,22 @@ def stream_ptr():
     return torch.cuda.current_stream().cuda_stream
 
 
+_ws_cache: dict = {}
+
+
 def workspace(nbytes: int):
-    """A cached device scratch buffer (grown on demand, per device/stream use)."""
+    """A cached device scratch buffer per (device, stream), grown on demand.
+
+    Calls on one stream are ordered, so they may share it; a different stream
+    gets its own buffer (the C ABI itself takes per-call workspaces)."""
     import torch
     nbytes = max(int(nbytes), 256)
-    buf = getattr(workspace, "_buf", None)
-    if buf is None or buf.numel() < nbytes or buf.device != torch.device("cuda",
-                                                                          torch.cuda.current_device()):
-        buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
-        workspace._buf = buf
+    key = (torch.cuda.current_device(), torch.cuda.current_stream().cuda_stream)
+    with _lock:
+        buf = _ws_cache.get(key)
+        if buf is None or buf.numel() < nbytes:
+            buf = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+            _ws_cache[key] = buf
     return buf
 
 
