@@ -42,6 +42,8 @@ __global__ void k_code_bias(DecView dv, const double *__restrict__ codes, int S,
     for (int k = 0; k < D; ++k) v = fma(codes[(size_t)s * D + k], dv.W0z[(size_t)k * n0 + j], v);
     c0[idx] = v;
     reinterpret_cast<float *>(c0 + total)[idx] = (float)v;   // fp32 copy (kernels.cuh c0_f32)
+    // per-shape max |c0| (kernels.cuh c0_absmax): non-negative floats order as ints
+    atomicMax(reinterpret_cast<int *>(c0 + total) + total + s, __float_as_int(fabsf((float)v)));
   }
   if (dv.skip > 0) {
     const int ns = dv.nskip;
@@ -60,6 +62,8 @@ int launch_code_bias(const DecView &dv, const double *codes, int S, double *c0, 
                      cudaStream_t st) {
   if (S <= 0) return DIST_OK;
   const int n = S * dv.np[0];
+  cudaError_t e = cudaMemsetAsync(const_cast<float *>(c0_absmax(c0, S, dv.np[0])), 0, sizeof(float) * S, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(c0 max)");
   k_code_bias<<<(int)std::min<int64_t>(ceil_div(n, 256), 1024), 256, 0, st>>>(dv, codes, S, c0,
                                                                               cskip);
   DIST_CHECK_LAUNCH("k_code_bias");

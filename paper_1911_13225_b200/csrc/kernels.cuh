@@ -9,12 +9,16 @@ namespace dist {
 int sm_count();
 // c0 buffers hold [s1][np0] fp64 followed by the same values in fp32 (read by
 // the tensor-core prologues, which would otherwise convert per row and column)
+// and then [s1] per-shape max |c0| (bounds the fp16 row scale of layer 0)
 inline size_t c0_doubles(int s1, int np0) {
   const size_t n = (size_t)s1 * np0;
-  return n + (n + 1) / 2;
+  return n + (n + 1) / 2 + ((size_t)s1 + 1) / 2;
 }
 inline const float *c0_f32(const double *c0, int s1, int np0) {
   return reinterpret_cast<const float *>(c0 + (size_t)s1 * np0);
+}
+inline const float *c0_absmax(const double *c0, int s1, int np0) {
+  return c0_f32(c0, s1, np0) + (size_t)s1 * np0;
 }
 int launch_code_bias(const DecView &dv, const double *codes, int S, double *c0, double *cskip,
                      cudaStream_t st);

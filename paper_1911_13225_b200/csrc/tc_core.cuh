@@ -237,11 +237,12 @@ __device__ __forceinline__ void put8(char *smem, int row, int k0, const float (&
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     if constexpr (F16) {
-      uint16_t h0, h1, l0, l1;
-      split2<F16>(x[2 * i], h0, l0);
-      split2<F16>(x[2 * i + 1], h1, l1);
-      hi[i] = (uint32_t)h0 | ((uint32_t)h1 << 16);
-      lo[i] = (uint32_t)l0 | ((uint32_t)l1 << 16);
+      // packed: one cvt.rn.f16x2.f32 for hi, one back to f32x2, one for lo
+      const __half2 h = __floats2half2_rn(x[2 * i], x[2 * i + 1]);
+      const float2 hf = __half22float2(h);
+      const __half2 l = __floats2half2_rn(x[2 * i] - hf.x, x[2 * i + 1] - hf.y);
+      hi[i] = *reinterpret_cast<const uint32_t *>(&h);
+      lo[i] = *reinterpret_cast<const uint32_t *>(&l);
     } else {
       // one cvt.rn.bf16x2 per pair; bf16 -> f32 is a 16-bit shift
       const __nv_bfloat162 h = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);

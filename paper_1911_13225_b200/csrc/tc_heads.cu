@@ -523,7 +523,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
 // ---------------------------------------------------------------------------
 bool tc_heads_supported(const DecView &dv) {
-  return dv.prec == DIST_PREC_BF16X3 && tc_supported(dv) && dv.tc_w[1] != nullptr;
+  // the head kernel's forward is bf16x3 in both split modes: slot 0 of a bf16x3
+  // decoder, slot 3 of an fp16x3 one (tc_mlp.cu packs)
+  const int fs = dv.prec == DIST_PREC_FP16X3 ? 3 : 0;
+  return tc_supported(dv) && dv.tc_w[1] != nullptr && dv.tc_w[fs] != nullptr;
 }
 
 
@@ -531,15 +534,16 @@ template <class Gen>
 int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
                     double *part0, int grid_cap, int *grid_out, cudaStream_t st, double *gpts) {
   CUtensorMap mf, mb;
-  int rc = tc_make_map(dv, 0, &mf);
+  const int fs = dv.prec == DIST_PREC_FP16X3 ? 3 : 0;   // bf16x3 forward pack
+  int rc = tc_make_map(dv, fs, &mf);
   if (!rc) rc = tc_make_map(dv, 1, &mb);
   if (rc) return rc;
   tc::HParams P;
   P.dv = dv;
   P.c0 = c0;
   P.c0f = c0_f32(c0, S, dv.np[0]);
-  P.bias = dv.tc_bias[0];
-  P.w_out = dv.tc_bias[0] + (size_t)(dv.n_layers - 2) * tc::KDIM;
+  P.bias = dv.tc_bias[fs];
+  P.w_out = dv.tc_bias[fs] + (size_t)(dv.n_layers - 2) * tc::KDIM;
   P.winv_b = dv.tc_bias[1];
   P.nrm_b = dv.tc_bias[1] + (dv.n_layers - 2);
 

@@ -46,6 +46,8 @@ struct Params {
   const float *bias;      // [L-2][512] hidden biases 1..L-2 (fp32)
   const float *w_out;     // [512]
   const float *winv;      // [L-2] inverse power-of-2 weight scales (fp16x3), 1 for bf16x3
+  const float *cn, *bm, *w0m;  // fp16 row-scale bounds (tc_mlp.cu fill_fwd)
+  const float *c0max;     // [S] max |c0| per shape
   int n_gemm;             // hidden GEMM layers (L-2)
   int acc_mode;           // 0: one accumulator; 1: two (even/odd K blocks); 2: hi*hi | corrections
   int timeline;           // DIST_TC_TIMELINE: phase marks of CTA 0 (debug)
@@ -319,6 +321,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       r.id = -1;
       if (t < ntiles && r.gi < nrows) r.id = load_row(R, m, r.gi, r.p, r.s);
     };
+    bool xpend = false;   // an xch_read's barrier-2 arrive awaits its matching sync
     bool pend = false, pvalid = false;
     int64_t pgi = 0;
     int pid = -1;
@@ -391,7 +394,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
       };
       float sc = 1.f, rinv = 1.f;
-      if constexpr (F16) {
+      // fp16 without pairs: every row scale comes from an a-priori bound, so
+      // each layer is one pass; the true row max of what is written (amax)
+      // feeds the next layer's bound through m.xch.  Named barrier 2 orders a
+      // post after every warp's read of the previous one (xch_read arrives,
+      // the next xch_post syncs).
+      constexpr bool kBound = F16 && !PAIR;
+      float amax = 0.f;
+      auto xch_post = [&](float v) {
+        if (xpend) named_sync(2, 2 * N_EPI_WARPS * 32);
+        xpend = false;
+        m.xch[half * 2 + sub][row] = v;
+      };
+      auto xch_read = [&]() -> float {
+        const float r = fmaxf(fmaxf(m.xch[0][row], m.xch[1][row]), fmaxf(m.xch[2][row], m.xch[3][row]));
+        named_arrive(2, 2 * N_EPI_WARPS * 32);
+        xpend = true;
+        return r;
+      };
+      if constexpr (kBound) {
+        const float b0 = s >= 0 ? (P.c0max[s] + fabsf(px) * P.w0m[0] + fabsf(py) * P.w0m[1] +
+                                   fabsf(pz) * P.w0m[2]) * 1.000001f
+                                : 0.f;
+        sc = pow2_scale(b0);
+        rinv = 1.f / sc;
+      } else if constexpr (F16) {
         float tmax = 0.f;
         for (int nh = 0; nh < 2; ++nh)
 #pragma unroll 1
@@ -403,20 +430,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           }
         row_scale(tmax, sc, rinv);
       }
-      for (int nh = 0; nh < 2; ++nh) {
-        const int cb = nh * 256 + half * 128 + sub * 64;
+      {
+        float part = 0.f;
+        for (int nh = 0; nh < 2; ++nh) {
+          const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll 2
-        for (int j = 0; j < 64; j += 8) {
-          float x[8];
-          h0x8(cb + j, x);
+          for (int j = 0; j < 64; j += 8) {
+            float x[8];
+            h0x8(cb + j, x);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) x[e] *= sc;
-          put8<F16>(smem, row, cb + j, x);
+            for (int e = 0; e < 8; ++e) {
+              if constexpr (kBound) part = fmaxf(part, x[e]);
+              x[e] *= sc;
+            }
+            put8<F16>(smem, row, cb + j, x);
+          }
         }
+        if constexpr (kBound) xch_post(part);
       }
       fence_proxy_async();
       epi_sync();
       a_ready_all();
+      if constexpr (kBound) amax = xch_read();
       TL(2);
       // the previous tile's row results, while this tile's first GEMM runs
       if (row_thread && pend) R.finish(m, pgi, pid, pvalid, pfv);
@@ -455,7 +490,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         // fp16: pass 1 finds the row max for the next scale (and the head on the
         // last layer); bf16 needs no scale, so one pass reads D and writes A.
         float tmax = 0.f;
-        if (F16 || last) {
+        if ((F16 && !kBound) || last) {
           for (int nh = 0; nh < 2; ++nh) {
             const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll
@@ -479,9 +514,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         if (!last) {
           float inv;
-          row_scale(tmax, sc, inv);
+          if constexpr (kBound) {
+            sc = pow2_scale((amax * P.cn[l] + P.bm[l]) * 1.000001f);
+            inv = 1.f / sc;
+          } else {
+            row_scale(tmax, sc, inv);
+          }
+          float part = 0.f;
           for (int nh = 0; nh < 2; ++nh) {
-            if (!F16 && nh == 1) {   // columns 0..255 of every row are in A: announce them
+            if ((!F16 || kBound) && nh == 1) {   // columns 0..255 of every row are in A: announce them
               fence_proxy_async();
               tc_fence_before();
               epi_sync();
@@ -498,24 +539,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 ldg8(bias + cb + c * 32 + g8 * 8, bb);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                  x[e] = act(v[g8 * 8 + e], bb[e]) * sc;
+                  const float y = act(v[g8 * 8 + e], bb[e]);
+                  if constexpr (kBound) part = fmaxf(part, y);
+                  x[e] = y * sc;
                 }
                 put8<F16>(smem, row, cb + c * 32 + g8 * 8, x);
               }
             }
           }
+          if constexpr (kBound) xch_post(part);
           rinv = inv;
         }
         tc_fence_before();
         if (!last) {
           fence_proxy_async();
           epi_sync();
-          if (F16) a_ready_all();
+          if (F16 && !kBound) a_ready_all();
           else a_ready_hi();
+          if constexpr (kBound) amax = xch_read();
           TL(4);
         }
       }
       // ---- head: combine the four partial dot products of each row ----
+      if (xpend) named_sync(2, 2 * N_EPI_WARPS * 32);
+      xpend = false;
       m.xch[half * 2 + sub][row] = head;
       epi_sync();
       if (row_thread) {
@@ -598,18 +645,19 @@ bool tc_supported(const DecView &dv) {
 //   2: bf16x3 only -- fp16x3 forward pack for the (mid, diff) normal probes:
 //      fp16's 11-bit halves carry the diff rows to ~1e-5 where bf16's 8-bit
 //      halves leave ~1e-4 (normals)
+//   3: fp16x3 only -- bf16x3 forward pack for the fused head kernel (its
+//      forward phases are bf16x3 in both modes)
 void tc_pack_sizes(const DecView &dv, const std::function<void(int, size_t, size_t)> &put) {
   for (int l = 0; l <= dv.n_layers - 2; ++l)
     if (dv.np[l] != tc::KDIM) return;
   if (dv.skip >= 0 || dv.n_layers < 3) return;
   const int G = dv.n_layers - 2;
   const size_t wb = (size_t)G * 2 * tc::KDIM * tc::KDIM * 2;
-  const size_t bb = ((size_t)(G + 1) * tc::KDIM + G) * sizeof(float);
+  // biases, w_out, winv[G], then the fp16 row-scale bounds cn[G], bm[G], w0m[3]
+  const size_t bb = ((size_t)(G + 1) * tc::KDIM + 3 * G + 3) * sizeof(float);
   put(0, wb, bb);
-  if (dv.prec == DIST_PREC_BF16X3) {
-    put(1, wb, ((size_t)(2 * G + 1) * sizeof(float) + 15) / 16 * 16);
-    put(2, wb, bb);
-  }
+  put(1, wb, ((size_t)(2 * G + 1) * sizeof(float) + 15) / 16 * 16);
+  put(dv.prec == DIST_PREC_BF16X3 ? 2 : 3, wb, bb);
 }
 
 static void fill_fwd(const DecView &dv, const double *const *W, const double *const *b,
@@ -623,8 +671,8 @@ void tc_pack_fill(const DecView &dv, const double *const *W, const double *const
   if (dv.skip >= 0 || dv.n_layers < 3) return;
   const bool f16 = dv.prec == DIST_PREC_FP16X3;
   fill_fwd(dv, W, b, dims, f16, reinterpret_cast<uint16_t *>(wdst(0)), bdst(0));
-  if (f16) return;
-  fill_fwd(dv, W, b, dims, true, reinterpret_cast<uint16_t *>(wdst(2)), bdst(2));
+  const int other = f16 ? 3 : 2;   // the forward pack in the other 16-bit type
+  fill_fwd(dv, W, b, dims, !f16, reinterpret_cast<uint16_t *>(wdst(other)), bdst(other));
   const int G = dv.n_layers - 2, K = tc::KDIM;
   auto to16 = [](float x) -> uint16_t { return __half_as_ushort(__float2half_rn(x)); };
   auto from16 = [](uint16_t h) -> float { return __half2float(__ushort_as_half(h)); };
@@ -696,6 +744,29 @@ static void fill_fwd(const DecView &dv, const double *const *W, const double *co
   }
   const int L = dv.n_layers;
   for (int k = 0; k < K; ++k) bb[(size_t)G * K + k] = k < dims[L - 1] ? (float)W[L - 1][k] : 0.f;
+  // a-priori bounds for single-pass fp16 row scales (true units, rounded up):
+  // |relu(h W_l + b_l)| <= max|h| * cn[l] + bm[l], cn = max column l1 norm;
+  // layer 0: |relu(c0 + p W0p)| <= max|c0| + sum_a |p_a| w0m[a]
+  float *cn = winv + G, *bm = cn + G, *w0m = bm + G;
+  for (int g = 0; g < G; ++g) {
+    const int l = g + 1;
+    const int kin = dims[l], nout = dims[l + 1];
+    double c = 0.0, m = 0.0;
+    for (int n = 0; n < nout; ++n) {
+      double s = 0.0;
+      for (int k = 0; k < kin; ++k) s += std::fabs(W[l][(size_t)k * nout + n]);
+      c = std::max(c, s);
+      m = std::max(m, std::fabs(b[l][n]));
+    }
+    cn[g] = (float)(c * (1.0 + 1e-6));
+    bm[g] = (float)(m * (1.0 + 1e-6));
+  }
+  const int D = dv.latent_dim, n0 = dims[1];
+  for (int a = 0; a < 3; ++a) {
+    double m = 0.0;
+    for (int n = 0; n < n0; ++n) m = std::max(m, std::fabs(W[0][(size_t)(D + a) * n0 + n]));
+    w0m[a] = (float)(m * (1.0 + 1e-6));
+  }
 }
 
 int tc_make_map(const DecView &dv, int slot, CUtensorMap *map) {
@@ -706,7 +777,7 @@ int tc_make_map(const DecView &dv, int slot, CUtensorMap *map) {
   cuuint64_t gstride[1] = {(cuuint64_t)tc::KDIM * 2};
   cuuint32_t box[2] = {64, 128};
   cuuint32_t estr[2] = {1, 1};
-  const bool f16 = slot != 0 || dv.prec == DIST_PREC_FP16X3;
+  const bool f16 = slot == 1 || slot == 2 || (slot == 0 && dv.prec == DIST_PREC_FP16X3);
   const CUtensorMapDataType dt = f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
   CUresult r = enc(map, dt, 2, const_cast<void *>(dv.tc_w[slot]), gdim,
                    gstride, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -729,6 +800,10 @@ static int launch_tc_t(const DecView &dv, const double *c0, int S, const Rows &r
   P.w_out = dv.tc_bias[slot] + (size_t)(dv.n_layers - 2) * tc::KDIM;
   P.n_gemm = dv.n_layers - 2;
   P.winv = P.w_out + tc::KDIM;
+  P.cn = P.winv + (dv.n_layers - 2);
+  P.bm = P.cn + (dv.n_layers - 2);
+  P.w0m = P.bm + (dv.n_layers - 2);
+  P.c0max = c0_absmax(c0, S, dv.np[0]);
   {
     const char *am = getenv("DIST_TC_ACC");
     P.acc_mode = am ? atoi(am) : 3;

@@ -3,7 +3,7 @@ JSON line per config (time per iterate / render, rays/s, queries).  C3 is the
 bench.py workload; the others are parity-tested at small sizes in tests/ and
 run here for scale.
 
-  python scripts/run_configs.py [--only C4] [--precision bf16x3]
+  python scripts/run_configs.py [--only C4] [--precision fp16x3|bf16x3|fp32]
 """
 
 from __future__ import annotations
@@ -116,7 +116,7 @@ def c5(prec):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default=None)
-    ap.add_argument("--precision", default="bf16x3")
+    ap.add_argument("--precision", default="fp16x3")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     for name, fn in [("C1", c1), ("C2", c2), ("C3", c3), ("C4", c4), ("C5", c5)]:
