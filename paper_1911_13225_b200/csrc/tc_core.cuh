@@ -230,10 +230,9 @@ __device__ __forceinline__ void split2(float x, uint16_t &h, uint16_t &l) {
   }
 }
 
-// write 8 consecutive activations (k0..k0+7, k0 % 8 == 0) of `row` as hi/lo
+// split 8 activations into packed hi / lo 16-bit pairs of the MMA element type
 template <bool F16>
-__device__ __forceinline__ void put8(char *smem, int row, int k0, const float (&x)[8]) {
-  uint32_t hi[4], lo[4];
+__device__ __forceinline__ void pack8(const float (&x)[8], uint32_t (&hi)[4], uint32_t (&lo)[4]) {
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     if constexpr (F16) {
@@ -254,10 +253,36 @@ __device__ __forceinline__ void put8(char *smem, int row, int k0, const float (&
       lo[i] = *reinterpret_cast<const uint32_t *>(&l);
     }
   }
+}
+
+// store packed hi / lo words of 8 consecutive activations (k0 % 8 == 0) of `row`
+__device__ __forceinline__ void st8(char *smem, int row, int k0, const uint32_t *hi, const uint32_t *lo) {
   const uint32_t off = a_off(row, k0);
   *reinterpret_cast<uint4 *>(smem + OFF_AHI + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
   *reinterpret_cast<uint4 *>(smem + OFF_ALO + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
 }
+
+// write 8 consecutive activations (k0..k0+7, k0 % 8 == 0) of `row` as hi/lo
+template <bool F16>
+__device__ __forceinline__ void put8(char *smem, int row, int k0, const float (&x)[8]) {
+  uint32_t hi[4], lo[4];
+  pack8<F16>(x, hi, lo);
+  st8(smem, row, k0, hi, lo);
+}
+
+// 32 columns of this warp's TMEM lanes <- 32 registers (the early half's
+// packed A words parked in the accumulator columns they came from)
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]),
+      "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]),
+      "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // write 8 consecutive values (k0 % 8 == 0) of `row` as fp16 into A_hi only
 // (the single-term fp16 activation operand of the backward GEMMs)

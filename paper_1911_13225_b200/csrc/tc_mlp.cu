@@ -459,12 +459,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       TL(10);
       // ---- hidden layers ----
       float head = 0.f;
+      // Single-pass paths (bf16, bound-scaled fp16): the nh = 0 half of a GEMM
+      // completes ~6 us before the nh = 1 half.  Its columns are computed right
+      // away (bias, ReLU, split) and the packed hi/lo words parked in the TMEM
+      // columns just read -- they cannot go to A yet, the nh = 1 MMAs still read
+      // A.  After the GEMM, the parked words are copied to A, K blocks 0..3 are
+      // announced, then the nh = 1 columns are processed.
+      constexpr bool kEarly = !PAIR && (!F16 || kBound);
       for (int l = 0; l < G; ++l, ++layer) {
         if (l == G - 1) fetch(t + nclusters, nx);
-        mbar_wait(&m.dfull[1], layer & 1);
-        TL(3);
-        mbar_wait(&m.dfull[0], layer & 1);
-        tc_fence_after();
         const bool last = (l == G - 1);
         const float *bias = P.bias + (size_t)l * KDIM;
         const float unscale = rinv * P.winv[l];   // exact: both are powers of two
@@ -479,6 +482,122 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             return y > 0.f ? y : 0.f;
           }
         };
+        if (kEarly && P.debug != 1) {
+          float inv = 1.f, part = 0.f;
+          if (!last && kBound) {
+            sc = pow2_scale((amax * P.cn[l] + P.bm[l]) * 1.000001f);
+            inv = 1.f / sc;
+          }
+          mbar_wait(&m.dfull[0], layer & 1);
+          TL(3);
+          tc_fence_after();
+          // ---- early half: columns nh = 0 while the nh = 1 MMAs run ----
+          {
+            const int cb = half * 128 + sub * 64;
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+              float v[32];
+              load_d(sub * 64 + c * 32, v);
+              uint32_t r[32];
+#pragma unroll
+              for (int g8 = 0; g8 < 4; ++g8) {
+                float bb[8], x[8];
+                ldg8(bias + cb + c * 32 + g8 * 8, bb);
+                if (last) {
+                  float wo[8];
+                  ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) head = fmaf(act(v[g8 * 8 + e], bb[e]), wo[e], head);
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) {
+                    const float y = act(v[g8 * 8 + e], bb[e]);
+                    if constexpr (kBound) part = fmaxf(part, y);
+                    x[e] = y * sc;
+                  }
+                  uint32_t hi[4], lo[4];
+                  pack8<F16>(x, hi, lo);
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    r[g8 * 4 + i] = hi[i];
+                    r[16 + g8 * 4 + i] = lo[i];
+                  }
+                }
+              }
+              if (!last) tmem_st32(tq + sub * 64 + c * 32, r);
+            }
+            if (!last) tmem_wait_st();
+          }
+          mbar_wait(&m.dfull[1], layer & 1);
+          tc_fence_after();
+          if (!last) {
+            // parked words -> A (K blocks 0..3), announce, then the nh = 1 half
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+              float v[32];
+              tmem_ld32(tq + sub * 64 + c * 32, v);
+              const int k0 = half * 128 + sub * 64 + c * 32;
+#pragma unroll
+              for (int g8 = 0; g8 < 4; ++g8) {
+                uint32_t hi[4], lo[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  hi[i] = __float_as_uint(v[g8 * 4 + i]);
+                  lo[i] = __float_as_uint(v[16 + g8 * 4 + i]);
+                }
+                st8(smem, row, k0 + g8 * 8, hi, lo);
+              }
+            }
+            fence_proxy_async();
+            tc_fence_before();
+            epi_sync();
+            a_ready_lo();
+          }
+          {
+            const int cb = 256 + half * 128 + sub * 64;
+#pragma unroll 1
+            for (int c = 0; c < 2; ++c) {
+              float v[32];
+              load_d(128 + sub * 64 + c * 32, v);
+#pragma unroll
+              for (int g8 = 0; g8 < 4; ++g8) {
+                float x[8], bb[8];
+                ldg8(bias + cb + c * 32 + g8 * 8, bb);
+                if (last) {
+                  float wo[8];
+                  ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) head = fmaf(act(v[g8 * 8 + e], bb[e]), wo[e], head);
+                } else {
+#pragma unroll
+                  for (int e = 0; e < 8; ++e) {
+                    const float y = act(v[g8 * 8 + e], bb[e]);
+                    if constexpr (kBound) part = fmaxf(part, y);
+                    x[e] = y * sc;
+                  }
+                  put8<F16>(smem, row, cb + c * 32 + g8 * 8, x);
+                }
+              }
+            }
+          }
+          if (!last) {
+            if constexpr (kBound) xch_post(part);
+            rinv = inv;
+          }
+          tc_fence_before();
+          if (!last) {
+            fence_proxy_async();
+            epi_sync();
+            a_ready_hi();
+            if constexpr (kBound) amax = xch_read();
+            TL(4);
+          }
+          continue;
+        }
+        mbar_wait(&m.dfull[1], layer & 1);
+        TL(3);
+        mbar_wait(&m.dfull[0], layer & 1);
+        tc_fence_after();
         if (P.debug == 1) {
           tc_fence_before();
           if (!last) {
@@ -487,10 +606,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           }
           continue;
         }
-        // fp16: pass 1 finds the row max for the next scale (and the head on the
-        // last layer); bf16 needs no scale, so one pass reads D and writes A.
+        // two-pass fp16 (pair probes): pass 1 finds the row max for the next
+        // scale (and the head on the last layer), pass 2 writes A.
         float tmax = 0.f;
-        if ((F16 && !kBound) || last) {
+        if (F16 || last) {
           for (int nh = 0; nh < 2; ++nh) {
             const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll
@@ -514,20 +633,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         if (!last) {
           float inv;
-          if constexpr (kBound) {
-            sc = pow2_scale((amax * P.cn[l] + P.bm[l]) * 1.000001f);
-            inv = 1.f / sc;
-          } else {
-            row_scale(tmax, sc, inv);
-          }
-          float part = 0.f;
+          row_scale(tmax, sc, inv);
           for (int nh = 0; nh < 2; ++nh) {
-            if ((!F16 || kBound) && nh == 1) {   // columns 0..255 of every row are in A: announce them
-              fence_proxy_async();
-              tc_fence_before();
-              epi_sync();
-              a_ready_lo();
-            }
             const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
@@ -538,25 +645,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 float x[8], bb[8];
                 ldg8(bias + cb + c * 32 + g8 * 8, bb);
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  const float y = act(v[g8 * 8 + e], bb[e]);
-                  if constexpr (kBound) part = fmaxf(part, y);
-                  x[e] = y * sc;
-                }
+                for (int e = 0; e < 8; ++e) x[e] = act(v[g8 * 8 + e], bb[e]) * sc;
                 put8<F16>(smem, row, cb + c * 32 + g8 * 8, x);
               }
             }
           }
-          if constexpr (kBound) xch_post(part);
           rinv = inv;
         }
         tc_fence_before();
         if (!last) {
           fence_proxy_async();
           epi_sync();
-          if (F16 && !kBound) a_ready_all();
-          else a_ready_hi();
-          if constexpr (kBound) amax = xch_read();
+          a_ready_all();
           TL(4);
         }
       }
