@@ -4,22 +4,30 @@
 // as one persistent kernel per CTA pair (cluster of 2, tcgen05 cta_group::2):
 //
 //   * A pair owns a tile of 128 query rows (64 per CTA).  Activations stay
-//     in shared memory for all layers as a bf16 hi/lo split (A = A_hi + A_lo,
-//     |A_lo| <= 2^-9 |A|), K-major, 128-byte swizzled: 2 x 64 KB per CTA.
+//     in shared memory for all layers as a 16-bit hi/lo split (A = A_hi +
+//     A_lo), K-major, 128-byte swizzled: 2 x 64 KB per CTA.  bf16x3: A_lo <=
+//     2^-9 |A|; fp16x3: each row scaled by a power of two (bounded a priori,
+//     one pass per layer), A_lo <= 2^-12 |A|.
 //   * Each hidden layer is D[128 x 512] = A_hi W_hi + A_hi W_lo + A_lo W_hi
-//     accumulated in fp32 in TMEM (bf16x3).  The leader CTA's
-//     single MMA thread issues tcgen05.mma.cta_group::2 M=128 N=256 K=16;
-//     each CTA supplies its 64 rows of A and half of N of the weights.
-//   * Weights (W^T, bf16 hi and lo) stream from L2 through TMA
+//      accumulated in fp32 in TMEM, hi*hi and the corrections
+//     in separate accumulators (mode 3).  The leader CTA's single MMA thread
+//     issues tcgen05.mma.cta_group::2 M=128 N=256 K=16; each CTA supplies its
+//     64 rows of A and half of N of the weights.
+//   * Weights (W^T, 16-bit hi and lo) stream from L2 through TMA
 //     (cp.async.bulk.tensor, SWIZZLE_128B, cta_group::2 completion on the
 //     leader's mbarrier) in 3 stages of 32 KB per CTA.
 //   * The epilogue warps read D with tcgen05.ld, add bias, apply ReLU, split
-//     into hi/lo and write the next layer's A in place; on the last hidden
-//     layer they fold the 512 -> 1 head (fp32 dot) and tanh directly from the
-//     fp32 accumulator.  Layer 0 (latent part folded into a per-shape bias,
-//     SURVEY 0 finding 8) runs on the epilogue warps in fp64.
+//     into hi/lo and write the next layer's A in place.  The nh = 0 half is
+//     processed while the nh = 1 MMAs still run (packed words parked in
+//     TMEM), and A is announced in two K halves so the next GEMM starts
+//     early.  On the last hidden layer they fold the 512 -> 1 head (fp32 dot)
+//     and tanh.  Layer 0 (latent part folded into a per-shape bias c0,
+//     SURVEY 0 finding 8) runs on the epilogue warps in fp32.
 //   * In march mode the tile epilogue applies the update of tracer.py:170-192
-//     and appends survivors to the next live list (march.cuh).
+//     and appends survivors to the next live list (march.cuh), deferred
+//     until the next tile's layer 0 is handed to the MMA warp.
+//   * PAIR: the normal probes as (mid, diff) pairs (always fp16x3, two-pass
+//     row scales because diffs are signed and small).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
