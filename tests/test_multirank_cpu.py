@@ -9,6 +9,7 @@ from __future__ import annotations
 import os
 
 import numpy as np
+import pytest
 import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
@@ -71,3 +72,25 @@ def test_two_rank_allreduce_matches_single_process():
         z = adam.step(z, grad)
     np.testing.assert_allclose(out[0], z, rtol=1e-12, atol=1e-14)
     np.testing.assert_allclose(out[1], out[0], rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_interleaved_view_sharding_partitions_the_ring(world):
+    """bench.py's weak-scaling shard: rank r traces ring views r, r+N, ..., r+7N
+    of an 8N-view ring; together the ranks cover every view exactly once, and
+    N=1 is the plain 8-view ring."""
+    from paper_1911_13225_b200.workloads import ring_eye, ring_views
+    total = 8 * world
+    seen = []
+    for r in range(world):
+        views = ring_views(8, 16, first=r, total=total, stride=world)
+        assert len(views) == 8
+        for j, (_, pose) in enumerate(views):
+            k = r + j * world
+            np.testing.assert_allclose(pose.center(), ring_eye(k, total), rtol=0, atol=1e-8)
+            seen.append(k)
+    assert sorted(seen) == list(range(total))
+    if world == 1:
+        plain = ring_views(8, 16)
+        for (_, a), (_, b) in zip(plain, ring_views(8, 16, first=0, total=8, stride=1)):
+            np.testing.assert_array_equal(a.params(), b.params())
