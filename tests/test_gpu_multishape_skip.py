@@ -16,7 +16,7 @@ def st():
     return st
 
 
-@pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("bf16x3", 2e-3)])
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-9), ("bf16x3", 2e-3), ("fp16x3", 2e-3)])
 def test_two_shapes_two_views_each(st, prec, tol):
     res, S, VPS = 32, 2, 2
     rng = np.random.default_rng(5)
