@@ -284,40 +284,107 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (row_thread && gi < nrows && s >= 0) sp = gen.prep(gi);
       // ---- forward hidden layers ----
       float head = 0.f;
+      // The nh = 0 half of each forward GEMM is processed while the nh = 1
+      // MMAs run: its packed A words are parked in the TMEM columns just read
+      // and copied to A once the GEMM is done (tc_mlp.cu, same scheme).
       for (int l = 0; l < G; ++l, ++phase) {
-        mbar_wait(&m.dfull[1], phase & 1);
-        TL(3);
-        mbar_wait(&m.dfull[0], phase & 1);
-        tc_fence_after();
         const bool last = (l == G - 1);
         const float *bias = P.bias + (size_t)l * KDIM;
         uint32_t mk[4] = {0, 0, 0, 0};
-        for (int nh = 0; nh < 2; ++nh) {
-          if (nh == 1 && !last) announce_lo();
-          const int cb = nh * 256 + half * 128 + sub * 64;
+        // early half (nh = 0): bias loaded per 8 columns (latency hidden under
+        // the nh = 1 MMAs), packed words returned in r for parking
+        auto fwd_early = [&](int c, uint32_t (&r)[32]) -> uint32_t {
+          const int cb = half * 128 + sub * 64;
+          float v[32];
+          tmem_ld32(tq + sub * 64 + c * 32, v);
+          uint32_t bits = 0;
 #pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            float v[32], bbc[32];
-            ldg32(bias + cb + c * 32, bbc);   // in flight across the TMEM load
-            tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
-            uint32_t bits = 0;
+          for (int g8 = 0; g8 < 4; ++g8) {
+            float x[8], bb[8];
+            ldg8(bias + cb + c * 32 + g8 * 8, bb);
+            if (last) {
+              float wo[8];
+              ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
 #pragma unroll
-            for (int g8 = 0; g8 < 4; ++g8) {
-              float x[8], wo[8];
-              const float *bb = bbc + g8 * 8;
-              if (last) ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
+              for (int e = 0; e < 8; ++e) {
+                const float y = v[g8 * 8 + e] + bb[e];
+                bits |= (y > 0.f ? 1u : 0u) << (g8 * 8 + e);
+                head = fmaf(y > 0.f ? y : 0.f, wo[e], head);
+              }
+            } else {
 #pragma unroll
               for (int e = 0; e < 8; ++e) {
                 const float y = v[g8 * 8 + e] + bb[e];
                 x[e] = y > 0.f ? y : 0.f;
                 bits |= (y > 0.f ? 1u : 0u) << (g8 * 8 + e);
-                if (last) head = fmaf(x[e], wo[e], head);
               }
-              if (!last) put8<false>(smem, row, cb + c * 32 + g8 * 8, x);
+              uint32_t hi[4], lo[4];
+              pack8<false>(x, hi, lo);
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                r[g8 * 4 + i] = hi[i];
+                r[16 + g8 * 4 + i] = lo[i];
+              }
             }
-            set4(mk, nh * 2 + c, bits);
           }
+          return bits;
+        };
+        // late half (nh = 1): on the critical path, bias loads issued ahead
+        auto fwd_late = [&](int c) -> uint32_t {
+          const int cb = 256 + half * 128 + sub * 64;
+          float v[32], bbc[32];
+          ldg32(bias + cb + c * 32, bbc);
+          tmem_ld32(tq + 128 + sub * 64 + c * 32, v);
+          uint32_t bits = 0;
+#pragma unroll
+          for (int g8 = 0; g8 < 4; ++g8) {
+            float x[8], wo[8];
+            const float *bb = bbc + g8 * 8;
+            if (last) ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              const float y = v[g8 * 8 + e] + bb[e];
+              x[e] = y > 0.f ? y : 0.f;
+              bits |= (y > 0.f ? 1u : 0u) << (g8 * 8 + e);
+              if (last) head = fmaf(x[e], wo[e], head);
+            }
+            if (!last) put8<false>(smem, row, cb + c * 32 + g8 * 8, x);
+          }
+          return bits;
+        };
+        mbar_wait(&m.dfull[0], phase & 1);
+        TL(3);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {   // early half (nh = 0)
+          uint32_t r[32];
+          set4(mk, c, fwd_early(c, r));
+          if (!last) tmem_st32(tq + sub * 64 + c * 32, r);
         }
+        if (!last) tmem_wait_st();
+        mbar_wait(&m.dfull[1], phase & 1);
+        tc_fence_after();
+        if (!last) {
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {   // parked words -> A (K blocks 0..3)
+            float v[32];
+            tmem_ld32(tq + sub * 64 + c * 32, v);
+            const int k0 = half * 128 + sub * 64 + c * 32;
+#pragma unroll
+            for (int g8 = 0; g8 < 4; ++g8) {
+              uint32_t hi[4], lo[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                hi[i] = __float_as_uint(v[g8 * 4 + i]);
+                lo[i] = __float_as_uint(v[16 + g8 * 4 + i]);
+              }
+              st8(smem, row, k0 + g8 * 8, hi, lo);
+            }
+          }
+          announce_lo();
+        }
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) set4(mk, 2 + c, fwd_late(c));   // nh = 1
         tmem_st4(mask_addr(l + 1), mk);
         tc_fence_before();
         if (!last) {
@@ -382,12 +449,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       // ---- backward through GEMM layers G-1 .. 0 ----
       for (int gl = G - 1; gl >= 0; --gl, ++phase) {
         if (gl == 0) fetch(t + nclusters, nxp, nxs);
-        mbar_wait(&m.dfull[1], phase & 1);
-        TL(7);
-        mbar_wait(&m.dfull[0], phase & 1);
-        tc_fence_after();
         uint32_t mk[4];
-        tmem_ld4(mask_addr(gl), mk);
+        tmem_ld4(mask_addr(gl), mk);   // written in the forward, readable now
         // D = (g / rinv) (W / winv_b): true dgrad = D * unscale
         const float unscale = rinv * P.winv_b[gl];
         if (gl > 0) {
@@ -398,24 +461,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const float f = unscale * sc;   // exact: powers of two
           rinv = 1.f / sc;
           float part = 0.f;
-          for (int nh = 0; nh < 2; ++nh) {
-            if (nh == 1) announce_lo();
-            const int cb = nh * 256 + half * 128 + sub * 64;
+          // 8 masked, scaled values of chunk (nh, c) -> 4 packed fp16 words
+          auto bwd8 = [&](const float (&v)[32], uint32_t bits, int g8, uint32_t (&h)[4]) {
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-              float v[32];
-              tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
-              const uint32_t bits = get4(mk, nh * 2 + c);
+            for (int i = 0; i < 4; ++i) {
+              const int e = g8 * 8 + 2 * i;
+              const float x0 = ((bits >> e) & 1u) ? v[e] * f : 0.f;
+              const float x1 = ((bits >> (e + 1)) & 1u) ? v[e + 1] * f : 0.f;
+              part = fmaxf(part, fmaxf(fabsf(x0), fabsf(x1)));
+              const __half2 hv = __floats2half2_rn(x0, x1);
+              h[i] = *reinterpret_cast<const uint32_t *>(&hv);
+            }
+          };
+          mbar_wait(&m.dfull[0], phase & 1);
+          TL(7);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {   // early half (nh = 0), parked in TMEM
+            float v[32];
+            tmem_ld32(tq + sub * 64 + c * 32, v);
+            const uint32_t bits = get4(mk, c);
+            uint32_t r[32];
 #pragma unroll
-              for (int g8 = 0; g8 < 4; ++g8) {
-                float x[8];
+            for (int g8 = 0; g8 < 4; ++g8) {
+              uint32_t h[4];
+              bwd8(v, bits, g8, h);
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                  x[e] = ((bits >> (g8 * 8 + e)) & 1u) ? v[g8 * 8 + e] * f : 0.f;
-                  part = fmaxf(part, fabsf(x[e]));
-                }
-                put8h(smem, row, cb + c * 32 + g8 * 8, x);
-              }
+              for (int i = 0; i < 4; ++i) r[g8 * 4 + i] = h[i];
+            }
+#pragma unroll
+            for (int i = 16; i < 32; ++i) r[i] = 0u;
+            tmem_st32(tq + sub * 64 + c * 32, r);
+          }
+          tmem_wait_st();
+          mbar_wait(&m.dfull[1], phase & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {   // parked words -> A (K blocks 0..3)
+            float v[32];
+            tmem_ld32(tq + sub * 64 + c * 32, v);
+            const int k0 = half * 128 + sub * 64 + c * 32;
+#pragma unroll
+            for (int g8 = 0; g8 < 4; ++g8)
+              *reinterpret_cast<uint4 *>(smem + OFF_AHI + a_off(row, k0 + g8 * 8)) =
+                  make_uint4(__float_as_uint(v[g8 * 4]), __float_as_uint(v[g8 * 4 + 1]),
+                             __float_as_uint(v[g8 * 4 + 2]), __float_as_uint(v[g8 * 4 + 3]));
+          }
+          announce_lo();
+#pragma unroll 1
+          for (int c = 0; c < 2; ++c) {   // nh = 1
+            float v[32];
+            tmem_ld32(tq + 128 + sub * 64 + c * 32, v);
+            const uint32_t bits = get4(mk, 2 + c);
+            const int k0 = 256 + half * 128 + sub * 64 + c * 32;
+#pragma unroll
+            for (int g8 = 0; g8 < 4; ++g8) {
+              uint32_t h[4];
+              bwd8(v, bits, g8, h);
+              *reinterpret_cast<uint4 *>(smem + OFF_AHI + a_off(row, k0 + g8 * 8)) =
+                  make_uint4(h[0], h[1], h[2], h[3]);
             }
           }
           // post this warp's part max; barrier 2 orders it after every warp's
@@ -430,6 +534,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           a_ready_hi();
           TL(8);
         } else {
+          mbar_wait(&m.dfull[1], phase & 1);
+          TL(7);
+          mbar_wait(&m.dfull[0], phase & 1);
+          tc_fence_after();
           // g_pre0 = D * mask0 * unscale; column sums over the CTA's rows, per
           // shape.  TMEM is read inside the shape loop (usually one pass), so no
           // per-thread copy of the 128 values is kept (it lived in local memory).
