@@ -330,6 +330,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (t < ntiles && r.gi < nrows) r.id = load_row(R, m, r.gi, r.p, r.s);
     };
     bool xpend = false;   // an xch_read's barrier-2 arrive awaits its matching sync
+    // Next tile's layer 0, first half (columns 0..255), computed during this
+    // tile's last GEMM and parked in TMEM (single-pass paths only)
+    bool have_stash = false;
+    float stash_part = 0.f, stash_sc = 1.f, stash_rinv = 1.f;
+    // layer-0 activations of 8 columns for an explicit point (non-pair paths;
+    // the same arithmetic as the per-tile h0x8 below)
+    auto h0x8_pt = [&](float qx, float qy, float qz, int qs, int col, float (&x)[8]) {
+      const int n0 = P.dv.np[0];
+      const float *cf0 = P.c0f + (size_t)(qs < 0 ? 0 : qs) * n0;
+      float w0[8], w1[8], w2[8], cf[8];
+      ldg8(P.dv.W0pf + col, w0);
+      ldg8(P.dv.W0pf + n0 + col, w1);
+      ldg8(P.dv.W0pf + 2 * n0 + col, w2);
+      ldg8(cf0 + col, cf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float v = fmaf(qz, w2[e], fmaf(qy, w1[e], fmaf(qx, w0[e], cf[e])));
+        x[e] = (qs >= 0 && v > 0.f) ? v : 0.f;
+      }
+    };
     bool pend = false, pvalid = false;
     int64_t pgi = 0;
     int pid = -1;
@@ -420,6 +440,52 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         xpend = true;
         return r;
       };
+      constexpr bool kEarly = !PAIR && (!F16 || kBound);
+      if (kEarly && have_stash) {
+        // columns 0..255 were computed during the previous tile's last GEMM
+        sc = stash_sc;
+        rinv = stash_rinv;
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          float v[32];
+          tmem_ld32(tq + sub * 64 + c * 32, v);
+          const int k0 = half * 128 + sub * 64 + c * 32;
+#pragma unroll
+          for (int g8 = 0; g8 < 4; ++g8) {   // [hi 4 | lo 4] per 8 columns
+            uint32_t hi[4], lo[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              hi[i] = __float_as_uint(v[g8 * 8 + i]);
+              lo[i] = __float_as_uint(v[g8 * 8 + 4 + i]);
+            }
+            st8(smem, row, k0 + g8 * 8, hi, lo);
+          }
+        }
+        fence_proxy_async();
+        tc_fence_before();
+        epi_sync();
+        a_ready_lo();
+        float part = stash_part;
+        const int cb = 256 + half * 128 + sub * 64;
+#pragma unroll 2
+        for (int j = 0; j < 64; j += 8) {
+          float x[8];
+          h0x8_pt(px, py, pz, s, cb + j, x);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            if constexpr (kBound) part = fmaxf(part, x[e]);
+            x[e] *= sc;
+          }
+          put8<F16>(smem, row, cb + j, x);
+        }
+        if constexpr (kBound) xch_post(part);
+        fence_proxy_async();
+        epi_sync();
+        a_ready_hi();
+        if constexpr (kBound) amax = xch_read();
+        have_stash = false;
+        TL(2);
+      } else {
       if constexpr (kBound) {
         const float b0 = s >= 0 ? (P.c0max[s] + fabsf(px) * P.w0m[0] + fabsf(py) * P.w0m[1] +
                                    fabsf(pz) * P.w0m[2]) * 1.000001f
@@ -461,6 +527,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       a_ready_all();
       if constexpr (kBound) amax = xch_read();
       TL(2);
+      }
       // the previous tile's row results, while this tile's first GEMM runs
       if (row_thread && pend) R.finish(m, pgi, pid, pvalid, pfv);
       pend = false;
@@ -473,7 +540,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       // columns just read -- they cannot go to A yet, the nh = 1 MMAs still read
       // A.  After the GEMM, the parked words are copied to A, K blocks 0..3 are
       // announced, then the nh = 1 columns are processed.
-      constexpr bool kEarly = !PAIR && (!F16 || kBound);
       for (int l = 0; l < G; ++l, ++layer) {
         if (l == G - 1) fetch(t + nclusters, nx);
         const bool last = (l == G - 1);
@@ -534,7 +600,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               }
               if (!last) tmem_st32(tq + sub * 64 + c * 32, r);
             }
-            if (!last) tmem_wait_st();
+            if (last && t + nclusters < ntiles) {
+              // the next tile's layer 0, columns 0..255, into the TMEM columns
+              // the head just consumed (nx: its rows, fetched above)
+              const float qx = (float)nx.p[0], qy = (float)nx.p[1], qz = (float)nx.p[2];
+              const int qs = nx.s;
+              float sc0 = 1.f;
+              if constexpr (kBound) {
+                const float b0 = qs >= 0 ? (P.c0max[qs] + fabsf(qx) * P.w0m[0] + fabsf(qy) * P.w0m[1] +
+                                            fabsf(qz) * P.w0m[2]) * 1.000001f
+                                         : 0.f;
+                sc0 = pow2_scale(b0);
+              }
+              float part0 = 0.f;
+              // parked as [hi 4 | lo 4] per 8 columns (x8 stores keep registers low)
+#pragma unroll 1
+              for (int j = 0; j < 64; j += 8) {
+                float x[8];
+                h0x8_pt(qx, qy, qz, qs, half * 128 + sub * 64 + j, x);
+#pragma unroll
+                for (int e = 0; e < 8; ++e) {
+                  if constexpr (kBound) part0 = fmaxf(part0, x[e]);
+                  x[e] *= sc0;
+                }
+                uint32_t hi[4], lo[4];
+                pack8<F16>(x, hi, lo);
+                tmem_st8(tq + sub * 64 + j, hi, lo);
+              }
+              have_stash = true;
+              stash_part = part0;
+              stash_sc = sc0;
+              stash_rinv = 1.f / sc0;
+            }
+            if (!last || have_stash) tmem_wait_st();
           }
           mbar_wait(&m.dfull[1], layer & 1);
           tc_fence_after();
