@@ -57,15 +57,20 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
 }
 
 // one block per view: n_px, n_conv, silhouette loss + per-pixel seed
+// gridDim.y blocks per view sum fixed pixel chunks into part[v][b][3];
+// k_view_prep_finish adds them in order (deterministic)
+constexpr int kPrepBlocks = 32;
 __global__ void k_view_prep(const dist_camera *__restrict__ cams, LevelState ls, int K, double eps,
-                            ObjIn in, int32_t *npx, double *terms, double *sil_seed) {
+                            ObjIn in, double *part, double *sil_seed) {
   __shared__ double red[32];
-  const int v = blockIdx.x;
+  const int v = blockIdx.x, b = blockIdx.y, nb = gridDim.y;
   const int64_t WH = (int64_t)ls.lw * ls.lh;
   const int64_t g0 = v * WH;
+  const int64_t chunk = (WH + nb - 1) / nb;
+  const int64_t q0 = b * chunk, q1 = min(WH, q0 + chunk);
   double n_px = 0, n_conv = 0, sl = 0;
   const double inv_n = 1.0 / (double)WH;
-  for (int64_t q = threadIdx.x; q < WH; q += blockDim.x) {
+  for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
     const int64_t g = g0 + q;
     const bool conv = ls.status[g] == DIST_CONVERGED;
     const bool rec = isfinite(ls.tk_a[g * K]);
@@ -91,14 +96,31 @@ __global__ void k_view_prep(const dist_camera *__restrict__ cams, LevelState ls,
     }
   }
   const double a = block_sum(n_px, red);
-  const double b = block_sum(n_conv, red);
+  const double bc = block_sum(n_conv, red);
   const double c = block_sum(sl, red);
   if (threadIdx.x == 0) {
+    double *o = part + ((size_t)v * nb + b) * 3;
+    o[0] = a;
+    o[1] = bc;
+    o[2] = c;
+  }
+}
+
+__global__ void k_view_prep_finish(int V, int nb, int64_t WH, const double *__restrict__ part,
+                                   bool sil, int32_t *npx, double *terms) {
+  for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < V; v += gridDim.x * blockDim.x) {
+    double a = 0.0, bc = 0.0, c = 0.0;
+    for (int b = 0; b < nb; ++b) {
+      const double *o = part + ((size_t)v * nb + b) * 3;
+      a += o[0];
+      bc += o[1];
+      c += o[2];
+    }
     npx[v] = (int32_t)a;
     terms[v * 4 + 0] = 0.0;
-    terms[v * 4 + 1] = in.obs_sil ? c / (double)WH : 0.0;
+    terms[v * 4 + 1] = sil ? c / (double)WH : 0.0;
     terms[v * 4 + 2] = a;
-    terms[v * 4 + 3] = b;
+    terms[v * 4 + 3] = bc;
   }
 }
 
@@ -239,7 +261,7 @@ static ObjLayout obj_layout(const DecView &dv, int V, int W, int H, int K, int S
   L.conv = cv.take<int32_t>(mode == 1 ? n : 1);
   L.conv_count = cv.take<int32_t>(4);
   L.npx = cv.take<int32_t>(V);
-  L.loss_part = cv.take<double>((size_t)V * kLossBlocks);
+  L.loss_part = cv.take<double>((size_t)V * std::max(kLossBlocks, 3 * kPrepBlocks));
   L.bcount = cv.take<int32_t>(ceil_div(n * K, kScanBlock) + 1);
   L.c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
   L.cs = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
@@ -307,8 +329,11 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
   k_heads_index<<<std::max(gi, 1), 256, 0, sm>>>(L.h, K, V, WH);
   DIST_CHECK_LAUNCH("k_heads_index");
   // 2. per-view loss preparation
-  k_view_prep<<<V, 1024, 0, sm>>>(cams, ls, K, cfg->epsilon, in, L.npx, io->view_terms, L.sil_seed);
+  k_view_prep<<<dim3(V, kPrepBlocks), 256, 0, sm>>>(cams, ls, K, cfg->epsilon, in, L.loss_part, L.sil_seed);
   DIST_CHECK_LAUNCH("k_view_prep");
+  k_view_prep_finish<<<(int)ceil_div(V, 128), 128, 0, sm>>>(V, kPrepBlocks, (int64_t)W * H, L.loss_part,
+                                                            in.obs_sil != nullptr, L.npx, io->view_terms);
+  DIST_CHECK_LAUNCH("k_view_prep_finish");
   // 3. fused forward -> seed -> backward
   rc = launch_code_bias(dv, dv.latent_dim > 0 ? codes : nullptr, s1, L.c0, L.cs, sm);
   if (rc) return rc;
