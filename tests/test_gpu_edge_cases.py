@@ -1,0 +1,115 @@
+"""Edge cases the reference tests for this path (test_tracer.py, test_optimize.py,
+test_fields.py): all-background views, a camera inside the unit sphere, empty
+point sets, the configuration boundaries, and the validation errors -- the GPU
+path against the CPU oracle or the reference's documented behaviour."""
+from __future__ import annotations
+
+import warnings
+
+import numpy as np
+import pytest
+
+import sdf_oracle as orc  # noqa: E402  (checker only)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def st():
+    import paper_1911_13225_b200 as st
+    return st
+
+
+def _tiny(st, prec="fp64"):
+    rng = np.random.default_rng(7)
+    net = st.NeuralField.init(latent_dim=2, hidden=(16, 16), rng=rng, precision=prec)
+    return net, rng.normal(0.0, 0.3, 2)
+
+
+def _oracle_trace(net, code, res, pose, **cfg):
+    dec = orc.Decoder(net.weights, 2)
+    return orc.trace(lambda p: dec(p, code), orc.Cam(res, res, pose.omega, pose.t), orc.Cfg(**cfg))
+
+
+def test_all_background_view(st):
+    """Looking away from the shape: every ray escapes, the depth map is +inf,
+    and complete_shape without a silhouette refuses to start
+    (optimize.py:160-165, test_optimize.py:163)."""
+    net, code = _tiny(st)
+    intr, pose = st.Intrinsics(width=32, height=32), st.look_at((0.0, 0.0, -2.0), (0.0, 0.0, -4.0))
+    r = st.trace(net, code, intr, pose, st.TraceConfig())
+    T = _oracle_trace(net, code, 32, pose)
+    assert np.array_equal(r.state.status, T.status)
+    assert not np.any(r.state.status == 1)
+    assert np.all(np.isinf(st.depth_map(r)))
+    obs = [st.Observation("depth", np.full((32, 32), 1.5))]
+    with pytest.raises(st.OptimizationError):
+        st.complete_shape(net, obs, intr, pose, iters=2)
+
+
+def test_camera_inside_unit_sphere(st):
+    """Camera centre inside the unit sphere: a RuntimeWarning and every ray
+    starts at d = 0 (tracer.py:100-102, test_tracer.py:91-98); the march then
+    matches the oracle bit for bit."""
+    net, code = _tiny(st)
+    pose = st.look_at((0.0, 0.0, -0.5))
+    with pytest.warns(RuntimeWarning):
+        r = st.trace(net, code, st.Intrinsics(width=32, height=32), pose, st.TraceConfig())
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        T = _oracle_trace(net, code, 32, pose)
+    assert r.live_counts == T.live_counts
+    assert np.array_equal(r.state.status, T.status)
+    assert np.array_equal(r.state.steps, T.steps)
+
+
+@pytest.mark.parametrize("prec", ["fp64", "bf16x3"])
+def test_empty_point_set(st, prec):
+    """Zero points evaluate to an empty array and a zero code gradient."""
+    import torch
+    if prec == "fp64":
+        net, code = _tiny(st)
+    else:
+        net = st.NeuralField.geometric(256, (512,) * 8, 0, precision=prec)
+        code = np.zeros(256)
+    assert net.evaluate(np.zeros((0, 3)), code).shape == (0,)
+    f, gc, gp = net.vjp_device(torch.zeros((0, 3), dtype=torch.float64), code,
+                               torch.zeros(0, dtype=torch.float64))
+    assert f.numel() == 0 and float(gc.abs().sum()) == 0.0 and gp.numel() == 0
+
+
+@pytest.mark.parametrize("max_steps,k", [(1, 1), (2, 16), (100, 16), (7, 1)])
+def test_config_boundaries_bitexact_fp64(st, max_steps, k):
+    """max_steps down to 1 and k_samples at both ends (1, 16): the fp64 GPU
+    march equals the oracle -- counts, status and steps exactly, distances to
+    the last ulp (FMA contraction differs from numpy)."""
+    net, code = _tiny(st)
+    pose = st.look_at((0.0, 0.0, -2.0))
+    cfg = st.TraceConfig(max_steps=max_steps, k_samples=k)
+    r = st.trace(net, code, st.Intrinsics(width=64, height=64), pose, cfg)
+    T = _oracle_trace(net, code, 64, pose, max_steps=max_steps, k_samples=k)
+    assert r.live_counts == T.live_counts and r.total_queries == T.total_queries
+    assert np.array_equal(r.state.status, T.status) and np.array_equal(r.state.steps, T.steps)
+    np.testing.assert_allclose(r.state.d, T.d, rtol=1e-14, atol=0)
+    fin = np.isfinite(T.tk_a)
+    assert np.array_equal(np.isfinite(r.state.topk_absf), fin)
+    np.testing.assert_allclose(r.state.topk_absf[fin], T.tk_a[fin], rtol=1e-12, atol=1e-15)
+
+
+def test_validation_errors(st):
+    """Configuration and shape errors raise ValueError before any launch."""
+    net, code = _tiny(st)
+    pose = st.look_at((0.0, 0.0, -2.0))
+    with pytest.raises(ValueError):
+        st.TraceConfig(k_samples=0)
+    with pytest.raises(ValueError):
+        st.TraceConfig(alpha=2.0)
+    with pytest.raises(ValueError):   # 30 is not divisible by the coarse scale 4
+        st.trace(net, code, st.Intrinsics(width=30, height=32), pose, st.TraceConfig())
+    with pytest.raises(ValueError):   # one trace call, one resolution
+        st.trace_views(net, code, [(st.Intrinsics(width=32, height=32), pose),
+                                   (st.Intrinsics(width=64, height=64), pose)])
+    with pytest.raises(ValueError):   # the field expects a latent code
+        net.evaluate(np.zeros((4, 3)), None)
+    with pytest.raises(ValueError):
+        net.evaluate(np.zeros((4, 3)), np.zeros(3))
