@@ -26,7 +26,7 @@ from paper_1911_13225_b200 import _lib  # noqa: E402
 from paper_1911_13225_b200.workloads import render_depth_observations, ring_views, target_code  # noqa: E402
 
 MLP = {1: "tile start", 2: "layer0 A ready", 10: "prev tile rows done", 3: "D (nh=0 half) ready", 4: "A ready",
-       9: "head done"}
+       9: "head done", 11: "GEMM done", 12: "parked copied", 13: "K 0..3 announced", 14: "nh=1 half done"}
 HEADS = {1: "tile start", 2: "layer0 A ready", 3: "fwd D ready", 4: "fwd A ready", 5: "seed done",
          6: "bwd A0 ready", 7: "bwd D ready", 8: "bwd A ready", 9: "colsum done"}
 
