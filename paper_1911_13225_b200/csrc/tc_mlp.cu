@@ -635,6 +635,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             if (!last || have_stash) tmem_wait_st();
           }
           mbar_wait(&m.dfull[1], layer & 1);
+          TL(11);
           tc_fence_after();
           if (!last) {
             // parked words -> A (K blocks 0..3), announce, then the nh = 1 half
@@ -654,10 +655,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 st8(smem, row, k0 + g8 * 8, hi, lo);
               }
             }
+            TL(12);
             fence_proxy_async();
             tc_fence_before();
             epi_sync();
             a_ready_lo();
+            TL(13);
           }
           {
             const int cb = 256 + half * 128 + sub * 64;
@@ -686,6 +689,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               }
             }
           }
+          TL(14);
           if (!last) {
             if constexpr (kBound) xch_post(part);
             rinv = inv;
