@@ -32,6 +32,7 @@ struct Misc {
   uint64_t dfull[2];
   uint64_t aready;    // next layer's A, K blocks 0..3 (output columns 0..255) written
   uint64_t aready2;   // ... and K blocks 4..7
+  uint64_t afree;     // the GEMM's nh = 1 MMAs have consumed A's K blocks 0..3
   uint32_t tmem_base;
   int32_t go, cur, cnt, nan;
   int32_t ray[ROWS];

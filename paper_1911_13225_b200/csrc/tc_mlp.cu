@@ -179,6 +179,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const uint32_t rank = cta_rank();
 
   if (!R.begin(m)) return;  // uniform across the grid (all CTAs read the same controller)
+  // single-pass (bf16, bound-scaled fp16) epilogues: early half + afree
+  constexpr bool kAfree = !PAIR;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -189,6 +191,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     mbar_init(&m.dfull[1], 1);
     mbar_init(&m.aready, 2);
     mbar_init(&m.aready2, 2);
+    mbar_init(&m.afree, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -282,6 +285,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 }
               }
               commit_2sm(&m.empty[s]);
+              // single-pass epilogues copy the early half into A's K blocks
+              // 0..3 as soon as the nh = 1 MMAs are past them (kc = NKB/2 - 1)
+              if (kAfree && nh == 1 && kc == NKB / 2 - 1 && l < G - 1 && P.debug != 1)
+                commit_2sm(&m.afree);
             }
             commit_2sm(&m.dfull[nh]);
           }
@@ -329,6 +336,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       r.id = -1;
       if (t < ntiles && r.gi < nrows) r.id = load_row(R, m, r.gi, r.p, r.s);
     };
+    uint32_t afree_n = 0;  // afree phases consumed (one per non-last kEarly layer)
     bool xpend = false;   // an xch_read's barrier-2 arrive awaits its matching sync
     // Next tile's layer 0, first half (columns 0..255), computed during this
     // tile's last GEMM and parked in TMEM (single-pass paths only)
@@ -634,11 +642,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             }
             if (!last || have_stash) tmem_wait_st();
           }
-          mbar_wait(&m.dfull[1], layer & 1);
-          TL(11);
-          tc_fence_after();
           if (!last) {
-            // parked words -> A (K blocks 0..3), announce, then the nh = 1 half
+            // parked words -> A (K blocks 0..3) once the nh = 1 MMAs are past
+            // them, and announce: the next GEMM follows this one without a gap
+            mbar_wait(&m.afree, afree_n & 1);
+            ++afree_n;
+            TL(11);
+            tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
               float v[32];
@@ -662,6 +672,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             a_ready_lo();
             TL(13);
           }
+          mbar_wait(&m.dfull[1], layer & 1);
+          tc_fence_after();
           {
             const int cb = 256 + half * 128 + sub * 64;
 #pragma unroll 1
