@@ -115,6 +115,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     mbar_init(&m.dfull[1], 1);
     mbar_init(&m.aready, 2);
     mbar_init(&m.aready2, 2);
+    mbar_init(&m.afree, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -194,6 +195,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 }
               }
               commit_2sm(&m.empty[s]);
+              // phases that write the next operand: A's K blocks 0..3 are free
+              // once the nh = 1 MMAs are past them (tc_mlp.cu, same barrier)
+              if (nh == 1 && kc == NKB / 2 - 1 && (ph < G - 1 || (ph >= G && ph < 2 * G - 1)))
+                commit_2sm(&m.afree);
             }
             commit_2sm(&m.dfull[nh]);
           }
@@ -224,6 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     auto mask_addr = [&](int ml) { return tq + 256 + ml * 8 + sub * 4; };
     const int n0 = P.dv.np[0];
     uint32_t phase = 0;
+    uint32_t afree_n = 0;   // afree phases consumed (phases that write the next operand)
     // [64] per-row head gradient; m.ray is unused by this kernel, so gout does
     // not alias the m.xch row exchange
     float *gout = reinterpret_cast<float *>(&m.ray[0]);
@@ -361,10 +367,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           set4(mk, c, fwd_early(c, r));
           if (!last) tmem_st32(tq + sub * 64 + c * 32, r);
         }
-        if (!last) tmem_wait_st();
-        mbar_wait(&m.dfull[1], phase & 1);
-        tc_fence_after();
         if (!last) {
+          tmem_wait_st();
+          mbar_wait(&m.afree, afree_n & 1);
+          ++afree_n;
+          tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < 2; ++c) {   // parked words -> A (K blocks 0..3)
             float v[32];
@@ -383,6 +390,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           }
           announce_lo();
         }
+        mbar_wait(&m.dfull[1], phase & 1);
+        tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < 2; ++c) set4(mk, 2 + c, fwd_late(c));   // nh = 1
         tmem_st4(mask_addr(l + 1), mk);
@@ -494,7 +503,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             tmem_st32(tq + sub * 64 + c * 32, r);
           }
           tmem_wait_st();
-          mbar_wait(&m.dfull[1], phase & 1);
+          mbar_wait(&m.afree, afree_n & 1);
+          ++afree_n;
           tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < 2; ++c) {   // parked words -> A (K blocks 0..3)
@@ -508,6 +518,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                              __float_as_uint(v[g8 * 4 + 2]), __float_as_uint(v[g8 * 4 + 3]));
           }
           announce_lo();
+          mbar_wait(&m.dfull[1], phase & 1);
+          tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < 2; ++c) {   // nh = 1
             float v[32];
