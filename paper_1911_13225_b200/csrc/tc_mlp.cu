@@ -57,7 +57,8 @@ struct Params {
   const float *cn, *bm, *w0m;  // fp16 row-scale bounds (tc_mlp.cu fill_fwd)
   const float *c0max;     // [S] max |c0| per shape
   int n_gemm;             // hidden GEMM layers (L-2)
-  int acc_mode;           // 0: one accumulator; 1: two (even/odd K blocks); 2: hi*hi | corrections
+  int acc_mode;           // 0: one accumulator; 1: two (even/odd K blocks); 2: hi*hi | corrections;
+                          // 3 (default): as 2, stage-grouped; 4 (experiment): single pass, hi*hi only
   int timeline;           // DIST_TC_TIMELINE: phase marks of CTA 0 (debug)
   int debug;              // timing experiments: 1 = no epilogue math, 2 = no MMAs (results invalid)
 };
@@ -269,7 +270,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 const uint32_t ak = kc * (ROWS * 128) + q * 32;
                 const uint64_t dah = sdesc(a_hi + ak), dal = sdesc(a_lo + ak);
                 const uint64_t dbh = sdesc(b_hi + q * 32), dbl = sdesc(b_lo + q * 32);
-                if (P.acc_mode == 0) {
+                if (P.acc_mode == 4) {   // experiment: single pass (hi x hi only)
+                  mma_2sm<F16>(d, dah, dbh, (kc | q) ? 1u : 0u);
+                } else if (P.acc_mode == 0) {
                   mma_2sm<F16>(d, dah, dbh, (kc | q) ? 1u : 0u);
                   mma_2sm<F16>(d, dah, dbl, 1u);
                   mma_2sm<F16>(d, dal, dbh, 1u);
@@ -311,7 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     auto a_ready_all = [&] { a_ready_lo(); a_ready_hi(); };
     // D columns [col, col+32) of this thread's lane (+ the correction accumulator)
     auto load_d = [&](int col, float (&v)[32]) {
-      if (P.acc_mode) {
+      if (P.acc_mode >= 1 && P.acc_mode <= 3) {
         float w2[32];
         tmem_ld32x2(tq + col, tq + 256 + col, v, w2);
 #pragma unroll
