@@ -167,7 +167,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     # fp16x3: the march in fp16x3 (tight trace parity), heads bf16x3 forward +
-    # fp16x2 backward; bf16x3 is ~3.6% faster with looser trace parity
+    # fp16x2 backward; bf16x3 is 1-4% faster with looser trace parity
     ap.add_argument("--precision", default=os.environ.get("DIST_BENCH_PRECISION", "fp16x3"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
