@@ -197,3 +197,25 @@ def test_c3_full_size_vs_fp32(st, prec):
     assert abs(q16 - q32) <= 1e-3 * q32
     assert abs(l16 - l32) <= 3e-4 * abs(l32)   # measured 8.4e-5
     assert np.linalg.norm(g16 - g32) <= 1e-3 * np.linalg.norm(g32)
+
+
+def test_optimisation_loss_curves_track_fp32(st):
+    """The latent-optimisation loop (trace + fused heads + backward + Adam) over
+    8 ring views at 128^2 for 10 iterates: the split-precision loss curves track
+    the fp32 SIMT run (at full size and 200 iterates: 5e-5)."""
+    from paper_1911_13225_b200.workloads import render_depth_observations, ring_views, target_code
+    views = ring_views(8, 128)
+    cfg = st.TraceConfig(k_samples=3)
+    ref = st.NeuralField.geometric(256, (512,) * 8, 0, precision="fp32")
+    obs = render_depth_observations(ref, target_code(1), views, cfg)
+    curves = {}
+    for prec in ("fp32", "fp16x3", "bf16x3"):
+        field = ref if prec == "fp32" else ref.with_precision(prec)
+        opt = st.LatentOptimizer(field, views, {"depth": obs}, np.zeros((1, 256)), cfg, max_iters=10)
+        for _ in range(10):
+            opt.step()
+        curves[prec] = opt.losses()[:, 0]
+    assert curves["fp32"][-1] < 0.7 * curves["fp32"][0]   # the loop makes progress
+    for prec in ("fp16x3", "bf16x3"):
+        rel = np.abs(curves[prec] - curves["fp32"]) / np.abs(curves["fp32"])
+        assert rel.max() < 1e-3, (prec, rel.max())
