@@ -72,7 +72,11 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *b, uint32_t tx) 
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t *b, uint32_t rank) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(b)), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+  // default semantics (release, CTA scope) as CUTLASS's ClusterBarrier::arrive:
+  // .release.cluster compiles to MEMBAR.ALL.GPU, which waits for every
+  // outstanding global store (the march update) on the operand hand-off path.
+  // The operand writes reach the tensor core through fence.proxy.async.
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
 }
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
