@@ -219,3 +219,24 @@ def test_optimisation_loss_curves_track_fp32(st):
     for prec in ("fp16x3", "bf16x3"):
         rel = np.abs(curves[prec] - curves["fp32"]) / np.abs(curves["fp32"])
         assert rel.max() < 1e-3, (prec, rel.max())
+
+
+@pytest.mark.parametrize("depth", [4, 12])
+@pytest.mark.parametrize("prec", ["fp16x3", "bf16x3"])
+def test_other_depths_on_tensor_cores(st, depth, prec):
+    """The tensor-core kernels take the number of hidden GEMMs at run time:
+    4x512 and 12x512 geometric decoders, evaluation and the fused objective
+    gradient against fp64 SIMT on the same 64^2 view."""
+    rng = np.random.default_rng(3)
+    code = rng.normal(0.0, 0.1, 256)
+    pts = rng.uniform(-0.8, 0.8, (4096, 3))
+    f64 = st.NeuralField.geometric(256, (512,) * depth, 0, precision="fp64")
+    tcf = f64.with_precision(prec)
+    assert np.max(np.abs(tcf.evaluate(pts, code) - f64.evaluate(pts, code))) < 5e-5
+    intr, pose = st.Intrinsics(width=64, height=64), st.look_at((0.0, 0.3, -2.0))
+    cfg = st.TraceConfig(k_samples=3)
+    obs = [st.Observation("depth", st.depth_map(st.trace(f64, code + 0.05, intr, pose, cfg)))]
+    t64, _, g64, _, _ = st.completion_objective(f64, code, obs, intr, pose, cfg, st.LossWeights())
+    ttc, _, gtc, _, _ = st.completion_objective(tcf, code, obs, intr, pose, cfg, st.LossWeights())
+    assert abs(ttc - t64) <= 1e-3 * abs(t64)
+    assert np.linalg.norm(gtc - g64) <= 1e-3 * np.linalg.norm(g64)
