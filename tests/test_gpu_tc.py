@@ -240,3 +240,22 @@ def test_other_depths_on_tensor_cores(st, depth, prec):
     ttc, _, gtc, _, _ = st.completion_objective(tcf, code, obs, intr, pose, cfg, st.LossWeights())
     assert abs(ttc - t64) <= 1e-3 * abs(t64)
     assert np.linalg.norm(gtc - g64) <= 1e-3 * np.linalg.norm(g64)
+
+
+@pytest.mark.parametrize("latent", [0, 64])
+def test_other_latent_sizes_on_tensor_cores(st, latent):
+    """Latent size only enters the folded layer-0 bias c0: an unconditioned
+    8x512 decoder (latent 0) and latent 64, fp16x3 against fp64."""
+    rng = np.random.default_rng(4)
+    code = rng.normal(0.0, 0.1, latent) if latent else None
+    pts = rng.uniform(-0.8, 0.8, (4096, 3))
+    f64 = st.NeuralField.geometric(latent, (512,) * 8, 0, precision="fp64")
+    tcf = f64.with_precision("fp16x3")
+    assert np.max(np.abs(tcf.evaluate(pts, code) - f64.evaluate(pts, code))) < 5e-5
+    intr, pose = st.Intrinsics(width=64, height=64), st.look_at((0.0, 0.3, -2.0))
+    r64 = st.trace(f64, code, intr, pose, st.TraceConfig())
+    rtc = st.trace(tcf, code, intr, pose, st.TraceConfig())
+    assert np.array_equal(r64.state.status, rtc.state.status)
+    both = np.isfinite(st.depth_map(r64)) & np.isfinite(st.depth_map(rtc))
+    assert np.max(np.abs(st.depth_map(rtc)[both] - st.depth_map(r64)[both]) /
+                  st.depth_map(r64)[both]) < 2e-4
