@@ -168,7 +168,8 @@ typedef struct dist_objective_io {
   double *view_terms;            /* out [V*4]: depth loss, silhouette loss, n_px, n_converged */
   double *shape_terms;           /* out [S*2]: total objective, |z|^2 */
   int32_t grad_mode;             /* 0: the reference's frozen-sample surrogate (shading.py:9-11);
-                                    1: implicit gradient -(df/dz)/(grad f . v) at converged pixels */
+                                    1: implicit gradient -(df/dz)/(grad f . v) at converged pixels;
+                                    2: the paper's literal -(df/dz)/(n . v), n the unit Eq. 3 normal */
   int32_t reserved;
   int32_t *counts_out;           /* optional out [2]: recorded rays, seeded head samples (device) */
 } dist_objective_io;

@@ -564,7 +564,8 @@ def objective(dec: Decoder, code, cam: Cam, cfg: Cfg, w: Weights, depth=None,
               depth_valid=None, silhouette=None, normals=None, normals_valid=None,
               implicit=False):
     """completion_objective (optimize.py:102-138).  implicit=True replaces the
-    surrogate depth gradient by the implicit one."""
+    surrogate depth gradient by the implicit one (SURVEY 8c item 2);
+    implicit="unit" uses the unit normal in the denominator."""
     T = trace(lambda p: dec(p, code), cam, cfg)
     H = heads(T, lambda p: dec(p, code), cfg, want_normals=(normals is not None) or implicit)
     terms = {}
@@ -575,7 +576,7 @@ def objective(dec: Decoder, code, cam: Cam, cfg: Cfg, w: Weights, depth=None,
         terms["depth"] = l
         ds = w.depth * s
         if implicit:
-            ds = implicit_depth_seeds(H, ds, T.rays.dirs[H.ray_index])
+            ds = implicit_depth_seeds(H, ds, T.rays.dirs[H.ray_index], unit_normal=implicit == "unit")
     if silhouette is not None:
         l, gi = silhouette_loss(soft_silhouette(T, cfg), silhouette)
         terms["silhouette"] = l

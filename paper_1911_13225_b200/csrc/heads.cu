@@ -256,9 +256,9 @@ static ObjLayout obj_layout(const DecView &dv, int V, int W, int H, int K, int S
   L.h.view_samp = cv.take<int32_t>(V + 1);
   L.h.counts = cv.take<int32_t>(4);
   L.sil_seed = cv.take<double>(n);
-  L.gdotv = cv.take<double>(mode == 1 ? n : 1);
-  L.probe_f = cv.take<double>(mode == 1 ? n * 6 : 1);   // implicit mode only
-  L.conv = cv.take<int32_t>(mode == 1 ? n : 1);
+  L.gdotv = cv.take<double>(mode >= 1 ? n : 1);
+  L.probe_f = cv.take<double>(mode >= 1 ? n * 6 : 1);   // implicit modes only
+  L.conv = cv.take<int32_t>(mode >= 1 ? n : 1);
   L.conv_count = cv.take<int32_t>(4);
   L.npx = cv.take<int32_t>(V);
   L.loss_part = cv.take<double>((size_t)V * std::max(kLossBlocks, 3 * kPrepBlocks));
@@ -342,15 +342,15 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
   if (e == cudaSuccess && dv.nskip) e = cudaMemsetAsync(L.parts, 0, sizeof(double) * G * s1 * dv.nskip, sm);
   if (e == cudaSuccess) e = cudaMemsetAsync(io->grad, 0, sizeof(double) * s1 * std::max(dv.latent_dim, 1), sm);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(objective)");
-  if (io->grad_mode == 1) {
+  if (io->grad_mode == 1 || io->grad_mode == 2) {
     rc = normals_pass(dv, L.c0, L.cs, s1, cams, ls, cfg, nullptr, L.gdotv, L.conv, L.conv_count,
-                      L.bcount, L.probe_f, sm);
+                      L.bcount, L.probe_f, sm, io->grad_mode == 2);
     if (rc) return rc;
   } else if (io->grad_mode != 0) {
-    return fail(DIST_ERR_CONFIG, "grad_mode must be 0 (surrogate) or 1 (implicit)");
+    return fail(DIST_ERR_CONFIG, "grad_mode must be 0 (surrogate), 1 (implicit) or 2 (implicit, unit normal)");
   }
   ObjGen gen{cams, ls, K, WH, L.h, in, L.npx, io->obs_sil ? L.sil_seed : nullptr,
-             io->grad_mode == 1 ? L.gdotv : nullptr};
+             io->grad_mode >= 1 ? L.gdotv : nullptr};
   int grid = 0;
   if (tc_heads_supported(dv))
     rc = launch_tc_heads<ObjGen>(dv, L.c0, gen, n * K, s1, L.part0, G, &grid, sm);

@@ -57,7 +57,8 @@ int tc_eval_probes(const DecView &dv, const double *c0, int S, const ProbeGen &g
                    cudaStream_t st);
 int normals_pass(const DecView &dv, const double *c0, const double *cs, int S, const dist_camera *cams,
                  const LevelState &ls, const dist_trace_config *cfg, double *normals, double *gdotv,
-                 int32_t *conv, int32_t *count, int32_t *bcount, double *f, cudaStream_t st);
+                 int32_t *conv, int32_t *count, int32_t *bcount, double *f, cudaStream_t st,
+                 int gdotv_unit = 0);
 
 // stable device-wide compaction of flags -> ascending indices (scan.cu)
 size_t compact_ws_bytes(int64_t n);

@@ -21,6 +21,10 @@ from . import _lib
 from .losses import LossWeights, Observation
 from .tracer import TraceConfig, trace_views
 
+# dist_objective_io.grad_mode (include/dist.h): the reference's frozen-sample
+# surrogate, and the implicit-gradient extensions
+GRAD_MODES = {"surrogate": 0, "implicit": 1, "implicit_unit": 2}
+
 
 class OptimizationError(RuntimeError):
     """No usable gradient signal or a non-finite objective (optimize.py:28-29)."""
@@ -154,8 +158,8 @@ class LatentOptimizer:
         self.obs_depth = put("depth", np.float64)
         self.obs_mask = put("depth_mask", np.uint8)
         self.obs_sil = put("silhouette", np.float64)
-        if grad_mode not in ("surrogate", "implicit"):
-            raise ValueError("grad_mode must be 'surrogate' or 'implicit'")
+        if grad_mode not in GRAD_MODES:
+            raise ValueError(f"grad_mode must be one of {sorted(GRAD_MODES)}")
         self.grad_mode = grad_mode
         self.adam_cfg = _lib.dist_adam_config(lr, 0.9, 0.999, 1e-8)
         self.iter = 0
@@ -175,13 +179,13 @@ class LatentOptimizer:
         h = self.field.handle()
         K = self.cfg.k_samples
         ws = _lib.workspace(lib.dist_objective_workspace_size(h, self.V, self.W, self.H, K, self.S,
-                                                              1 if self.grad_mode == "implicit" else 0))
+                                                              GRAD_MODES[self.grad_mode]))
         io = _lib.dist_objective_io(_lib.ptr(self.obs_depth), _lib.ptr(self.obs_mask),
                                     _lib.ptr(self.obs_sil), self.weights.depth,
                                     self.weights.silhouette, self.weights.latent,
                                     self.grad.data_ptr(), self.view_terms.data_ptr(),
                                     self.shape_terms.data_ptr(),
-                                    1 if self.grad_mode == "implicit" else 0, 0,
+                                    GRAD_MODES[self.grad_mode], 0,
                                     self.head_counts.data_ptr())
         c = _lib.config_struct(self.cfg)
         st = dt.state_struct()
@@ -221,7 +225,8 @@ def completion_objective(field, code, observations, intr, pose, cfg: TraceConfig
     """(total, terms, grad_code, n_converged, queries) of one iterate (optimize.py:102-138).
 
     grad_mode="implicit" (extension) replaces the reference's
-    frozen-sample depth surrogate gradient by -(df/dz)/(grad f . v)."""
+    frozen-sample depth surrogate gradient by -(df/dz)/(grad f . v);
+    "implicit_unit" uses the paper's literal -(df/dz)/(n . v) with the unit normal."""
     obs = _split_observations(observations)
     if "normal" in obs:
         if grad_mode != "surrogate":

@@ -126,6 +126,30 @@ def test_implicit_gradient_mode_vs_oracle(st, prec, tol):
     assert np.linalg.norm(g_o - g["obj_grad"]) / np.linalg.norm(g["obj_grad"]) > 1e-2
 
 
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-8), ("fp16x3", 2e-2)])
+def test_implicit_unit_normal_mode_vs_oracle(st, prec, tol):
+    """grad_mode="implicit_unit": the north_star's literal dd/dz = -(1/(n.v)) df/dz
+    with n the unit Eq. 3 normal, against the oracle's restatement."""
+    g = load_golden("geo64.npz")
+    seed = int(g["seed"])
+    net = st.NeuralField.geometric(256, (512,) * 8, seed, precision=prec)
+    intr, pose = st.Intrinsics(width=64, height=64), st.Pose(g["omega"], g["t"])
+    cfg = st.TraceConfig(**cfg_from(g["cfg"]))
+    obs = [st.Observation("depth", g["obs_depth"])]
+    tot, _, grad, _, _ = st.completion_objective(net, g["code"], obs, intr, pose, cfg,
+                                                 st.LossWeights(), grad_mode="implicit_unit")
+    dec = orc.Decoder(orc.geometric_init(256, (512,) * 8, seed), 256)
+    cam = orc.Cam(64, 64, g["omega"], g["t"])
+    tot_o, _, g_o, _, _, _ = orc.objective(dec, g["code"], cam, orc.Cfg(k_samples=3), orc.Weights(),
+                                           depth=g["obs_depth"], implicit="unit")
+    _, _, g_raw, _, _, _ = orc.objective(dec, g["code"], cam, orc.Cfg(k_samples=3), orc.Weights(),
+                                         depth=g["obs_depth"], implicit=True)
+    assert abs(tot - tot_o) < 1e-9 + tol * abs(tot_o)
+    assert np.linalg.norm(grad - g_o) / np.linalg.norm(g_o) < tol
+    # |grad f| != 1 for the random-init decoder, so the two implicit variants differ
+    assert np.linalg.norm(g_o - g_raw) / np.linalg.norm(g_raw) > 1e-3
+
+
 @pytest.mark.gpu
 def test_complete_shape_report_matches_reference_file(st, tmp_path):
     """The reference CLI's report of a 3-iteration complete_shape (tiny net, 32^2,
