@@ -170,6 +170,8 @@ def main():
     # fp16x2 backward; bf16x3 is 1-4% faster with looser trace parity
     ap.add_argument("--precision", default=os.environ.get("DIST_BENCH_PRECISION", "fp16x3"))
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-relu-masks", action="store_true",
+                    help="re-run the taped forward for every head sample (no ReLU-mask record)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -203,7 +205,8 @@ def main():
     weights = st.LossWeights(latent=1.0 if rank == 0 else 0.0)   # regulariser added once
     iters = args.warmup + args.steps
     opt = st.LatentOptimizer(field, views, {"depth": obs}, np.zeros((1, 256)), cfg, weights,
-                             max_iters=2 * iters + 2)
+                             max_iters=2 * iters + 2,
+                             relu_masks=False if args.no_relu_masks else "auto")
 
     def allreduce(grad, shape_terms):
         if world > 1:
@@ -231,7 +234,8 @@ def main():
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
-            dt = st.trace_views(field, opt.code, views, cfg, reuse=opt.last_trace)
+            dt = st.trace_views(field, opt.code, views, cfg, reuse=opt.last_trace,
+                                relu_masks=opt.relu_masks)
             b.record(stream)
             opt.last_trace = dt
             q0 += dt.stats_dev[0]

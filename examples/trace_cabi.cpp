@@ -4,7 +4,7 @@
 // status, normals and the trace statistics back to a flat binary file.  This
 // is the call sequence a non-Python integrator of the reference's render path
 // (tracer.py:221-252 trace, shading.py:48-113 depth_map / normal_map) would
-// write.  tests/test_gpu_cabi_example.py writes the job from a NeuralField and
+// write.  tests/test_cabi_example.py writes the job from a NeuralField and
 // checks the output against the Python package bit for bit.
 //
 // Build:  make -C examples        (links ../paper_1911_13225_b200/libdist_b200.so)
@@ -119,6 +119,8 @@ int main(int argc, char** argv) {
   rs.topk_d = dev_alloc<double>(n * K);
   rs.topk_f = dev_alloc<double>(n * K);
   rs.topk_absf = dev_alloc<double>(n * K);
+  rs.relu_masks = nullptr;   // no objective here: the mask record stays off
+  rs.topk_slot = nullptr;
   int64_t* live_dev = dev_alloc<int64_t>(cfg.max_steps);
   int64_t* stats_dev = dev_alloc<int64_t>(4);
 

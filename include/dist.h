@@ -75,12 +75,23 @@ typedef struct dist_trace_config {
 } dist_trace_config;
 
 /* Full-resolution SoA ray state, RayState of tracer.py:53-73, for V views of
- * H x W rays, ray index = (view * H + j) * W + i.  topk_* are [n][K]. */
+ * H x W rays, ray index = (view * H + j) * W + i.  topk_* are [n][K].
+ *
+ * Optional (both NULL = off; honoured by the tensor-core precisions): the
+ * ReLU masks of every recorded sample, written by the full-resolution march
+ * as it queries, so that dist_objective runs only the backward sweep for
+ * them instead of re-evaluating the taped forward at the frozen points
+ * (shading.py:185-206 recomputes exactly the values the march computed).
+ *   relu_masks  [n][K+1][n_layers-1][16] uint32 (512 bits per layer of 512)
+ *   topk_slot   [n][K+1] uint8: physical mask slot of logical record k
+ *               (bit 7 set when this ray's own query wrote it), slot K spare. */
 typedef struct dist_ray_state {
   double *d, *b;
   uint8_t *status;
   int32_t *steps;
   double *topk_d, *topk_f, *topk_absf;
+  uint32_t *relu_masks;
+  uint8_t *topk_slot;
 } dist_ray_state;
 
 /* ---- library ---------------------------------------------------------- */

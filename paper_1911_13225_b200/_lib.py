@@ -39,7 +39,7 @@ class dist_trace_config(C.Structure):
 class dist_ray_state(C.Structure):
     _fields_ = [("d", C.c_void_p), ("b", C.c_void_p), ("status", C.c_void_p),
                 ("steps", C.c_void_p), ("topk_d", C.c_void_p), ("topk_f", C.c_void_p),
-                ("topk_absf", C.c_void_p)]
+                ("topk_absf", C.c_void_p), ("relu_masks", C.c_void_p), ("topk_slot", C.c_void_p)]
 
 
 class dist_objective_io(C.Structure):

@@ -238,6 +238,7 @@ struct ObjLayout {
   HeadsDev h;
   double *c0, *cs, *part0, *parts, *col0, *cols, *sil_seed, *gdotv, *probe_f, *loss_part;
   int32_t *npx, *bcount, *conv, *conv_count;
+  int32_t *sel_own, *sel_oth, *sel_counts;   // samples with / without a ReLU-mask record
   size_t bytes;
 };
 
@@ -255,6 +256,9 @@ static ObjLayout obj_layout(const DecView &dv, int V, int W, int H, int K, int S
   L.h.view_rec = cv.take<int32_t>(V + 1);
   L.h.view_samp = cv.take<int32_t>(V + 1);
   L.h.counts = cv.take<int32_t>(4);
+  L.sel_own = cv.take<int32_t>(n * K);
+  L.sel_oth = cv.take<int32_t>(n * K);
+  L.sel_counts = cv.take<int32_t>(4);
   L.sil_seed = cv.take<double>(n);
   L.gdotv = cv.take<double>(mode >= 1 ? n : 1);
   L.probe_f = cv.take<double>(mode >= 1 ? n * 6 : 1);   // implicit modes only
@@ -300,6 +304,14 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
   if (L.bytes > ws_bytes) return fail(DIST_ERR_CONFIG, "objective workspace too small");
   const int64_t n = (int64_t)V * W * H, WH = (int64_t)W * H;
   LevelState ls{st->d, st->b, st->status, st->steps, st->topk_d, st->topk_f, st->topk_absf, W, H, 1, n};
+  // the march's ReLU-mask record (include/dist.h): samples its own queries
+  // wrote skip the taped forward
+  const bool use_masks = st->relu_masks && st->topk_slot && tc_heads_supported(dv);
+  if (use_masks) {
+    ls.masks = st->relu_masks;
+    ls.tk_p = st->topk_slot;
+    ls.nmask = dv.n_layers - 1;
+  }
   ObjIn in{io->obs_depth, io->obs_depth_mask, io->obs_sil, io->w_depth, io->w_sil, io->w_latent};
 
   // 1. sample list
@@ -352,7 +364,30 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
   ObjGen gen{cams, ls, K, WH, L.h, in, L.npx, io->obs_sil ? L.sil_seed : nullptr,
              io->grad_mode >= 1 ? L.gdotv : nullptr};
   int grid = 0;
-  if (tc_heads_supported(dv))
+  if (use_masks) {
+    // split the sample list: rows with a mask record -> backward-only kernel
+    const int32_t *samp = L.h.samp, *nsamp = L.h.counts + 1;
+    const uint8_t *tkp = st->topk_slot;
+    for (int want = 1; want >= 0 && !rc; --want)
+      rc = compact(
+          [samp, nsamp, tkp, Kc, want] __device__(int64_t i) {
+            if (i >= *nsamp) return false;
+            const int64_t flat = samp[i];
+            const int64_t g = flat / Kc;
+            return (int)((tkp[g * (Kc + 1) + (flat - g * Kc)] & 0x80) != 0) == want;
+          },
+          n * K, want ? L.sel_own : L.sel_oth, L.sel_counts + (want ? 0 : 1), L.bcount, sm);
+    if (rc) return rc;
+    ObjGen gown = gen, goth = gen;
+    gown.sel = L.sel_own;
+    gown.sel_count = L.sel_counts + 0;
+    goth.sel = L.sel_oth;
+    goth.sel_count = L.sel_counts + 1;
+    int grid2 = 0;
+    rc = launch_tc_heads_bwd(dv, L.c0, gown, n * K, s1, L.part0, G, &grid, sm);
+    if (!rc) rc = launch_tc_heads<ObjGen>(dv, L.c0, goth, n * K, s1, L.part0, G, &grid2, sm);
+    grid = std::max(grid, grid2);
+  } else if (tc_heads_supported(dv))
     rc = launch_tc_heads<ObjGen>(dv, L.c0, gen, n * K, s1, L.part0, G, &grid, sm);
   else if (dv.prec == DIST_PREC_FP64)
     rc = launch_vjp_gen<double>(dv, L.c0, L.cs, gen, n * K, s1, L.part0, L.parts, nullptr, G, &grid, sm);

@@ -48,9 +48,22 @@ struct ObjGen {
   const int32_t *npx;
   const double *sil_seed;
   const double *gdotv;   // implicit mode: grad f . v per ray (raw Eq. 3 vector), else null
-  __device__ int64_t count() const { return h.counts[1]; }
+  // optional row -> sample map: the samples split by the ReLU-mask record
+  // (rows of the backward-only head kernel / of the full one)
+  const int32_t *sel = nullptr;
+  const int32_t *sel_count = nullptr;
+  __device__ int64_t at(int64_t r) const { return sel ? (int64_t)sel[r] : r; }
+  __device__ int64_t count() const { return sel ? (int64_t)*sel_count : (int64_t)h.counts[1]; }
+  // backward-only rows: the march's f at the sample (tracer.py:141 records it)
+  // and the ReLU masks its query left in the ray's record (march.cuh)
+  __device__ double f_rec(int64_t r) const { return ls.tk_f[h.samp[at(r)]]; }
+  __device__ const uint32_t *masks_rec(int64_t r) const {
+    const int64_t flat = h.samp[at(r)];
+    const int64_t g = flat / K;
+    return mask_record(ls, K, g, ls.tk_p[g * (K + 1) + (flat - g * K)] & 0x7f);
+  }
   __device__ bool point(int64_t i, double p[3], int &s) const {
-    const int64_t flat = h.samp[i];
+    const int64_t flat = h.samp[at(i)];
     const int64_t g = flat / K;
     const int v = (int)(g / WH);
     const int64_t q = g - v * WH;
@@ -63,7 +76,7 @@ struct ObjGen {
     return true;
   }
   __device__ double seed(int64_t i, double f) const {
-    const int64_t flat = h.samp[i];
+    const int64_t flat = h.samp[at(i)];
     const int64_t g = flat / K;
     const int v = (int)(g / WH);
     double sd = 0.0;
@@ -86,7 +99,7 @@ struct ObjGen {
     if (sil_seed && flat - g * K == 0) sd = __dadd_rn(sd, sil_seed[g]);
     return sd;
   }
-  __device__ void store(int64_t i, double v) const { h.f[i] = v; }
+  __device__ void store(int64_t i, double v) const { h.f[at(i)] = v; }
 
   // seed(i, f) split in two for the tensor-core head kernel: prep() does every
   // load at tile start (overlapping the forward GEMMs), apply() needs only f.
@@ -97,7 +110,7 @@ struct ObjGen {
   };
   __device__ Prep prep(int64_t i) const {
     Prep r{0.0, 0.0, 0.0, 0.0, 1.0, 0.0};
-    const int64_t flat = h.samp[i];
+    const int64_t flat = h.samp[at(i)];
     const int64_t g = flat / K;
     const int v = (int)(g / WH);
     if (in.obs_depth && ls.status[g] == DIST_CONVERGED && depth_valid(in, g) && npx[v] > 0) {

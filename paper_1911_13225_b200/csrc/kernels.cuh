@@ -53,6 +53,10 @@ int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t
 
 struct LevelState;
 struct ProbeGen;
+struct ObjGen;
+// backward-only head rows (f and ReLU masks from the march's mask record)
+int launch_tc_heads_bwd(const DecView &dv, const double *c0, const ObjGen &gen, int64_t n_bound, int S,
+                        double *part0, int grid_cap, int *grid_out, cudaStream_t st);
 int tc_eval_probes(const DecView &dv, const double *c0, int S, const ProbeGen &gen, int64_t n_bound,
                    cudaStream_t st);
 int normals_pass(const DecView &dv, const double *c0, const double *cs, int S, const dist_camera *cams,

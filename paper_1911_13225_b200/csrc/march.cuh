@@ -12,7 +12,19 @@ struct LevelState {
   double *tk_d, *tk_f, *tk_a;
   int lw, lh, level;
   int64_t n;  // V * lw * lh
+  // Optional ReLU-mask record (full resolution, tensor-core march only;
+  // include/dist.h dist_ray_state.relu_masks): tk_p[g][k] is the physical mask
+  // slot of logical record k (bit 7: the masks were written by this ray's own
+  // query), tk_p[g][K] the spare slot the current query's masks go to.
+  uint32_t *masks;   // [n][K+1][nmask][16]
+  uint8_t *tk_p;     // [n][K+1]
+  int nmask;         // ReLU layers (hidden GEMMs + 1)
 };
+
+// words of one (ray, physical slot) mask record
+__device__ __forceinline__ uint32_t *mask_record(const LevelState &ls, int K, int64_t g, int slot) {
+  return ls.masks + ((size_t)g * (K + 1) + slot) * ls.nmask * 16;
+}
 
 struct Ctl {
   int32_t cnt[2];
@@ -67,16 +79,23 @@ __device__ __forceinline__ bool march_update(const LevelState &ls, const MarchAr
   const int K = a.K;
   double *ta = ls.tk_a + g * K, *tf = ls.tk_f + g * K, *td = ls.tk_d + g * K;
   if (av < ta[K - 1]) {  // strict: the earliest query wins ties (tracer.py:133-134)
+    uint8_t *tp = ls.tk_p ? ls.tk_p + g * (K + 1) : nullptr;
+    const uint8_t evicted = tp ? tp[K - 1] : 0;
     int pos = K - 1;
     while (pos > 0 && ta[pos - 1] > av) {
       ta[pos] = ta[pos - 1];
       tf[pos] = tf[pos - 1];
       td[pos] = td[pos - 1];
+      if (tp) tp[pos] = tp[pos - 1];
       --pos;
     }
     ta[pos] = av;
     tf[pos] = f;
     td[pos] = dk;
+    if (tp) {  // this query's masks sit in the spare slot; the evicted one's becomes spare
+      tp[pos] = tp[K] | 0x80;
+      tp[K] = evicted & 0x7f;
+    }
   }
   ls.steps[g] += 1;
   ls.b[g] = f;

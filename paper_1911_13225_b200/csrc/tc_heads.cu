@@ -94,7 +94,10 @@ __device__ __forceinline__ void warp_colsum64(float (&v)[64]) {
 static __device__ unsigned long long g_heads_tl[4096];
 #define TL(id) DIST_TL_MARK(g_heads_tl, id)
 
-template <class Gen>
+// BWD: backward-only rows (the ReLU-mask record, include/dist.h): f and the
+// masks of every layer come from the march's own query of the sample, so the
+// forward phases are skipped and a tile is the G backward GEMMs alone.
+template <class Gen, bool BWD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     k_tc_heads(const __grid_constant__ CUtensorMap wfwd, const __grid_constant__ CUtensorMap wbwd,
                HParams P, Gen gen) {
@@ -140,7 +143,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (lane == 0) {
       uint32_t it = 0;
       for (int64_t t = cluster; t < ntiles; t += nclusters)
-        for (int ph = 0; ph < NPH; ++ph) {
+        for (int ph = BWD ? G : 0; ph < NPH; ++ph) {
           const bool fwd = ph < G;
           const int l = fwd ? ph : 2 * G - 1 - ph;
           const CUtensorMap *map = fwd ? &wfwd : &wbwd;
@@ -162,7 +165,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint32_t it = 0, phase = 0;
       const uint32_t a_hi = smem_u32(smem + OFF_AHI), a_lo = smem_u32(smem + OFF_ALO);
       for (int64_t t = cluster; t < ntiles; t += nclusters)
-        for (int ph = 0; ph < NPH; ++ph, ++phase) {
+        for (int ph = BWD ? G : 0; ph < NPH; ++ph, ++phase) {
           mbar_wait(&m.aready, phase & 1);
           tc_fence_after();
           for (int nh = 0; nh < 2; ++nh) {
@@ -235,22 +238,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     float *gout = reinterpret_cast<float *>(&m.ray[0]);
     // the next tile's sample point is fetched during the current tile's last
     // backward GEMM (a dependent chain of global loads)
-    auto fetch = [&](int64_t tt, double (&q)[3], int &ss) {
+    // backward-only rows: this thread's words of each layer's mask record
+    const int mword = 4 * half + 2 * sub;
+    auto fetch = [&](int64_t tt, double (&q)[3], int &ss, const uint32_t *&mr) {
       const int64_t g2 = tt * (2 * ROWS) + (int64_t)rank * ROWS + row;
       q[0] = q[1] = q[2] = 0.0;
       ss = -1;
+      mr = nullptr;
       if (tt < ntiles && g2 < nrows && !gen.point(g2, q, ss)) ss = -1;
+      if constexpr (BWD) {
+        if (ss >= 0) mr = gen.masks_rec(g2);
+      }
     };
     double nxp[3];
     int nxs;
-    fetch(cluster, nxp, nxs);
+    const uint32_t *nxm;
+    fetch(cluster, nxp, nxs, nxm);
     for (int64_t t = cluster; t < ntiles; t += nclusters) {
       TL(1);
       const int64_t gi = t * (2 * ROWS) + (int64_t)rank * ROWS + row;
       double p[3] = {nxp[0], nxp[1], nxp[2]};
       const int s = nxs;
+      const uint32_t *const mrec = nxm;
 
       if (row_thread) m.shape[row] = s;
+      float head = 0.f;
+      typename Gen::Prep sp{};
+      double fbwd = 0.0;   // BWD: the march's f of this row's sample
+      if constexpr (BWD) {
+        // masks of layers 0..G from the record into this thread's TMEM columns
+#pragma unroll 1
+        for (int ml = 0; ml <= G; ++ml) {
+          uint32_t mk[4] = {0u, 0u, 0u, 0u};
+          if (mrec) {
+            const uint2 a = __ldg(reinterpret_cast<const uint2 *>(mrec + ml * 16 + mword));
+            const uint2 b = __ldg(reinterpret_cast<const uint2 *>(mrec + ml * 16 + 8 + mword));
+            mk[0] = a.x; mk[1] = a.y; mk[2] = b.x; mk[3] = b.y;
+          }
+          tmem_st4(mask_addr(ml), mk);
+        }
+        if (row_thread && gi < nrows && s >= 0) {
+          sp = gen.prep(gi);
+          fbwd = gen.f_rec(gi);
+        }
+        tc_fence_before();
+      } else {
       // ---- layer 0 (folded bias + p . W0p, fp32) + mask 0 ----
       {
         const float *c0f = P.c0f + (size_t)(s < 0 ? 0 : s) * n0;
@@ -286,10 +318,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       TL(2);
       // the seed's loads, issued once layer 0 is handed to the MMA warp so
       // they land during the forward GEMMs
-      typename Gen::Prep sp{};
       if (row_thread && gi < nrows && s >= 0) sp = gen.prep(gi);
       // ---- forward hidden layers ----
-      float head = 0.f;
       // The nh = 0 half of each forward GEMM is processed while the nh = 1
       // MMAs run: its packed A words are parked in the TMEM columns just read
       // and copied to A once the GEMM is done (tc_mlp.cu, same scheme).
@@ -403,14 +433,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           TL(4);
         }
       }
-      // ---- head, seed, d loss / d h_G ----
+      // ---- head: the four partial dot products of each row ----
       m.xch[half * 2 + sub][row] = head;
       epi_sync();
+      }   // !BWD
+      // ---- seed, d loss / d h_G ----
       double go = 0.0;
       if (row_thread) {
-        const double sum = (double)m.xch[0][row] + (double)m.xch[1][row] +
-                           (double)m.xch[2][row] + (double)m.xch[3][row] + P.dv.b_out;
-        const double fv = head_act(P.dv.final_act, sum);
+        double fv;
+        if constexpr (BWD) {
+          fv = fbwd;
+        } else {
+          const double sum = (double)m.xch[0][row] + (double)m.xch[1][row] +
+                             (double)m.xch[2][row] + (double)m.xch[3][row] + P.dv.b_out;
+          fv = head_act(P.dv.final_act, sum);
+        }
         if (gi < nrows && s >= 0) {
           gen.store(gi, fv);
           const double sd = gen.apply(sp, fv);
@@ -457,7 +494,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       TL(6);
       // ---- backward through GEMM layers G-1 .. 0 ----
       for (int gl = G - 1; gl >= 0; --gl, ++phase) {
-        if (gl == 0) fetch(t + nclusters, nxp, nxs);
+        if (gl == 0) fetch(t + nclusters, nxp, nxs, nxm);
         uint32_t mk[4];
         tmem_ld4(mask_addr(gl), mk);   // written in the forward, readable now
         // D = (g / rinv) (W / winv_b): true dgrad = D * unscale
@@ -650,9 +687,9 @@ bool tc_heads_supported(const DecView &dv) {
 }
 
 
-template <class Gen>
-int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
-                    double *part0, int grid_cap, int *grid_out, cudaStream_t st, double *gpts) {
+template <class Gen, bool BWD>
+static int launch_heads_impl(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
+                             double *part0, int grid_cap, int *grid_out, cudaStream_t st, double *gpts) {
   CUtensorMap mf, mb;
   const int fs = dv.prec == DIST_PREC_FP16X3 ? 3 : 0;   // bf16x3 forward pack
   int rc = tc_make_map(dv, fs, &mf);
@@ -675,15 +712,26 @@ int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t
   }
   P.part0 = part0;
   P.gpts = gpts;
-  const void *fn = (const void *)tc::k_tc_heads<Gen>;
+  const void *fn = (const void *)tc::k_tc_heads<Gen, BWD>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc heads)");
   int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_bound, 128), sm_count() / 2));
   pairs = std::min(pairs, grid_cap / 2);
   *grid_out = 2 * pairs;
-  tc::k_tc_heads<Gen><<<2 * pairs, tc::THREADS, tc::SMEM_BYTES, st>>>(mf, mb, P, gen);
+  tc::k_tc_heads<Gen, BWD><<<2 * pairs, tc::THREADS, tc::SMEM_BYTES, st>>>(mf, mb, P, gen);
   DIST_CHECK_LAUNCH("k_tc_heads");
   return DIST_OK;
+}
+
+template <class Gen>
+int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
+                    double *part0, int grid_cap, int *grid_out, cudaStream_t st, double *gpts) {
+  return launch_heads_impl<Gen, false>(dv, c0, gen, n_bound, S, part0, grid_cap, grid_out, st, gpts);
+}
+
+int launch_tc_heads_bwd(const DecView &dv, const double *c0, const ObjGen &gen, int64_t n_bound, int S,
+                        double *part0, int grid_cap, int *grid_out, cudaStream_t st) {
+  return launch_heads_impl<ObjGen, true>(dv, c0, gen, n_bound, S, part0, grid_cap, grid_out, st, nullptr);
 }
 
 extern "C" DIST_API int dist_debug_heads_timeline(unsigned long long *out, int n) {

@@ -129,6 +129,11 @@ struct MarchRows {
     warp_append(keep, g, out, &ctl->cnt[m.cur ^ 1]);
   }
   __device__ void end(Misc &m) { step_epilogue(ctl, m.cur, rows(m), m.nan, live, stats); }
+  // where ray g's ReLU masks of this query go: its spare record (march.cuh)
+  __device__ uint32_t *mask_dst(int g) const {
+    if (!ls.masks) return nullptr;
+    return mask_record(ls, a.K, g, ls.tk_p[(int64_t)g * (a.K + 1) + a.K]);
+  }
 };
 
 template <class Rows>
@@ -331,13 +336,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       double p[3];
       int s, id;
       int64_t gi;
+      uint32_t *md;   // ReLU-mask record of this query (march with masks), else null
+    };
+    // ReLU masks (march with a mask record): this thread's 2 x 64 columns of a
+    // layer are words 8 nh + 4 half + 2 sub + {0, 1} of the layer's 16
+    constexpr bool kMasks = std::is_same<Rows, MarchRows>::value && !PAIR;
+    const int mword = 4 * half + 2 * sub;
+    auto put_mask = [&](uint32_t *md, int ml, int nh, uint32_t w0, uint32_t w1) {
+      if constexpr (kMasks) {
+        if (md) *reinterpret_cast<uint2 *>(md + ml * 16 + nh * 8 + mword) = make_uint2(w0, w1);
+      }
     };
     auto fetch = [&](int64_t t, RowIn &r) {
       r.gi = t * (2 * ROWS) + (int64_t)rank * ROWS + row;
       r.p[0] = r.p[1] = r.p[2] = 0.0;
       r.s = -1;
       r.id = -1;
+      r.md = nullptr;
       if (t < ntiles && r.gi < nrows) r.id = load_row(R, m, r.gi, r.p, r.s);
+      if constexpr (kMasks) {
+        if (r.id >= 0) r.md = R.mask_dst(r.id);
+      }
     };
     uint32_t afree_n = 0;  // afree phases consumed (one per non-last kEarly layer)
     bool xpend = false;   // an xch_read's barrier-2 arrive awaits its matching sync
@@ -374,6 +393,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       double p[3] = {nx.p[0], nx.p[1], nx.p[2]};
       const int s = nx.s, id = nx.id;
       const int64_t gi = nx.gi;
+      uint32_t *const md = nx.md;
       const bool odd = PAIR && (lane & 1);
       const int n0 = P.dv.np[0];
       const float *c0f = P.c0f + (size_t)(s < 0 ? 0 : s) * n0;
@@ -478,17 +498,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         a_ready_lo();
         float part = stash_part;
         const int cb = 256 + half * 128 + sub * 64;
+        uint32_t mwa = 0u, mwb = 0u;   // mask words of columns +0..31, +32..63
 #pragma unroll 2
         for (int j = 0; j < 64; j += 8) {
           float x[8];
           h0x8_pt(px, py, pz, s, cb + j, x);
+          uint32_t bits = 0;
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             if constexpr (kBound) part = fmaxf(part, x[e]);
+            if constexpr (kMasks) bits |= (x[e] > 0.f ? 1u : 0u) << e;
             x[e] *= sc;
+          }
+          if constexpr (kMasks) {
+            if (j < 32) mwa |= bits << j;
+            else mwb |= bits << (j - 32);
           }
           put8<F16>(smem, row, cb + j, x);
         }
+        put_mask(md, 0, 1, mwa, mwb);
         if constexpr (kBound) xch_post(part);
         fence_proxy_async();
         epi_sync();
@@ -519,17 +547,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         float part = 0.f;
         for (int nh = 0; nh < 2; ++nh) {
           const int cb = nh * 256 + half * 128 + sub * 64;
+          uint32_t mwa = 0u, mwb = 0u;   // mask words of columns +0..31, +32..63
 #pragma unroll 2
           for (int j = 0; j < 64; j += 8) {
             float x[8];
             h0x8(cb + j, x);
+            uint32_t bits = 0;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               if constexpr (kBound) part = fmaxf(part, x[e]);
+              if constexpr (kMasks) bits |= (x[e] > 0.f ? 1u : 0u) << e;
               x[e] *= sc;
             }
+            if constexpr (kMasks) {
+            if (j < 32) mwa |= bits << j;
+            else mwb |= bits << (j - 32);
+          }
             put8<F16>(smem, row, cb + j, x);
           }
+          put_mask(md, 0, nh, mwa, mwb);
         }
         if constexpr (kBound) xch_post(part);
       }
@@ -579,11 +615,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           // ---- early half: columns nh = 0 while the nh = 1 MMAs run ----
           {
             const int cb = half * 128 + sub * 64;
+            uint32_t mwa = 0u, mwb = 0u;   // mask words of columns +0..31, +32..63
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
               float v[32];
               load_d(sub * 64 + c * 32, v);
               uint32_t r[32];
+              uint32_t bits = 0;
 #pragma unroll
               for (int g8 = 0; g8 < 4; ++g8) {
                 float bb[8], x[8];
@@ -592,12 +630,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                   float wo[8];
                   ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
 #pragma unroll
-                  for (int e = 0; e < 8; ++e) head = fmaf(act(v[g8 * 8 + e], bb[e]), wo[e], head);
+                  for (int e = 0; e < 8; ++e) {
+                    const float y = act(v[g8 * 8 + e], bb[e]);
+                    if constexpr (kMasks) bits |= (y > 0.f ? 1u : 0u) << (g8 * 8 + e);
+                    head = fmaf(y, wo[e], head);
+                  }
                 } else {
 #pragma unroll
                   for (int e = 0; e < 8; ++e) {
                     const float y = act(v[g8 * 8 + e], bb[e]);
                     if constexpr (kBound) part = fmaxf(part, y);
+                    if constexpr (kMasks) bits |= (y > 0.f ? 1u : 0u) << (g8 * 8 + e);
                     x[e] = y * sc;
                   }
                   uint32_t hi[4], lo[4];
@@ -610,7 +653,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 }
               }
               if (!last) tmem_st32(tq + sub * 64 + c * 32, r);
+              if (c == 0) mwa = bits;
+              else mwb = bits;
             }
+            put_mask(md, l + 1, 0, mwa, mwb);
             if (last && t + nclusters < ntiles) {
               // the next tile's layer 0, columns 0..255, into the TMEM columns
               // the head just consumed (nx: its rows, fetched above)
@@ -624,20 +670,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 sc0 = pow2_scale(b0);
               }
               float part0 = 0.f;
+              uint32_t mw0a = 0u, mw0b = 0u;
               // parked as [hi 4 | lo 4] per 8 columns (x8 stores keep registers low)
 #pragma unroll 1
               for (int j = 0; j < 64; j += 8) {
                 float x[8];
                 h0x8_pt(qx, qy, qz, qs, half * 128 + sub * 64 + j, x);
+                uint32_t bits = 0;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                   if constexpr (kBound) part0 = fmaxf(part0, x[e]);
+                  if constexpr (kMasks) bits |= (x[e] > 0.f ? 1u : 0u) << e;
                   x[e] *= sc0;
+                }
+                if constexpr (kMasks) {
+                  if (j < 32) mw0a |= bits << j;
+                  else mw0b |= bits << (j - 32);
                 }
                 uint32_t hi[4], lo[4];
                 pack8<F16>(x, hi, lo);
                 tmem_st8(tq + sub * 64 + j, hi, lo);
               }
+              put_mask(nx.md, 0, 0, mw0a, mw0b);
               have_stash = true;
               stash_part = part0;
               stash_sc = sc0;
@@ -679,10 +733,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           tc_fence_after();
           {
             const int cb = 256 + half * 128 + sub * 64;
+            uint32_t mwa = 0u, mwb = 0u;   // mask words of columns +0..31, +32..63
 #pragma unroll 1
             for (int c = 0; c < 2; ++c) {
               float v[32];
               load_d(128 + sub * 64 + c * 32, v);
+              uint32_t bits = 0;
 #pragma unroll
               for (int g8 = 0; g8 < 4; ++g8) {
                 float x[8], bb[8];
@@ -691,18 +747,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                   float wo[8];
                   ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
 #pragma unroll
-                  for (int e = 0; e < 8; ++e) head = fmaf(act(v[g8 * 8 + e], bb[e]), wo[e], head);
+                  for (int e = 0; e < 8; ++e) {
+                    const float y = act(v[g8 * 8 + e], bb[e]);
+                    if constexpr (kMasks) bits |= (y > 0.f ? 1u : 0u) << (g8 * 8 + e);
+                    head = fmaf(y, wo[e], head);
+                  }
                 } else {
 #pragma unroll
                   for (int e = 0; e < 8; ++e) {
                     const float y = act(v[g8 * 8 + e], bb[e]);
                     if constexpr (kBound) part = fmaxf(part, y);
+                    if constexpr (kMasks) bits |= (y > 0.f ? 1u : 0u) << (g8 * 8 + e);
                     x[e] = y * sc;
                   }
                   put8<F16>(smem, row, cb + c * 32 + g8 * 8, x);
                 }
               }
+              if (c == 0) mwa = bits;
+              else mwb = bits;
             }
+            put_mask(md, l + 1, 1, mwa, mwb);
           }
           TL(14);
           if (!last) {

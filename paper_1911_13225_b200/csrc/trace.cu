@@ -58,6 +58,8 @@ __global__ void k_init(const dist_camera *__restrict__ cams, LevelState ls, int 
         ls.tk_f[g * K + k] = 0.0;
         ls.tk_a[g * K + k] = __longlong_as_double(0x7ff0000000000000ll);
       }
+      if (ls.tk_p)
+        for (int k = 0; k <= K; ++k) ls.tk_p[g * (K + 1) + k] = (uint8_t)k;
       live = stt == DIST_MARCHING;
     }
     warp_append(live, (int32_t)g, list, &ctl->cnt[0]);
@@ -86,6 +88,9 @@ __global__ void k_split(LevelState par, LevelState ch, int K, int32_t *__restric
         ch.tk_f[g * K + k] = par.tk_f[p * K + k];
         ch.tk_a[g * K + k] = par.tk_a[p * K + k];
       }
+      // inherited records carry no masks of this ray (own bit clear)
+      if (ch.tk_p)
+        for (int k = 0; k <= K; ++k) ch.tk_p[g * (K + 1) + k] = (uint8_t)k;
       live = s == DIST_MARCHING;
     }
     warp_append(live, (int32_t)g, list, &ctl->cnt[0]);
@@ -301,6 +306,11 @@ static TraceLayout layout(const DecView &dv, const dist_trace_config *cfg, int V
       if (out) {
         ls.d = out->d; ls.b = out->b; ls.status = out->status; ls.steps = out->steps;
         ls.tk_d = out->topk_d; ls.tk_f = out->topk_f; ls.tk_a = out->topk_absf;
+        if (out->relu_masks && out->topk_slot && tc_heads_supported(dv)) {
+          ls.masks = out->relu_masks;
+          ls.tk_p = out->topk_slot;
+          ls.nmask = dv.n_layers - 1;
+        }
       }
     } else {
       ls.d = cv.take<double>(ls.n);

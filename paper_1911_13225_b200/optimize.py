@@ -19,11 +19,13 @@ import numpy as np
 
 from . import _lib
 from .losses import LossWeights, Observation
-from .tracer import TraceConfig, trace_views
+from .tracer import TraceConfig, relu_mask_bytes, trace_views
 
 # dist_objective_io.grad_mode (include/dist.h): the reference's frozen-sample
 # surrogate, and the implicit-gradient extensions
 GRAD_MODES = {"surrogate": 0, "implicit": 1, "implicit_unit": 2}
+# LatentOptimizer(relu_masks="auto") records the ReLU masks up to this size
+RELU_MASK_AUTO_BYTES = 16 << 30
 
 
 class OptimizationError(RuntimeError):
@@ -109,11 +111,15 @@ class LatentOptimizer:
     optional "depth_mask").  One `step()` = trace + heads + fused backward +
     Adam for every view at once; depth terms are normalised per view and the
     latent regulariser is added once per shape.
+
+    relu_masks: record the ReLU masks of the samples during the march so the
+    objective runs only the backward sweep for them (tensor-core precisions;
+    "auto" = on when the record fits in RELU_MASK_AUTO_BYTES).
     """
 
     def __init__(self, field, views, observations: dict, code0, cfg: TraceConfig | None = None,
                  weights: LossWeights | None = None, lr: float = 1e-2, shape_of_view=None,
-                 max_iters: int = 1024, grad_mode: str = "surrogate"):
+                 max_iters: int = 1024, grad_mode: str = "surrogate", relu_masks="auto"):
         import torch
         _lib.require_device()
         self.field = field
@@ -141,6 +147,10 @@ class LatentOptimizer:
         self.shape_terms = torch.zeros((self.S, 2), dtype=torch.float64, device=dev)
         self.head_counts = torch.zeros(2, dtype=torch.int32, device=dev)  # recorded rays, seeded samples
         n = V * self.W * self.H
+        if relu_masks == "auto":
+            relu_masks = (field.precision in ("fp16x3", "bf16x3") and
+                          relu_mask_bytes(field, n, self.cfg.k_samples) <= RELU_MASK_AUTO_BYTES)
+        self.relu_masks = bool(relu_masks)
 
         def put(key, dtype):
             if key not in observations or observations[key] is None:
@@ -169,7 +179,7 @@ class LatentOptimizer:
     def objective(self):
         """Trace + heads + fused backward at the current code (no Adam)."""
         dt = trace_views(self.field, self.code, self.views, self.cfg, self.shape_of_view,
-                         reuse=self.last_trace)
+                         reuse=self.last_trace, relu_masks=self.relu_masks)
         self.last_trace = dt
         self._objective_after_trace(dt)
         return dt

@@ -73,7 +73,8 @@ class RayState:
 class DeviceTrace:
     """Device-resident result of tracing V views (all tensors on cuda)."""
 
-    def __init__(self, field, codes, cams, intrs, poses, cfg: TraceConfig, W: int, H: int):
+    def __init__(self, field, codes, cams, intrs, poses, cfg: TraceConfig, W: int, H: int,
+                 relu_masks: bool = False):
         import torch
         self.field, self.codes, self.cfg = field, codes, cfg
         self.cams, self.intrs, self.poses = cams, intrs, poses
@@ -90,11 +91,19 @@ class DeviceTrace:
         self.topk_absf = torch.empty((n, K), dtype=torch.float64, device=dev)
         self.live_counts_dev = torch.zeros(cfg.max_steps, dtype=torch.int64, device=dev)
         self.stats_dev = torch.zeros(4, dtype=torch.int64, device=dev)
+        # ReLU masks of the recorded samples (include/dist.h dist_ray_state):
+        # lets dist_objective skip the taped forward for them
+        self.relu_masks = self.topk_slot = None
+        if relu_masks:
+            nm = len(field.weights) - 1
+            self.relu_masks = torch.empty(n * (K + 1) * nm * 16, dtype=torch.int32, device=dev)
+            self.topk_slot = torch.empty((n, K + 1), dtype=torch.uint8, device=dev)
 
     def state_struct(self) -> _lib.dist_ray_state:
         return _lib.dist_ray_state(self.d.data_ptr(), self.b.data_ptr(), self.status.data_ptr(),
                                    self.steps.data_ptr(), self.topk_d.data_ptr(),
-                                   self.topk_f.data_ptr(), self.topk_absf.data_ptr())
+                                   self.topk_f.data_ptr(), self.topk_absf.data_ptr(),
+                                   _lib.ptr(self.relu_masks), _lib.ptr(self.topk_slot))
 
     def stats(self) -> dict:
         s = self.stats_dev.cpu().numpy()
@@ -117,13 +126,21 @@ def _code_tensor(field, codes):
     return z, z.shape[0]
 
 
+def relu_mask_bytes(field, n_rays: int, k_samples: int) -> int:
+    """Device bytes of the optional ReLU-mask record of n_rays rays."""
+    return n_rays * (k_samples + 1) * (len(field.weights) - 1) * 64 + n_rays * (k_samples + 1)
+
+
 def trace_views(field, codes, views, cfg: TraceConfig | None = None,
-                shape_of_view=None, reuse: DeviceTrace | None = None) -> DeviceTrace:
+                shape_of_view=None, reuse: DeviceTrace | None = None,
+                relu_masks: bool = False) -> DeviceTrace:
     """Trace V views (list of (Intrinsics, Pose)) of one resolution in one call.
 
     codes: [D] or [S, D]; shape_of_view[v] picks the code row of view v.
     reuse: a DeviceTrace of the same views/config whose buffers (and uploaded
     cameras) are overwritten in place -- the optimisation loop's fast path.
+    relu_masks: also record the ReLU masks of every recorded sample (tensor-core
+    precisions; the objective then runs only the backward sweep for them).
     """
     import torch
     cfg = cfg or TraceConfig()
@@ -144,7 +161,7 @@ def trace_views(field, codes, views, cfg: TraceConfig | None = None,
     else:
         sv = [0] * len(views) if shape_of_view is None else [int(s) for s in shape_of_view]
         cams = _lib.cameras_to_device([camera_struct(i, p, s) for i, p, s in zip(intrs, poses, sv)])
-        dt = DeviceTrace(field, z, cams, intrs, poses, cfg, W, H)
+        dt = DeviceTrace(field, z, cams, intrs, poses, cfg, W, H, relu_masks=relu_masks)
     cams = dt.cams
     lib = _lib.lib()
     c = _lib.config_struct(cfg)
