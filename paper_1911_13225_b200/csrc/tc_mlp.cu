@@ -503,18 +503,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int j = 0; j < 64; j += 8) {
           float x[8];
           h0x8_pt(px, py, pz, s, cb + j, x);
-          uint32_t bits = 0;
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             if constexpr (kBound) part = fmaxf(part, x[e]);
-            if constexpr (kMasks) bits |= (x[e] > 0.f ? 1u : 0u) << e;
             x[e] *= sc;
           }
           if constexpr (kMasks) {
+            const uint32_t bits = put8m<F16>(smem, row, cb + j, x);
             if (j < 32) mwa |= bits << j;
             else mwb |= bits << (j - 32);
+          } else {
+            put8<F16>(smem, row, cb + j, x);
           }
-          put8<F16>(smem, row, cb + j, x);
         }
         put_mask(md, 0, 1, mwa, mwb);
         if constexpr (kBound) xch_post(part);
@@ -552,18 +552,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int j = 0; j < 64; j += 8) {
             float x[8];
             h0x8(cb + j, x);
-            uint32_t bits = 0;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
               if constexpr (kBound) part = fmaxf(part, x[e]);
-              if constexpr (kMasks) bits |= (x[e] > 0.f ? 1u : 0u) << e;
               x[e] *= sc;
             }
             if constexpr (kMasks) {
-            if (j < 32) mwa |= bits << j;
-            else mwb |= bits << (j - 32);
-          }
-            put8<F16>(smem, row, cb + j, x);
+              const uint32_t bits = put8m<F16>(smem, row, cb + j, x);
+              if (j < 32) mwa |= bits << j;
+              else mwb |= bits << (j - 32);
+            } else {
+              put8<F16>(smem, row, cb + j, x);
+            }
           }
           put_mask(md, 0, nh, mwa, mwb);
         }
@@ -640,11 +640,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                   for (int e = 0; e < 8; ++e) {
                     const float y = act(v[g8 * 8 + e], bb[e]);
                     if constexpr (kBound) part = fmaxf(part, y);
-                    if constexpr (kMasks) bits |= (y > 0.f ? 1u : 0u) << (g8 * 8 + e);
                     x[e] = y * sc;
                   }
                   uint32_t hi[4], lo[4];
                   pack8<F16>(x, hi, lo);
+                  if constexpr (kMasks) bits |= nz_bits8(hi) << (g8 * 8);
 #pragma unroll
                   for (int i = 0; i < 4; ++i) {
                     r[g8 * 4 + i] = hi[i];
@@ -676,19 +676,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               for (int j = 0; j < 64; j += 8) {
                 float x[8];
                 h0x8_pt(qx, qy, qz, qs, half * 128 + sub * 64 + j, x);
-                uint32_t bits = 0;
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
                   if constexpr (kBound) part0 = fmaxf(part0, x[e]);
-                  if constexpr (kMasks) bits |= (x[e] > 0.f ? 1u : 0u) << e;
                   x[e] *= sc0;
-                }
-                if constexpr (kMasks) {
-                  if (j < 32) mw0a |= bits << j;
-                  else mw0b |= bits << (j - 32);
                 }
                 uint32_t hi[4], lo[4];
                 pack8<F16>(x, hi, lo);
+                if constexpr (kMasks) {
+                  const uint32_t bits = nz_bits8(hi);
+                  if (j < 32) mw0a |= bits << j;
+                  else mw0b |= bits << (j - 32);
+                }
                 tmem_st8(tq + sub * 64 + j, hi, lo);
               }
               put_mask(nx.md, 0, 0, mw0a, mw0b);
@@ -757,10 +756,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                   for (int e = 0; e < 8; ++e) {
                     const float y = act(v[g8 * 8 + e], bb[e]);
                     if constexpr (kBound) part = fmaxf(part, y);
-                    if constexpr (kMasks) bits |= (y > 0.f ? 1u : 0u) << (g8 * 8 + e);
                     x[e] = y * sc;
                   }
-                  put8<F16>(smem, row, cb + c * 32 + g8 * 8, x);
+                  if constexpr (kMasks) bits |= put8m<F16>(smem, row, cb + c * 32 + g8 * 8, x) << (g8 * 8);
+                  else put8<F16>(smem, row, cb + c * 32 + g8 * 8, x);
                 }
               }
               if (c == 0) mwa = bits;
