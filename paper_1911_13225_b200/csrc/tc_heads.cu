@@ -209,7 +209,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
   } else {
     // ===== epilogue warps =====
-    const bool tl_on = P.timeline && blockIdx.x == 0 && threadIdx.x == 64;
+    // DIST_TC_TIMELINE bit 0 records the full kernel, bit 1 the backward-only one
+    const bool tl_on = (P.timeline & (BWD ? 2 : 1)) && blockIdx.x == 0 && threadIdx.x == 64;
     int tl_i = 0;
     const int q = warp & 3;
     const int sub = (warp - 2) >> 2;
@@ -254,6 +255,64 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int nxs;
     const uint32_t *nxm;
     fetch(cluster, nxp, nxs, nxm);
+    // BWD: the first backward operand is mask_G * w_out alone -- the row's seed
+    // scales the first backward epilogue instead (one fp32 rounding) -- so the
+    // next tile's operand is built during this tile's last GEMM and parked in
+    // TMEM columns 320 + 64 sub + 32 nh (free in this kernel: D 0..255, masks 256..319)
+    const float sc0 = BWD ? pow2_scale(P.nrm_b[G]) : 1.f;   // |w_out| <= nrm_b[G]
+    bool have_park = false;
+    // this thread's 64 fp16 operand columns of N half nh (32 packed words)
+    auto a0_words = [&](uint32_t wlo, uint32_t whi, int nh, uint32_t (&w)[32]) {
+      const int cb = nh * 256 + half * 128 + sub * 64;
+#pragma unroll
+      for (int j = 0; j < 64; j += 8) {
+        float wo[8];
+        ldg8(P.w_out + cb + j, wo);
+        const uint32_t wb = (j < 32 ? wlo : whi) >> (j & 31);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float x0 = ((wb >> (2 * i)) & 1u) ? wo[2 * i] * sc0 : 0.f;
+          const float x1 = ((wb >> (2 * i + 1)) & 1u) ? wo[2 * i + 1] * sc0 : 0.f;
+          const __half2 hv = __floats2half2_rn(x0, x1);
+          w[j / 2 + i] = *reinterpret_cast<const uint32_t *>(&hv);
+        }
+      }
+    };
+    auto a0_store = [&](int nh, const uint32_t (&w)[32]) {
+      const int cb = nh * 256 + half * 128 + sub * 64;
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        *reinterpret_cast<uint4 *>(smem + OFF_AHI + a_off(row, cb + 8 * j)) =
+            make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+    };
+    // masks of layers 0..G of a record into this thread's TMEM mask columns;
+    // returns mask G's words (lo, hi of N half 0, lo, hi of N half 1)
+    auto load_masks = [&](const uint32_t *mr, uint32_t (&mg)[4]) {
+#pragma unroll 1
+      for (int m0 = 0; m0 <= G; m0 += 4) {
+        uint2 a[4], b[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          a[i] = b[i] = make_uint2(0u, 0u);
+          if (mr && m0 + i <= G) {
+            a[i] = __ldg(reinterpret_cast<const uint2 *>(mr + (m0 + i) * 16 + mword));
+            b[i] = __ldg(reinterpret_cast<const uint2 *>(mr + (m0 + i) * 16 + 8 + mword));
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (m0 + i > G) break;
+          const uint32_t mk[4] = {a[i].x, a[i].y, b[i].x, b[i].y};
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(mask_addr(m0 + i)),
+                       "r"(mk[0]), "r"(mk[1]), "r"(mk[2]), "r"(mk[3])
+                       : "memory");
+          if (m0 + i == G) {
+            mg[0] = mk[0]; mg[1] = mk[1]; mg[2] = mk[2]; mg[3] = mk[3];
+          }
+        }
+      }
+      tmem_wait_st();
+    };
     for (int64_t t = cluster; t < ntiles; t += nclusters) {
       TL(1);
       const int64_t gi = t * (2 * ROWS) + (int64_t)rank * ROWS + row;
@@ -264,24 +323,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (row_thread) m.shape[row] = s;
       float head = 0.f;
       typename Gen::Prep sp{};
-      double fbwd = 0.0;   // BWD: the march's f of this row's sample
+      float gr_b = 0.f;    // BWD: this row's seed, applied in the first backward epilogue
       if constexpr (BWD) {
-        // masks of layers 0..G from the record into this thread's TMEM columns
+        if (have_park) {   // operand built during the previous tile's last GEMM
 #pragma unroll 1
-        for (int ml = 0; ml <= G; ++ml) {
-          uint32_t mk[4] = {0u, 0u, 0u, 0u};
-          if (mrec) {
-            const uint2 a = __ldg(reinterpret_cast<const uint2 *>(mrec + ml * 16 + mword));
-            const uint2 b = __ldg(reinterpret_cast<const uint2 *>(mrec + ml * 16 + 8 + mword));
-            mk[0] = a.x; mk[1] = a.y; mk[2] = b.x; mk[3] = b.y;
+          for (int nh = 0; nh < 2; ++nh) {
+            float v[32];
+            tmem_ld32(tq + 320 + sub * 64 + nh * 32, v);
+            uint32_t w[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(v[i]);
+            a0_store(nh, w);
           }
-          tmem_st4(mask_addr(ml), mk);
+        } else {
+          uint32_t mg[4];
+          load_masks(mrec, mg);
+#pragma unroll 1
+          for (int nh = 0; nh < 2; ++nh) {
+            uint32_t w[32];
+            a0_words(nh ? mg[2] : mg[0], nh ? mg[3] : mg[1], nh, w);
+            a0_store(nh, w);
+          }
         }
+        fence_proxy_async();
+        tc_fence_before();
+        epi_sync();
+        named_arrive(2, 2 * N_EPI_WARPS * 32);   // pairs with phase G-1's post (no A0 max exchange)
+        a_ready_all();
+        TL(6);
+        // the seed: its loads overlap the first backward GEMM
+        double go = 0.0;
         if (row_thread && gi < nrows && s >= 0) {
           sp = gen.prep(gi);
-          fbwd = gen.f_rec(gi);
+          const double fv = gen.f_rec(gi);
+          gen.store(gi, fv);
+          go = gen.apply(sp, fv) * head_dact(P.dv.final_act, fv);
         }
-        tc_fence_before();
+        if (row_thread) gout[row] = (float)go;
+        epi_sync();
+        TL(5);
+        gr_b = gout[row];
       } else {
       // ---- layer 0 (folded bias + p . W0p, fp32) + mask 0 ----
       {
@@ -437,17 +518,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       m.xch[half * 2 + sub][row] = head;
       epi_sync();
       }   // !BWD
+      float rinv = BWD ? 1.f / sc0 : 1.f;   // 1 / (this row's scale of the A operand now in smem)
+      float amax = BWD ? P.nrm_b[G] : 0.f;  // max |g| of this row's A operand (true units; BWD: before the seed)
+      if constexpr (!BWD) {
       // ---- seed, d loss / d h_G ----
       double go = 0.0;
       if (row_thread) {
-        double fv;
-        if constexpr (BWD) {
-          fv = fbwd;
-        } else {
-          const double sum = (double)m.xch[0][row] + (double)m.xch[1][row] +
-                             (double)m.xch[2][row] + (double)m.xch[3][row] + P.dv.b_out;
-          fv = head_act(P.dv.final_act, sum);
-        }
+        const double sum = (double)m.xch[0][row] + (double)m.xch[1][row] +
+                           (double)m.xch[2][row] + (double)m.xch[3][row] + P.dv.b_out;
+        const double fv = head_act(P.dv.final_act, sum);
         if (gi < nrows && s >= 0) {
           gen.store(gi, fv);
           const double sd = gen.apply(sp, fv);
@@ -457,8 +536,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       if (row_thread) gout[row] = (float)go;   // gout does not alias m.xch: no barrier before
       epi_sync();
       TL(5);
-      float rinv;   // 1 / (this row's scale of the A operand now in smem)
-      float amax;   // max |g| of this row's A operand (true units)
       {
         // one pass: the scale comes from the bound |gout| * max|w_out|; the true
         // row max of what is written feeds the first backward phase's bound
@@ -492,19 +569,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       named_arrive(2, 2 * N_EPI_WARPS * 32);   // this read happens before phase G-1 posts its maxima
       a_ready_all();
       TL(6);
+      }   // !BWD
       // ---- backward through GEMM layers G-1 .. 0 ----
       for (int gl = G - 1; gl >= 0; --gl, ++phase) {
         if (gl == 0) fetch(t + nclusters, nxp, nxs, nxm);
         uint32_t mk[4];
         tmem_ld4(mask_addr(gl), mk);   // written in the forward, readable now
+        // BWD: the first backward GEMM ran on mask_G * w_out; the seed enters here
+        const float gfac = (BWD && gl == G - 1) ? gr_b : 1.f;
+        if constexpr (BWD) {
+          if (gl == 0) {
+            // this tile's masks are in mk / done: the next tile's go to TMEM and
+            // its first operand is parked while the last GEMM runs
+            have_park = false;
+            if (t + nclusters < ntiles) {
+              uint32_t mg[4];
+              load_masks(nxm, mg);
+#pragma unroll 1
+              for (int nh = 0; nh < 2; ++nh) {
+                uint32_t w[32];
+                a0_words(nh ? mg[2] : mg[0], nh ? mg[3] : mg[1], nh, w);
+                tmem_st32(tq + 320 + sub * 64 + nh * 32, w);
+              }
+              tmem_wait_st();
+              have_park = true;
+            }
+          }
+        }
         // D = (g / rinv) (W / winv_b): true dgrad = D * unscale
-        const float unscale = rinv * P.winv_b[gl];
+        const float unscale = rinv * P.winv_b[gl] * gfac;
         if (gl > 0) {
           // One pass: the scale comes from a rigorous bound, |g_next| <= amax *
           // nrm_b[gl], so the fp16 operand cannot overflow; the true row max
           // of what is written becomes the next phase's amax.
-          const float sc = pow2_scale(amax * P.nrm_b[gl]);
-          const float f = unscale * sc;   // exact: powers of two
+          const float sc = pow2_scale(amax * fabsf(gfac) * P.nrm_b[gl]);
+          const float f = unscale * sc;   // exact (powers of two) except the BWD seed factor
           rinv = 1.f / sc;
           float part = 0.f;
           // 8 masked, scaled values of chunk (nh, c) -> 4 packed fp16 words

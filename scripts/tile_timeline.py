@@ -5,7 +5,8 @@ With DIST_TC_TIMELINE=1 the first epilogue thread of CTA 0 appends
 (csrc/tc_core.cuh DIST_TL_MARK); this script runs
   * k_tc_mlp on a 1M-point evaluation (same tile loop as a march step) and
   * k_tc_heads in one C3 latent-optimisation iterate (8 views x 512^2),
-and prints the phase durations of two tiles of each.
+and prints the phase durations of two tiles of each (the head kernel with
+and without the ReLU-mask record: DIST_TC_TIMELINE=1 / 2 select which).
 
   python scripts/tile_timeline.py
 """
@@ -59,11 +60,15 @@ def main():
     views = ring_views(8, 512)
     cfg = st.TraceConfig(k_samples=3)
     obs = render_depth_observations(field, target_code(1), views, cfg)
-    opt = st.LatentOptimizer(field, views, {"depth": obs}, np.zeros((1, 256)), cfg, max_iters=4)
-    opt.step()
-    opt.step()
-    torch.cuda.synchronize()
-    show(lib.dist_debug_heads_timeline, HEADS, "k_tc_heads")
+    for env, label, rm in (("1", "k_tc_heads (full: taped forward + backward)", False),
+                           ("2", "k_tc_heads<BWD> (ReLU-mask record: backward only)", True)):
+        os.environ["DIST_TC_TIMELINE"] = env
+        opt = st.LatentOptimizer(field, views, {"depth": obs}, np.zeros((1, 256)), cfg, max_iters=4,
+                                 relu_masks=rm)
+        opt.step()
+        opt.step()
+        torch.cuda.synchronize()
+        show(lib.dist_debug_heads_timeline, HEADS, label)
 
 
 if __name__ == "__main__":
