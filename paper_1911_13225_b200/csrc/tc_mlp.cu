@@ -136,9 +136,13 @@ struct MarchRows {
   }
 };
 
+// march steps that also write the ReLU-mask record (a separate instantiation,
+// so traces without the record pay nothing for it)
+struct MarchRowsM : MarchRows {};
+
 template <class Rows>
 __device__ __forceinline__ int load_row(const Rows &r, const Misc &m, int64_t i, double p[3], int &s) {
-  if constexpr (std::is_same<Rows, MarchRows>::value) return r.load_m(m, i, p, s);
+  if constexpr (std::is_base_of<MarchRows, Rows>::value) return r.load_m(m, i, p, s);
   else return r.load(i, p, s);
 }
 
@@ -340,7 +344,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     };
     // ReLU masks (march with a mask record): this thread's 2 x 64 columns of a
     // layer are words 8 nh + 4 half + 2 sub + {0, 1} of the layer's 16
-    constexpr bool kMasks = std::is_same<Rows, MarchRows>::value && !PAIR;
+    constexpr bool kMasks = std::is_same<Rows, MarchRowsM>::value && !PAIR;
     const int mword = 4 * half + 2 * sub;
     auto put_mask = [&](uint32_t *md, int ml, int nh, uint32_t w0, uint32_t w1) {
       if constexpr (kMasks) {
@@ -1145,8 +1149,10 @@ int tc_run_steps(const DecView &dv, const double *c0, const double *cskip, int S
                  int slots, int64_t *live, int64_t *stats, cudaStream_t st) {
   (void)cskip;
   tc::MarchRows rows{cams, ls, ctl, l0, l1, a, live, stats};
+  tc::MarchRowsM rows_m{rows};
   for (int s = 0; s < slots; ++s) {
-    int rc = launch_tc(dv, c0, S, rows, ceil_div(ls.n, 128), st);
+    int rc = ls.masks ? launch_tc(dv, c0, S, rows_m, ceil_div(ls.n, 128), st)
+                      : launch_tc(dv, c0, S, rows, ceil_div(ls.n, 128), st);
     if (rc) return rc;
   }
   return DIST_OK;
