@@ -157,7 +157,8 @@ def _config(args):
                         f"K=3, alpha 1.5, coarse 4, 100 steps",
             "views_per_gpu": VIEWS_PER_RANK, "resolution": RES, "precision": args.precision,
             "parallelism": f"views sharded over {args.gpus} GPU(s) (ring interleaved), latent all-reduce",
-            "l2": "working set > L2 (ray state ~320 MB per step)"}
+            "l2": "working set > L2 (ray state ~320 MB per step)",
+            "relu_mask_record": (not getattr(args, "no_relu_masks", False)) and args.precision in ("bf16x3", "fp16x3")}
 
 
 def main():
@@ -332,6 +333,7 @@ def main():
                      "objective_ms_per_step": obj_ms,
                      "head_samples_per_step": samples,
                      "objective_achieved_tflops": samples * (F_Q + F_B) / (obj_ms * 1e-3) / 1e12,
+                     "objective_achieved_note": "algorithmic: the reference's taped forward + dgrad per seeded sample (F_Q + F_B); the forward of samples the march itself queried is not recomputed (ReLU-mask record), so this exceeds the executed rate",
                      "objective_note": "heads + seeds + fused tcgen05 backward + reductions "
                                        "(k_tc_heads dominates; its ncu capture is in profiles/)"},
     }
