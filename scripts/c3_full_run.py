@@ -24,13 +24,14 @@ import paper_1911_13225_b200 as st  # noqa: E402
 from paper_1911_13225_b200.workloads import render_depth_observations, ring_views, target_code  # noqa: E402
 
 
-def run(mode: str, iters: int):
+def run(mode: str, iters: int, relu_masks="auto"):
     field = st.NeuralField.geometric(256, (512,) * 8, 0, precision=mode)
     views = ring_views(8, 512)
     cfg = st.TraceConfig(k_samples=3)
     z_true = target_code(1)
     obs = render_depth_observations(field, z_true, views, cfg)
-    opt = st.LatentOptimizer(field, views, {"depth": obs}, np.zeros((1, 256)), cfg, max_iters=iters)
+    opt = st.LatentOptimizer(field, views, {"depth": obs}, np.zeros((1, 256)), cfg, max_iters=iters,
+                             relu_masks=relu_masks)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -41,7 +42,8 @@ def run(mode: str, iters: int):
     losses = opt.losses()[:, 0]
     z = opt.code.cpu().numpy()[0]
     zb = opt.best_code.cpu().numpy()[0]
-    return {"mode": mode, "iters": iters, "ms_per_iter": e0.elapsed_time(e1) / iters,
+    return {"mode": mode, "relu_mask_record": opt.relu_masks, "iters": iters,
+            "ms_per_iter": e0.elapsed_time(e1) / iters,
             "loss_first": float(losses[0]), "loss_last": float(losses[-1]),
             "loss_every_10": [float(x) for x in losses[::10]],
             "best_iter": int(opt.best_iter[0].item()), "best_loss": float(opt.best_loss[0].item()),
@@ -55,12 +57,18 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=200)
     ap.add_argument("--modes", default="fp16x3,bf16x3")
+    ap.add_argument("--compare-record", action="store_true",
+                    help="run the first mode with and without the ReLU-mask record")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     out = {}
-    for mode in args.modes.split(","):
-        out[mode] = run(mode, args.iters)
-        print(json.dumps(out[mode]), flush=True)
+    runs = [(m, "auto") for m in args.modes.split(",")]
+    if args.compare_record:
+        runs = [(runs[0][0], True), (runs[0][0], False)]
+    for mode, rm in runs:
+        key = f"{mode}/{rm}"
+        out[key] = run(mode, args.iters, rm)
+        print(json.dumps(out[key]), flush=True)
     if len(out) == 2:
         a, b = (np.asarray(v["loss_every_10"]) for v in out.values())
         print(json.dumps({"max_rel_loss_curve_difference": float(np.max(np.abs(a - b) / np.abs(a)))}))
