@@ -124,3 +124,34 @@ def test_mask_record_c3_scale_gradient(st):
     assert abs(out[True][0] - out[False][0]) < 1e-4 * abs(out[False][0])
     gr = out[False][1]
     assert np.linalg.norm(out[True][1] - gr) / np.linalg.norm(gr) < 5e-4
+
+
+@pytest.mark.parametrize("prec", ["fp16x3", "bf16x3"])
+def test_mask_record_silhouette_and_shapes(st, prec):
+    """Silhouette seeds (slot 0 of every recorded ray, escaped rays included)
+    and two shapes in one optimiser: the record changes nothing beyond the
+    split arithmetic's noise, per shape."""
+    from paper_1911_13225_b200.shading import device_maps
+    from paper_1911_13225_b200.workloads import ring_views
+    net = st.NeuralField.geometric(256, (512,) * 8, 0, precision=prec)
+    views = ring_views(4, 128)
+    cfg = st.TraceConfig(k_samples=3)
+    rng = np.random.default_rng(11)
+    z_true = rng.normal(0, 0.1, (2, 256))
+    sov = [0, 1, 0, 1]
+    dt = st.trace_views(net, z_true, views, cfg, shape_of_view=sov)
+    status = dt.status.cpu().numpy().reshape(4, 128, 128)
+    depth, _, _ = device_maps(dt, True, False, False)
+    obs = {"silhouette": (status == 1).astype(np.float64), "depth": depth}
+    z0 = rng.normal(0, 0.05, (2, 256))
+    out = {}
+    for rm in (False, True):
+        opt = st.LatentOptimizer(net, views, obs, z0, cfg, shape_of_view=sov, relu_masks=rm)
+        opt.objective()
+        out[rm] = (opt.shape_terms[:, 0].cpu().numpy(), opt.grad.cpu().numpy(),
+                   opt.head_counts.cpu().numpy().tolist())
+    assert out[True][2] == out[False][2]
+    np.testing.assert_allclose(out[True][0], out[False][0], rtol=1e-4)
+    for s in range(2):
+        gr = out[False][1][s]
+        assert np.linalg.norm(out[True][1][s] - gr) / np.linalg.norm(gr) < 1e-3
