@@ -82,7 +82,8 @@ typedef struct dist_trace_config {
  * as it queries, so that dist_objective runs only the backward sweep for
  * them instead of re-evaluating the taped forward at the frozen points
  * (shading.py:185-206 recomputes exactly the values the march computed).
- *   relu_masks  [n][K+1][n_layers-1][16] uint32 (512 bits per layer of 512)
+ *   relu_masks  [n][K+1][n_layers-1][16] uint32 (512 bits per layer of 512,
+ *               word order internal to the library)
  *   topk_slot   [n][K+1] uint8: physical mask slot of logical record k
  *               (bit 7 set when this ray's own query wrote it), slot K spare. */
 typedef struct dist_ray_state {

@@ -239,8 +239,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     float *gout = reinterpret_cast<float *>(&m.ray[0]);
     // the next tile's sample point is fetched during the current tile's last
     // backward GEMM (a dependent chain of global loads)
-    // backward-only rows: this thread's words of each layer's mask record
-    const int mword = 4 * half + 2 * sub;
+    // backward-only rows: this thread's 4 words of each layer's mask record
+    // (tc_mlp.cu put_mask: words 4 q4 .. 4 q4 + 3, q4 = 2 half + sub)
+    const int mq = 4 * (2 * half + sub);
     auto fetch = [&](int64_t tt, double (&q)[3], int &ss, const uint32_t *&mr) {
       const int64_t g2 = tt * (2 * ROWS) + (int64_t)rank * ROWS + row;
       q[0] = q[1] = q[2] = 0.0;
@@ -290,19 +291,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     auto load_masks = [&](const uint32_t *mr, uint32_t (&mg)[4]) {
 #pragma unroll 1
       for (int m0 = 0; m0 <= G; m0 += 4) {
-        uint2 a[4], b[4];
+        uint4 a[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          a[i] = b[i] = make_uint2(0u, 0u);
-          if (mr && m0 + i <= G) {
-            a[i] = __ldg(reinterpret_cast<const uint2 *>(mr + (m0 + i) * 16 + mword));
-            b[i] = __ldg(reinterpret_cast<const uint2 *>(mr + (m0 + i) * 16 + 8 + mword));
-          }
+          a[i] = make_uint4(0u, 0u, 0u, 0u);
+          if (mr && m0 + i <= G) a[i] = __ldg(reinterpret_cast<const uint4 *>(mr + (m0 + i) * 16 + mq));
         }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           if (m0 + i > G) break;
-          const uint32_t mk[4] = {a[i].x, a[i].y, b[i].x, b[i].y};
+          const uint32_t mk[4] = {a[i].x, a[i].y, a[i].z, a[i].w};
           asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(mask_addr(m0 + i)),
                        "r"(mk[0]), "r"(mk[1]), "r"(mk[2]), "r"(mk[3])
                        : "memory");

@@ -60,7 +60,8 @@ struct Params {
   int acc_mode;           // 0: one accumulator; 1: two (even/odd K blocks); 2: hi*hi | corrections;
                           // 3 (default): as 2, stage-grouped; 4 (experiment): single pass, hi*hi only
   int timeline;           // DIST_TC_TIMELINE: phase marks of CTA 0 (debug)
-  int debug;              // timing experiments: 1 = no epilogue math, 2 = no MMAs (results invalid)
+  int debug;              // timing experiments: 1 = no epilogue math, 2 = no MMAs, 3 = no mask-record
+                          // stores (results invalid)
 };
 
 // ---------------------------------------------------------------------------
@@ -345,12 +346,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     // ReLU masks (march with a mask record): this thread's 2 x 64 columns of a
     // layer are words 8 nh + 4 half + 2 sub + {0, 1} of the layer's 16
     constexpr bool kMasks = std::is_same<Rows, MarchRowsM>::value && !PAIR;
-    const int mword = 4 * half + 2 * sub;
-    auto put_mask = [&](uint32_t *md, int ml, int nh, uint32_t w0, uint32_t w1) {
+    // Record layout per layer (16 words): thread quarter q4 = 2 half + sub owns
+    // words 4 q4 .. 4 q4 + 3 = (nh 0: cols +0..31, +32..63; nh 1: the same),
+    // columns nh 256 + 64 q4 + 32 c + bit -- one 16-byte store per layer
+    const int mq = 4 * (2 * half + sub);
+    auto put_mask = [&](uint32_t *md, int ml, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3) {
       if constexpr (kMasks) {
-        if (md) *reinterpret_cast<uint2 *>(md + ml * 16 + nh * 8 + mword) = make_uint2(w0, w1);
+        if (md && P.debug != 3) *reinterpret_cast<uint4 *>(md + ml * 16 + mq) = make_uint4(w0, w1, w2, w3);
       }
     };
+    uint32_t me0 = 0u, me1 = 0u;   // this layer's nh = 0 mask words until its nh = 1 half
+    uint32_t ms0 = 0u, ms1 = 0u;   // the stashed next tile's layer-0 nh = 0 mask words
     auto fetch = [&](int64_t t, RowIn &r) {
       r.gi = t * (2 * ROWS) + (int64_t)rank * ROWS + row;
       r.p[0] = r.p[1] = r.p[2] = 0.0;
@@ -520,7 +526,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             put8<F16>(smem, row, cb + j, x);
           }
         }
-        put_mask(md, 0, 1, mwa, mwb);
+        put_mask(md, 0, ms0, ms1, mwa, mwb);
         if constexpr (kBound) xch_post(part);
         fence_proxy_async();
         epi_sync();
@@ -569,7 +575,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               put8<F16>(smem, row, cb + j, x);
             }
           }
-          put_mask(md, 0, nh, mwa, mwb);
+          if (nh == 0) {
+            me0 = mwa;
+            me1 = mwb;
+          } else {
+            put_mask(md, 0, me0, me1, mwa, mwb);
+          }
         }
         if constexpr (kBound) xch_post(part);
       }
@@ -660,7 +671,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               if (c == 0) mwa = bits;
               else mwb = bits;
             }
-            put_mask(md, l + 1, 0, mwa, mwb);
+            me0 = mwa;
+            me1 = mwb;
             if (last && t + nclusters < ntiles) {
               // the next tile's layer 0, columns 0..255, into the TMEM columns
               // the head just consumed (nx: its rows, fetched above)
@@ -694,7 +706,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 }
                 tmem_st8(tq + sub * 64 + j, hi, lo);
               }
-              put_mask(nx.md, 0, 0, mw0a, mw0b);
+              ms0 = mw0a;
+              ms1 = mw0b;
               have_stash = true;
               stash_part = part0;
               stash_sc = sc0;
@@ -769,7 +782,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               if (c == 0) mwa = bits;
               else mwb = bits;
             }
-            put_mask(md, l + 1, 1, mwa, mwb);
+            put_mask(md, l + 1, me0, me1, mwa, mwb);
           }
           TL(14);
           if (!last) {

@@ -67,6 +67,13 @@ def test_recorded_masks_match_fp64_forward(st, prec):
     # the march's f of the record against fp64 at the same point
     np.testing.assert_allclose(tk_f[r_idx, k_idx], f64, atol=2e-5, rtol=0)
     words = rec[r_idx, slots[r_idx, k_idx] & 0x7F]                # [m, nm, 16]
+    # record word 4 q4 + 2 nh + c holds columns nh 256 + 64 q4 + 32 c + bit (tc_mlp.cu put_mask)
+    perm = np.empty(16, dtype=np.int64)
+    for q4 in range(4):
+        for nh in range(2):
+            for c in range(2):
+                perm[nh * 8 + 2 * q4 + c] = 4 * q4 + 2 * nh + c
+    words = np.ascontiguousarray(words[..., perm])
     bits = np.unpackbits(words.view(np.uint8), axis=-1, bitorder="little").reshape(len(r_idx), nm, 512)
     flips = 0
     for layer in range(nm):
