@@ -24,8 +24,9 @@ from .tracer import TraceConfig, relu_mask_bytes, trace_views
 # dist_objective_io.grad_mode (include/dist.h): the reference's frozen-sample
 # surrogate, and the implicit-gradient extensions
 GRAD_MODES = {"surrogate": 0, "implicit": 1, "implicit_unit": 2}
-# LatentOptimizer(relu_masks="auto") records the ReLU masks up to this size
-RELU_MASK_AUTO_BYTES = 16 << 30
+# LatentOptimizer(relu_masks="auto") records the ReLU masks when the record
+# takes at most this fraction of the free device memory
+RELU_MASK_AUTO_FRACTION = 0.35
 
 
 class OptimizationError(RuntimeError):
@@ -114,7 +115,7 @@ class LatentOptimizer:
 
     relu_masks: record the ReLU masks of the samples during the march so the
     objective runs only the backward sweep for them (tensor-core precisions;
-    "auto" = on when the record fits in RELU_MASK_AUTO_BYTES).
+    "auto" = on when the record fits in RELU_MASK_AUTO_FRACTION of free memory).
     """
 
     def __init__(self, field, views, observations: dict, code0, cfg: TraceConfig | None = None,
@@ -149,7 +150,8 @@ class LatentOptimizer:
         n = V * self.W * self.H
         if relu_masks == "auto":
             relu_masks = (field.precision in ("fp16x3", "bf16x3") and
-                          relu_mask_bytes(field, n, self.cfg.k_samples) <= RELU_MASK_AUTO_BYTES)
+                          relu_mask_bytes(field, n, self.cfg.k_samples)
+                          <= RELU_MASK_AUTO_FRACTION * torch.cuda.mem_get_info()[0])
         self.relu_masks = bool(relu_masks)
 
         def put(key, dtype):

@@ -82,7 +82,8 @@ def _latent_opt(name, prec, views, codes0, targets, shape_of_view, cfg, sil=Fals
     ms, _ = timed(opt.step, 2)
     rays = len(views) * views[0][0].width * views[0][0].height
     q = int(opt.last_trace.stats_dev[0].item())
-    return {"config": name, "precision": prec, "ms_per_iter": ms, "rays_per_s": rays / ms * 1e3,
+    return {"config": name, "precision": prec, "relu_mask_record": opt.relu_masks,
+            "ms_per_iter": ms, "rays_per_s": rays / ms * 1e3,
             "rays_per_iter": rays, "trace_queries": q,
             "peak_mem_gb": torch.cuda.max_memory_allocated() / 2**30}
 
