@@ -352,7 +352,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int mq = 4 * (2 * half + sub);
     auto put_mask = [&](uint32_t *md, int ml, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3) {
       if constexpr (kMasks) {
-        if (md && P.debug != 3) *reinterpret_cast<uint4 *>(md + ml * 16 + mq) = make_uint4(w0, w1, w2, w3);
+        // streaming store: written once here, read once by the objective
+        if (md && P.debug != 3) __stcs(reinterpret_cast<uint4 *>(md + ml * 16 + mq), make_uint4(w0, w1, w2, w3));
       }
     };
     uint32_t me0 = 0u, me1 = 0u;   // this layer's nh = 0 mask words until its nh = 1 half
