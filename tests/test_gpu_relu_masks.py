@@ -162,3 +162,32 @@ def test_mask_record_silhouette_and_shapes(st, prec):
     for s in range(2):
         gr = out[False][1][s]
         assert np.linalg.norm(out[True][1][s] - gr) / np.linalg.norm(gr) < 1e-3
+
+
+@pytest.mark.parametrize("cfg_kw", [
+    {"k_samples": 3, "use_dynamic_mask": False},   # every ray queried every step
+    {"k_samples": 1, "coarse_start_scale": 1},     # one level: the record starts at init
+    {"k_samples": 2, "max_steps": 4},              # the budget ends inside the coarse levels
+])
+def test_mask_record_trace_variants(st, cfg_kw):
+    """Configurations that change which queries reach the record: the
+    objective with the record equals the re-evaluated one."""
+    from paper_1911_13225_b200.workloads import ring_views
+    from paper_1911_13225_b200.shading import device_maps
+    net = st.NeuralField.geometric(256, (512,) * 8, 0, precision="fp16x3")
+    views = ring_views(2, 128)
+    cfg = st.TraceConfig(**cfg_kw)
+    z_true = np.random.default_rng(3).normal(0, 0.1, 256)
+    depth, _, _ = device_maps(st.trace_views(net, z_true, views, cfg), True, False, False)
+    z0 = np.random.default_rng(4).normal(0, 0.05, (1, 256))
+    out = {}
+    for rm in (False, True):
+        opt = st.LatentOptimizer(net, views, {"depth": depth}, z0, cfg, relu_masks=rm)
+        opt.objective()
+        out[rm] = (opt.shape_terms[0, 0].item(), opt.grad[0].cpu().numpy(),
+                   opt.head_counts.cpu().numpy().tolist())
+    assert out[True][2] == out[False][2]
+    assert abs(out[True][0] - out[False][0]) <= 1e-4 * abs(out[False][0]) + 1e-12
+    gr = out[False][1]
+    if np.linalg.norm(gr) > 0:
+        assert np.linalg.norm(out[True][1] - gr) / np.linalg.norm(gr) < 1e-3
