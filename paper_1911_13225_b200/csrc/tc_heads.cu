@@ -190,9 +190,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                   mma_2sm<false>(d, dal, dbh, 1u);
                 }
               } else {        // backward: fp16x2, g x (W_hi + W_lo)
+                // BWD: a tile's first operand is built in A_lo (parked there
+                // during the previous tile's last GEMM); every later one in A_hi
+                const uint32_t ab = (BWD && ph == G) ? a_lo : a_hi;
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
-                  const uint64_t dah = sdesc(a_hi + kc * (ROWS * 128) + q * 32);
+                  const uint64_t dah = sdesc(ab + kc * (ROWS * 128) + q * 32);
                   mma_2sm<true>(d, dah, sdesc(b_hi + q * 32), (kc | q) ? 1u : 0u);
                   mma_2sm<true>(d, dah, sdesc(b_lo + q * 32), 1u);
                 }
@@ -258,8 +261,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     fetch(cluster, nxp, nxs, nxm);
     // BWD: the first backward operand is mask_G * w_out alone -- the row's seed
     // scales the first backward epilogue instead (one fp32 rounding) -- so the
-    // next tile's operand is built during this tile's last GEMM and parked in
-    // TMEM columns 320 + 64 sub + 32 nh (free in this kernel: D 0..255, masks 256..319)
+    // next tile's operand is built during this tile's last GEMM, into A_lo
+    // (unused by backward GEMMs), which that tile's first GEMM reads
     const float sc0 = BWD ? pow2_scale(P.nrm_b[G]) : 1.f;   // |w_out| <= nrm_b[G]
     bool have_park = false;
     // this thread's 64 fp16 operand columns of N half nh (32 packed words)
@@ -279,11 +282,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
       }
     };
-    auto a0_store = [&](int nh, const uint32_t (&w)[32]) {
+    auto a0_store = [&](int nh, const uint32_t (&w)[32]) {   // -> A_lo (the BWD first operand)
       const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        *reinterpret_cast<uint4 *>(smem + OFF_AHI + a_off(row, cb + 8 * j)) =
+        *reinterpret_cast<uint4 *>(smem + OFF_ALO + a_off(row, cb + 8 * j)) =
             make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
     };
     // masks of layers 0..G of a record into this thread's TMEM mask columns;
@@ -323,17 +326,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       typename Gen::Prep sp{};
       float gr_b = 0.f;    // BWD: this row's seed, applied in the first backward epilogue
       if constexpr (BWD) {
-        if (have_park) {   // operand built during the previous tile's last GEMM
-#pragma unroll 1
-          for (int nh = 0; nh < 2; ++nh) {
-            float v[32];
-            tmem_ld32(tq + 320 + sub * 64 + nh * 32, v);
-            uint32_t w[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) w[i] = __float_as_uint(v[i]);
-            a0_store(nh, w);
-          }
-        } else {
+        if (!have_park) {   // else: built in A_lo during the previous tile's last GEMM
           uint32_t mg[4];
           load_masks(mrec, mg);
 #pragma unroll 1
@@ -587,9 +580,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               for (int nh = 0; nh < 2; ++nh) {
                 uint32_t w[32];
                 a0_words(nh ? mg[2] : mg[0], nh ? mg[3] : mg[1], nh, w);
-                tmem_st32(tq + 320 + sub * 64 + nh * 32, w);
+                a0_store(nh, w);
               }
-              tmem_wait_st();
               have_park = true;
             }
           }

@@ -191,3 +191,27 @@ def test_mask_record_trace_variants(st, cfg_kw):
     gr = out[False][1]
     if np.linalg.norm(gr) > 0:
         assert np.linalg.norm(out[True][1] - gr) / np.linalg.norm(gr) < 1e-3
+
+
+def test_mask_record_deep_decoder_many_tiles(st):
+    """A 12 x 512 decoder (12 mask layers) with enough samples for several
+    backward-only tiles per CTA pair, so the next tile's masks and first
+    operand are staged while the current tile's last GEMM runs."""
+    from paper_1911_13225_b200.shading import device_maps
+    from paper_1911_13225_b200.workloads import ring_views
+    net = st.NeuralField.geometric(256, (512,) * 12, 0, precision="fp16x3")
+    views = ring_views(4, 128)
+    cfg = st.TraceConfig(k_samples=3)
+    z_true = np.random.default_rng(3).normal(0, 0.1, 256)
+    depth, _, _ = device_maps(st.trace_views(net, z_true, views, cfg), True, False, False)
+    z0 = np.random.default_rng(4).normal(0, 0.05, (1, 256))
+    out = {}
+    for rm in (False, True):
+        opt = st.LatentOptimizer(net, views, {"depth": depth}, z0, cfg, relu_masks=rm)
+        opt.objective()
+        out[rm] = (opt.shape_terms[0, 0].item(), opt.grad[0].cpu().numpy(),
+                   opt.head_counts.cpu().numpy().tolist())
+    assert out[True][2][1] > 4 * 148 * 64    # > 4 tiles per CTA pair on a B200
+    assert abs(out[True][0] - out[False][0]) <= 1e-4 * abs(out[False][0])
+    gr = out[False][1]
+    assert np.linalg.norm(out[True][1] - gr) / np.linalg.norm(gr) < 1e-3
