@@ -60,12 +60,26 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled during the timed region.
+
+    Started before the warm-up so nvidia-smi's own start-up (NVML init) does
+    not fall inside the timed region; mark() at the region's start drops the
+    rows written before it."""
 
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.proc = None
         self.path = f"/tmp/bench_clocks_{os.getpid()}.csv"
+        self.skip = 0
+
+    def _rows(self):
+        try:
+            return [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
+        except Exception:
+            return []
+
+    def mark(self):
+        self.skip = len(self._rows())
 
     def __enter__(self):
         try:
@@ -88,10 +102,8 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        try:
-            rows = [r.split(",") for r in open(self.path).read().strip().splitlines() if r.strip()]
-        except Exception:
-            rows = []
+        rows = self._rows()
+        rows = rows[self.skip:] if len(rows) > self.skip else rows
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         sm = [float(r[0]) for r in rows]
@@ -215,6 +227,7 @@ def main():
             dist.all_reduce(shape_terms)
 
     stream = torch.cuda.current_stream()
+    clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
         opt.step(allreduce)
     torch.cuda.synchronize()
@@ -227,7 +240,8 @@ def main():
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
+    clk.mark()
+    try:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -251,6 +265,8 @@ def main():
             opt._adam()
         e1.record(stream)
         torch.cuda.synchronize()
+    finally:
+        clk.__exit__()
     launches = _lib.lib().dist_launch_count() - n0
     ms = e0.elapsed_time(e1) / args.steps
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
