@@ -28,8 +28,32 @@ int cuda_fail(cudaError_t e, const char *where) {
 void count_launch(int n) { g_launches += n; }
 
 // ---------------------------------------------------------------------------
+// acc + sum_{k<n} a[k*as] * b[k*bs] as one fma chain in ascending k (the same
+// rounding as the plain loop), with the operands of U steps loaded ahead so
+// the chain waits on one round of L2/HBM latency per U steps, not per step.
+template <int U>
+__device__ __forceinline__ double dot_ordered(const double *__restrict__ a, int64_t as,
+                                              const double *__restrict__ b, int64_t bs, int n,
+                                              double acc) {
+  int k = 0;
+  for (; k + U <= n; k += U) {
+    double x[U], y[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      x[u] = __ldg(a + (int64_t)(k + u) * as);
+      y[u] = __ldg(b + (int64_t)(k + u) * bs);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc = fma(x[u], y[u], acc);
+  }
+  for (; k < n; ++k) acc = fma(__ldg(a + (int64_t)k * as), __ldg(b + (int64_t)k * bs), acc);
+  return acc;
+}
+
 // per-shape folded biases: c0[s][j] = b0[j] + sum_k z[s][k] W0z[k][j]  (fp64)
 // and the skip layer's code part cskip[s][j] = sum_k z[s][k] Wsz[k][j].
+// One thread per output (64-thread blocks: S x 512 outputs spread over many
+// SMs); each output is a latency-bound 256-step chain, so loads run 16 ahead.
 __global__ void k_code_bias(DecView dv, const double *__restrict__ codes, int S,
                             double *__restrict__ c0, double *__restrict__ cskip) {
   const int n0 = dv.np[0];
@@ -38,8 +62,7 @@ __global__ void k_code_bias(DecView dv, const double *__restrict__ codes, int S,
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
        idx += gridDim.x * blockDim.x) {
     const int s = idx / n0, j = idx % n0;
-    double v = dv.b0[j];
-    for (int k = 0; k < D; ++k) v = fma(codes[(size_t)s * D + k], dv.W0z[(size_t)k * n0 + j], v);
+    const double v = dot_ordered<16>(codes + (size_t)s * D, 1, dv.W0z + j, n0, D, dv.b0[j]);
     c0[idx] = v;
     reinterpret_cast<float *>(c0 + total)[idx] = (float)v;   // fp32 copy (kernels.cuh c0_f32)
     // per-shape max |c0| (kernels.cuh c0_absmax): non-negative floats order as ints
@@ -51,9 +74,7 @@ __global__ void k_code_bias(DecView dv, const double *__restrict__ codes, int S,
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < tot2;
          idx += gridDim.x * blockDim.x) {
       const int s = idx / ns, j = idx % ns;
-      double v = 0.0;
-      for (int k = 0; k < D; ++k) v = fma(codes[(size_t)s * D + k], dv.Wsz[(size_t)k * ns + j], v);
-      cskip[idx] = v;
+      cskip[idx] = dot_ordered<16>(codes + (size_t)s * D, 1, dv.Wsz + j, ns, D, 0.0);
     }
   }
 }
@@ -64,35 +85,51 @@ int launch_code_bias(const DecView &dv, const double *codes, int S, double *c0, 
   const int n = S * dv.np[0];
   cudaError_t e = cudaMemsetAsync(const_cast<float *>(c0_absmax(c0, S, dv.np[0])), 0, sizeof(float) * S, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(c0 max)");
-  k_code_bias<<<(int)std::min<int64_t>(ceil_div(n, 256), 1024), 256, 0, st>>>(dv, codes, S, c0,
-                                                                              cskip);
+  const int nmax = std::max(n, S * std::max(dv.nskip, 0));
+  k_code_bias<<<(int)std::min<int64_t>(ceil_div(nmax, 64), 4096), 64, 0, st>>>(dv, codes, S, c0, cskip);
   DIST_CHECK_LAUNCH("k_code_bias");
   return DIST_OK;
 }
 
 // grad[s][k] = sum_j (sum_cta part0[cta][s][j]) W0z[k][j] + skip part.
-__global__ void k_reduce_code_grad(DecView dv, int S, int G, const double *__restrict__ part0,
-                                   const double *__restrict__ parts, double *__restrict__ colsum0,
-                                   double *__restrict__ colsums, double *__restrict__ grad) {
-  const int s = blockIdx.x;
+// Two kernels so both phases spread over many SMs; every sum keeps the
+// ascending order of the single-block version (bitwise the same results).
+__global__ void k_reduce_colsums(DecView dv, int S, int G, const double *__restrict__ part0,
+                                 const double *__restrict__ parts, double *__restrict__ colsum0,
+                                 double *__restrict__ colsums) {
+  const int n0 = dv.np[0], ns = dv.nskip;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_all = (int64_t)S * (n0 + ns);
+  if (t >= n_all) return;
+  constexpr int U = 16;
+  const bool main_part = t < (int64_t)S * n0;
+  const int64_t q = main_part ? t : t - (int64_t)S * n0;
+  const int w = main_part ? n0 : ns;
+  const int s = (int)(q / w), j = (int)(q - (int64_t)s * w);
+  const double *src = (main_part ? part0 : parts) + (size_t)s * w + j;
+  const int64_t stride = (int64_t)S * w;
+  double acc = 0.0;
+  int c = 0;
+  for (; c + U <= G; c += U) {
+    double x[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) x[u] = src[(c + u) * stride];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc += x[u];
+  }
+  for (; c < G; ++c) acc += src[c * stride];
+  (main_part ? colsum0 : colsums)[q] = acc;
+}
+
+__global__ void k_reduce_code_grad(DecView dv, int S, const double *__restrict__ colsum0,
+                                   const double *__restrict__ colsums, double *__restrict__ grad) {
   const int n0 = dv.np[0], ns = dv.nskip, D = dv.latent_dim;
-  for (int j = threadIdx.x; j < n0; j += blockDim.x) {
-    double acc = 0.0;
-    for (int c = 0; c < G; ++c) acc += part0[((size_t)c * S + s) * n0 + j];
-    colsum0[(size_t)s * n0 + j] = acc;
-  }
-  for (int j = threadIdx.x; j < ns; j += blockDim.x) {
-    double acc = 0.0;
-    for (int c = 0; c < G; ++c) acc += parts[((size_t)c * S + s) * ns + j];
-    colsums[(size_t)s * ns + j] = acc;
-  }
-  __syncthreads();
-  for (int k = threadIdx.x; k < D; k += blockDim.x) {
-    double acc = 0.0;
-    for (int j = 0; j < n0; ++j) acc = fma(colsum0[(size_t)s * n0 + j], dv.W0z[(size_t)k * n0 + j], acc);
-    for (int j = 0; j < ns; ++j) acc = fma(colsums[(size_t)s * ns + j], dv.Wsz[(size_t)k * ns + j], acc);
-    grad[(size_t)s * D + k] = acc;
-  }
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= S * D) return;
+  const int s = t / D, k = t - s * D;
+  double acc = dot_ordered<16>(colsum0 + (size_t)s * n0, 1, dv.W0z + (size_t)k * n0, 1, n0, 0.0);
+  if (ns > 0) acc = dot_ordered<16>(colsums + (size_t)s * ns, 1, dv.Wsz + (size_t)k * ns, 1, ns, acc);
+  grad[t] = acc;
 }
 
 int sm_count() {
@@ -139,7 +176,10 @@ int vjp_points(const DecView &dv, const double *c0, const double *cskip, const d
 int reduce_code_grad(const DecView &dv, int S, int G, const double *part0, const double *parts,
                      double *colsum0, double *colsums, double *grad, cudaStream_t st) {
   if (S <= 0 || dv.latent_dim == 0) return DIST_OK;
-  k_reduce_code_grad<<<S, 256, 0, st>>>(dv, S, G, part0, parts, colsum0, colsums, grad);
+  const int64_t nc = (int64_t)S * (dv.np[0] + std::max(dv.nskip, 0));
+  k_reduce_colsums<<<(int)ceil_div(nc, 64), 64, 0, st>>>(dv, S, G, part0, parts, colsum0, colsums);
+  DIST_CHECK_LAUNCH("k_reduce_colsums");
+  k_reduce_code_grad<<<(int)ceil_div((int64_t)S * dv.latent_dim, 64), 64, 0, st>>>(dv, S, colsum0, colsums, grad);
   DIST_CHECK_LAUNCH("k_reduce_code_grad");
   return DIST_OK;
 }

@@ -27,13 +27,17 @@
 
 namespace dist {
 
-__global__ void k_heads_index(HeadsDev h, int K, int V, int64_t WH) {
+// rec_rank[g] = index of recorded ray g in h.rec (written by the rec
+// compaction); every sample's ray is recorded (finite slot 0: topk_absf is
+// sorted ascending), so the lookup is one gather instead of a binary search.
+__global__ void k_heads_index(HeadsDev h, const int32_t *__restrict__ rec_rank, int K, int V,
+                              int64_t WH) {
   const int64_t nrec = h.counts[0], nsamp = h.counts[1];
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nsamp;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t flat = h.samp[i];
     const int64_t g = flat / K;
-    const int64_t r = lower_bound_i32(h.rec, nrec, g);
+    const int64_t r = rec_rank[g];
     h.samp_pix[i] = (int32_t)r;
     if (flat - g * K == 0) h.best[r] = (int32_t)i;
   }
@@ -239,6 +243,7 @@ struct ObjLayout {
   double *c0, *cs, *part0, *parts, *col0, *cols, *sil_seed, *gdotv, *probe_f, *loss_part;
   int32_t *npx, *bcount, *conv, *conv_count;
   int32_t *sel_own, *sel_oth, *sel_counts;   // samples with / without a ReLU-mask record
+  int32_t *rec_rank;                          // [n] index of a recorded ray in h.rec
   size_t bytes;
 };
 
@@ -249,6 +254,7 @@ static ObjLayout obj_layout(const DecView &dv, int V, int W, int H, int K, int S
   const int64_t n = (int64_t)V * W * H;
   const int s1 = std::max(S, 1);
   L.h.rec = cv.take<int32_t>(n);
+  L.rec_rank = cv.take<int32_t>(n);
   L.h.best = cv.take<int32_t>(n);
   L.h.samp = cv.take<int32_t>(n * K);
   L.h.samp_pix = cv.take<int32_t>(n * K);
@@ -318,7 +324,7 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
   const double *ta = st->topk_absf;
   const int Kc = K;
   int rc = compact([ta, Kc] __device__(int64_t g) { return (bool)isfinite(ta[g * Kc]); }, n, L.h.rec,
-                   L.h.counts + 0, L.bcount, sm);
+                   L.h.counts + 0, L.bcount, sm, L.rec_rank);
   if (rc) return rc;
   // Only samples that carry a seed enter the fused kernel: slot 0 of every
   // recorded ray when a silhouette term is present, and every sample of a
@@ -337,8 +343,8 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
       },
       n * K, L.h.samp, L.h.counts + 1, L.bcount, sm);
   if (rc) return rc;
-  const int gi = (int)std::min<int64_t>(ceil_div(n * K, 256), (int64_t)sm_count() * 8);
-  k_heads_index<<<std::max(gi, 1), 256, 0, sm>>>(L.h, K, V, WH);
+  const int gi = (int)std::min<int64_t>(ceil_div(n * K, 256), (int64_t)sm_count() * 16);
+  k_heads_index<<<std::max(gi, 1), 256, 0, sm>>>(L.h, L.rec_rank, K, V, WH);
   DIST_CHECK_LAUNCH("k_heads_index");
   // 2. per-view loss preparation
   k_view_prep<<<dim3(V, kPrepBlocks), 256, 0, sm>>>(cams, ls, K, cfg->epsilon, in, L.loss_part, L.sil_seed);
