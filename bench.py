@@ -274,6 +274,11 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
     trace_ms = float(np.mean([a.elapsed_time(b) for a, b in tr_ev]))
+    # per-step device time (trace start to the next trace start; the last to e1)
+    starts = [a for a, _ in tr_ev]
+    step_ms = [starts[i].elapsed_time(starts[i + 1]) for i in range(len(starts) - 1)]
+    step_ms.append(starts[-1].elapsed_time(e1))
+    lead_ms = e0.elapsed_time(starts[0])
     obj_ms = float(np.mean([a.elapsed_time(b) for a, b in obj_ev]))
     queries = int(q0.item()) / args.steps
     samples = int(s0.item()) / args.steps
@@ -347,6 +352,8 @@ def main():
                      "algorithmic_flop_per_query": F_Q, "queries_per_step": queries,
                      "trace_ms_per_step": trace_ms,
                      "objective_ms_per_step": obj_ms,
+                     "step_ms": [round(x, 2) for x in step_ms],
+                     "lead_ms": round(lead_ms, 3),
                      "head_samples_per_step": samples,
                      "objective_achieved_tflops": samples * (F_Q + F_B) / (obj_ms * 1e-3) / 1e12,
                      "objective_achieved_note": "algorithmic: the reference's taped forward + dgrad per seeded sample (F_Q + F_B); the forward of samples the march itself queried is not recomputed (ReLU-mask record), so this exceeds the executed rate",

@@ -189,7 +189,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cta_rank();
 
-  if (!R.begin(m)) return;  // uniform across the grid (all CTAs read the same controller)
+  // Programmatic dependent launch: the next step's grid may be scheduled as
+  // soon as every CTA of this one is resident (one wave, so its CTAs take SMs
+  // only as these exit); its barrier init and TMEM allocation run before
+  // griddepcontrol.wait, which returns once this grid has completed and its
+  // memory is visible.  Without the launch attribute both are no-ops.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   // single-pass (bf16, bound-scaled fp16) epilogues: early half + afree
   constexpr bool kAfree = !PAIR;
 
@@ -216,6 +221,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = m.tmem_base;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (!R.begin(m)) {  // uniform across the grid (all CTAs read the same controller)
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+    return;
+  }
 
   const int64_t nrows = R.rows(m);
   const int64_t ntiles = ceil_div(nrows, 2 * ROWS);
@@ -1122,7 +1136,22 @@ static int launch_tc_t(const DecView &dv, const double *c0, int S, const Rows &r
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
   if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc)");
   const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_bound, sm_count() / 2));
-  tc::k_tc_mlp<F16, Rows, PAIR><<<2 * pairs, tc::THREADS, tc::SMEM_BYTES, st>>>(map, P, rows);
+  static const bool pdl = [] {
+    const char *v = getenv("DIST_TC_PDL");
+    return !v || atoi(v) != 0;
+  }();
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3(2 * pairs);
+  lc.blockDim = dim3(tc::THREADS);
+  lc.dynamicSmemBytes = tc::SMEM_BYTES;
+  lc.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+  lc.attrs = attr;
+  lc.numAttrs = 1;
+  e = cudaLaunchKernelEx(&lc, tc::k_tc_mlp<F16, Rows, PAIR>, map, P, rows);
+  if (e != cudaSuccess) return cuda_fail(e, "k_tc_mlp launch");
   DIST_CHECK_LAUNCH("k_tc_mlp");
   return DIST_OK;
 }
