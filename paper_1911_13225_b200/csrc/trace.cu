@@ -97,6 +97,88 @@ __global__ void k_split(LevelState par, LevelState ch, int K, int32_t *__restric
   }
 }
 
+// The same split, one thread per PARENT: the parent's state is read once and
+// written to its 2 x 2 children with paired stores (children 2i, 2i+1 of a row
+// are adjacent, so every child array gets 2-element vector stores; a warp
+// writes whole 32 B sectors of each array).  Used when the child arrays are
+// aligned for those stores (run_trace checks) and K <= kSplitMaxK.
+constexpr int kSplitMaxK = 8;
+__global__ void k_split_quad(LevelState par, LevelState ch, int K, int32_t *__restrict__ list, Ctl *ctl) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t per_c = (int64_t)ch.lw * ch.lh, per_p = (int64_t)par.lw * par.lh;
+  const bool tkp4 = ch.tk_p && K == 3;   // one 8-byte store per child row
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < par.n; base += stride) {
+    const int64_t p = base + threadIdx.x;
+    bool live = false;
+    int64_t g0 = 0;
+    if (p < par.n) {
+      const int64_t v = p / per_p, pix = p - v * per_p;
+      const int j = (int)(pix / par.lw), i = (int)(pix - (int64_t)j * par.lw);
+      g0 = v * per_c + (int64_t)(2 * j) * ch.lw + 2 * i;
+      uint8_t s = par.status[p];
+      if (s == DIST_CONVERGED) s = DIST_MARCHING;
+      const double d = par.d[p], b = par.b[p];
+      const int32_t stp = par.steps[p];
+      double pd[kSplitMaxK], pf[kSplitMaxK], pa[kSplitMaxK];
+      for (int k = 0; k < K; ++k) {
+        pd[k] = par.tk_d[p * K + k];
+        pf[k] = par.tk_f[p * K + k];
+        pa[k] = par.tk_a[p * K + k];
+      }
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const int64_t g = g0 + (int64_t)r * ch.lw;
+        *reinterpret_cast<uchar2 *>(ch.status + g) = make_uchar2(s, s);
+        *reinterpret_cast<double2 *>(ch.d + g) = make_double2(d, d);
+        *reinterpret_cast<double2 *>(ch.b + g) = make_double2(b, b);
+        *reinterpret_cast<int2 *>(ch.steps + g) = make_int2(stp, stp);
+        // [child 2i: k = 0..K-1][child 2i+1: k = 0..K-1] = element e -> record e % K
+        double2 *od = reinterpret_cast<double2 *>(ch.tk_d + g * K);
+        double2 *of = reinterpret_cast<double2 *>(ch.tk_f + g * K);
+        double2 *oa = reinterpret_cast<double2 *>(ch.tk_a + g * K);
+        for (int e = 0; e < K; ++e) {
+          const int k0 = (2 * e) % K, k1 = (2 * e + 1) % K;
+          od[e] = make_double2(pd[k0], pd[k1]);
+          of[e] = make_double2(pf[k0], pf[k1]);
+          oa[e] = make_double2(pa[k0], pa[k1]);
+        }
+        // inherited records carry no masks of this ray (own bit clear)
+        if (tkp4) {
+          *reinterpret_cast<uint2 *>(ch.tk_p + g * 4) = make_uint2(0x03020100u, 0x03020100u);
+        } else if (ch.tk_p) {
+          for (int c = 0; c < 2; ++c)
+            for (int k = 0; k <= K; ++k) ch.tk_p[(g + c) * (K + 1) + k] = (uint8_t)k;
+        }
+      }
+      live = s == DIST_MARCHING;
+    }
+    // the four children join the live list together (its order is free: every
+    // row of a tile is evaluated independently)
+    const unsigned m = __ballot_sync(0xffffffffu, live);
+    if (m) {
+      const int lane = threadIdx.x & 31;
+      const int leader = __ffs(m) - 1;
+      int lb = 0;
+      if (lane == leader) lb = atomicAdd(&ctl->cnt[0], 4 * __popc(m));
+      lb = __shfl_sync(0xffffffffu, lb, leader);
+      if (live) {
+        int32_t *o = list + lb + 4 * __popc(m & ((1u << lane) - 1u));
+        o[0] = (int32_t)g0;
+        o[1] = (int32_t)(g0 + 1);
+        o[2] = (int32_t)(g0 + ch.lw);
+        o[3] = (int32_t)(g0 + ch.lw + 1);
+      }
+    }
+  }
+}
+
+static bool split_quad_ok(const LevelState &par, const LevelState &ch, int K) {
+  auto al = [](const void *q, uintptr_t a) { return q == nullptr || ((uintptr_t)q & (a - 1)) == 0; };
+  return K <= kSplitMaxK && ch.lw == 2 * par.lw && ch.lh == 2 * par.lh && al(ch.status, 2) &&
+         al(ch.d, 16) && al(ch.b, 16) && al(ch.steps, 8) && al(ch.tk_d, 16) && al(ch.tk_f, 16) &&
+         al(ch.tk_a, 16) && al(ch.tk_p, 8);
+}
+
 __global__ void k_finalize(LevelState ls) {
   for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < ls.n;
        g += (int64_t)gridDim.x * blockDim.x)
@@ -394,8 +476,13 @@ int dist_trace(const dist_decoder *dec, const double *codes, int S, const dist_c
       // fresh lists for the new level; steps_done (offset 16) persists
       e = cudaMemsetAsync(L.ctl, 0, 16, st);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(ctl)");
-      k_split<<<grid_for(ls.n, 256), 256, 0, st>>>(L.lv[li - 1], ls, K, L.list0, L.ctl);
-      DIST_CHECK_LAUNCH("k_split");
+      if (split_quad_ok(L.lv[li - 1], ls, K)) {
+        k_split_quad<<<grid_for(L.lv[li - 1].n, 256), 256, 0, st>>>(L.lv[li - 1], ls, K, L.list0, L.ctl);
+        DIST_CHECK_LAUNCH("k_split_quad");
+      } else {
+        k_split<<<grid_for(ls.n, 256), 256, 0, st>>>(L.lv[li - 1], ls, K, L.list0, L.ctl);
+        DIST_CHECK_LAUNCH("k_split");
+      }
     }
     const int slots = std::min(ls.level > 1 ? cfg->split_interval : cfg->max_steps, cfg->max_steps);
     if (dv.prec == DIST_PREC_FP64)
