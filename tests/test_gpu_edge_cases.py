@@ -96,6 +96,26 @@ def test_config_boundaries_bitexact_fp64(st, max_steps, k):
     np.testing.assert_allclose(r.state.topk_absf[fin], T.tk_a[fin], rtol=1e-12, atol=1e-15)
 
 
+@pytest.mark.parametrize("w,h,cs", [(48, 20, 4), (37, 23, 1), (64, 8, 2), (12, 100, 4)])
+def test_nonsquare_ragged_views_bitexact_fp64(st, w, h, cs):
+    """Non-square views whose ray counts are not a multiple of the 128-row
+    tile, with and without coarse-to-fine (camera.py:25-61 takes fx from the
+    width only; tracer.py:225-250 splits a w/cs x h/cs grid): the fp64 GPU march
+    equals the oracle exactly, and the depth map is laid out height x width."""
+    net, code = _tiny(st)
+    pose = st.look_at((0.3, 0.2, -2.0))
+    cfg = st.TraceConfig(coarse_start_scale=cs, k_samples=3)
+    r = st.trace(net, code, st.Intrinsics(width=w, height=h), pose, cfg)
+    dec = orc.Decoder(net.weights, 2)
+    T = orc.trace(lambda p: dec(p, code), orc.Cam(w, h, pose.omega, pose.t),
+                  orc.Cfg(coarse_start_scale=cs, k_samples=3))
+    assert r.live_counts == T.live_counts and r.total_queries == T.total_queries
+    assert np.array_equal(r.state.status, T.status) and np.array_equal(r.state.steps, T.steps)
+    np.testing.assert_allclose(r.state.d, T.d, rtol=1e-14, atol=0)
+    assert st.depth_map(r).shape == (h, w)
+    assert np.any(r.state.status == 1) and np.any(r.state.status != 1)
+
+
 def test_validation_errors(st):
     """Configuration and shape errors raise ValueError before any launch."""
     net, code = _tiny(st)
