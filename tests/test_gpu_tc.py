@@ -95,6 +95,32 @@ def test_tc_trace_nonsquare_ragged_vs_oracle(st, w, h, cs):
     assert np.max(np.abs(r.state.d[both] - T.d[both]) / T.d[both]) < 2e-4
 
 
+def test_tc_objective_gradient_nonsquare(st):
+    """Depth + silhouette completion objective (optimize.py:102-138) on a
+    72x40 view in fp16x3: loss and latent gradient within 1e-3 relative of
+    the fp64 oracle on the same observations."""
+    g = load_golden("geo64.npz")
+    w, h = 72, 40
+    seed = int(g["seed"])
+    intr, pose = st.Intrinsics(width=w, height=h), st.Pose(g["omega"], g["t"])
+    cfg = st.TraceConfig(**cfg_from(g["cfg"]))
+    obs_run = st.trace(st.NeuralField.geometric(256, (512,) * 8, seed, precision="fp64"),
+                       g["z_true"], intr, pose, cfg)
+    depth, sil = st.depth_map(obs_run), st.hard_mask(obs_run).astype(np.float64)
+    assert depth.shape == (h, w)
+    net = st.NeuralField.geometric(256, (512,) * 8, seed, precision="fp16x3")
+    tot, terms, grad, n_conv, q = st.completion_objective(
+        net, g["code"], [st.Observation("depth", depth), st.Observation("silhouette", sil)],
+        intr, pose, cfg, st.LossWeights())
+    dec = orc.Decoder(orc.geometric_init(256, (512,) * 8, seed), 256)
+    rt, rterms, rg, rconv, rq, _ = orc.objective(
+        dec, g["code"], orc.Cam(w, h, g["omega"], g["t"]), orc.Cfg(k_samples=3), orc.Weights(),
+        depth=depth, silhouette=sil)
+    assert np.linalg.norm(grad - rg) / np.linalg.norm(rg) < 1e-3
+    assert abs(tot - rt) < 1e-3 * abs(rt)
+    assert abs(q - rq) <= 2e-3 * rq
+
+
 def test_tc_objective_gradient(st):
     g = load_golden("geo64.npz")
     net = st.NeuralField.geometric(256, (512,) * 8, int(g["seed"]), precision="bf16x3")
