@@ -262,6 +262,27 @@ def attribute():
     print("attribute", maps.attribute.sum())
 
 
+def nonsquare():
+    """Non-square views with ragged ray counts (tiny_net recipe of tiny()):
+    camera.py:25-61 takes fx from the width only; tracer.py:225-250 splits a
+    (w/cs) x (h/cs) grid.  Pins the oracle's camera and split for w != h."""
+    rng = np.random.default_rng(7)
+    net = st.NeuralField.init(latent_dim=2, hidden=(16, 16), rng=rng)
+    code = rng.normal(0.0, 0.3, 2)
+    pose = st.look_at((0.3, 0.2, -2.0))
+    out = _pack_weights(net.weights)
+    out.update(code=code, omega=pose.omega, t=pose.t)
+    for w, h, cs in [(48, 20, 4), (37, 23, 1), (12, 100, 4)]:
+        cfg = st.TraceConfig(k_samples=3, coarse_start_scale=cs)
+        res = st.trace(net, code, st.Intrinsics(width=w, height=h), pose, cfg)
+        tag = f"v{w}x{h}_"
+        out.update(_state(res, tag))
+        out[tag + "cfg"] = _cfg_arr(cfg)
+        out[tag + "depth"] = st.depth_map(res)
+    np.savez_compressed(os.path.join(OUT, "nonsquare.npz"), **out)
+    print("nonsquare.npz")
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     warnings.simplefilter("ignore")
@@ -277,6 +298,7 @@ def main():
     pose()
     ladder()
     tiny()
+    nonsquare()
     geo(64, 0, "geo64")
     geo(32, 1, "geo32s1")
 

@@ -32,6 +32,24 @@ def test_oracle_tiny64_bitexact_vs_reference():
     assert np.array_equal(orc.normal_map(T, lambda p: dec(p, g["code"]), cfg), g["normal"])
 
 
+@pytest.mark.parametrize("w,h", [(48, 20), (37, 23), (12, 100)])
+def test_oracle_nonsquare_bitexact_vs_reference(w, h):
+    """Non-square views with ragged ray counts (oracle/make_golden.py:nonsquare):
+    the oracle's camera (fx from the width) and coarse split equal the reference."""
+    g = load_golden("nonsquare.npz")
+    dec = orc.Decoder(golden_weights(g), 2)
+    tag = f"v{w}x{h}_"
+    cfg = orc.Cfg(**cfg_from(g[tag + "cfg"]))
+    T = orc.trace(lambda p: dec(p, g["code"]), orc.Cam(w, h, g["omega"], g["t"]), cfg)
+    assert T.live_counts == list(g[tag + "live_counts"])
+    assert T.total_queries == int(g[tag + "total_queries"])
+    for a, k in [(T.status, "status"), (T.steps, "steps"), (T.d, "d"), (T.b, "b"),
+                 (T.tk_d, "topk_d"), (T.tk_a, "topk_absf")]:
+        assert np.array_equal(a, g[tag + k], equal_nan=True), k
+    assert np.array_equal(orc.depth_map(T, cfg), g[tag + "depth"])
+    assert g[tag + "depth"].shape == (h, w)
+
+
 def test_oracle_tiny64_heads_and_objective():
     g = load_golden("tiny64.npz")
     dec = orc.Decoder(golden_weights(g), 2)
