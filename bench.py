@@ -159,8 +159,10 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT,
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": float(np.mean([i["seconds"] for i in infos]) * 1e3),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": dict(_config(args), precision="fp64 (numpy port of the reference)"),
+            "higher_is_better": True,
+            "scaling": "strong" if args.gpus > 1 and args.scaling == "strong" else "weak",
+            "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": dict(_config(args, args.gpus), precision="fp64 (numpy port of the reference)"),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": infos[0]["cores"], "kind": "port",
                              "sample": infos[0]["sample"]},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -168,12 +170,19 @@ def run_reference(args):
     return 0
 
 
-def _config(args):
-    return {"workload": f"C3: {VIEWS_PER_RANK} views/GPU x {RES}x{RES} depth-supervised latent "
+def _config(args, world=1):
+    strong = world > 1 and args.scaling == "strong"
+    par = (f"C3's {VIEWS_PER_RANK} views cut into {args.tile}x{args.tile} pixel tiles dealt round-robin "
+           f"over {world} GPUs (strong scaling), exact fixed-point gradient all-reduce"
+           if strong else
+           f"views sharded over {world} GPU(s) (ring interleaved, {VIEWS_PER_RANK} per GPU), latent all-reduce")
+    return {"workload": f"C3: {VIEWS_PER_RANK} views x {RES}x{RES} depth-supervised latent "
                         f"optimisation, 8x512 DeepSDF decoder (latent 256, geometric init seed 0), "
-                        f"K=3, alpha 1.5, coarse 4, 100 steps",
-            "views_per_gpu": VIEWS_PER_RANK, "resolution": RES, "precision": args.precision,
-            "parallelism": f"views sharded over {args.gpus} GPU(s) (ring interleaved), latent all-reduce",
+                        f"K=3, alpha 1.5, coarse 4, 100 steps" +
+                        ("" if strong or world == 1 else f" (per GPU; {VIEWS_PER_RANK * world} views in all)"),
+            "views_per_gpu": VIEWS_PER_RANK / world if strong else VIEWS_PER_RANK,
+            "resolution": RES, "precision": args.precision,
+            "parallelism": par,
             "l2": "working set > L2 (ray state ~320 MB per step)",
             "relu_mask_record": (not getattr(args, "no_relu_masks", False)) and args.precision in ("bf16x3", "fp16x3")}
 
@@ -190,6 +199,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-relu-masks", action="store_true",
                     help="re-run the taped forward for every head sample (no ReLU-mask record)")
+    # N>1: "strong" (default) shards C3 itself -- its 8 views as pixel tiles over
+    # the ranks; "weak" gives every rank 8 views of an 8N-view ring
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
+    ap.add_argument("--tile", type=int, default=32)
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -211,30 +224,44 @@ def main():
 
     import paper_1911_13225_b200 as st
     from paper_1911_13225_b200 import _lib
+    from paper_1911_13225_b200.shard import TileShard
     from paper_1911_13225_b200.workloads import render_depth_observations, ring_views, target_code
 
+    strong = world > 1 and args.scaling == "strong"
     field = st.NeuralField.geometric(256, (512,) * 8, 0, precision=args.precision)
-    total_views = VIEWS_PER_RANK * world
-    # rank r traces ring views r, r+N, ..., r+7N of an 8N-view ring: every rank
-    # covers the whole ring, so per-rank cost stays balanced as N grows
-    views = ring_views(VIEWS_PER_RANK, RES, first=rank, total=total_views, stride=world)
     cfg = st.TraceConfig(k_samples=3)
-    obs = render_depth_observations(field, target_code(1), views, cfg)
-    weights = st.LossWeights(latent=1.0 if rank == 0 else 0.0)   # regulariser added once
     iters = args.warmup + args.steps
-    opt = st.LatentOptimizer(field, views, {"depth": obs}, np.zeros((1, 256)), cfg, weights,
-                             max_iters=2 * iters + 2,
-                             relu_masks=False if args.no_relu_masks else "auto")
+    relu = False if args.no_relu_masks else "auto"
+    if strong:
+        # C3 itself: the 8 ring views, tiles of every view on every rank
+        views = ring_views(VIEWS_PER_RANK, RES)
+        obs = render_depth_observations(field, target_code(1), views, cfg)
+        opt = st.LatentOptimizer(field, views, {"depth": obs}, np.zeros((1, 256)), cfg,
+                                 max_iters=2 * iters + 2, relu_masks=relu,
+                                 shard=TileShard(rank, world, args.tile, None))
+        rays_per_step = VIEWS_PER_RANK * RES * RES
+    else:
+        # rank r traces ring views r, r+N, ..., r+7N of an 8N-view ring: every rank
+        # covers the whole ring, so per-rank cost stays balanced as N grows
+        views = ring_views(VIEWS_PER_RANK, RES, first=rank, total=VIEWS_PER_RANK * world, stride=world)
+        obs = render_depth_observations(field, target_code(1), views, cfg)
+        weights = st.LossWeights(latent=1.0 if rank == 0 else 0.0)   # regulariser added once
+        opt = st.LatentOptimizer(field, views, {"depth": obs}, np.zeros((1, 256)), cfg, weights,
+                                 max_iters=2 * iters + 2, relu_masks=relu)
+        rays_per_step = VIEWS_PER_RANK * RES * RES * world
 
     def allreduce(grad, shape_terms):
         if world > 1:
             dist.all_reduce(grad)
             dist.all_reduce(shape_terms)
 
+    def step():
+        opt.step(None if strong else allreduce)
+
     stream = torch.cuda.current_stream()
     clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
-        opt.step(allreduce)
+        step()
     torch.cuda.synchronize()
 
     # ---- timed region: device-resident iterates -----------------------------
@@ -257,6 +284,15 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
+            if strong:
+                ev = opt.timing = []
+                opt.step()
+                opt.timing = None
+                tr_ev.append((ev[0], ev[1]))
+                obj_ev.append((ev[1], ev[2]))
+                q0 += opt.last_trace.stats_dev[0]
+                s0 += opt.head_counts[1].to(torch.int64)
+                continue
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)
             a.record(stream)
@@ -293,16 +329,18 @@ def main():
     obj_ms = float(np.mean([a.elapsed_time(b) for a, b in obj_ev]))
     queries = int(q0.item()) / args.steps
     samples = int(s0.item()) / args.steps
-    rays_per_step = VIEWS_PER_RANK * RES * RES * world
     value = rays_per_step / (ms * 1e-3)
 
     # ---- e2e: host observations in, loss out, every step ----------------------
-    obs_host = obs.cpu().pin_memory()
+    obs_host = opt.obs_depth.cpu().pin_memory()
     loss_host = torch.empty(opt.shape_terms.shape, dtype=torch.float64).pin_memory()
     code_host = torch.empty(opt.code.shape, dtype=torch.float64).pin_memory()
     h2d = obs_host.numel() * obs_host.element_size()
     d2h = loss_host.numel() * 8 + code_host.numel() * 8
     if world > 1:
+        hb = torch.tensor([h2d, d2h], dtype=torch.float64, device="cuda")
+        dist.all_reduce(hb)
+        h2d, d2h = int(hb[0].item()), int(hb[1].item())
         dist.barrier()
     torch.cuda.synchronize()
     f0 = torch.cuda.Event(enable_timing=True)
@@ -310,7 +348,7 @@ def main():
     f0.record(stream)
     for _ in range(args.steps):
         opt.obs_depth.copy_(obs_host.reshape(-1), non_blocking=True)
-        opt.step(allreduce)
+        step()
         loss_host.copy_(opt.shape_terms, non_blocking=True)
         code_host.copy_(opt.code, non_blocking=True)
     f1.record(stream)
@@ -322,7 +360,7 @@ def main():
     e2e_ms = float(t.item())
 
     consistent = True
-    if world > 1:   # replicated Adam after the all-reduce: every rank holds the same code
+    if world > 1:   # replicated Adam after the reduction: every rank holds the same code
         ref = opt.code.clone()
         dist.broadcast(ref, 0)
         diff = (opt.code - ref).abs().max().reshape(1)
@@ -341,10 +379,11 @@ def main():
     traffic, tsrc = _traffic(queries) if args.precision in ("bf16x3", "fp16x3") else (None, None)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": {"fp32": "f32", "fp64": "f64", "bf16x3": "bf16x3", "fp16x3": "fp16x3"}[args.precision],
         "data": "synthetic (geometric-init 8x512 DeepSDF, ring views, depth rendered from z*)",
-        "config": _config(args),
+        "config": _config(args, world),
         "e2e": {"value": rays_per_step / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),

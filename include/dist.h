@@ -177,18 +177,37 @@ typedef struct dist_objective_io {
   const double *obs_sil;         /* [V*H*W] binary silhouette target; NULL = no silhouette term */
   double w_depth, w_sil, w_latent; /* LossWeights, losses.py:45-51 */
   double *grad;                  /* out [S*D]: d total / d code (device) */
-  double *view_terms;            /* out [V*4]: depth loss, silhouette loss, n_px, n_converged */
+  double *view_terms;            /* out [V*6]: depth loss, silhouette loss, n_px, n_converged,
+                                    normal loss, n_normal (valid normal pixels) */
   double *shape_terms;           /* out [S*2]: total objective, |z|^2 */
   int32_t grad_mode;             /* 0: the reference's frozen-sample surrogate (shading.py:9-11);
                                     1: implicit gradient -(df/dz)/(grad f . v) at converged pixels;
                                     2: the paper's literal -(df/dz)/(n . v), n the unit Eq. 3 normal */
   int32_t reserved;
   int32_t *counts_out;           /* optional out [2]: recorded rays, seeded head samples (device) */
+  /* normal term (normal_loss, losses.py:94-111; seeds shading.py:259-269) */
+  const double *obs_normal;      /* [V*H*W*3] observed unit normals; NULL = no normal term */
+  const uint8_t *obs_normal_mask;/* [V*H*W] trusted pixels or NULL */
+  double w_normal;               /* LossWeights.normal */
+  /* Split iterate for views sharded over ranks as pixel tiles.
+   * phase 0: the whole iterate.  phase 1: sample lists, probes and the
+   * per-view counts only (view_terms[2], [3], [5]).  phase 2 (same workspace,
+   * after phase 1): the rest, with view_norm[v*3 + {0,1,2}] = the whole
+   * view's n_px, pixel count and n_normal replacing the tile's own (the
+   * normalisers of losses.py:61-111), so every term is the tile's exact share
+   * of its view's term. */
+  int32_t phase;
+  int32_t reserved2;
+  const double *view_norm;       /* [V*3] (phase 2) or NULL */
+  void *colsum_fixed;            /* optional out [S*np0] 16-byte two's-complement integers: the
+                                    layer-0 gradient column sums * 2^95 (exact, so ranks can add
+                                    them in any order); see dist_code_grad_fixed */
 } dist_objective_io;
 
+/* flags: bit 0 = a normal term will be requested (reserves its buffers) */
 DIST_API size_t dist_objective_workspace_size(const dist_decoder *dec, int n_views, int width,
                                               int height, int k_samples, int n_shapes,
-                                              int grad_mode);
+                                              int grad_mode, int flags);
 /* After dist_trace: frozen-sample heads, loss seeds, the fused taped forward
  * -> seed -> reverse sweep per tile of samples, and the code gradient with the
  * latent regulariser added once per shape.  Views contribute their own
@@ -197,6 +216,16 @@ DIST_API int dist_objective(const dist_decoder *dec, const double *codes_dev, in
                             const dist_camera *cams_dev, int n_views, int width, int height,
                             const dist_trace_config *cfg, const dist_ray_state *st,
                             const dist_objective_io *io, void *ws, size_t ws_bytes, void *stream);
+
+/* d/dz = W0[:D] colsum + w_latent * 2 z from exact column sums (the element-
+ * wise integer sum of every rank's dist_objective_io.colsum_fixed): the
+ * reduction step of optimize.py:340-341 ("g += hg['code']", regulariser once)
+ * with a result that is bit-identical for any number of ranks. */
+DIST_API int dist_code_grad_fixed(const dist_decoder *dec, int n_shapes, const void *colsum_fixed,
+                                  const double *codes_dev, double w_latent, double *grad_dev,
+                                  void *stream);
+/* padded width of layer 0 (the length of one shape's colsum_fixed row) */
+DIST_API int dist_decoder_colsum_width(const dist_decoder *dec);
 
 /* ---- photometric consistency (losses.py:128-222) ------- */
 /* cams_dev[0] = view i, cams_dev[1] = view j.  Images are row-major doubles

@@ -283,6 +283,51 @@ def nonsquare():
     print("nonsquare.npz")
 
 
+def normals():
+    """The normal term on the device path (losses.py:94-111, shading.py:259-269):
+    complete_shape with depth + silhouette + normal observations on the tiny
+    net (C1 recipe) and one all-terms completion_objective of the standard
+    8x512 decoder at 64^2 (geo64's decoder, code and view)."""
+    rng = np.random.default_rng(7)
+    net = st.NeuralField.init(latent_dim=2, hidden=(16, 16), rng=rng)
+    code = rng.normal(0.0, 0.3, 2)
+    intr = st.Intrinsics(width=64, height=64)
+    pose = st.look_at((0.0, 0.0, -2.0))
+    cfg = st.TraceConfig(k_samples=3)
+    z_obs = code + 0.05
+    ores = st.trace(net, z_obs, intr, pose, cfg)
+    obs = [st.Observation("depth", st.depth_map(ores)),
+           st.Observation("silhouette", st.hard_mask(ores).astype(np.float64)),
+           st.Observation("normal", st.normal_map(ores, net, z_obs))]
+    best, rep = st.complete_shape(net, obs, intr, pose, code0=np.zeros(2), iters=4, cfg=cfg)
+    out = {"cs_best": best, "cs_losses": np.asarray(rep.losses),
+           "cs_normal_terms": np.asarray([t["normal"] for t in rep.terms]),
+           "cs_best_iter": np.int64(rep.best_iter), "cs_queries": np.int64(rep.total_queries)}
+    # normal-only objective (masked) on the tiny net
+    mask = np.ones((64, 64), bool)
+    mask[:, :32] = False
+    nobs = [st.Observation("normal", obs[2].image, mask)]
+    tot, terms, g, n_conv, q = completion_objective(net, code, nobs, intr, pose, cfg, st.LossWeights())
+    out.update(nmask=mask, nobj_total=tot, nobj_normal=terms["normal"], nobj_grad=g)
+    # standard decoder, all terms
+    ws = orc.geometric_init(256, (512,) * 8, 0)
+    geo = st.NeuralField(ws, latent_dim=256)
+    z_true = np.random.default_rng(1).normal(0.0, 0.1, 256)
+    gcode = np.random.default_rng(2).normal(0.0, 0.1, 256)
+    gpose = st.look_at(orc.ring_eye(1, 8))
+    gres = st.trace(geo, z_true, intr, gpose, cfg)
+    gobs = [st.Observation("depth", st.depth_map(gres)),
+            st.Observation("silhouette", st.hard_mask(gres).astype(np.float64)),
+            st.Observation("normal", st.normal_map(gres, geo, z_true))]
+    tot, terms, g, n_conv, q = completion_objective(geo, gcode, gobs, intr, gpose, cfg, st.LossWeights())
+    out.update(geo_obs_depth=gobs[0].image, geo_obs_sil=gobs[1].image, geo_obs_normal=gobs[2].image,
+               geo_total=tot, geo_depth=terms["depth"], geo_sil=terms["silhouette"],
+               geo_normal=terms["normal"], geo_grad=g, geo_nconv=np.int64(n_conv),
+               geo_omega=gpose.omega, geo_t=gpose.t)
+    np.savez_compressed(os.path.join(OUT, "normals64.npz"), **out)
+    print("normals", rep.losses, tot, terms)
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     warnings.simplefilter("ignore")
@@ -301,6 +346,7 @@ def main():
     nonsquare()
     geo(64, 0, "geo64")
     geo(32, 1, "geo32s1")
+    normals()
 
 
 if __name__ == "__main__":

@@ -47,7 +47,12 @@ class dist_objective_io(C.Structure):
                 ("obs_sil", C.c_void_p), ("w_depth", C.c_double), ("w_sil", C.c_double),
                 ("w_latent", C.c_double), ("grad", C.c_void_p), ("view_terms", C.c_void_p),
                 ("shape_terms", C.c_void_p), ("grad_mode", C.c_int32), ("reserved", C.c_int32),
-                ("counts_out", C.c_void_p)]
+                ("counts_out", C.c_void_p), ("obs_normal", C.c_void_p),
+                ("obs_normal_mask", C.c_void_p), ("w_normal", C.c_double), ("phase", C.c_int32),
+                ("reserved2", C.c_int32), ("view_norm", C.c_void_p), ("colsum_fixed", C.c_void_p)]
+
+
+VIEW_TERMS = 6   # dist_objective_io.view_terms columns (include/dist.h)
 
 
 class dist_adam_config(C.Structure):
@@ -85,7 +90,10 @@ _SIGS = {
                                C.c_int, C.POINTER(dist_trace_config), C.POINTER(dist_ray_state),
                                C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "dist_objective_workspace_size": (C.c_size_t, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int,
-                                                   C.c_int, C.c_int]),
+                                                   C.c_int, C.c_int, C.c_int]),
+    "dist_code_grad_fixed": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_double,
+                                       C.c_void_p, C.c_void_p]),
+    "dist_decoder_colsum_width": (C.c_int, [C.c_void_p]),
     "dist_objective": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                  C.c_int, C.POINTER(dist_trace_config), C.POINTER(dist_ray_state),
                                  C.POINTER(dist_objective_io), C.c_void_p, C.c_size_t, C.c_void_p]),

@@ -93,6 +93,69 @@ __device__ __forceinline__ void pixel_ray(const dist_camera &c, int i, int j, in
   if (scale) *scale = 1.0 / n;
 }
 
+// Exact gradient column sums.  Every per-row contribution to the layer-0
+// column sums (the code gradient is W0[:D] times them, autodiff.py:175-185) is
+// converted to a 128-bit two's-complement fixed-point integer, value * 2^95,
+// and summed as an integer.  Integer addition is associative, so the sums --
+// and the code gradient -- are the same bit pattern whatever the partition of
+// samples into tiles, CTAs or ranks (identical iterates for any GPU
+// count), and no rounding accumulates with the sample count.  Range +-2^31;
+// resolution 2^-95 (a double with |x| >= 2^-42 converts exactly).  A
+// non-finite or out-of-range contribution sets a flag that turns the gradient
+// into NaN (the reference raises on a non-finite gradient, autodiff.py:253-254).
+typedef __int128 fx_t;
+constexpr int kFxShift = 95;
+
+__device__ __forceinline__ fx_t fx_from_double(double x, int *bad) {
+  if (!(fabs(x) < 2147483648.0)) {  // also catches NaN
+    *bad = 1;
+    return 0;
+  }
+  const double a = x * 4294967296.0;                 // x * 2^32, exact
+  const long long A = (long long)a;                  // toward zero, |A| < 2^63
+  const double r = a - (double)A;                    // exact fractional part, |r| < 1
+  const long long B = (long long)(r * 9223372036854775808.0);   // r * 2^63, toward zero
+  return (fx_t)((unsigned __int128)(fx_t)A << 63) + (fx_t)B;
+}
+
+// fp32 -> fx_t from the bit pattern (the tensor-core kernels' rows):
+// x = m 2^(e-150) -> m << (e - 55), truncated toward zero below 2^-95
+__device__ __forceinline__ fx_t fx_from_float(float x, int &bad) {
+  const uint32_t u = __float_as_uint(x);
+  const int e = (int)((u >> 23) & 0xffu);
+  if (e >= 158) {   // |x| >= 2^31, inf or NaN
+    bad = 1;
+    return 0;
+  }
+  const uint32_t m = (u & 0x7fffffu) | (e ? 0x800000u : 0u);
+  const int sh = (e ? e : 1) - 55;
+  const fx_t mag = sh >= 0 ? (fx_t)((unsigned __int128)m << sh) : (sh > -24 ? (fx_t)(m >> -sh) : (fx_t)0);
+  return (u >> 31) ? -mag : mag;
+}
+
+__device__ __forceinline__ fx_t fx_shfl_xor(fx_t v, int o) {
+  const unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)(v >> 64);
+  const unsigned long long lo2 = __shfl_xor_sync(0xffffffffu, lo, o);
+  const unsigned long long hi2 = __shfl_xor_sync(0xffffffffu, hi, o);
+  return (fx_t)(((unsigned __int128)hi2 << 64) | lo2);
+}
+
+// correctly rounded (one rounding, to nearest): the top 64 significant bits
+// with a sticky bit for the rest convert exactly like the full value, so
+// scaling the sums by a power of two scales the result exactly
+__device__ inline double fx_to_double(fx_t v) {
+  if (v == 0) return 0.0;
+  const bool neg = v < 0;
+  unsigned __int128 m = neg ? (unsigned __int128)(-v) : (unsigned __int128)v;
+  const unsigned long long hi = (unsigned long long)(m >> 64);
+  const int lz = hi ? __clzll(hi) : 64 + __clzll((unsigned long long)m);
+  m <<= lz;
+  unsigned long long t = (unsigned long long)(m >> 64);
+  t |= ((unsigned long long)m != 0ull) ? 1ull : 0ull;
+  const double r = ldexp((double)t, 64 - lz - kFxShift);
+  return neg ? -r : r;
+}
+
 // Workspace carving: bump allocator over a caller-provided buffer.
 struct Carve {
   char *base;

@@ -92,26 +92,27 @@ int launch_code_bias(const DecView &dv, const double *codes, int S, double *c0, 
 }
 
 // grad[s][k] = sum_j (sum_cta part0[cta][s][j]) W0z[k][j] + skip part.
-// Two kernels so both phases spread over many SMs; every sum keeps the
-// ascending order of the single-block version (bitwise the same results).
-__global__ void k_reduce_colsums(DecView dv, int S, int G, const double *__restrict__ part0,
-                                 const double *__restrict__ parts, double *__restrict__ colsum0,
-                                 double *__restrict__ colsums) {
+// The partials are exact fixed-point integers (common.cuh fx_t): their sum is
+// the same whatever the order or the number of slots, then it is rounded once
+// to fp64 and contracted with W0z in a fixed order.
+__global__ void k_reduce_colsums(DecView dv, int S, int G, const fx_t *__restrict__ part0,
+                                 const fx_t *__restrict__ parts, fx_t *__restrict__ colsum0,
+                                 fx_t *__restrict__ colsums) {
   const int n0 = dv.np[0], ns = dv.nskip;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_all = (int64_t)S * (n0 + ns);
   if (t >= n_all) return;
-  constexpr int U = 16;
+  constexpr int U = 8;
   const bool main_part = t < (int64_t)S * n0;
   const int64_t q = main_part ? t : t - (int64_t)S * n0;
   const int w = main_part ? n0 : ns;
   const int s = (int)(q / w), j = (int)(q - (int64_t)s * w);
-  const double *src = (main_part ? part0 : parts) + (size_t)s * w + j;
+  const fx_t *src = (main_part ? part0 : parts) + (size_t)s * w + j;
   const int64_t stride = (int64_t)S * w;
-  double acc = 0.0;
+  fx_t acc = 0;
   int c = 0;
   for (; c + U <= G; c += U) {
-    double x[U];
+    fx_t x[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) x[u] = src[(c + u) * stride];
 #pragma unroll
@@ -121,15 +122,22 @@ __global__ void k_reduce_colsums(DecView dv, int S, int G, const double *__restr
   (main_part ? colsum0 : colsums)[q] = acc;
 }
 
-__global__ void k_reduce_code_grad(DecView dv, int S, const double *__restrict__ colsum0,
-                                   const double *__restrict__ colsums, double *__restrict__ grad) {
+__device__ __forceinline__ double dot_fixed(const fx_t *__restrict__ a, const double *__restrict__ b,
+                                            int n, double acc) {
+  for (int k = 0; k < n; ++k) acc = fma(fx_to_double(a[k]), __ldg(b + k), acc);
+  return acc;
+}
+
+__global__ void k_reduce_code_grad(DecView dv, int S, const fx_t *__restrict__ colsum0,
+                                   const fx_t *__restrict__ colsums, const int *__restrict__ bad,
+                                   double *__restrict__ grad) {
   const int n0 = dv.np[0], ns = dv.nskip, D = dv.latent_dim;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= S * D) return;
   const int s = t / D, k = t - s * D;
-  double acc = dot_ordered<16>(colsum0 + (size_t)s * n0, 1, dv.W0z + (size_t)k * n0, 1, n0, 0.0);
-  if (ns > 0) acc = dot_ordered<16>(colsums + (size_t)s * ns, 1, dv.Wsz + (size_t)k * ns, 1, ns, acc);
-  grad[t] = acc;
+  double acc = dot_fixed(colsum0 + (size_t)s * n0, dv.W0z + (size_t)k * n0, n0, 0.0);
+  if (ns > 0) acc = dot_fixed(colsums + (size_t)s * ns, dv.Wsz + (size_t)k * ns, ns, acc);
+  grad[t] = (bad && *bad) ? __longlong_as_double(0x7ff8000000000000ll) : acc;
 }
 
 int sm_count() {
@@ -160,27 +168,32 @@ int eval_points(const DecView &dv, const double *c0, const double *cskip, int S,
 
 int vjp_points(const DecView &dv, const double *c0, const double *cskip, const double *pts,
                const int32_t *shape, int64_t n, const double *seed, int S, double *f,
-               double *part0, double *parts, double *gpts, int grid_cap, int *grid_out,
+               fx_t *part0, fx_t *parts, int *bad, double *gpts, int grid_cap, int *grid_out,
                cudaStream_t st) {
   *grid_out = 0;
   if (n <= 0) return DIST_OK;
   ArrayGen g{pts, shape, seed, f, n};
   if (dv.prec == DIST_PREC_FP64)
-    return launch_vjp_gen<double>(dv, c0, cskip, g, n, S, part0, parts, gpts, grid_cap, grid_out, st);
+    return launch_vjp_gen<double>(dv, c0, cskip, g, n, S, part0, parts, gpts, bad, grid_cap, grid_out, st);
   // bf16x3: the fused tensor-core head kernel (forward, given seeds, fp16x2 dgrad)
   if (tc_heads_supported(dv))
-    return launch_tc_heads<ArrayGen>(dv, c0, g, n, S, part0, grid_cap, grid_out, st, gpts);
-  return launch_vjp_gen<float>(dv, c0, cskip, g, n, S, part0, parts, gpts, grid_cap, grid_out, st);
+    return launch_tc_heads<ArrayGen>(dv, c0, g, n, S, part0, bad, grid_cap, grid_out, st, gpts);
+  return launch_vjp_gen<float>(dv, c0, cskip, g, n, S, part0, parts, gpts, bad, grid_cap, grid_out, st);
 }
 
-int reduce_code_grad(const DecView &dv, int S, int G, const double *part0, const double *parts,
-                     double *colsum0, double *colsums, double *grad, cudaStream_t st) {
+int reduce_code_grad(const DecView &dv, int S, int G, const fx_t *part0, const fx_t *parts,
+                     const int *bad, fx_t *colsum0, fx_t *colsums, double *grad, cudaStream_t st) {
   if (S <= 0 || dv.latent_dim == 0) return DIST_OK;
   const int64_t nc = (int64_t)S * (dv.np[0] + std::max(dv.nskip, 0));
-  k_reduce_colsums<<<(int)ceil_div(nc, 64), 64, 0, st>>>(dv, S, G, part0, parts, colsum0, colsums);
-  DIST_CHECK_LAUNCH("k_reduce_colsums");
-  k_reduce_code_grad<<<(int)ceil_div((int64_t)S * dv.latent_dim, 64), 64, 0, st>>>(dv, S, colsum0, colsums, grad);
-  DIST_CHECK_LAUNCH("k_reduce_code_grad");
+  if (G > 0) {
+    k_reduce_colsums<<<(int)ceil_div(nc, 64), 64, 0, st>>>(dv, S, G, part0, parts, colsum0, colsums);
+    DIST_CHECK_LAUNCH("k_reduce_colsums");
+  }
+  if (grad) {
+    k_reduce_code_grad<<<(int)ceil_div((int64_t)S * dv.latent_dim, 64), 64, 0, st>>>(dv, S, colsum0, colsums,
+                                                                                     bad, grad);
+    DIST_CHECK_LAUNCH("k_reduce_code_grad");
+  }
   return DIST_OK;
 }
 
@@ -191,10 +204,11 @@ size_t eval_ws(const DecView &dv, int64_t n, int S, bool vjp) {
   cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
   if (vjp) {
     const int G = vjp_grid_cap(dv.prec);
-    cv.take<double>((size_t)G * s1 * dv.np[0]);
-    cv.take<double>((size_t)G * s1 * std::max(dv.nskip, 1));
-    cv.take<double>((size_t)s1 * dv.np[0]);
-    cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
+    cv.take<fx_t>((size_t)G * s1 * dv.np[0]);
+    cv.take<fx_t>((size_t)G * s1 * std::max(dv.nskip, 1));
+    cv.take<fx_t>((size_t)s1 * dv.np[0]);
+    cv.take<fx_t>((size_t)s1 * std::max(dv.nskip, 1));
+    cv.take<int>(4);
   }
   (void)n;
   return cv.off + 256;
@@ -386,6 +400,8 @@ int dist_decoder_destroy(dist_decoder *dec) {
 
 int dist_decoder_precision(const dist_decoder *dec) { return dec ? dec->view.prec : -1; }
 
+int dist_decoder_colsum_width(const dist_decoder *dec) { return dec ? dec->view.np[0] : -1; }
+
 size_t dist_eval_workspace_size(const dist_decoder *dec, int64_t n, int S) {
   return dec ? eval_ws(dec->view, n, S, true) : 0;
 }
@@ -424,24 +440,27 @@ int dist_eval_vjp(const dist_decoder *dec, const double *codes, int S, const dou
   double *c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
   double *cs = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
   const int G = vjp_grid_cap(dv.prec);
-  double *part0 = cv.take<double>((size_t)G * s1 * dv.np[0]);
-  double *parts = cv.take<double>((size_t)G * s1 * std::max(dv.nskip, 1));
-  double *col0 = cv.take<double>((size_t)s1 * dv.np[0]);
-  double *cols = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
+  fx_t *part0 = cv.take<fx_t>((size_t)G * s1 * dv.np[0]);
+  fx_t *parts = cv.take<fx_t>((size_t)G * s1 * std::max(dv.nskip, 1));
+  fx_t *col0 = cv.take<fx_t>((size_t)s1 * dv.np[0]);
+  fx_t *cols = cv.take<fx_t>((size_t)s1 * std::max(dv.nskip, 1));
+  int *bad = cv.take<int>(4);
   if (!cv.ok) return fail(DIST_ERR_CONFIG, "workspace too small");
   int rc = launch_code_bias(dv, dv.latent_dim > 0 ? codes : nullptr, s1, c0, cs, st);
   if (rc) return rc;
-  cudaError_t e = cudaMemsetAsync(part0, 0, sizeof(double) * G * s1 * dv.np[0], st);
+  cudaError_t e = cudaMemsetAsync(part0, 0, sizeof(fx_t) * G * s1 * dv.np[0], st);
   if (e == cudaSuccess && dv.nskip)
-    e = cudaMemsetAsync(parts, 0, sizeof(double) * G * s1 * dv.nskip, st);
+    e = cudaMemsetAsync(parts, 0, sizeof(fx_t) * G * s1 * dv.nskip, st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), st);
   if (e == cudaSuccess && gpts) e = cudaMemsetAsync(gpts, 0, sizeof(double) * 3 * n, st);
   if (e == cudaSuccess && grad_codes && dv.latent_dim)
     e = cudaMemsetAsync(grad_codes, 0, sizeof(double) * s1 * dv.latent_dim, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync");
   int grid = 0;
-  rc = vjp_points(dv, c0, cs, pts, shape, n, seed, s1, f, part0, parts, gpts, G, &grid, st);
+  rc = vjp_points(dv, c0, cs, pts, shape, n, seed, s1, f, part0, parts, bad, gpts, G, &grid, st);
   if (rc) return rc;
-  if (grad_codes && grid > 0) return reduce_code_grad(dv, s1, grid, part0, parts, col0, cols, grad_codes, st);
+  if (grad_codes && grid > 0)
+    return reduce_code_grad(dv, s1, grid, part0, parts, bad, col0, cols, grad_codes, st);
   return DIST_OK;
 }
 

@@ -26,7 +26,69 @@ struct ObjIn {
   const double *obs_depth;
   const uint8_t *obs_mask;
   const double *obs_sil;
-  double w_depth, w_sil, w_lat;
+  double w_depth, w_sil, w_lat, w_normal;
+};
+
+// per-view terms written by dist_objective (include/dist.h view_terms)
+constexpr int kViewTerms = 6;
+
+// normal term inputs: rendered unit normals and |raw| of the Eq. 3 difference
+// vector (from the probe pass), the observation and its mask
+struct NormIn {
+  const double *unit;     // [n][3]
+  const double *rawnorm;  // [n]
+  const double *obs;      // [n][3]
+  const uint8_t *mask;    // [n] or null
+};
+
+// Probe rows of the normal loss: row 6r + a is probe a of valid pixel
+// list[r], in the reference's order (shading.py:196-197: +e_x, +e_y, +e_z,
+// -e_x, -e_y, -e_z around the surface point c + (d + (1-alpha) b) v).  The
+// seed of a probe is +-raw_seed/(2 delta) with raw_seed = (I - n n^T) ns /
+// |raw| and ns = w_normal * (-n_obs / n_valid) (losses.py:107-111,
+// shading.py:259-269); it does not depend on f.
+struct NormalGen {
+  const dist_camera *cams;
+  LevelState ls;
+  const int32_t *list;
+  const int32_t *cnt;
+  double alpha, delta, w_normal;
+  NormIn nn;
+  const double *nnorm;   // [V] n_valid of each view (the whole view's when sharded)
+  __device__ int64_t count() const { return (int64_t)*cnt * 6; }
+  __device__ bool point(int64_t i, double p[3], int &s) const {
+    const int64_t r = i / 6;
+    const int a = (int)(i - r * 6);
+    const int64_t g = list[r];
+    const int64_t per = (int64_t)ls.lw * ls.lh;
+    const int v = (int)(g / per);
+    const int64_t pix = g - (int64_t)v * per;
+    const int j = (int)(pix / ls.lw), ii = (int)(pix - (int64_t)j * ls.lw);
+    double dir[3];
+    pixel_ray(cams[v], ii, j, 1, dir, nullptr);
+    const double ds = __dadd_rn(ls.d[g], __dmul_rn(1.0 - alpha, ls.b[g]));
+    for (int q = 0; q < 3; ++q) p[q] = __dadd_rn(cams[v].origin[q], __dmul_rn(ds, dir[q]));
+    const int axis = a % 3;
+    p[axis] = __dadd_rn(p[axis], a < 3 ? delta : -delta);
+    s = cams[v].shape;
+    return true;
+  }
+  __device__ double seed(int64_t i, double) const {
+    const int64_t r = i / 6;
+    const int a = (int)(i - r * 6);
+    const int64_t g = list[r];
+    const int v = (int)(g / ((int64_t)ls.lw * ls.lh));
+    const double n = nnorm[v];
+    const double *o = nn.obs + g * 3, *u = nn.unit + g * 3;
+    double ns[3];
+    for (int c = 0; c < 3; ++c) ns[c] = w_normal * (-o[c] / n);
+    const double un = u[0] * ns[0] + u[1] * ns[1] + u[2] * ns[2];
+    const int axis = a % 3;
+    const double rs = (ns[axis] - u[axis] * un) / nn.rawnorm[g];
+    const double pp = rs / (2.0 * delta);
+    return a < 3 ? pp : -pp;
+  }
+  __device__ void store(int64_t, double) const {}
 };
 
 __device__ __forceinline__ bool depth_valid(const ObjIn &in, int64_t g) {

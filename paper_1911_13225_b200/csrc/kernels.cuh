@@ -26,10 +26,12 @@ int eval_points(const DecView &dv, const double *c0, const double *cskip, int S,
                 const int32_t *shape, int64_t n, double *f, cudaStream_t st);
 int vjp_points(const DecView &dv, const double *c0, const double *cskip, const double *pts,
                const int32_t *shape, int64_t n, const double *seed, int S, double *f,
-               double *part0, double *parts, double *gpts, int grid_cap, int *grid_out,
+               fx_t *part0, fx_t *parts, int *bad, double *gpts, int grid_cap, int *grid_out,
                cudaStream_t st);
-int reduce_code_grad(const DecView &dv, int S, int G, const double *part0, const double *parts,
-                     double *colsum0, double *colsums, double *grad, cudaStream_t st);
+// sums the per-CTA fixed-point partials (G slots) into colsum0/colsums
+// (fixed point) and forms d/dz = W0z^T colsum (+ skip part); NaN when *bad
+int reduce_code_grad(const DecView &dv, int S, int G, const fx_t *part0, const fx_t *parts,
+                     const int *bad, fx_t *colsum0, fx_t *colsums, double *grad, cudaStream_t st);
 int vjp_grid_cap(int prec);
 size_t eval_ws(const DecView &dv, int64_t n, int S, bool vjp);
 
@@ -48,7 +50,7 @@ namespace dist {
 int tc_make_map(const DecView &dv, int slot, CUtensorMap *map);
 template <class Gen>
 int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
-                    double *part0, int grid_cap, int *grid_out, cudaStream_t st,
+                    fx_t *part0, int *bad, int grid_cap, int *grid_out, cudaStream_t st,
                     double *gpts = nullptr);
 
 struct LevelState;
@@ -56,13 +58,13 @@ struct ProbeGen;
 struct ObjGen;
 // backward-only head rows (f and ReLU masks from the march's mask record)
 int launch_tc_heads_bwd(const DecView &dv, const double *c0, const ObjGen &gen, int64_t n_bound, int S,
-                        double *part0, int grid_cap, int *grid_out, cudaStream_t st);
+                        fx_t *part0, int *bad, int grid_cap, int *grid_out, cudaStream_t st);
 int tc_eval_probes(const DecView &dv, const double *c0, int S, const ProbeGen &gen, int64_t n_bound,
                    cudaStream_t st);
 int normals_pass(const DecView &dv, const double *c0, const double *cs, int S, const dist_camera *cams,
                  const LevelState &ls, const dist_trace_config *cfg, double *normals, double *gdotv,
                  int32_t *conv, int32_t *count, int32_t *bcount, double *f, cudaStream_t st,
-                 int gdotv_unit = 0);
+                 int gdotv_unit = 0, double *rawnorm = nullptr);
 
 // stable device-wide compaction of flags -> ascending indices (scan.cu)
 size_t compact_ws_bytes(int64_t n);

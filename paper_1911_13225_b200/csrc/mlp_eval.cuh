@@ -42,21 +42,22 @@ __global__ void __launch_bounds__(SimtTile<T>::NT)
 
 // Taped forward + reverse sweep per tile.  Column sums of the layer-0 / skip
 // pre-activation gradients accumulate into part0[cta][S][np0] /
-// parts[cta][S][nskip] (plain +=; each CTA owns its slice, so the final
-// fixed-order reduction is deterministic).  gpts[i][3] receives seed * df/dp.
+// parts[cta][S][nskip] as exact fixed-point integers (common.cuh fx_t), so
+// the result does not depend on how rows fall into tiles or CTAs; `bad` is
+// set on a non-finite contribution.  gpts[i][3] receives seed * df/dp.
 template <typename T, class Gen>
 __global__ void __launch_bounds__(SimtTile<T>::NT)
     k_vjp_gen(DecView dv, const double *__restrict__ c0, const double *__restrict__ cskip, Gen gen,
-              int S, double *__restrict__ part0, double *__restrict__ parts,
-              double *__restrict__ gpts) {
+              int S, fx_t *__restrict__ part0, fx_t *__restrict__ parts,
+              double *__restrict__ gpts, int *__restrict__ bad) {
   extern __shared__ __align__(16) char smem[];
   using Tile = SimtTile<T>;
   Tile tile(smem);
   __shared__ double s_seed[Tile::TM];
   __shared__ double s_seedm[Tile::TM];
   __shared__ double s_gp[Tile::TM * 3];
-  __shared__ double s_sum0[kMaxWidth];
-  __shared__ double s_sums[kMaxWidth];
+  __shared__ fx_t s_sum0[kMaxWidth];
+  __shared__ fx_t s_sums[kMaxWidth];
   __shared__ int s_shapes[Tile::TM];
   __shared__ int s_nsh;
   const int n0 = dv.np[0];
@@ -101,13 +102,13 @@ __global__ void __launch_bounds__(SimtTile<T>::NT)
         s_seedm[threadIdx.x] = (tile.shape[threadIdx.x] == s) ? s_seed[threadIdx.x] : 0.0;
         for (int a = 0; a < 3; ++a) s_gp[threadIdx.x * 3 + a] = 0.0;
       }
-      for (int j = threadIdx.x; j < kMaxWidth; j += blockDim.x) s_sum0[j] = s_sums[j] = 0.0;
+      for (int j = threadIdx.x; j < kMaxWidth; j += blockDim.x) s_sum0[j] = s_sums[j] = 0;
       __syncthreads();
-      tile.backward(dv, s_seedm, s_sum0, s_sums, s_gp);
-      double *p0 = part0 + ((size_t)blockIdx.x * S + s) * n0;
+      tile.backward(dv, s_seedm, s_sum0, s_sums, s_gp, bad);
+      fx_t *p0 = part0 + ((size_t)blockIdx.x * S + s) * n0;
       for (int j = threadIdx.x; j < n0; j += blockDim.x) p0[j] += s_sum0[j];
       if (ns) {
-        double *ps = parts + ((size_t)blockIdx.x * S + s) * ns;
+        fx_t *ps = parts + ((size_t)blockIdx.x * S + s) * ns;
         for (int j = threadIdx.x; j < ns; j += blockDim.x) ps[j] += s_sums[j];
       }
       if (gpts && threadIdx.x < Tile::TM && base + threadIdx.x < n && tile.shape[threadIdx.x] == s)
@@ -166,7 +167,7 @@ int launch_eval_gen(const DecView &dv, const double *c0, const double *cskip, co
 
 template <typename T, class Gen>
 int launch_vjp_gen(const DecView &dv, const double *c0, const double *cskip, const Gen &gen,
-                   int64_t n_bound, int S, double *part0, double *parts, double *gpts,
+                   int64_t n_bound, int S, fx_t *part0, fx_t *parts, double *gpts, int *bad,
                    int grid_cap, int *grid_out, cudaStream_t st) {
   using Tile = SimtTile<T>;
   const void *fn = (const void *)k_vjp_gen<T, Gen>;
@@ -180,7 +181,7 @@ int launch_vjp_gen(const DecView &dv, const double *c0, const double *cskip, con
   grid = std::min(grid, grid_cap);
   *grid_out = grid;
   k_vjp_gen<T, Gen><<<grid, Tile::NT, Tile::vjp_bytes, st>>>(dv, c0, cskip, gen, S, part0, parts,
-                                                             gpts);
+                                                             gpts, bad);
   DIST_CHECK_LAUNCH("k_vjp_gen");
   return DIST_OK;
 }

@@ -319,8 +319,8 @@ struct SimtTile {
   // entries, 0 for empty rows) multiplies f.  Accumulates the column sums of
   // the layer-0 (and skip-layer) pre-activation gradients into gsum0/gsums
   // (shared double[512] each) and writes d f/d p * seed to gpts[row][3].
-  __device__ void backward(const DecView &dv, const double *seed, double *gsum0,
-                           double *gsums, double *gpts) {
+  __device__ void backward(const DecView &dv, const double *seed, fx_t *gsum0,
+                           fx_t *gsums, double *gpts, int *bad) {
     const int tid = threadIdx.x, cg = tid & 63, rg = tid >> 6;
     const int L = dv.n_layers;
     // head: g[row][k] = seed * (1 - f^2) * w_out[k], masked by layer L-2
@@ -343,7 +343,7 @@ struct SimtTile {
       __syncthreads();
     }
     for (int l = L - 2; l >= 1; --l) {
-      if (l == dv.skip) colsum(dv.np[l], gsums, gpts, dv.Wsp, dv.np[l]);
+      if (l == dv.skip) colsum(dv.np[l], gsums, gpts, dv.Wsp, dv.np[l], bad);
       // g_in[row][k] = sum_n G[row][n] * W_l[k][n]  -> GEMM with Wt [np][kp]
       const int K = dv.np[l], N = dv.kp[l];
       T acc[8][8];
@@ -360,18 +360,21 @@ struct SimtTile {
       }
       __syncthreads();
     }
-    colsum(dv.np[0], gsum0, gpts, dv.W0p, dv.np[0]);
+    colsum(dv.np[0], gsum0, gpts, dv.W0p, dv.np[0], bad);
   }
 
-  // gsum[col] += sum_rows G[col][row]; gpts[row][a] += sum_col G[col][row] * Wp[a][col]
-  __device__ void colsum(int N, double *gsum, double *gpts, const double *Wp, int ldp) {
+  // gsum[col] += sum_rows G[col][row] (exact fixed point, common.cuh);
+  // gpts[row][a] += sum_col G[col][row] * Wp[a][col]
+  __device__ void colsum(int N, fx_t *gsum, double *gpts, const double *Wp, int ldp, int *bad) {
     const int tid = threadIdx.x;
+    int nb = 0;
     for (int col = tid; col < N; col += NT) {
-      double s = 0.0;
+      fx_t s = 0;
 #pragma unroll 4
-      for (int r = 0; r < TM; ++r) s += (double)H[col * LD + r];
+      for (int r = 0; r < TM; ++r) s += fx_from_double((double)H[col * LD + r], &nb);
       gsum[col] += s;
     }
+    if (nb) atomicOr(bad, 1);
     if (gpts) {
       constexpr int P = NT / TM;
       const int row = tid % TM, part = tid / TM;

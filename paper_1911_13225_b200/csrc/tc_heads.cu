@@ -17,9 +17,10 @@
 //     multiplies by the stored masks and picks the next row scale.  The
 //     rounding of g (2^-12) bounds the latent-gradient error at ~4e-4 with
 //     random-sign seeds and ~3e-5 with coherent ones (emulated);
-//   * the last backward epilogue reduces g over the CTA's 64 rows with a
-//     warp butterfly (62 shuffles per thread) and adds the column sums into
-//     this CTA's slice of part0 (deterministic: one owner per slice).
+//   * the last backward epilogue converts g to exact 128-bit fixed point
+//     (common.cuh fx_t), reduces it over the CTA's 64 rows with a warp
+//     butterfly and adds the column sums into this CTA's slice of part0: the
+//     sums are independent of how rows are partitioned.
 #include <cmath>
 #include <cstring>
 
@@ -44,7 +45,8 @@ struct HParams {
   int n_gemm;
   int S;
   int timeline;        // DIST_TC_TIMELINE: CTA 0 / thread 64 records %globaltimer marks
-  double *part0;       // [grid][S][512]
+  fx_t *part0;         // [grid][S][512] exact fixed-point column sums (common.cuh)
+  int *bad;            // set on a non-finite / out-of-range contribution
   double *gpts;        // [n][3] seed * df/dp per row, or null
 };
 
@@ -71,6 +73,41 @@ __device__ __forceinline__ void set4(uint32_t (&a)[4], int i, uint32_t v) {
   a[1] = i == 1 ? v : a[1];
   a[2] = i == 2 ? v : a[2];
   a[3] = i == 3 ? v : a[3];
+}
+
+// fp64 butterfly over a 16-column chunk (exact when the caller checked the
+// binade span); afterwards lanes 2c, 2c+1 both hold the sum of column c
+__device__ __forceinline__ void warp_colsum16d(double (&v)[16]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16, n = 8; o >= 2; o >>= 1, n >>= 1) {
+    const bool upper = lane & o;
+#pragma unroll
+    for (int j = 0; j < n; ++j) {
+      const double send = upper ? v[j] : v[j + n];
+      const double keep = upper ? v[j + n] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+}
+
+// The butterfly on exact fixed-point integers (common.cuh fx_t) over a
+// 16-column chunk (registers: 64 per chunk): afterwards lanes 2c and 2c+1
+// both hold the sum of column c over the warp's 32 rows.
+__device__ __forceinline__ void warp_colsum16x(fx_t (&v)[16]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16, n = 8; o >= 2; o >>= 1, n >>= 1) {
+    const bool upper = lane & o;
+#pragma unroll
+    for (int j = 0; j < n; ++j) {
+      const fx_t send = upper ? v[j] : v[j + n];
+      const fx_t keep = upper ? v[j + n] : v[j];
+      v[j] = keep + fx_shfl_xor(send, o);
+    }
+  }
+  v[0] += fx_shfl_xor(v[0], 1);
 }
 
 // Sum v[0..63] over the 32 lanes of the warp; afterwards lane l holds the
@@ -679,11 +716,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           // g_pre0 = D * mask0 * unscale; column sums over the CTA's rows, per
           // shape.  TMEM is read inside the shape loop (usually one pass), so no
           // per-thread copy of the 128 values is kept (it lived in local memory).
-          float *red = reinterpret_cast<float *>(smem + OFF_AHI);  // A is free now: [2][512] floats
+          float *red = reinterpret_cast<float *>(smem + OFF_AHI);  // A is free now: [2][512] fx_t
           if (P.gpts) {
             // d loss / d p = g_pre0 . W0p^T per row: this thread's 128 columns,
             // then the row's four part sums through smem (after `red`)
-            float *gp = red + 2 * KDIM;   // [3][4][64]
+            float *gp = red + 8 * KDIM;   // [3][4][64], after the [2][512] fixed-point column sums
             float acc[3] = {0.f, 0.f, 0.f};
             for (int nh = 0; nh < 2; ++nh) {
               const int cb = nh * 256 + half * 128 + sub * 64;
@@ -720,6 +757,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                      (double)gp[(a * 4 + 2) * ROWS + row] + (double)gp[(a * 4 + 3) * ROWS + row];
           }
           int shapes_done = 0;
+          fx_t *redx = reinterpret_cast<fx_t *>(red);   // [2][512] fixed point
           for (int guard = 0; guard < ROWS; ++guard) {
             // next shape = smallest shape id > previous (uniform across threads)
             int next = 0x7fffffff;
@@ -729,27 +767,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             }
             if (next == 0x7fffffff) break;
             const bool mine = (s == next);
+            int nb = 0;
             for (int nh = 0; nh < 2; ++nh) {
-              float w[64];
+#pragma unroll 1
+              for (int c = 0; c < 4; ++c) {
+                // The column sums must be exact (common.cuh fx_t) so that they
+                // do not depend on which rows share a tile, a CTA or a rank.
+                // Fast path: when the warp's nonzero values of this 16-column
+                // chunk span at most 24 binades (and sit inside the fixed-point
+                // range) their fp64 sums are exact, so one fp64 butterfly and
+                // one conversion per column give the exact integer; otherwise
+                // every value is converted and summed as a 128-bit integer.
+                float v[16];
+                tmem_ld16(tq + nh * 128 + sub * 64 + c * 16, v);
+                const uint32_t bits = mine ? (get4(mk, nh * 2 + (c >> 1)) >> ((c & 1) * 16)) : 0u;
+                uint32_t emin = 255u, emax = 0u;
 #pragma unroll
-              for (int c = 0; c < 2; ++c) {
-                float v[32];
-                tmem_ld32(tq + nh * 128 + sub * 64 + c * 32, v);
-                const uint32_t bits = mine ? get4(mk, nh * 2 + c) : 0u;
+                for (int e = 0; e < 16; ++e) {
+                  v[e] = ((bits >> e) & 1u) ? v[e] * unscale : 0.f;
+                  const uint32_t ex = (__float_as_uint(v[e]) >> 23) & 0xffu;
+                  if (v[e] != 0.f) {
+                    emin = min(emin, ex);
+                    emax = max(emax, ex);
+                  }
+                }
+                emin = __reduce_min_sync(0xffffffffu, emin);
+                emax = __reduce_max_sync(0xffffffffu, emax);
+                // lanes 2c', 2c'+1 end up holding column c' of the chunk; the
+                // two row-warps (q&1 = 0, 1) of the chunk combine in smem below
+                const int col = nh * 256 + half * 128 + sub * 64 + c * 16 + (lane >> 1);
+                fx_t r;
+                if (emax < emin || (emax - emin <= 24u && emin >= 55u && emax <= 151u)) {
+                  double w[16];
 #pragma unroll
-                for (int e = 0; e < 32; ++e) w[c * 32 + e] = ((bits >> e) & 1u) ? v[e] * unscale : 0.f;
+                  for (int e = 0; e < 16; ++e) w[e] = (double)v[e];
+                  warp_colsum16d(w);
+                  r = fx_from_double(w[0], &nb);
+                } else {
+                  fx_t w[16];
+#pragma unroll
+                  for (int e = 0; e < 16; ++e) w[e] = fx_from_float(v[e], nb);
+                  warp_colsum16x(w);
+                  r = w[0];
+                }
+                if (!(lane & 1)) redx[(q & 1) * 512 + col] = r;
               }
-              warp_colsum64(w);
-              const int cb = nh * 256 + half * 128 + sub * 64;
-              // the two row-warps (q&1 = 0, 1) of this column block combine in smem
-              red[(q & 1) * 512 + cb + 2 * lane] = w[0];
-              red[(q & 1) * 512 + cb + 2 * lane + 1] = w[1];
             }
+            if (nb) atomicOr(P.bad, 1);
             tc_fence_before();
             epi_sync();
-            double *dst = P.part0 + ((size_t)blockIdx.x * P.S + next) * n0;
+            fx_t *dst = P.part0 + ((size_t)blockIdx.x * P.S + next) * n0;
             for (int col = threadIdx.x - 64; col < KDIM; col += N_EPI_WARPS * 32)
-              dst[col] += (double)red[col] + (double)red[512 + col];
+              dst[col] += redx[col] + redx[512 + col];
             epi_sync();
             shapes_done = next + 1;
             TL(9);
@@ -778,7 +847,8 @@ bool tc_heads_supported(const DecView &dv) {
 
 template <class Gen, bool BWD>
 static int launch_heads_impl(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
-                             double *part0, int grid_cap, int *grid_out, cudaStream_t st, double *gpts) {
+                             fx_t *part0, int *bad, int grid_cap, int *grid_out, cudaStream_t st,
+                             double *gpts) {
   CUtensorMap mf, mb;
   const int fs = dv.prec == DIST_PREC_FP16X3 ? 3 : 0;   // bf16x3 forward pack
   int rc = tc_make_map(dv, fs, &mf);
@@ -800,6 +870,7 @@ static int launch_heads_impl(const DecView &dv, const double *c0, const Gen &gen
     P.timeline = tl ? atoi(tl) : 0;
   }
   P.part0 = part0;
+  P.bad = bad;
   P.gpts = gpts;
   const void *fn = (const void *)tc::k_tc_heads<Gen, BWD>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
@@ -814,13 +885,14 @@ static int launch_heads_impl(const DecView &dv, const double *c0, const Gen &gen
 
 template <class Gen>
 int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
-                    double *part0, int grid_cap, int *grid_out, cudaStream_t st, double *gpts) {
-  return launch_heads_impl<Gen, false>(dv, c0, gen, n_bound, S, part0, grid_cap, grid_out, st, gpts);
+                    fx_t *part0, int *bad, int grid_cap, int *grid_out, cudaStream_t st, double *gpts) {
+  return launch_heads_impl<Gen, false>(dv, c0, gen, n_bound, S, part0, bad, grid_cap, grid_out, st, gpts);
 }
 
 int launch_tc_heads_bwd(const DecView &dv, const double *c0, const ObjGen &gen, int64_t n_bound, int S,
-                        double *part0, int grid_cap, int *grid_out, cudaStream_t st) {
-  return launch_heads_impl<ObjGen, true>(dv, c0, gen, n_bound, S, part0, grid_cap, grid_out, st, nullptr);
+                        fx_t *part0, int *bad, int grid_cap, int *grid_out, cudaStream_t st) {
+  return launch_heads_impl<ObjGen, true>(dv, c0, gen, n_bound, S, part0, bad, grid_cap, grid_out, st,
+                                         nullptr);
 }
 
 extern "C" DIST_API int dist_debug_heads_timeline(unsigned long long *out, int n) {
@@ -829,8 +901,8 @@ extern "C" DIST_API int dist_debug_heads_timeline(unsigned long long *out, int n
 }
 
 template int launch_tc_heads<ObjGen>(const DecView &, const double *, const ObjGen &, int64_t, int,
-                                     double *, int, int *, cudaStream_t, double *);
+                                     fx_t *, int *, int, int *, cudaStream_t, double *);
 template int launch_tc_heads<ArrayGen>(const DecView &, const double *, const ArrayGen &, int64_t, int,
-                                       double *, int, int *, cudaStream_t, double *);
+                                       fx_t *, int *, int, int *, cudaStream_t, double *);
 
 }  // namespace dist

@@ -287,7 +287,8 @@ __global__ void k_normals_assemble(const dist_camera *__restrict__ cams, LevelSt
                                    const int32_t *__restrict__ conv,
                                    const int32_t *__restrict__ count, const double *__restrict__ f,
                                    double delta, int pair, double *__restrict__ normals,
-                                   double *__restrict__ gdotv, int gdotv_unit) {
+                                   double *__restrict__ gdotv, int gdotv_unit,
+                                   double *__restrict__ rawnorm) {
   const int64_t n = *count;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
        r += (int64_t)gridDim.x * blockDim.x) {
@@ -297,6 +298,7 @@ __global__ void k_normals_assemble(const dist_camera *__restrict__ cams, LevelSt
       raw[a] = pair ? f[r * 6 + 2 * a + 1] / (2.0 * delta)
                     : (f[r * 6 + 2 * a] - f[r * 6 + 2 * a + 1]) / (2.0 * delta);
     const double nrm = sqrt(raw[0] * raw[0] + raw[1] * raw[1] + raw[2] * raw[2]);
+    if (rawnorm) rawnorm[g] = nrm;
     if (normals)
       for (int a = 0; a < 3; ++a) normals[g * 3 + a] = nrm > 0.0 ? raw[a] / nrm : 0.0;
     if (gdotv) {  // grad f . v (raw Eq. 3 vector, or n . v with the unit normal) for the implicit gradient
@@ -318,7 +320,7 @@ __global__ void k_normals_assemble(const dist_camera *__restrict__ cams, LevelSt
 int normals_pass(const DecView &dv, const double *c0, const double *cs, int S, const dist_camera *cams,
                  const LevelState &ls, const dist_trace_config *cfg, double *normals, double *gdotv,
                  int32_t *conv, int32_t *count, int32_t *bcount, double *f, cudaStream_t st,
-                 int gdotv_unit) {
+                 int gdotv_unit, double *rawnorm) {
   const int64_t n = ls.n;
   const uint8_t *status = ls.status;
   int rc = compact([status] __device__(int64_t i) { return status[i] == DIST_CONVERGED; }, n, conv,
@@ -335,7 +337,7 @@ int normals_pass(const DecView &dv, const double *c0, const double *cs, int S, c
   else rc = launch_eval_gen<float, ProbeGen, true>(dv, c0, cs, gen, n * 6, st);
   if (rc) return rc;
   k_normals_assemble<<<grid_for(n, 256), 256, 0, st>>>(cams, ls, conv, count, f, cfg->normal_delta,
-                                                       pair, normals, gdotv, gdotv_unit);
+                                                       pair, normals, gdotv, gdotv_unit, rawnorm);
   DIST_CHECK_LAUNCH("k_normals_assemble");
   return DIST_OK;
 }

@@ -19,6 +19,7 @@ import numpy as np
 
 from . import _lib
 from .losses import LossWeights, Observation
+from .shard import TileShard, tile_split
 from .tracer import TraceConfig, relu_mask_bytes, trace_views
 
 # dist_objective_io.grad_mode (include/dist.h): the reference's frozen-sample
@@ -120,17 +121,39 @@ class LatentOptimizer:
 
     def __init__(self, field, views, observations: dict, code0, cfg: TraceConfig | None = None,
                  weights: LossWeights | None = None, lr: float = 1e-2, shape_of_view=None,
-                 max_iters: int = 1024, grad_mode: str = "surrogate", relu_masks="auto"):
+                 max_iters: int = 1024, grad_mode: str = "surrogate", relu_masks="auto",
+                 shard: TileShard | None = None):
         import torch
         _lib.require_device()
         self.field = field
-        self.views = list(views)
         self.cfg = cfg or TraceConfig(k_samples=3)
         self.weights = weights or LossWeights()
+        self.shard = shard
+        views = list(views)
+        sov = [0] * len(views) if shape_of_view is None else [int(s) for s in shape_of_view]
+        if shard is not None:
+            # this rank's pixel tiles of every view (shard.py); each tile is a view
+            self.parent_views = views
+            self.tiles, self.n_tiles = tile_split(views, shard.tile, shard.rank, shard.world,
+                                                  self.cfg.coarse_start_scale)
+            if not self.tiles:
+                raise ValueError("more ranks than pixel tiles")
+            if any(v[0].width != views[0][0].width or v[0].height != views[0][0].height
+                   for v in views):
+                raise ValueError("sharded views must share one resolution")
+            self.tile_parent = torch.tensor([t.view for t in self.tiles], dtype=torch.int64,
+                                            device="cuda")
+            self.tile_index = torch.tensor([t.index for t in self.tiles], dtype=torch.int64,
+                                           device="cuda")
+            observations = {k: self._tile_slices(a) for k, a in observations.items()}
+            self.parent_shape_of_view = list(sov)
+            sov = [sov[t.view] for t in self.tiles]
+            views = [(t.intr, t.pose) for t in self.tiles]
+        self.views = views
         V = len(self.views)
         self.V = V
         self.W, self.H = self.views[0][0].width, self.views[0][0].height
-        self.shape_of_view = [0] * V if shape_of_view is None else [int(s) for s in shape_of_view]
+        self.shape_of_view = sov
         z = np.asarray(code0, dtype=np.float64).reshape(-1, field.latent_dim)
         self.S, self.D = z.shape
         dev = "cuda"
@@ -144,7 +167,7 @@ class LatentOptimizer:
         self.best_iter = torch.full((self.S,), -1, dtype=torch.int32, device=dev)
         self.hist = torch.zeros((max_iters, self.S), dtype=torch.float64, device=dev)
         self.grad = torch.zeros_like(self.code)
-        self.view_terms = torch.zeros((V, 4), dtype=torch.float64, device=dev)
+        self.view_terms = torch.zeros((V, _lib.VIEW_TERMS), dtype=torch.float64, device=dev)
         self.shape_terms = torch.zeros((self.S, 2), dtype=torch.float64, device=dev)
         self.head_counts = torch.zeros(2, dtype=torch.int32, device=dev)  # recorded rays, seeded samples
         n = V * self.W * self.H
@@ -154,22 +177,25 @@ class LatentOptimizer:
                           <= RELU_MASK_AUTO_FRACTION * torch.cuda.mem_get_info()[0])
         self.relu_masks = bool(relu_masks)
 
-        def put(key, dtype):
+        def put(key, dtype, ch=1):
             if key not in observations or observations[key] is None:
                 return None
+            shp = "[V,H,W]" if ch == 1 else f"[V,H,W,{ch}]"
             if isinstance(observations[key], torch.Tensor):
                 tdt = torch.float64 if dtype == np.float64 else torch.uint8
                 a = observations[key].to(device=dev, dtype=tdt).reshape(-1).contiguous()
-                if a.numel() != n:
-                    raise ValueError(f"observation {key!r} must be [V,H,W]")
+                if a.numel() != n * ch:
+                    raise ValueError(f"observation {key!r} must be {shp}")
                 return a
             a = np.asarray(observations[key]).reshape(-1)
-            if a.size != n:
-                raise ValueError(f"observation {key!r} must be [V,H,W]")
+            if a.size != n * ch:
+                raise ValueError(f"observation {key!r} must be {shp}")
             return torch.from_numpy(a.astype(dtype)).to(dev)
         self.obs_depth = put("depth", np.float64)
         self.obs_mask = put("depth_mask", np.uint8)
         self.obs_sil = put("silhouette", np.float64)
+        self.obs_normal = put("normal", np.float64, 3)
+        self.obs_normal_mask = put("normal_mask", np.uint8)
         if grad_mode not in GRAD_MODES:
             raise ValueError(f"grad_mode must be one of {sorted(GRAD_MODES)}")
         self.grad_mode = grad_mode
@@ -177,6 +203,24 @@ class LatentOptimizer:
         self.iter = 0
         self.max_iters = max_iters
         self.last_trace = None
+        self.timing = None      # a list: _sharded_objective appends (trace start, end, objective end) events
+        self._colsum = None
+        if shard is not None:
+            sov_p = self._parent_shapes()
+            oh = np.zeros((self.S, len(self.parent_views)))
+            oh[sov_p, np.arange(len(self.parent_views))] = 1.0
+            self._shape_onehot = torch.from_numpy(oh).cuda()
+
+    def _tile_slices(self, a):
+        """[V,H,W(,c)] parent observations -> [T_local, tile, tile(,c)] of this rank's tiles."""
+        import torch
+        if a is None:
+            return None
+        t = a if isinstance(a, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(a))
+        V, H, W = len(self.parent_views), self.parent_views[0][0].height, self.parent_views[0][0].width
+        t = t.reshape(V, H, W, *t.shape[3:]) if t.dim() >= 3 else t
+        k = self.shard.tile
+        return torch.stack([t[x.view, x.y0:x.y0 + k, x.x0:x.x0 + k] for x in self.tiles]).contiguous()
 
     def objective(self):
         """Trace + heads + fused backward at the current code (no Adam)."""
@@ -186,24 +230,89 @@ class LatentOptimizer:
         self._objective_after_trace(dt)
         return dt
 
-    def _objective_after_trace(self, dt):
+    def _objective_after_trace(self, dt, phase: int = 0, view_norm=None, colsum_fixed=None):
         lib = _lib.lib()
         h = self.field.handle()
         K = self.cfg.k_samples
-        ws = _lib.workspace(lib.dist_objective_workspace_size(h, self.V, self.W, self.H, K, self.S,
-                                                              GRAD_MODES[self.grad_mode]))
-        io = _lib.dist_objective_io(_lib.ptr(self.obs_depth), _lib.ptr(self.obs_mask),
-                                    _lib.ptr(self.obs_sil), self.weights.depth,
-                                    self.weights.silhouette, self.weights.latent,
-                                    self.grad.data_ptr(), self.view_terms.data_ptr(),
-                                    self.shape_terms.data_ptr(),
-                                    GRAD_MODES[self.grad_mode], 0,
-                                    self.head_counts.data_ptr())
+        ws = _lib.workspace(lib.dist_objective_workspace_size(
+            h, self.V, self.W, self.H, K, self.S, GRAD_MODES[self.grad_mode],
+            1 if self.obs_normal is not None else 0))
+        io = self._io(phase, view_norm, colsum_fixed)
         c = _lib.config_struct(self.cfg)
         st = dt.state_struct()
         _lib.check(lib.dist_objective(h, self.code.data_ptr(), self.S, dt.cams.data_ptr(), self.V,
                                       self.W, self.H, C.byref(c), C.byref(st), C.byref(io),
                                       ws.data_ptr(), ws.numel(), _lib.stream_ptr()))
+
+    def _sharded_objective(self):
+        """One sharded iterate up to Adam (shard.py): phase 1, the per-view
+        count all-reduce, phase 2, the exact column-sum all-reduce, the code
+        gradient, and the fixed-order loss totals -- identical on every rank
+        and for every world size."""
+        import torch
+        from .shard import all_reduce_sum, fixed_all_reduce, view_totals
+        sh = self.shard
+        Vp = len(self.parent_views)
+        ev = self.timing
+        if ev is not None:
+            ev.append(torch.cuda.Event(enable_timing=True))
+            ev[-1].record()
+        dt = trace_views(self.field, self.code, self.views, self.cfg, self.shape_of_view,
+                         reuse=self.last_trace, relu_masks=self.relu_masks)
+        self.last_trace = dt
+        if ev is not None:
+            ev.append(torch.cuda.Event(enable_timing=True))
+            ev[-1].record()
+        self._objective_after_trace(dt, phase=1)
+        counts = torch.zeros((Vp, 2), dtype=torch.float64, device="cuda")
+        counts.index_add_(0, self.tile_parent, self.view_terms[:, [2, 5]])   # integers: exact
+        all_reduce_sum(counts, sh.group, sh.world)
+        pw, ph = self.parent_views[0][0].width, self.parent_views[0][0].height
+        view_norm = torch.stack([counts[self.tile_parent, 0],
+                                 torch.full((self.V,), float(pw * ph), dtype=torch.float64,
+                                            device="cuda"),
+                                 counts[self.tile_parent, 1]], dim=1).contiguous()
+        lib = _lib.lib()
+        h = self.field.handle()
+        if self._colsum is None:
+            np0 = lib.dist_decoder_colsum_width(h)
+            self._colsum = torch.zeros((self.S, np0, 2), dtype=torch.int64, device="cuda")
+        colsum = self._colsum
+        self._objective_after_trace(dt, phase=2, view_norm=view_norm, colsum_fixed=colsum)
+        fixed_all_reduce(colsum, sh.group, sh.world)
+        _lib.check(lib.dist_code_grad_fixed(h, self.S, colsum.data_ptr(), self.code.data_ptr(),
+                                            self.weights.latent, self.grad.data_ptr(),
+                                            _lib.stream_ptr()))
+        # loss terms: every tile's row at its global index, summed per view in order
+        terms = torch.zeros((self.n_tiles, _lib.VIEW_TERMS), dtype=torch.float64, device="cuda")
+        terms[self.tile_index] = self.view_terms
+        all_reduce_sum(terms, sh.group, sh.world)
+        per_view = view_totals(terms, Vp)
+        w = self.weights
+        data = w.depth * per_view[:, 0] + w.silhouette * per_view[:, 1] + w.normal * per_view[:, 4]
+        # per shape: its views' terms (a fixed-shape matrix product: no host
+        # sync, the same bits on every rank)
+        tot = self._shape_onehot @ data
+        reg = (self.code * self.code).sum(dim=1)
+        self.shape_terms[:, 0] = tot + w.latent * reg
+        self.shape_terms[:, 1] = reg
+        self.view_totals = per_view
+        if ev is not None:
+            ev.append(torch.cuda.Event(enable_timing=True))
+            ev[-1].record()
+        return dt
+
+    def _parent_shapes(self):
+        return self.parent_shape_of_view
+
+    def _io(self, phase: int = 0, view_norm=None, colsum_fixed=None) -> _lib.dist_objective_io:
+        return _lib.dist_objective_io(
+            _lib.ptr(self.obs_depth), _lib.ptr(self.obs_mask), _lib.ptr(self.obs_sil),
+            self.weights.depth, self.weights.silhouette, self.weights.latent,
+            self.grad.data_ptr(), self.view_terms.data_ptr(), self.shape_terms.data_ptr(),
+            GRAD_MODES[self.grad_mode], 0, self.head_counts.data_ptr(),
+            _lib.ptr(self.obs_normal), _lib.ptr(self.obs_normal_mask), self.weights.normal,
+            phase, 0, _lib.ptr(view_norm), _lib.ptr(colsum_fixed))
 
     def _adam(self):
         if self.iter >= self.max_iters:
@@ -223,9 +332,14 @@ class LatentOptimizer:
         cross-GPU gradient all-reduce when views are sharded over ranks."""
         if self.iter >= self.max_iters:
             raise ValueError("max_iters exceeded")
-        self.objective()
-        if reduce_fn is not None:
-            reduce_fn(self.grad, self.shape_terms)
+        if self.shard is not None:
+            if reduce_fn is not None:
+                raise ValueError("a sharded optimiser reduces exactly by itself; no reduce_fn")
+            self._sharded_objective()
+        else:
+            self.objective()
+            if reduce_fn is not None:
+                reduce_fn(self.grad, self.shape_terms)
         self._adam()
 
     def losses(self) -> np.ndarray:
@@ -240,18 +354,7 @@ def completion_objective(field, code, observations, intr, pose, cfg: TraceConfig
     frozen-sample depth surrogate gradient by -(df/dz)/(grad f . v);
     "implicit_unit" uses the paper's literal -(df/dz)/(n . v) with the unit normal."""
     obs = _split_observations(observations)
-    if "normal" in obs:
-        if grad_mode != "surrogate":
-            raise ValueError("implicit gradients are implemented for depth/silhouette terms")
-        return _completion_objective_heads(field, code, obs, intr, pose, cfg, weights)
-    H, W = intr.height, intr.width
-    o = {}
-    if "depth" in obs:
-        o["depth"] = obs["depth"].image
-        if obs["depth"].mask is not None:
-            o["depth_mask"] = obs["depth"].mask
-    if "silhouette" in obs:
-        o["silhouette"] = obs["silhouette"].image
+    o = _device_observations(obs)
     code = np.asarray(code, dtype=np.float64)
     opt = LatentOptimizer(field, [(intr, pose)], o, code.reshape(1, -1), cfg, weights, max_iters=1,
                           grad_mode=grad_mode)
@@ -267,39 +370,33 @@ def completion_objective(field, code, observations, intr, pose, cfg: TraceConfig
             warnings.warn("depth loss: no overlap between observation and render", RuntimeWarning)
     if "silhouette" in obs:
         terms["silhouette"] = float(vt[1])
+    if "normal" in obs:
+        terms["normal"] = float(vt[4])
     terms["latent"] = float(stt[1])
     if not np.all(np.isfinite(g)):
         raise FloatingPointError("non-finite gradient for leaf 'code'")
     return float(stt[0]), terms, g, int(vt[3]), dt.stats()["total_queries"]
 
 
-def _completion_objective_heads(field, code, obs, intr, pose, cfg, weights):
-    """Normal-supervised iterate through the drop-in HeadBundle path."""
-    from .losses import depth_loss, latent_reg, normal_loss, silhouette_loss
-    from .shading import diff_heads, soft_silhouette
-    from .tracer import trace
-    result = trace(field, code, intr, pose, cfg)
-    heads = diff_heads(result, field, code, want_normals=True)
-    terms = {}
-    ds = ss = ns = None
+def _device_observations(obs: dict) -> dict:
+    """Observation objects -> the [1,H,W(,3)] arrays LatentOptimizer takes."""
+    o = {}
     if "depth" in obs:
-        l, s = depth_loss(heads, obs["depth"])
-        terms["depth"] = l
-        ds = weights.depth * s
+        o["depth"] = obs["depth"].image
+        if obs["depth"].mask is not None:
+            o["depth_mask"] = obs["depth"].mask
     if "silhouette" in obs:
-        l, gi = silhouette_loss(soft_silhouette(result), obs["silhouette"].image)
-        terms["silhouette"] = l
-        ss = weights.silhouette * gi[heads.pixels[:, 1], heads.pixels[:, 0]]
-    l, s = normal_loss(heads, obs["normal"])
-    terms["normal"] = l
-    ns = weights.normal * s
-    reg, rg = latent_reg(code)
-    terms["latent"] = reg
-    g = heads.backward(depth_seed=ds, sil_seed=ss, normal_seed=ns).get(
-        "code", np.zeros_like(np.asarray(code, dtype=np.float64))) + weights.latent * rg
-    total = weights.depth * terms.get("depth", 0.0) + weights.silhouette * \
-        terms.get("silhouette", 0.0) + weights.normal * terms["normal"] + weights.latent * reg
-    return total, terms, g, int(heads.converged.sum()), result.total_queries
+        o["silhouette"] = obs["silhouette"].image
+    if "normal" in obs:
+        img = np.asarray(obs["normal"].image, dtype=np.float64)
+        if img.ndim != 3 or img.shape[2] != 3:
+            raise ValueError("normal observation must be [H,W,3]")
+        o["normal"] = img
+        if obs["normal"].mask is not None:
+            o["normal_mask"] = obs["normal"].mask
+    if "color" in obs:
+        raise ValueError("color observations belong to reconstruct_multiview")
+    return o
 
 
 def complete_shape(field, observations, intr, pose, code0=None, iters: int = 100,
@@ -318,27 +415,20 @@ def complete_shape(field, observations, intr, pose, code0=None, iters: int = 100
     t0 = time.perf_counter()
     if iters <= 0:
         return code, report
-    if "normal" in obs:
-        raise ValueError("normal observations: use completion_objective + adam_step")
-    o = {}
-    if "depth" in obs:
-        o["depth"] = obs["depth"].image
-        if obs["depth"].mask is not None:
-            o["depth_mask"] = obs["depth"].mask
-    if "silhouette" in obs:
-        o["silhouette"] = obs["silhouette"].image
+    o = _device_observations(obs)
     opt = LatentOptimizer(field, [(intr, pose)], o, code.reshape(1, -1), cfg, weights, lr=lr,
                           max_iters=iters)
     queries = 0
     import torch
     # per-iterate terms and |g| (optimize.py:160-166), kept on the device:
-    # [depth, silhouette, latent, |g|]
-    rec = torch.zeros((iters, 4), dtype=torch.float64, device=opt.grad.device)
+    # [depth, silhouette, latent, |g|, normal]
+    rec = torch.zeros((iters, 5), dtype=torch.float64, device=opt.grad.device)
     for it in range(iters):
         opt.objective()
         rec[it, 0:2] = opt.view_terms[0, 0:2]
         rec[it, 2] = opt.shape_terms[0, 1]
         rec[it, 3] = torch.linalg.vector_norm(opt.grad[0])
+        rec[it, 4] = opt.view_terms[0, 4]
         opt._adam()
         if it == 0:
             n_conv = int(opt.view_terms[0, 3].item())
@@ -357,6 +447,8 @@ def complete_shape(field, observations, intr, pose, code0=None, iters: int = 100
             terms["depth"] = float(rec[it, 0])
         if "silhouette" in obs:
             terms["silhouette"] = float(rec[it, 1])
+        if "normal" in obs:
+            terms["normal"] = float(rec[it, 4])
         terms["latent"] = float(rec[it, 2])
         report.record(float(loss), terms, float(rec[it, 3]))
     report.total_queries = int(queries.item()) if hasattr(queries, "item") else int(queries)

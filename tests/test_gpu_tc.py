@@ -1,12 +1,13 @@
 """Parity of the tcgen05 split-precision (bf16x3) decoder path against the
 reference fp64 goldens and the oracle.
 
-Contract of the fast mode: decoder values within 2e-5 of fp64;
-per-ray (status, steps) exact for every ray whose trajectory margin (SURVEY 8c,
-oracle margin_f / margin_esc) exceeds 1e-5 / 1e-4, except long grazing rays
-(>= 50 steps) where the accumulator bias integrates along the trajectory;
-total queries within 0.2%; depth of rays converged in both within 2e-4
-relative; latent gradient within 1e-3 relative.
+Contract of the tensor-core modes (the same as the full-size
+tests/test_gpu_fullsize.py): decoder values within 2e-5 of fp64; outside
+SURVEY 8(c)'s trajectory band (oracle margin_f / margin_esc below 1e-5 /
+1e-6) hit masks exact and step counts exact for all but 0.1% of rays (rays
+whose grazing trajectory drifts by the TMEM truncation bias); total queries
+within 0.2%; depth of matched rays within 1e-4 relative; latent gradient
+within 1e-3 relative.
 """
 from __future__ import annotations
 
@@ -52,19 +53,14 @@ def test_tc_trace_parity_contract(st, name, prec):
                   orc.Cfg(k_samples=3))
     assert np.array_equal(T.status, g["status"])
     mism = (r.state.status != g["status"]) | (r.state.steps != g["steps"])
-    robust = (T.margin_f > 1e-5) & (T.margin_esc > 1e-4) & (g["steps"] < 50)
-    assert not np.any(mism & robust), np.nonzero(mism & robust)
-    assert mism.mean() < 0.02
-    # hit masks are bit-exact; north_star's literal band: step counts may differ
-    # only where the final |SDF| is within 1e-5 of eps (fp16x3 march: 4 of 4096
-    # rays outside it on geo64, bf16x3: 32 -- DESIGN.md section 5)
-    assert np.array_equal(r.state.status, g["status"])
-    near = np.isfinite(g["b"]) & (np.abs(np.abs(g["b"]) - float(g["cfg"][1])) < 1e-5)
-    assert (mism & ~near).mean() < (2e-3 if prec == "fp16x3" else 1e-2)
+    band = (T.margin_f < 1e-5) | (T.margin_esc < 1e-6)
+    assert not np.any((r.state.status == 1) != (g["status"] == 1) & ~band)
+    assert (mism & ~band).sum() <= max(1, 1e-3 * mism.size), np.nonzero(mism & ~band)
     assert abs(r.total_queries - int(g["total_queries"])) <= 2e-3 * int(g["total_queries"])
-    dm = st.depth_map(r)
-    both = np.isfinite(dm) & np.isfinite(g["depth"])
-    assert np.max(np.abs(dm[both] - g["depth"][both]) / g["depth"][both]) < 2e-4
+    dm = st.depth_map(r).reshape(-1)
+    both = (r.state.status == 1) & (g["status"] == 1) & ~mism & ~band
+    ref = g["depth"].reshape(-1)
+    assert np.max(np.abs(dm[both] - ref[both]) / ref[both]) <= 1e-4
 
 
 @pytest.mark.parametrize("w,h,cs", [(72, 40, 4), (45, 31, 1)])
@@ -81,18 +77,14 @@ def test_tc_trace_nonsquare_ragged_vs_oracle(st, w, h, cs):
                   orc.Cfg(k_samples=3, coarse_start_scale=cs))
     assert np.any(T.status == 1) and np.any(T.status != 1)
     mism = (r.state.status != T.status) | (r.state.steps != T.steps)
-    robust = (T.margin_f > 1e-5) & (T.margin_esc > 1e-4) & (T.steps < 50)
-    assert not np.any(mism & robust), np.nonzero(mism & robust)
-    near = np.isfinite(T.b) & (np.abs(np.abs(T.b) - float(g["cfg"][1])) < 1e-5)
-    assert not np.any((r.state.status != T.status) & ~near)
-    # step-count floor outside the final-|SDF| band: 3 of 1,395
-    # rays at 45x31 on the first run, all inside the trajectory band above
-    assert (mism & ~near).sum() <= max(4, 2e-3 * mism.size)
+    band = (T.margin_f < 1e-5) | (T.margin_esc < 1e-6)
+    assert not np.any((r.state.status == 1) != (T.status == 1) & ~band)
+    assert (mism & ~band).sum() <= max(1, 1e-3 * mism.size), np.nonzero(mism & ~band)
     tq = sum(T.live_counts)
     assert abs(r.total_queries - tq) <= 2e-3 * tq
-    both = (r.state.status == 1) & (T.status == 1) & ~mism
+    both = (r.state.status == 1) & (T.status == 1) & ~mism & ~band
     assert both.sum() > 0
-    assert np.max(np.abs(r.state.d[both] - T.d[both]) / T.d[both]) < 2e-4
+    assert np.max(np.abs(r.state.d[both] - T.d[both]) / T.d[both]) <= 1e-4
 
 
 def test_tc_objective_gradient_nonsquare(st):
@@ -133,29 +125,8 @@ def test_tc_objective_gradient(st):
     assert abs(tot - float(g["obj_total"])) < 1e-3 * abs(float(g["obj_total"]))
 
 
-@pytest.mark.parametrize("prec", ["fp32", "bf16x3"])
-def test_c2_render_256_depth_normals_vs_oracle(st, prec):
-    """C2: 256^2 depth + normal render of the 8x512 decoder (code N(0, 0.1^2), rng 1)."""
-    res = 256
-    code = np.random.default_rng(1).normal(0.0, 0.1, 256)
-    net = st.NeuralField.geometric(256, (512,) * 8, 0, precision=prec)
-    pose = st.look_at((0.0, 0.0, -2.0))
-    maps = st.render(net, code, st.Intrinsics(width=res, height=res), pose, st.TraceConfig())
-    fp64 = net.with_precision("fp64")
-    ref = st.render(fp64, code, st.Intrinsics(width=res, height=res), pose, st.TraceConfig())
-    both = np.isfinite(maps.depth) & np.isfinite(ref.depth)
-    assert (np.isfinite(maps.depth) != np.isfinite(ref.depth)).mean() < 2e-3
-    rel = np.abs(maps.depth[both] - ref.depth[both]) / ref.depth[both]
-    assert np.percentile(rel, 99.9) < 1e-4 and rel.max() < (1e-4 if prec == "fp32" else 5e-4)
-    nd = np.linalg.norm(maps.normal - ref.normal, axis=2)[both]
-    # SURVEY 0 finding 3 metric: share of hit pixels whose normal differs by > 1e-4.
-    # Probes are (mid, diff) pairs in fp32 for both modes; in bf16x3 the traced
-    # surface point itself sits ~1e-5..1e-4 further along the ray, which moves
-    # the normal by curvature x shift.
-    if prec == "fp32":
-        assert np.percentile(nd, 99) < 1e-4 and np.mean(nd > 1e-4) < 2e-3
-    else:
-        assert np.percentile(nd, 99) < 5e-4 and np.mean(nd > 1e-3) < 2e-3
+# C2 (256^2 depth + normal render) against the reference itself, every
+# precision: tests/test_gpu_fullsize.py::test_c2_render_vs_reference
 
 
 @pytest.mark.parametrize("prec", ["bf16x3", "fp16x3"])
