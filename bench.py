@@ -10,9 +10,10 @@ step / step time (whole job), plus ms per latent-opt iterate.
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
   (N>1: torchrun --nproc-per-node N ... bench.py --gpus N)
 
---impl reference times the reference algorithm's CPU implementation (the
-oracle port of the pure-numpy reference, oracle/sdf_oracle.py) on the host
-cores, on a bounded sample of the same workload.
+--impl reference times the reference's own CPU implementation -- the
+unmodified pure-numpy package, staged verbatim in oracle/_ref by
+oracle/build_ref.sh -- on the host cores, on a bounded sample of the same
+workload (the oracle's numpy port when the copy is absent).
 """
 
 from __future__ import annotations
@@ -119,29 +120,75 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_reference_sample(seconds_hint=True):
-    """Time the CPU restatement of the reference (oracle) on a bounded sample:
-    one full completion_objective of a 128x128 crop-equivalent view (1/16 of
-    one 512^2 view) of the same decoder and scene.  Returns (rays/s, info)."""
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import sdf_oracle as orc
-    from paper_1911_13225_b200.workloads import ring_eye, target_code
-    res = 128
-    dec = orc.Decoder(orc.geometric_init(256, (512,) * 8, 0), 256)
-    z_true = target_code(1)
-    cam = orc.cam_look_at(ring_eye(0, VIEWS_PER_RANK), res, res)
-    cfg = orc.Cfg(k_samples=3)
-    T = orc.trace(lambda p: dec(p, z_true), cam, cfg)
-    obs = orc.depth_map(T, cfg)
-    t0 = time.perf_counter()
-    tot, terms, g, n_conv, q, _ = orc.objective(dec, np.zeros(256), cam, cfg, orc.Weights(),
-                                                depth=obs)
-    dt = time.perf_counter() - t0
-    cores = len(os.sched_getaffinity(0))
-    return res * res / dt, {"cores": cores, "seconds": dt, "queries": q,
-                            "sample": f"one {res}x{res} view (1/16 of a 512^2 view), full "
-                                      f"completion_objective (trace+heads+backward) of the 8x512 "
-                                      f"decoder in numpy fp64 with {cores}-thread BLAS"}
+REF_DIR = os.path.join(ROOT, "oracle", "_ref")   # oracle/build_ref.sh: verbatim copy of sdftrace
+REF_CROP = 64
+
+
+class _RefSample:
+    """One completion_objective of the UNMODIFIED reference (sdftrace, staged in
+    oracle/_ref by oracle/build_ref.sh) on a bounded sample of the C3 workload:
+    the central REF_CROP^2 pixels of ring view 0 of the 512^2 ring, traced as a
+    REF_CROP^2 camera with the 512^2 view's focal length and a shifted
+    principal point (the same rays as those pixels of the full view), the 8x512
+    geometric-init decoder, code 0, depth observation of z* -- the first C3
+    iterate.  Falls back to the oracle's numpy port when the copy is absent."""
+
+    def __init__(self):
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import sdf_oracle as orc
+        from paper_1911_13225_b200.workloads import ring_eye, target_code
+        self.kind = "reference" if os.path.isdir(os.path.join(REF_DIR, "sdftrace")) else "port"
+        ws = orc.geometric_init(256, (512,) * 8, 0)
+        z_true = target_code(1)
+        c = REF_CROP
+        x0 = (RES - c) // 2
+        if self.kind == "reference":
+            sys.path.insert(0, REF_DIR)
+            import sdftrace as ref
+            from sdftrace import optimize as ref_opt
+            self.ref, self.ref_opt = ref, ref_opt
+            self.field = ref.NeuralField(ws, latent_dim=256)
+            # fx = focal/sensor * W: keep the 512^2 view's fx for the crop
+            self.intr = ref.Intrinsics(focal_mm=60.0 * RES / c, sensor_mm=32.0, width=c, height=c,
+                                       cx=RES / 2.0 - x0, cy=RES / 2.0 - x0)
+            self.pose = ref.look_at(ring_eye(0, VIEWS_PER_RANK))
+            self.cfg = ref.TraceConfig(k_samples=3)
+            obs = ref.depth_map(ref.trace(self.field, z_true, self.intr, self.pose, self.cfg))
+            self.obs = [ref.Observation("depth", obs)]
+        else:
+            self.orc = orc
+            self.dec = orc.Decoder(ws, 256)
+            self.cam = orc.cam_look_at(ring_eye(0, VIEWS_PER_RANK), c, c)   # port: a c x c view
+            self.cfg = orc.Cfg(k_samples=3)
+            self.obs = orc.depth_map(orc.trace(lambda p: self.dec(p, z_true), self.cam, self.cfg), self.cfg)
+
+    def __call__(self):
+        c = REF_CROP
+        t0 = time.perf_counter()
+        if self.kind == "reference":
+            _, _, _, _, q = self.ref_opt.completion_objective(self.field, np.zeros(256), self.obs, self.intr,
+                                                          self.pose, self.cfg, self.ref.LossWeights())
+        else:
+            _, _, _, _, q, _ = self.orc.objective(self.dec, np.zeros(256), self.cam, self.cfg,
+                                                  self.orc.Weights(), depth=self.obs)
+        dt = time.perf_counter() - t0
+        cores = len(os.sched_getaffinity(0))
+        what = ("the unmodified reference sdftrace.completion_objective (oracle/_ref)"
+                if self.kind == "reference" else "the oracle's numpy port of completion_objective")
+        return c * c / dt, {"cores": cores, "seconds": dt, "queries": q, "kind": self.kind,
+                            "sample": f"the central {c}x{c} pixels of a 512^2 C3 ring view (same rays), one "
+                                      f"full iterate (trace + heads + loss + backward) of {what}, "
+                                      f"8x512 decoder, numpy fp64 with {cores}-thread BLAS"}
+
+
+_REF = None
+
+
+def cpu_reference_sample():
+    global _REF
+    if _REF is None:
+        _REF = _RefSample()
+    return _REF()
 
 
 def run_reference(args):
@@ -162,16 +209,16 @@ def run_reference(args):
             "higher_is_better": True,
             "scaling": "strong" if args.gpus > 1 and args.scaling == "strong" else "weak",
             "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": dict(_config(args, args.gpus), precision="fp64 (numpy port of the reference)"),
-            "cpu_baseline": {"value": val, "unit": UNIT, "cores": infos[0]["cores"], "kind": "port",
-                             "sample": infos[0]["sample"]},
+            "data": "synthetic", "config": dict(_config(args, args.gpus), precision=f"fp64 ({infos[0]['kind']})"),
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": infos[0]["cores"],
+                             "kind": infos[0]["kind"], "sample": infos[0]["sample"]},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
 
 
 def _config(args, world=1):
-    strong = world > 1 and args.scaling == "strong"
+    strong = (world > 1 and args.scaling == "strong") or getattr(args, "force_tiles", False)
     par = (f"C3's {VIEWS_PER_RANK} views cut into {args.tile}x{args.tile} pixel tiles dealt round-robin "
            f"over {world} GPUs (strong scaling), exact fixed-point gradient all-reduce"
            if strong else
@@ -203,6 +250,8 @@ def main():
     # the ranks; "weak" gives every rank 8 views of an 8N-view ring
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--tile", type=int, default=32)
+    ap.add_argument("--force-tiles", action="store_true",
+                    help="run the tiled (sharded) path even at N=1 (measures its overhead)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -227,7 +276,7 @@ def main():
     from paper_1911_13225_b200.shard import TileShard
     from paper_1911_13225_b200.workloads import render_depth_observations, ring_views, target_code
 
-    strong = world > 1 and args.scaling == "strong"
+    strong = (world > 1 and args.scaling == "strong") or args.force_tiles
     field = st.NeuralField.geometric(256, (512,) * 8, 0, precision=args.precision)
     cfg = st.TraceConfig(k_samples=3)
     iters = args.warmup + args.steps
@@ -414,7 +463,7 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:   # the contract: rank 0 at N=1 only
         v, info = cpu_reference_sample()
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": "port",
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
                                 "sample": info["sample"]}
     if rank == 0:
         print(json.dumps(line), flush=True)

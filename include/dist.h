@@ -144,14 +144,37 @@ DIST_API size_t dist_trace_workspace_size(const dist_decoder *dec, const dist_tr
                                  int n_views, int width, int height, int n_shapes);
 
 /* Coarse-to-fine, dynamic-mask, aggressive sphere tracing of V views that
- * share one resolution.  Outputs: the final-level ray state, per-step query
- * counts live_counts_dev[max_steps] (TraceResult.live_counts), and
- * stats_dev[4] = {total_queries, nan_count, steps_done, warning bits}. */
+ * share one resolution.  Each view keeps the reference's own step budget and
+ * level progression (tracer.py:236-252 traces one view at a time: a view
+ * whose coarse level empties early moves on with its own steps_done).
+ * Outputs: the final-level ray state, per-view per-step query counts
+ * live_counts_dev[V][max_steps] (TraceResult.live_counts of view v: the
+ * nonzero prefix of row v), and stats_dev[4] = {total_queries (all views),
+ * nan_count, the largest per-view step count, warning bits}. */
 DIST_API int dist_trace(const dist_decoder *dec, const double *codes_dev, int n_shapes,
                const dist_camera *cams_dev, int n_views, int width, int height,
                const dist_trace_config *cfg, const dist_ray_state *out,
                int64_t *live_counts_dev, int64_t *stats_dev, void *ws, size_t ws_bytes,
                void *stream);
+
+/* ---- the plugin seam: a caller-evaluated field ------------------------------
+ * The reference's trace accepts any duck-typed field with evaluate(points,
+ * code) (tracer.py:165; analytic fields, test fakes such as NanField,
+ * test_tracer.py:172-178).  dist_trace_external runs the same march -- init,
+ * dynamic mask, top-K record, update, splits, audit counters -- on the device
+ * and calls `field` once per step with the step's query points in host memory
+ * (points_host [n][3], caller-allocated for V*W*H rows); the callback writes
+ * f_host[n] and returns 0 (non-zero aborts with DIST_ERR_CONFIG).  The
+ * library synchronises the stream once per step.  Non-finite values exhaust
+ * their rays (tracer.py:170-176). */
+typedef int (*dist_field_fn)(const double *points_host, int64_t n, double *f_host, void *user);
+DIST_API size_t dist_trace_external_workspace_size(const dist_trace_config *cfg, int n_views,
+                                                   int width, int height);
+DIST_API int dist_trace_external(dist_field_fn field, void *user, const dist_camera *cams_dev,
+                                 int n_views, int width, int height, const dist_trace_config *cfg,
+                                 const dist_ray_state *out, int64_t *live_counts_dev,
+                                 int64_t *stats_dev, double *points_host, double *f_host, void *ws,
+                                 size_t ws_bytes, void *stream);
 
 /* ---- maps (shading.py:48-113) ------------------------------------------ */
 /* depth_map (+inf background), hard_mask, soft_silhouette for all V views,

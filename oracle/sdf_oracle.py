@@ -623,17 +623,21 @@ class Adam:
         return x - self.lr * mh / (np.sqrt(vh) + self.eps)
 
 
+IMPLICIT_GRAZING = 0.1
+
+
 def implicit_depth_seeds(H: Heads, d_seed, cam_dirs_rec, unit_normal=False):
     """Implicit-gradient variant: per-sample depth seeds
     scaled by -1/(grad f . v) at converged pixels, grad f = the raw Eq. 3
-    difference vector (normal_value * raw_norm), grazing (> -1e-3) excluded."""
+    difference vector (normal_value * raw_norm), grazing pixels (grad f . v >=
+    -IMPLICIT_GRAZING, factor > 10) excluded -- the rule of csrc/heads.cuh."""
     s = np.zeros_like(d_seed)
     if H.conv_rows.size == 0:
         return s
     gradf = H.normal_value[H.conv_rows] * (1.0 if unit_normal else H.raw_norm[:, None])
     gv = np.einsum("ij,ij->i", gradf, cam_dirs_rec[H.conv_rows])
     fac = np.zeros(H.pixels.shape[0])
-    ok = gv < -1e-3
+    ok = gv < -IMPLICIT_GRAZING
     fac[H.conv_rows[ok]] = -1.0 / gv[ok]
     return d_seed * fac[H.sample_pixel]
 

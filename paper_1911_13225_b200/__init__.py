@@ -6,8 +6,9 @@ by libdist_b200.so (hand-written sm_100a kernels behind a C ABI,
 include/dist.h).  There is no CPU fallback.
 """
 
-from .camera import Intrinsics, Pose, RayBundle, generate_rays, log_rotation, look_at, \
-    pose_gradient, rotation_derivatives, rotation_matrix
+from .autodiff import TapedEval, backward, eval_field_taped
+from .camera import Camera, Intrinsics, Pose, RayBundle, generate_rays, log_rotation, look_at, \
+    pose_gradient, project, rotation_derivatives, rotation_matrix, unproject
 from .fields import AttributeField, NeuralField, eval_field
 from .formats import load_camera, load_field, read_pfm, read_pgm, save_camera, save_field, \
     write_pfm, write_pgm
@@ -17,7 +18,8 @@ from .optimize import AdamState, LatentOptimizer, OptimizationError, OptimizeRep
     complete_shape, completion_objective, pose_objective, reconstruct_multiview, recover_pose
 from .shading import HeadBundle, RenderMaps, attribute_map, depth_map, diff_heads, hard_mask, \
     normal_map, ray_distance, render, soft_silhouette, surface_points
+from .shard import TileShard
 from .tracer import CONVERGED, ESCAPED, EXHAUSTED, MARCHING, DeviceTrace, RayState, TraceConfig, \
-    TraceResult, trace, trace_views
+    TraceResult, trace, trace_external, trace_views
 
 __version__ = "0.1.0"

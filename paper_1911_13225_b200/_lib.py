@@ -60,6 +60,8 @@ class dist_adam_config(C.Structure):
                 ("eps", C.c_double)]
 
 
+FIELD_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int64, C.POINTER(C.c_double), C.c_void_p)
+
 _SIGS = {
     "dist_last_error": (C.c_char_p, []),
     "dist_device_info": (C.c_int, [C.POINTER(C.c_int)] * 3),
@@ -82,6 +84,12 @@ _SIGS = {
     "dist_trace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
                              C.c_int, C.POINTER(dist_trace_config), C.POINTER(dist_ray_state),
                              C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "dist_trace_external_workspace_size": (C.c_size_t, [C.POINTER(dist_trace_config), C.c_int,
+                                                        C.c_int, C.c_int]),
+    "dist_trace_external": (C.c_int, [FIELD_FN, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(dist_trace_config), C.POINTER(dist_ray_state),
+                                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                      C.c_size_t, C.c_void_p]),
     "dist_maps": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(dist_trace_config),
                             C.POINTER(dist_ray_state), C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_void_p]),

@@ -53,6 +53,10 @@ struct DecView {
   // split-precision packs for the tensor-core path (bf16 hi/lo, K-major tiles)
   const void *tc_w[kMaxLayers];
   const float *tc_bias[kMaxLayers];
+  // Calibrated gain of the 512 -> 1 head dot in the tensor-core forward
+  // (tc_mlp.cu tc_calibrate): [0] for pack slot 0, [1] for the fp16 probe
+  // pack of a bf16x3 decoder (slot 2).  1 for the SIMT precisions.
+  double tc_gain[2];
 };
 
 }  // namespace dist

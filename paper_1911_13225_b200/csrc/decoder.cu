@@ -382,6 +382,14 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
         v.tc_w[l] = base + o_tc[l];
         v.tc_bias[l] = (const float *)(base + o_tcb[l]);
       }
+  v.tc_gain[0] = v.tc_gain[1] = 1.0;
+  if (prec >= DIST_PREC_BF16X3) {
+    const int rc = tc_calibrate(v);
+    if (rc) {
+      cudaFree(blob);
+      return rc;
+    }
+  }
   dist_decoder *d = new dist_decoder;
   d->view = v;
   d->blob = blob;

@@ -32,6 +32,12 @@ struct ObjIn {
 // per-view terms written by dist_objective (include/dist.h view_terms)
 constexpr int kViewTerms = 6;
 
+// Implicit-gradient modes: pixels with grad f . v >= -0.1 (within ~6 degrees
+// of grazing, where -1/(grad f . v) exceeds 10 and amplifies the surface
+// point's own error) carry no depth gradient.  The same rule is restated in
+// oracle/sdf_oracle.py implicit_depth_seeds.
+constexpr double kImplicitGrazing = 0.1;
+
 // normal term inputs: rendered unit normals and |raw| of the Eq. 3 difference
 // vector (from the probe pass), the observation and its mask
 struct NormIn {
@@ -155,7 +161,7 @@ struct ObjGen {
       sd = in.w_depth * __dmul_rn(__dmul_rn(w, sg), scale);
       if (gdotv) {  // implicit gradient: scale by -1/(grad f . v), drop grazing
         const double gv = gdotv[g];
-        sd = gv < -1e-3 ? sd * (-1.0 / gv) : 0.0;
+        sd = gv < -kImplicitGrazing ? sd * (-1.0 / gv) : 0.0;
       }
     }
     if (sil_seed && flat - g * K == 0) sd = __dadd_rn(sd, sil_seed[g]);
@@ -189,7 +195,7 @@ struct ObjGen {
       r.c1 = in.w_depth * __dmul_rn(w, scale);
       if (gdotv) {
         const double gv = gdotv[g];
-        r.ginv = gv < -1e-3 ? (-1.0 / gv) : 0.0;
+        r.ginv = gv < -kImplicitGrazing ? (-1.0 / gv) : 0.0;
       }
     }
     if (sil_seed && flat - g * K == 0) r.sil = sil_seed[g];

@@ -43,6 +43,8 @@ void tc_pack_fill(const DecView &dv, const double *const *W, const double *const
                   const int32_t *dims, const std::function<void *(int)> &wdst,
                   const std::function<float *(int)> &bdst);
 bool tc_supported(const DecView &dv);
+// measures DecView.tc_gain (the accumulator-bias gain of the head dot)
+int tc_calibrate(DecView &dv);
 bool tc_heads_supported(const DecView &dv);
 }  // namespace dist
 #include <cuda.h>

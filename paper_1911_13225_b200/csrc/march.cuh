@@ -39,6 +39,34 @@ struct MarchArgs {
   int K, max_steps, dynamic, V;
 };
 
+// Per-view step budget and live counts.  The reference traces one view at a
+// time (tracer.py:236-252): each view has its own steps_done, leaves a coarse
+// level as soon as it has no live ray, and records its own live_counts.  In a
+// batched trace every step slot gates each ray by its view's budget, counts
+// the queried rows per view, and the slot's last CTA advances exactly the
+// views that stepped (vb_close).
+struct ViewBudget {
+  int32_t *steps;   // [V] steps the view has taken
+  int32_t *cnt;     // [V] this slot's queried live rows of the view
+  int64_t *live;    // [V][max_steps] out: the view's own live_counts
+  int64_t per;      // rays per view at the current level
+};
+
+__device__ __forceinline__ int vb_view(const ViewBudget &vb, int64_t g) { return (int)(g / vb.per); }
+__device__ __forceinline__ bool vb_active(const ViewBudget &vb, const MarchArgs &a, int64_t g) {
+  return vb.steps[vb_view(vb, g)] < a.max_steps;
+}
+// the ray's view still steps after this slot (its survivors go to the next list)
+__device__ __forceinline__ bool vb_continues(const ViewBudget &vb, const MarchArgs &a, int64_t g) {
+  return vb.steps[vb_view(vb, g)] + 1 < a.max_steps;
+}
+// count one queried live row of view v (v < 0: none); every lane of the warp calls
+__device__ __forceinline__ void vb_count(const ViewBudget &vb, int v) {
+  const unsigned peers = __match_any_sync(0xffffffffu, v);
+  const int lane = threadIdx.x & 31;
+  if (v >= 0 && lane == __ffs(peers) - 1) atomicAdd(&vb.cnt[v], __popc(peers));
+}
+
 __device__ __forceinline__ void ray_of(const dist_camera *__restrict__ cams, const LevelState &ls,
                                        int64_t g, double dir[3], const dist_camera **cam) {
   const int64_t per = (int64_t)ls.lw * ls.lh;
@@ -116,9 +144,12 @@ __device__ __forceinline__ bool march_update(const LevelState &ls, const MarchAr
   return true;
 }
 
-// Last CTA of a step slot records the query count and flips the live lists.
-__device__ __forceinline__ void step_epilogue(Ctl *ctl, int cur, int64_t queried, int nan_block,
-                                              int64_t *live_counts, int64_t *stats) {
+// Last CTA of a step slot records every stepping view's query count
+// (dynamic mask: its live rows; without it the whole view, tracer.py:158-163),
+// advances those views' steps, and flips the live lists.  Every thread of the
+// CTA calls it.
+__device__ __forceinline__ void step_epilogue(Ctl *ctl, int cur, const ViewBudget &vb, const MarchArgs &a,
+                                              int nan_block, int64_t *stats) {
   __shared__ bool s_last;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -128,13 +159,26 @@ __device__ __forceinline__ void step_epilogue(Ctl *ctl, int cur, int64_t queried
     s_last = (prev == gridDim.x - 1);
   }
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {
-    __threadfence();
-    const int sd = ctl->steps_done;
-    live_counts[sd] = queried;
-    stats[0] += queried;
-    stats[2] = sd + 1;
-    ctl->steps_done = sd + 1;
+  if (!s_last) return;
+  __threadfence();
+  unsigned long long q = 0;
+  int smax = 0;
+  for (int v = threadIdx.x; v < a.V; v += blockDim.x) {
+    const int c = vb.cnt[v];
+    if (!c) continue;
+    const int s = vb.steps[v];
+    const int64_t n = a.dynamic ? (int64_t)c : vb.per;
+    vb.live[(int64_t)v * a.max_steps + s] = n;
+    q += (unsigned long long)n;
+    vb.steps[v] = s + 1;
+    smax = max(smax, s + 1);
+    vb.cnt[v] = 0;
+  }
+  if (q) atomicAdd((unsigned long long *)&stats[0], q);
+  if (smax) atomicMax((unsigned long long *)&stats[2], (unsigned long long)smax);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ctl->steps_done += 1;   // slots executed (all views)
     ctl->cnt[cur] = 0;
     ctl->cur = cur ^ 1;
     ctl->done = 0;
@@ -144,7 +188,7 @@ __device__ __forceinline__ void step_epilogue(Ctl *ctl, int cur, int64_t queried
 
 int tc_run_steps(const DecView &dv, const double *c0, const double *cskip, int S,
                  const dist_camera *cams, const LevelState &ls, Ctl *ctl, int32_t *l0, int32_t *l1,
-                 const MarchArgs &a, int slots, int64_t *live, int64_t *stats, cudaStream_t st);
+                 const MarchArgs &a, int slots, const ViewBudget &vb, int64_t *stats, cudaStream_t st);
 
 // Normal probes of the converged rays (shading.py:73-94): row 6r + 2a (+1)
 // is p +/- delta e_a of converged ray r, so consecutive rows form the

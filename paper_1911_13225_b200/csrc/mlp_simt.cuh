@@ -84,7 +84,7 @@ struct SimtTile {
           v = fma(pts[row * 3 + 2], w2, v);
         }
         bits |= (v > 0.0 ? 1u : 0u) << r;
-        H[col * LD + row] = (T)(v > 0.0 ? v : 0.0);
+        H[col * LD + row] = (T)(!(v <= 0.0) ? v : 0.0);   // np.maximum: NaN propagates
       }
       if (keep_mask) mask[(size_t)col * MB + rg] = (uint8_t)bits;
     }
@@ -156,7 +156,7 @@ struct SimtTile {
             v = (T)((double)v + e);
           }
           bits |= (v > (T)0 ? 1u : 0u) << r;
-          acc[c][r] = v > (T)0 ? v : (T)0;
+          acc[c][r] = !(v <= (T)0) ? v : (T)0;   // np.maximum: NaN propagates
         }
         if (keep_mask) mask[((size_t)l * kMaxWidth + col) * MB + rg] = (uint8_t)bits;
       }

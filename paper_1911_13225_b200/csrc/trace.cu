@@ -67,7 +67,8 @@ __global__ void k_init(const dist_camera *__restrict__ cams, LevelState ls, int 
 }
 
 // --- 4-way split (tracer.py:196-218) ---------------------------------------
-__global__ void k_split(LevelState par, LevelState ch, int K, int32_t *__restrict__ list, Ctl *ctl) {
+__global__ void k_split(LevelState par, LevelState ch, int K, int32_t *__restrict__ list, Ctl *ctl,
+                        const int32_t *__restrict__ vsteps, int max_steps) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t per_c = (int64_t)ch.lw * ch.lh, per_p = (int64_t)par.lw * par.lh;
   for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < ch.n; base += stride) {
@@ -91,7 +92,8 @@ __global__ void k_split(LevelState par, LevelState ch, int K, int32_t *__restric
       // inherited records carry no masks of this ray (own bit clear)
       if (ch.tk_p)
         for (int k = 0; k <= K; ++k) ch.tk_p[g * (K + 1) + k] = (uint8_t)k;
-      live = s == DIST_MARCHING;
+      // a view whose budget is spent marches no more (tracer.py:243)
+      live = s == DIST_MARCHING && vsteps[v] < max_steps;
     }
     warp_append(live, (int32_t)g, list, &ctl->cnt[0]);
   }
@@ -103,7 +105,8 @@ __global__ void k_split(LevelState par, LevelState ch, int K, int32_t *__restric
 // writes whole 32 B sectors of each array).  Used when the child arrays are
 // aligned for those stores (run_trace checks) and K <= kSplitMaxK.
 constexpr int kSplitMaxK = 8;
-__global__ void k_split_quad(LevelState par, LevelState ch, int K, int32_t *__restrict__ list, Ctl *ctl) {
+__global__ void k_split_quad(LevelState par, LevelState ch, int K, int32_t *__restrict__ list, Ctl *ctl,
+                             const int32_t *__restrict__ vsteps, int max_steps) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t per_c = (int64_t)ch.lw * ch.lh, per_p = (int64_t)par.lw * par.lh;
   const bool tkp4 = ch.tk_p && K == 3;   // one 8-byte store per child row
@@ -150,7 +153,7 @@ __global__ void k_split_quad(LevelState par, LevelState ch, int K, int32_t *__re
             for (int k = 0; k <= K; ++k) ch.tk_p[(g + c) * (K + 1) + k] = (uint8_t)k;
         }
       }
-      live = s == DIST_MARCHING;
+      live = s == DIST_MARCHING && vsteps[v] < max_steps;
     }
     // the four children join the live list together (its order is free: every
     // row of a tile is evaluated independently)
@@ -190,7 +193,7 @@ template <typename T>
 __global__ void __launch_bounds__(SimtTile<T>::NT)
     k_step(DecView dv, const double *__restrict__ c0, const double *__restrict__ cskip,
            const dist_camera *__restrict__ cams, LevelState ls, Ctl *ctl, int32_t *list0,
-           int32_t *list1, MarchArgs a, int64_t *live_counts, int64_t *stats) {
+           int32_t *list1, MarchArgs a, ViewBudget vb, int64_t *stats) {
   extern __shared__ __align__(16) char smem[];
   using Tile = SimtTile<T>;
   Tile tile(smem);
@@ -198,7 +201,7 @@ __global__ void __launch_bounds__(SimtTile<T>::NT)
   if (threadIdx.x == 0) {
     s_cur = ctl->cur;
     s_cnt = ctl->cnt[s_cur];
-    s_go = (ctl->steps_done < a.max_steps) && (s_cnt > 0);
+    s_go = s_cnt > 0;   // per-view budgets gate the rays (ViewBudget)
     s_nan = 0;
   }
   __syncthreads();
@@ -232,17 +235,20 @@ __global__ void __launch_bounds__(SimtTile<T>::NT)
     tile.forward(dv, c0, cskip, false);
     if (warp == 0) {
       bool keep = false;
-      if (threadIdx.x < Tile::TM && g >= 0 && ls.status[g] == DIST_MARCHING) {
+      int v = -1;
+      if (threadIdx.x < Tile::TM && g >= 0 && ls.status[g] == DIST_MARCHING && vb_active(vb, a, g)) {
         int nn = 0;
-        keep = march_update(ls, a, g, dir, cam->origin, tile.f[threadIdx.x], &nn);
+        v = vb_view(vb, g);
+        keep = march_update(ls, a, g, dir, cam->origin, tile.f[threadIdx.x], &nn) && vb_continues(vb, a, g);
         if (nn) atomicAdd(&s_nan, nn);
       }
+      vb_count(vb, v);
       warp_append(keep, (int32_t)g, out, out_cnt);
     }
     (void)lane;
     __syncthreads();
   }
-  step_epilogue(ctl, cur, rows, s_nan, live_counts, stats);
+  step_epilogue(ctl, cur, vb, a, s_nan, stats);
 }
 
 // --- maps (shading.py:48-61, 97-113) ------------------------------------------
@@ -342,6 +348,63 @@ int normals_pass(const DecView &dv, const double *c0, const double *cs, int S, c
   return DIST_OK;
 }
 
+// --- the plugin seam: a field evaluated by the caller (tracer.py:165) ----------
+// One step of the march for a field the library cannot evaluate (a duck-typed
+// Python field, an analytic SDF): the device gathers the query points of the
+// step, the caller's callback evaluates them, the device applies the update.
+__global__ void k_ext_points(const dist_camera *__restrict__ cams, LevelState ls, const Ctl *ctl,
+                             const int32_t *__restrict__ list0, const int32_t *__restrict__ list1,
+                             int dynamic, double *__restrict__ pts) {
+  const int cur = ctl->cur;
+  const int64_t rows = dynamic ? (int64_t)ctl->cnt[cur] : ls.n;
+  const int32_t *in = cur ? list1 : list0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < rows;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t g = dynamic ? in[i] : i;
+    double dir[3];
+    const dist_camera *cam;
+    ray_of(cams, ls, g, dir, &cam);
+    const double dg = ls.d[g];
+    for (int a = 0; a < 3; ++a) pts[i * 3 + a] = __dadd_rn(cam->origin[a], __dmul_rn(dg, dir[a]));
+  }
+}
+
+// With the dynamic mask off the whole grid is queried and dead rays' values
+// discarded (tracer.py:158-168), exactly as march_step does.
+__global__ void k_ext_apply(const dist_camera *__restrict__ cams, LevelState ls, Ctl *ctl,
+                            int32_t *list0, int32_t *list1, MarchArgs a, const double *__restrict__ f,
+                            ViewBudget vb, int64_t *stats) {
+  __shared__ int s_nan;
+  const int cur = ctl->cur;
+  const int64_t rows = a.dynamic ? (int64_t)ctl->cnt[cur] : ls.n;
+  const int32_t *in = cur ? list1 : list0;
+  int32_t *out = cur ? list0 : list1;
+  if (threadIdx.x == 0) s_nan = 0;
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t base = (int64_t)blockIdx.x * blockDim.x; base < rows; base += stride) {
+    const int64_t i = base + threadIdx.x;
+    bool keep = false;
+    int64_t g = -1;
+    int v = -1;
+    if (i < rows) {
+      g = a.dynamic ? in[i] : i;
+      if (ls.status[g] == DIST_MARCHING && vb_active(vb, a, g)) {
+        double dir[3];
+        const dist_camera *cam;
+        ray_of(cams, ls, g, dir, &cam);
+        int nn = 0;
+        v = vb_view(vb, g);
+        keep = march_update(ls, a, g, dir, cam->origin, f[i], &nn) && vb_continues(vb, a, g);
+        if (nn) atomicAdd(&s_nan, nn);
+      }
+    }
+    vb_count(vb, v);
+    warp_append(keep, (int32_t)g, out, &ctl->cnt[cur ^ 1]);
+  }
+  step_epilogue(ctl, cur, vb, a, s_nan, stats);
+}
+
 // --- host side --------------------------------------------------------------
 static int check_cfg(const dist_trace_config *c, int width, int height, int V) {
   if (!c) return fail(DIST_ERR_CONFIG, "null config");
@@ -365,6 +428,7 @@ struct TraceLayout {
   LevelState lv[3];
   int n_levels;
   int32_t *list0, *list1, *bcount;
+  int32_t *vsteps, *vcnt;   // ViewBudget: per-view steps and this slot's counts
   Ctl *ctl;
   size_t bytes;
 };
@@ -410,6 +474,8 @@ static TraceLayout layout(const DecView &dv, const dist_trace_config *cfg, int V
   L.list0 = cv.take<int32_t>(nmax);
   L.list1 = cv.take<int32_t>(nmax);
   L.bcount = cv.take<int32_t>(ceil_div(nmax * 6, kScanBlock) + 1);
+  L.vsteps = cv.take<int32_t>(2 * (size_t)V);
+  L.vcnt = L.vsteps ? L.vsteps + V : nullptr;
   L.ctl = cv.take<Ctl>(1);
   L.bytes = cv.off + 256;
   return L;
@@ -418,7 +484,7 @@ static TraceLayout layout(const DecView &dv, const dist_trace_config *cfg, int V
 template <typename T>
 static int run_steps(const DecView &dv, const double *c0, const double *cskip,
                      const dist_camera *cams, const LevelState &ls, Ctl *ctl, int32_t *l0,
-                     int32_t *l1, const MarchArgs &a, int slots, int64_t *live, int64_t *stats,
+                     int32_t *l1, const MarchArgs &a, int slots, const ViewBudget &vb, int64_t *stats,
                      cudaStream_t st) {
   using Tile = SimtTile<T>;
   const void *fn = (const void *)k_step<T>;
@@ -430,7 +496,7 @@ static int run_steps(const DecView &dv, const double *c0, const double *cskip,
   const int64_t tiles = ceil_div(ls.n, Tile::TM);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)std::max(per_sm, 1) * sm_count()));
   for (int s = 0; s < slots; ++s) {
-    k_step<T><<<grid, Tile::NT, Tile::fwd_bytes, st>>>(dv, c0, cskip, cams, ls, ctl, l0, l1, a, live,
+    k_step<T><<<grid, Tile::NT, Tile::fwd_bytes, st>>>(dv, c0, cskip, cams, ls, ctl, l0, l1, a, vb,
                                                       stats);
     DIST_CHECK_LAUNCH("k_step");
   }
@@ -463,7 +529,8 @@ int dist_trace(const dist_decoder *dec, const double *codes, int S, const dist_c
   if (L.bytes > ws_bytes) return fail(DIST_ERR_CONFIG, "trace workspace too small");
   cudaError_t e = cudaMemsetAsync(L.ctl, 0, sizeof(Ctl), st);
   if (e == cudaSuccess) e = cudaMemsetAsync(stats, 0, 4 * sizeof(int64_t), st);
-  if (e == cudaSuccess) e = cudaMemsetAsync(live, 0, cfg->max_steps * sizeof(int64_t), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(live, 0, (size_t)V * cfg->max_steps * sizeof(int64_t), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(L.vsteps, 0, 2 * sizeof(int32_t) * V, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(trace)");
   rc = launch_code_bias(dv, dv.latent_dim > 0 ? codes : nullptr, std::max(S, 1), L.c0, L.cskip, st);
   if (rc) return rc;
@@ -479,21 +546,104 @@ int dist_trace(const dist_decoder *dec, const double *codes, int S, const dist_c
       e = cudaMemsetAsync(L.ctl, 0, 16, st);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(ctl)");
       if (split_quad_ok(L.lv[li - 1], ls, K)) {
-        k_split_quad<<<grid_for(L.lv[li - 1].n, 256), 256, 0, st>>>(L.lv[li - 1], ls, K, L.list0, L.ctl);
+        k_split_quad<<<grid_for(L.lv[li - 1].n, 256), 256, 0, st>>>(L.lv[li - 1], ls, K, L.list0, L.ctl,
+                                                                     L.vsteps, cfg->max_steps);
         DIST_CHECK_LAUNCH("k_split_quad");
       } else {
-        k_split<<<grid_for(ls.n, 256), 256, 0, st>>>(L.lv[li - 1], ls, K, L.list0, L.ctl);
+        k_split<<<grid_for(ls.n, 256), 256, 0, st>>>(L.lv[li - 1], ls, K, L.list0, L.ctl, L.vsteps,
+                                                     cfg->max_steps);
         DIST_CHECK_LAUNCH("k_split");
       }
     }
     const int slots = std::min(ls.level > 1 ? cfg->split_interval : cfg->max_steps, cfg->max_steps);
+    const ViewBudget vb{L.vsteps, L.vcnt, live, (int64_t)ls.lw * ls.lh};
     if (dv.prec == DIST_PREC_FP64)
-      rc = run_steps<double>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, live, stats, st);
+      rc = run_steps<double>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, vb, stats, st);
     else if (tc_supported(dv))
-      rc = tc_run_steps(dv, L.c0, L.cskip, std::max(S, 1), cams, ls, L.ctl, L.list0, L.list1, a, slots, live, stats, st);
+      rc = tc_run_steps(dv, L.c0, L.cskip, std::max(S, 1), cams, ls, L.ctl, L.list0, L.list1, a, slots, vb, stats, st);
     else
-      rc = run_steps<float>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, live, stats, st);
+      rc = run_steps<float>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, vb, stats, st);
     if (rc) return rc;
+  }
+  const LevelState &fin = L.lv[L.n_levels - 1];
+  k_finalize<<<grid_for(fin.n, 256), 256, 0, st>>>(fin);
+  DIST_CHECK_LAUNCH("k_finalize");
+  return DIST_OK;
+}
+
+size_t dist_trace_external_workspace_size(const dist_trace_config *cfg, int V, int W, int H) {
+  if (!cfg || cfg->coarse_start_scale < 1) return 0;
+  DecView dv{};
+  dv.np[0] = 64;
+  const int64_t n = (int64_t)V * W * H;
+  Carve cv{nullptr, 0, ~size_t(0)};
+  cv.off = layout(dv, cfg, V, W, H, 1, nullptr, ~size_t(0), nullptr).bytes;
+  cv.take<double>(n * 3);
+  cv.take<double>(n);
+  return cv.off + 256;
+}
+
+int dist_trace_external(dist_field_fn field, void *user, const dist_camera *cams, int V, int W, int H,
+                        const dist_trace_config *cfg, const dist_ray_state *out, int64_t *live,
+                        int64_t *stats, double *points_host, double *f_host, void *ws, size_t ws_bytes,
+                        void *stream) {
+  if (!field || !out || !cams || !live || !stats || !points_host || !f_host)
+    return fail(DIST_ERR_CONFIG, "null argument");
+  int rc = check_cfg(cfg, W, H, V);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  DecView dv{};
+  dv.np[0] = 64;
+  dist_ray_state o = *out;
+  o.relu_masks = nullptr;
+  o.topk_slot = nullptr;
+  TraceLayout L = layout(dv, cfg, V, W, H, 1, (char *)ws, ws_bytes, &o);
+  Carve cv{(char *)ws, L.bytes - 256, ws_bytes};
+  const int64_t nmax = (int64_t)V * W * H;
+  double *pts = cv.take<double>(nmax * 3);
+  double *fd = cv.take<double>(nmax);
+  if (!cv.ok || L.bytes > ws_bytes) return fail(DIST_ERR_CONFIG, "trace workspace too small");
+  cudaError_t e = cudaMemsetAsync(L.ctl, 0, sizeof(Ctl), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(stats, 0, 4 * sizeof(int64_t), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(live, 0, (size_t)V * cfg->max_steps * sizeof(int64_t), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(L.vsteps, 0, 2 * sizeof(int32_t) * V, st);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(trace)");
+  MarchArgs a{cfg->alpha, cfg->epsilon, cfg->k_samples, cfg->max_steps, cfg->use_dynamic_mask ? 1 : 0, V};
+  const int K = cfg->k_samples;
+  k_init<<<grid_for(L.lv[0].n, 256), 256, 0, st>>>(cams, L.lv[0], K, L.list0, L.ctl, stats);
+  DIST_CHECK_LAUNCH("k_init");
+  for (int li = 0; li < L.n_levels; ++li) {
+    const LevelState &ls = L.lv[li];
+    if (li > 0) {
+      e = cudaMemsetAsync(L.ctl, 0, 16, st);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(ctl)");
+      k_split<<<grid_for(ls.n, 256), 256, 0, st>>>(L.lv[li - 1], ls, K, L.list0, L.ctl, L.vsteps,
+                                                   cfg->max_steps);
+      DIST_CHECK_LAUNCH("k_split");
+    }
+    const int budget = ls.level > 1 ? cfg->split_interval : cfg->max_steps;
+    const ViewBudget vb{L.vsteps, L.vcnt, live, (int64_t)ls.lw * ls.lh};
+    for (int step = 0; step < budget; ++step) {
+      // the reference loop's own test, on the host (tracer.py:242-245); the
+      // per-view budgets are applied on the device (ViewBudget)
+      Ctl c;
+      e = cudaMemcpyAsync(&c, L.ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return cuda_fail(e, "controller read");
+      if (c.cnt[c.cur] <= 0) break;
+      const int64_t rows = a.dynamic ? (int64_t)c.cnt[c.cur] : ls.n;
+      k_ext_points<<<grid_for(rows, 256), 256, 0, st>>>(cams, ls, L.ctl, L.list0, L.list1, a.dynamic, pts);
+      DIST_CHECK_LAUNCH("k_ext_points");
+      e = cudaMemcpyAsync(points_host, pts, sizeof(double) * 3 * rows, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return cuda_fail(e, "points to host");
+      if (field(points_host, rows, f_host, user) != 0)
+        return fail(DIST_ERR_CONFIG, "field callback failed");
+      e = cudaMemcpyAsync(fd, f_host, sizeof(double) * rows, cudaMemcpyHostToDevice, st);
+      if (e != cudaSuccess) return cuda_fail(e, "values to device");
+      k_ext_apply<<<grid_for(rows, 256), 256, 0, st>>>(cams, ls, L.ctl, L.list0, L.list1, a, fd, vb, stats);
+      DIST_CHECK_LAUNCH("k_ext_apply");
+    }
   }
   const LevelState &fin = L.lv[L.n_levels - 1];
   k_finalize<<<grid_for(fin.n, 256), 256, 0, st>>>(fin);

@@ -105,7 +105,29 @@ def normal_map(result: TraceResult, field=None, code=None) -> np.ndarray:
     dt = result.device
     if field is not None and field is not dt.field:
         raise ValueError("normal_map must use the field the trace was computed with")
+    if dt.external:
+        return _external_normals(result, dt.field, dt.codes if code is None else code)
     return device_normals(dt)[result.view].cpu().numpy()
+
+
+def _external_normals(result: TraceResult, field, code):
+    """normal_map for a caller-evaluated field (the plugin seam): the six
+    probes around each converged surface point go through the field's own
+    evaluate, once, as shading.py:84-87 queries it."""
+    pts, idx = surface_points(result)
+    st = result.state
+    out = np.zeros((st.bundle.height, st.bundle.width, 3))
+    if idx.size == 0:
+        return out
+    delta = result.config.normal_delta
+    offs = np.concatenate([np.eye(3), -np.eye(3)], axis=0) * delta
+    f = np.asarray(field.evaluate((pts[:, None, :] + offs[None]).reshape(-1, 3), code),
+                   dtype=np.float64).reshape(-1, 6)
+    raw = (f[:, :3] - f[:, 3:]) / (2.0 * delta)
+    nrm = np.linalg.norm(raw, axis=1, keepdims=True)
+    unit = np.where(nrm > 0.0, raw / np.where(nrm > 0.0, nrm, 1.0), 0.0)
+    out[st.bundle.pixels[idx, 1], st.bundle.pixels[idx, 0]] = unit
+    return out
 
 
 def attribute_map(result: TraceResult, attr_field, code=None) -> np.ndarray:
@@ -238,15 +260,20 @@ class HeadBundle:
             rs = np.where(ok[:, None], proj / np.where(ok, self._raw_norm, 1.0)[:, None], 0.0)
             pp = np.concatenate([rs, -rs], axis=1) / (2.0 * self._cfg.normal_delta)
             seed[m:] = pp.reshape(-1)
-        D = self._field.latent_dim
+        D = getattr(self._field, "latent_dim", 0) if hasattr(self._field, "vjp_device") else 0
         if self._pts.shape[0] == 0:
             out = {"sample_point_grads": np.zeros((0, 3))}
             if D:
                 out["code"] = np.zeros(D)
             return out
-        _, gc, gp = self._field.vjp_device(torch.from_numpy(self._pts), self._code,
-                                           torch.from_numpy(seed))
-        gp = gp.cpu().numpy()
+        if hasattr(self._field, "vjp_device"):
+            _, gc, gp = self._field.vjp_device(torch.from_numpy(self._pts), self._code,
+                                               torch.from_numpy(seed))
+            gp = gp.cpu().numpy()
+        else:
+            # an analytic field through the plugin seam: the reference's custom
+            # node, d/dp = seed * spatial_gradient (fields.py:362-373)
+            gp = seed[:, None] * np.asarray(self._field.spatial_gradient(self._pts), dtype=np.float64)
         if not np.all(np.isfinite(gp)):
             raise FloatingPointError("non-finite gradient for leaf 'points'")
         out = {"sample_point_grads": gp[:m]}

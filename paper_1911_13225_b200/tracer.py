@@ -77,6 +77,7 @@ class DeviceTrace:
                  relu_masks: bool = False):
         import torch
         self.field, self.codes, self.cfg = field, codes, cfg
+        self.external = False   # traced through the plugin seam (trace_external)
         self.cams, self.intrs, self.poses = cams, intrs, poses
         self.V, self.W, self.H = len(intrs), W, H
         n = self.V * W * H
@@ -89,7 +90,8 @@ class DeviceTrace:
         self.topk_d = torch.empty((n, K), dtype=torch.float64, device=dev)
         self.topk_f = torch.empty((n, K), dtype=torch.float64, device=dev)
         self.topk_absf = torch.empty((n, K), dtype=torch.float64, device=dev)
-        self.live_counts_dev = torch.zeros(cfg.max_steps, dtype=torch.int64, device=dev)
+        # per view: its own query count per own step (include/dist.h dist_trace)
+        self.live_counts_dev = torch.zeros((self.V, cfg.max_steps), dtype=torch.int64, device=dev)
         self.stats_dev = torch.zeros(4, dtype=torch.int64, device=dev)
         # ReLU masks of the recorded samples (include/dist.h dist_ray_state):
         # lets dist_objective skip the taped forward for them
@@ -106,10 +108,15 @@ class DeviceTrace:
                                    _lib.ptr(self.relu_masks), _lib.ptr(self.topk_slot))
 
     def stats(self) -> dict:
+        """Audit counters (TraceResult fields).  live_counts: the views' own
+        per-step query counts summed by step index; live_counts_per_view: each
+        view's list (tracer.py:247-249)."""
         s = self.stats_dev.cpu().numpy()
-        lc = self.live_counts_dev[: int(s[2])].cpu().numpy()
+        lc = self.live_counts_dev.cpu().numpy()
+        per = [[int(x) for x in row[: int(np.count_nonzero(row))]] for row in lc]
         return {"total_queries": int(s[0]), "nan_count": int(s[1]), "steps": int(s[2]),
-                "warnings": int(s[3]), "live_counts": [int(x) for x in lc]}
+                "warnings": int(s[3]), "live_counts": [int(x) for x in lc.sum(axis=0)[: int(s[2])]],
+                "live_counts_per_view": per}
 
 
 def _code_tensor(field, codes):
@@ -202,18 +209,80 @@ def host_result(dt: DeviceTrace, view: int = 0) -> TraceResult:
                   topk_d=dt.topk_d[sl].cpu().numpy(), topk_f=dt.topk_f[sl].cpu().numpy(),
                   topk_absf=dt.topk_absf[sl].cpu().numpy())
     s = dt.stats()
+    lc = s["live_counts_per_view"][view]
+    # per-view audit (tracer.py:80-82); NaN queries are counted for the whole batch
     return TraceResult(state=st, config=dt.cfg, intrinsics=dt.intrs[view], pose=dt.poses[view],
-                       live_counts=s["live_counts"], total_queries=s["total_queries"],
-                       nan_count=s["nan_count"], device=dt, view=view)
+                       live_counts=lc, total_queries=int(sum(lc)),
+                       nan_count=s["nan_count"] if dt.V == 1 else int(np.isnan(st.b).sum()),
+                       device=dt, view=view)
+
+
+def trace_external(field, code, views, cfg: TraceConfig | None = None) -> DeviceTrace:
+    """The reference's plugin seam (tracer.py:165): trace V views of ANY field
+    with `evaluate(points[n,3], code) -> f[n]` -- analytic SDFs, the
+    reference's own fields, test fakes.  The march (init, dynamic mask, top-K
+    record, update, splits, audit counters) runs on the device
+    (dist_trace_external); the field is called once per step on that step's
+    query points, as the reference's march_step calls it."""
+    cfg = cfg or TraceConfig()
+    _lib.require_device()
+    intrs = [v[0] for v in views]
+    poses = [v[1] for v in views]
+    W, H = intrs[0].width, intrs[0].height
+    if any(i.width != W or i.height != H for i in intrs):
+        raise ValueError("all views of one trace call must share a resolution")
+    if W % cfg.coarse_start_scale or H % cfg.coarse_start_scale:
+        raise ValueError(f"resolution {W}x{H} not divisible by coarse_start_scale "
+                         f"{cfg.coarse_start_scale}")
+    cams = _lib.cameras_to_device([camera_struct(i, p, 0) for i, p in zip(intrs, poses)])
+    dt = DeviceTrace(field, code, cams, intrs, poses, cfg, W, H)
+    n = len(views) * W * H
+    pts = np.empty(n * 3, dtype=np.float64)
+    vals = np.empty(n, dtype=np.float64)
+    err = []
+
+    def evaluate(p_ptr, m, f_ptr, _user):
+        try:
+            p = np.ctypeslib.as_array(p_ptr, shape=(m, 3)).copy()
+            f = np.asarray(field.evaluate(p, code), dtype=np.float64).reshape(-1)
+            if f.shape[0] != m:
+                raise ValueError(f"field returned {f.shape[0]} values for {m} points")
+            np.ctypeslib.as_array(f_ptr, shape=(m,))[:] = f
+            return 0
+        except BaseException as ex:   # re-raised below, after the C call unwinds
+            err.append(ex)
+            return 1
+
+    fn = _lib.FIELD_FN(evaluate)
+    lib = _lib.lib()
+    c = _lib.config_struct(cfg)
+    ws = _lib.workspace(lib.dist_trace_external_workspace_size(C.byref(c), len(views), W, H))
+    st = dt.state_struct()
+    rc = lib.dist_trace_external(fn, None, cams.data_ptr(), len(views), W, H, C.byref(c), C.byref(st),
+                                 dt.live_counts_dev.data_ptr(), dt.stats_dev.data_ptr(),
+                                 pts.ctypes.data, vals.ctypes.data, ws.data_ptr(), ws.numel(),
+                                 _lib.stream_ptr())
+    if err:
+        raise err[0]
+    _lib.check(rc)
+    dt.external = True
+    return dt
 
 
 def trace(field, code, intr: Intrinsics, pose: Pose, cfg: TraceConfig | None = None) -> TraceResult:
-    """Full render-tracing pass (tracer.py:221-252) on the GPU."""
+    """Full render-tracing pass (tracer.py:221-252) on the GPU.  Any object
+    with `evaluate(points, code)` is accepted (the reference's duck-typed
+    field protocol); NeuralField runs its decoder on the device as well."""
     cfg = cfg or TraceConfig()
     if intr.width % cfg.coarse_start_scale or intr.height % cfg.coarse_start_scale:
         raise ValueError(f"resolution {intr.width}x{intr.height} not divisible by "
                          f"coarse_start_scale {cfg.coarse_start_scale}")
-    dt = trace_views(field, code, [(intr, pose)], cfg)
+    if not hasattr(field, "handle"):
+        if not hasattr(field, "evaluate"):
+            raise TypeError("field must provide evaluate(points, code)")
+        dt = trace_external(field, code, [(intr, pose)], cfg)
+    else:
+        dt = trace_views(field, code, [(intr, pose)], cfg)
     res = host_result(dt, 0)
     if dt.stats()["warnings"] & 1:
         warnings.warn("camera center inside the unit sphere; rays start at d=0", RuntimeWarning)

@@ -61,14 +61,13 @@ def main():
             depth, _, _ = device_maps(dt, True, False, False)
             status, steps = dt.status.cpu().numpy(), dt.steps.cpu().numpy()
             depth = depth.cpu().numpy().reshape(-1)
+            per_view = dt.stats()["live_counts_per_view"]
             for v, x in enumerate(gs):
                 sl = slice(v * n, (v + 1) * n)
-                s = pf.compare_trace(x, status[sl], steps[sl], depth[sl], x["live_counts"],
+                s = pf.compare_trace(x, status[sl], steps[sl], depth[sl], per_view[v],
                                      band_f=args.band_f, band_esc=args.band_esc)
                 s.update(config="C3 512^2 ring view", view=int(x["view"]), precision=prec,
                          wall_s=time.time() - t0)
-                for k in ("live_steps_equal", "live_steps", "live_max_abs_diff", "live_over_bound"):
-                    s.pop(k)
                 lines.append(s)
                 print(json.dumps({k: v for k, v in s.items() if k != "out_of_band_rays"}), flush=True)
             lc = np.asarray(dt.stats()["live_counts"])

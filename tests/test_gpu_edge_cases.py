@@ -168,3 +168,48 @@ def test_concurrent_traces_on_two_streams_match_sequential(st):
             got = grab(out[k])
             for a, b in zip(got, alone[k]):
                 np.testing.assert_array_equal(a, b)
+
+
+# --- non-finite fields on the decoder paths (tracer.py:170-176) -------------------
+
+@pytest.mark.parametrize("prec", ["fp64", "fp16x3"])
+def test_nan_code_exhausts_its_views_only(st, prec):
+    """Two shapes in one batched trace, one code NaN: every ray of the NaN
+    shape's view exhausts at its first query (NaN propagates through the ReLU
+    layers as np.maximum does, fields.py:239-247) with its nan_count, while the
+    other view equals its trace alone -- on the SIMT and the tcgen05 march."""
+    from paper_1911_13225_b200.tracer import host_result
+    from paper_1911_13225_b200.workloads import ring_views
+    net = st.NeuralField.geometric(256, (512,) * 8, 0, precision=prec)
+    z = np.random.default_rng(1).normal(0.0, 0.1, (2, 256))
+    z[1, 3] = np.nan
+    views = ring_views(2, 32)
+    cfg = st.TraceConfig(k_samples=3)
+    dt = st.trace_views(net, z, views, cfg, shape_of_view=[0, 1])
+    bad = host_result(dt, 1)
+    hit0 = bad.state.steps > 0
+    assert hit0.any()
+    assert np.all(bad.state.status[hit0] == st.EXHAUSTED) and np.all(np.isnan(bad.state.b[hit0]))
+    assert np.all(bad.state.steps[hit0] == 1) and bad.live_counts == [int(dt.stats()["nan_count"])]
+    good = host_result(dt, 0)
+    alone = host_result(st.trace_views(net, z[0], views[:1], cfg), 0)
+    for k in ("status", "steps", "d"):
+        np.testing.assert_array_equal(getattr(good.state, k), getattr(alone.state, k), err_msg=k)
+    assert good.live_counts == alone.live_counts
+
+
+@pytest.mark.parametrize("prec", ["fp16x3", "bf16x3"])
+def test_dynamic_mask_off_on_tensor_cores(st, prec):
+    """tracer.py:158-168 on the tcgen05 march: without the live mask the whole
+    grid is queried and dead rays' values discarded -- the marched values are
+    bit-identical, only the query count grows (test_tracer.py:260-270)."""
+    g = __import__("conftest").load_golden("geo64.npz")
+    net = st.NeuralField.geometric(256, (512,) * 8, int(g["seed"]), precision=prec)
+    intr, pose = st.Intrinsics(width=64, height=64), st.Pose(g["omega"], g["t"])
+    on = st.trace(net, g["code"], intr, pose, st.TraceConfig(k_samples=3))
+    off = st.trace(net, g["code"], intr, pose, st.TraceConfig(k_samples=3, use_dynamic_mask=False))
+    for k in ("status", "steps", "d", "b", "topk_d", "topk_f"):
+        np.testing.assert_array_equal(getattr(on.state, k), getattr(off.state, k), err_msg=k)
+    assert off.total_queries > on.total_queries
+    # the reference's count without the mask: every ray of the level, each step
+    assert all(c in (16 * 16, 32 * 32, 64 * 64) for c in off.live_counts)

@@ -13,17 +13,17 @@ The contract, per precision mode:
   quantities) status and steps are exact, live counts differ only by
   band-lineage rays, depth and normals within 1e-4.  fp64 is exact on every
   ray of C2 and C3 (all 100 live counts equal).
-* the tensor-core modes (fp16x3, bf16x3): hit masks exact outside the band;
-  depth of every matched ray within 1e-4; live counts within the band bound;
-  out-of-band step differences stay below 0.1% of rays: 99% of them are
-  escaping rays that leave the unit sphere one step later -- the fp32
-  accumulators in TMEM truncate toward zero, so f is biased low by ~1e-6 and
-  the distance of a long grazing trajectory lags by up to ~n * 5e-6, which
-  moves an exit across a sphere-crossing step (profiles/r02_fullsize_parity.jsonl
-  lists every such ray with its margins).  Normals of the tensor-core renders are bounded at
-  3e-3 (the surface point inherits the last query's ~3e-6 error and the
-  delta = 1e-3 central differences amplify it across ReLU kinks); the C2
-  normal bar of 1e-4 is met in fp32 and fp64.
+* the tensor-core modes (fp16x3, bf16x3; the head dot's calibrated
+  accumulator-bias gain on, tc_mlp.cu tc_calibrate): hit masks exact outside
+  the band; depth of every matched ray within 1e-4; per-view live counts
+  within the band bound; out-of-band step differences below 1e-4 of the rays
+  (fp16x3: 1 of 65,536 at C2, 18 of 2.1M at C3, the same class and order as
+  fp32 SIMT's 5: escaping rays whose exit moves by one step, either way,
+  because a long grazing trajectory's distance drifts by the per-query
+  rounding; profiles/r02_fullsize_parity.jsonl lists each with its margins).
+  fp16x3 normals: 3 of 38,929 C2 pixels above 1e-4 (max 1.4e-4; the delta =
+  1e-3 central differences amplify the surface point's ~1e-7 error across
+  ReLU kinks); bf16x3 normals within 1e-3.
 """
 from __future__ import annotations
 
@@ -69,9 +69,12 @@ def test_c2_render_vs_reference(st, decoder, prec):
     if prec in ("fp64", "fp32"):
         assert s["mismatch_out_of_band"] == 0, s["out_of_band_rays"][:10]
         assert s["normal_max"] <= 1e-4, (s["normal_max"], s["normal_over_1e4"])
+    elif prec == "fp16x3":
+        assert s["mismatch_out_of_band"] <= 1e-4 * s["rays"], s["out_of_band_rays"]
+        assert s["normal_over_1e4"] <= 1e-3 * s["normal_pixels"] and s["normal_max"] <= 2e-4
     else:
-        assert s["mismatch_out_of_band"] <= 1e-3 * s["rays"]
-        assert s["normal_max"] <= 3e-3
+        assert s["mismatch_out_of_band"] <= 1e-4 * s["rays"], s["out_of_band_rays"]
+        assert s["normal_max"] <= 1e-3
     if prec == "fp64":
         assert s["mismatch_all"] == 0 and s["live_steps_equal"] == s["live_steps"]
         assert s["queries"] == s["queries_ref"]
@@ -91,17 +94,22 @@ def test_c3_ring_views_vs_reference(st, decoder, prec):
     n = 512 * 512
     status, steps = dt.status.cpu().numpy(), dt.steps.cpu().numpy()
     depth = depth.cpu().numpy().reshape(-1)
-    lc = np.asarray(dt.stats()["live_counts"])
+    stats = dt.stats()
+    lc = np.asarray(stats["live_counts"])
     total_oob = 0
     for v, g in enumerate(gs):
         sl = slice(v * n, (v + 1) * n)
-        s = pf.compare_trace(g, status[sl], steps[sl], depth[sl], g["live_counts"])
+        # each view's own per-step query counts (the batched trace keeps the
+        # reference's per-view level loop and budget)
+        s = pf.compare_trace(g, status[sl], steps[sl], depth[sl], stats["live_counts_per_view"][v])
         total_oob += s["mismatch_out_of_band"]
         assert s["hitmask_diff_out_of_band"] == 0, (v, s["out_of_band_rays"][:10])
         assert s["depth_rel_max"] <= 1e-4, (v, s["depth_rel_max"])
+        assert s["live_over_bound"] == 0, v
         if prec == "fp64":
             assert s["mismatch_all"] == 0
-    assert total_oob <= 1e-3 * n * len(gs)
+            assert s["live_steps_equal"] == s["live_steps"], v
+    assert total_oob <= 1e-4 * n * len(gs)
     ref_sum = np.zeros(max(len(g["live_counts"]) for g in gs), np.int64)
     for g in gs:
         ref_sum[:len(g["live_counts"])] += g["live_counts"]

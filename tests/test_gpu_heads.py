@@ -104,9 +104,10 @@ def test_geo64_objective(st, prec, tol):
     assert np.linalg.norm(grad - ref) / np.linalg.norm(ref) < tol
 
 
-# bf16x3: the -1/(grad f . v) factor reaches ~200 at grazing pixels (SURVEY 0 finding 4), so
-# the few rays whose converged set differs from fp64 dominate the deviation.
-@pytest.mark.parametrize("prec,tol", [("fp64", 1e-8), ("bf16x3", 2e-2)])
+# Grazing pixels (grad f . v >= -0.1, factor > 10) are excluded by one rule in
+# the kernel and the oracle (heads.cuh kImplicitGrazing), so no single pixel's
+# surface-point error is amplified past 10x.
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-8), ("bf16x3", 1e-3), ("fp16x3", 1e-3)])
 def test_implicit_gradient_mode_vs_oracle(st, prec, tol):
     g = load_golden("geo64.npz")
     seed = int(g["seed"])
@@ -126,7 +127,7 @@ def test_implicit_gradient_mode_vs_oracle(st, prec, tol):
     assert np.linalg.norm(g_o - g["obj_grad"]) / np.linalg.norm(g["obj_grad"]) > 1e-2
 
 
-@pytest.mark.parametrize("prec,tol", [("fp64", 1e-8), ("fp16x3", 2e-2)])
+@pytest.mark.parametrize("prec,tol", [("fp64", 1e-8), ("fp16x3", 1e-3)])
 def test_implicit_unit_normal_mode_vs_oracle(st, prec, tol):
     """grad_mode="implicit_unit": the north_star's literal dd/dz = -(1/(n.v)) df/dz
     with n the unit Eq. 3 normal, against the oracle's restatement."""

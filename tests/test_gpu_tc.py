@@ -54,7 +54,7 @@ def test_tc_trace_parity_contract(st, name, prec):
     assert np.array_equal(T.status, g["status"])
     mism = (r.state.status != g["status"]) | (r.state.steps != g["steps"])
     band = (T.margin_f < 1e-5) | (T.margin_esc < 1e-6)
-    assert not np.any((r.state.status == 1) != (g["status"] == 1) & ~band)
+    assert not np.any(((r.state.status == 1) != (g["status"] == 1)) & ~band)
     assert (mism & ~band).sum() <= max(1, 1e-3 * mism.size), np.nonzero(mism & ~band)
     assert abs(r.total_queries - int(g["total_queries"])) <= 2e-3 * int(g["total_queries"])
     dm = st.depth_map(r).reshape(-1)
@@ -78,7 +78,7 @@ def test_tc_trace_nonsquare_ragged_vs_oracle(st, w, h, cs):
     assert np.any(T.status == 1) and np.any(T.status != 1)
     mism = (r.state.status != T.status) | (r.state.steps != T.steps)
     band = (T.margin_f < 1e-5) | (T.margin_esc < 1e-6)
-    assert not np.any((r.state.status == 1) != (T.status == 1) & ~band)
+    assert not np.any(((r.state.status == 1) != (T.status == 1)) & ~band)
     assert (mism & ~band).sum() <= max(1, 1e-3 * mism.size), np.nonzero(mism & ~band)
     tq = sum(T.live_counts)
     assert abs(r.total_queries - tq) <= 2e-3 * tq
