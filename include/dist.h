@@ -249,6 +249,13 @@ DIST_API int dist_code_grad_fixed(const dist_decoder *dec, int n_shapes, const v
                                   void *stream);
 /* padded width of layer 0 (the length of one shape's colsum_fixed row) */
 DIST_API int dist_decoder_colsum_width(const dist_decoder *dec);
+/* The tensor-core decoders' calibrated head gain (measured at creation):
+ * tcgen05 accumulates fp32 in TMEM with truncation toward zero, which shrinks
+ * every hidden pre-activation by a nearly constant relative amount; the
+ * 512 -> 1 head dot is scaled by g = sum(d64^2)/sum(dtc d64) fitted on 65,536
+ * fixed quasi-random points of the unit ball (code 0).  gain2[0]: the
+ * march/eval pack; gain2[1]: the fp16 probe pack.  1.0 for fp64/fp32. */
+DIST_API int dist_decoder_head_gain(const dist_decoder *dec, double *gain2);
 
 /* ---- photometric consistency (losses.py:128-222) ------- */
 /* cams_dev[0] = view i, cams_dev[1] = view j.  Images are row-major doubles
@@ -269,12 +276,15 @@ typedef struct dist_adam_config {
 /* One bias-corrected step per shape; a shape whose gradient has a non-finite
  * entry is skipped and counted.  With shape_terms/best_*: records the loss
  * history hist[iter*S + s] and keeps the best-loss iterate (optimize.py:170-176)
- * before updating. */
+ * before updating.  iter_dev (optional device int32): the iteration index is
+ * read from it instead of `iter` and incremented after the step, so a
+ * captured iterate (CUDA graph) replays correctly. */
 DIST_API int dist_adam_step(int n_shapes, int dim, double *params_dev, const double *grad_dev,
                             double *m_dev, double *v_dev, int32_t *t_dev, int32_t *skipped_dev,
                             const double *shape_terms_dev, double *best_loss_dev,
                             double *best_params_dev, int32_t *best_iter_dev, int iter,
-                            double *hist_dev, const dist_adam_config *cfg, void *stream);
+                            double *hist_dev, const dist_adam_config *cfg, int32_t *iter_dev,
+                            void *stream);
 
 #ifdef __cplusplus
 }

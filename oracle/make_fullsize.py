@@ -174,12 +174,35 @@ def c3(views, check=False):
               f"trace {t1 - t0:.1f}s", flush=True)
 
 
+def c4(views=(0,)):
+    """C4: 1024^2 coarse-to-fine views of a 32-view ring (TraceConfig defaults:
+    alpha 1.5, coarse 4), code z* = N(0,0.1^2) rng 1 -- one view is ~5 min of
+    reference CPU time, so the fixture pins one view of the 32."""
+    field = _decoder()
+    code = np.random.default_rng(1).normal(0.0, 0.1, 256)
+    intr = st.Intrinsics(width=1024, height=1024)
+    cfg = st.TraceConfig()
+    for k in views:
+        pose = st.look_at(orc.ring_eye(k, 32))
+        t0 = time.time()
+        res, mf, me, lvl = harness_trace(field, code, intr, pose, cfg)
+        t1 = time.time()
+        out = _record(res, mf, me, lvl)
+        out.update(seed=np.int64(0), code_seed=np.int64(1), view=np.int64(k), n_ring=np.int64(32),
+                   res=np.int64(1024), omega=pose.omega, t=pose.t, trace_s=t1 - t0)
+        np.savez_compressed(os.path.join(OUT, f"c4_1024_v{k}.npz"), **out)
+        print("c4 view", k, res.total_queries, int((res.state.status == CONVERGED).sum()),
+              f"trace {t1 - t0:.1f}s", flush=True)
+
+
 def main():
     warnings.simplefilter("ignore")
     os.makedirs(OUT, exist_ok=True)
     what = sys.argv[1] if len(sys.argv) > 1 else "c2"
     if what == "c2":
         c2()
+    elif what == "c4":
+        c4([int(a) for a in sys.argv[2:]] or [0])
     elif what == "c3":
         views = [int(a) for a in sys.argv[2:]] or list(range(8))
         # the harness is checked against the reference's own trace on view 0

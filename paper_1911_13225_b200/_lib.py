@@ -102,6 +102,7 @@ _SIGS = {
     "dist_code_grad_fixed": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_double,
                                        C.c_void_p, C.c_void_p]),
     "dist_decoder_colsum_width": (C.c_int, [C.c_void_p]),
+    "dist_decoder_head_gain": (C.c_int, [C.c_void_p, C.POINTER(C.c_double)]),
     "dist_objective": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                  C.c_int, C.POINTER(dist_trace_config), C.POINTER(dist_ray_state),
                                  C.POINTER(dist_objective_io), C.c_void_p, C.c_size_t, C.c_void_p]),
@@ -112,7 +113,7 @@ _SIGS = {
     "dist_adam_step": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_int, C.c_void_p, C.POINTER(dist_adam_config),
-                                 C.c_void_p]),
+                                 C.c_void_p, C.c_void_p]),
 }
 
 _lib = None

@@ -268,6 +268,16 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
   v.np[L - 1] = 1;
   for (int l = 1; l < L; ++l) v.kp[l] = v.np[l - 1];
   v.nskip = skip > 0 ? v.np[skip] : 0;
+  if (prec >= DIST_PREC_BF16X3) {
+    // the tensor-core kernels tile 512-wide hidden layers without a skip
+    // input; any other shape would silently run SIMT fp32 -- refuse instead
+    bool ok = skip < 0 && L >= 3;
+    for (int l = 0; l <= L - 2 && ok; ++l) ok = v.np[l] == kMaxWidth && dims[l + 1] == kMaxWidth;
+    if (!ok)
+      return fail(DIST_ERR_CONFIG,
+                  "tensor-core precisions (bf16x3, fp16x3) need >= 2 hidden layers, all 512 wide, and no "
+                  "skip layer; use precision fp32 or fp64 for this decoder");
+  }
 
   // host staging of every packed array, then one device blob
   std::vector<char> host;
@@ -401,6 +411,7 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
 
 int dist_decoder_destroy(dist_decoder *dec) {
   if (!dec) return DIST_OK;
+  if (dec->view.prec >= DIST_PREC_BF16X3) tc_forget_maps(dec->view);
   cudaFree(dec->blob);
   delete dec;
   return DIST_OK;
@@ -409,6 +420,13 @@ int dist_decoder_destroy(dist_decoder *dec) {
 int dist_decoder_precision(const dist_decoder *dec) { return dec ? dec->view.prec : -1; }
 
 int dist_decoder_colsum_width(const dist_decoder *dec) { return dec ? dec->view.np[0] : -1; }
+
+int dist_decoder_head_gain(const dist_decoder *dec, double *gain2) {
+  if (!dec || !gain2) return fail(DIST_ERR_CONFIG, "null argument");
+  gain2[0] = dec->view.tc_gain[0];
+  gain2[1] = dec->view.tc_gain[1];
+  return DIST_OK;
+}
 
 size_t dist_eval_workspace_size(const dist_decoder *dec, int64_t n, int S) {
   return dec ? eval_ws(dec->view, n, S, true) : 0;

@@ -252,11 +252,12 @@ __global__ void k_shape_finish(const dist_camera *__restrict__ cams, int V, int 
 // complete_shape (optimize.py:170-176) and the loss history.
 __global__ void k_adam(int S, int D, double *params, const double *grad, double *m, double *v,
                        int32_t *t, int32_t *skipped, const double *shape_terms, double *best_loss,
-                       double *best_params, int32_t *best_iter, int iter, double *hist,
-                       dist_adam_config cfg) {
+                       double *best_params, int32_t *best_iter, int iter_host, const int32_t *iter_dev,
+                       double *hist, dist_adam_config cfg) {
   __shared__ int s_bad;
   __shared__ int s_best;
   const int s = blockIdx.x;
+  const int iter = iter_dev ? *iter_dev : iter_host;
   if (threadIdx.x == 0) {
     s_bad = 0;
     s_best = 0;
@@ -301,6 +302,8 @@ __global__ void k_add_reg(int S, int D, const double *__restrict__ codes, double
   for (int k = threadIdx.x; k < D; k += blockDim.x)
     grad[(size_t)s * D + k] += w_lat * (2.0 * codes[(size_t)s * D + k]);
 }
+
+__global__ void k_iter_inc(int32_t *it) { *it += 1; }
 
 struct ObjLayout {
   HeadsDev h;
@@ -597,13 +600,18 @@ int dist_code_grad_fixed(const dist_decoder *dec, int S, const void *colsum_fixe
 int dist_adam_step(int S, int D, double *params, const double *grad, double *m, double *v,
                    int32_t *t, int32_t *skipped, const double *shape_terms, double *best_loss,
                    double *best_params, int32_t *best_iter, int iter, double *hist,
-                   const dist_adam_config *cfg, void *stream) {
+                   const dist_adam_config *cfg, int32_t *iter_dev, void *stream) {
   if (!params || !grad || !m || !v || !t || !skipped || !cfg) return fail(DIST_ERR_CONFIG, "null argument");
   if (S < 1 || D < 0) return fail(DIST_ERR_CONFIG, "bad Adam shape");
   if (D == 0) return DIST_OK;
-  k_adam<<<S, 256, 0, (cudaStream_t)stream>>>(S, D, params, grad, m, v, t, skipped, shape_terms,
-                                              best_loss, best_params, best_iter, iter, hist, *cfg);
+  cudaStream_t st = (cudaStream_t)stream;
+  k_adam<<<S, 256, 0, st>>>(S, D, params, grad, m, v, t, skipped, shape_terms, best_loss, best_params,
+                            best_iter, iter, iter_dev, hist, *cfg);
   DIST_CHECK_LAUNCH("k_adam");
+  if (iter_dev) {   // the iteration index lives on the device (a captured iterate replays as is)
+    k_iter_inc<<<1, 1, 0, st>>>(iter_dev);
+    DIST_CHECK_LAUNCH("k_iter_inc");
+  }
   return DIST_OK;
 }
 

@@ -50,6 +50,7 @@ bool tc_heads_supported(const DecView &dv);
 #include <cuda.h>
 namespace dist {
 int tc_make_map(const DecView &dv, int slot, CUtensorMap *map);
+void tc_forget_maps(const DecView &dv);
 template <class Gen>
 int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
                     fx_t *part0, int *bad, int grid_cap, int *grid_out, cudaStream_t st,

@@ -873,8 +873,14 @@ static int launch_heads_impl(const DecView &dv, const double *c0, const Gen &gen
   P.bad = bad;
   P.gpts = gpts;
   const void *fn = (const void *)tc::k_tc_heads<Gen, BWD>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc heads)");
+  static int attr_dev = -1;   // per instantiation: set once per device
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  if (attr_dev != cur_dev) {
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc heads)");
+    attr_dev = cur_dev;
+  }
   int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n_bound, 128), sm_count() / 2));
   pairs = std::min(pairs, grid_cap / 2);
   *grid_out = 2 * pairs;

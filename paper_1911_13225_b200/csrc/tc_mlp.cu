@@ -35,8 +35,10 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <iterator>
 #include <mutex>
 #include <type_traits>
+#include <unordered_map>
 #include <vector>
 
 #include "common.cuh"
@@ -1097,7 +1099,44 @@ static void fill_fwd(const DecView &dv, const double *const *W, const double *co
   }
 }
 
+// The tensor maps depend only on the (immutable) pack: encoded once per pack
+// and device, then copied (a 128-byte struct) into every launch.
+static std::mutex g_map_mu;
+static std::unordered_map<uint64_t, CUtensorMap> g_maps;
+
+static int tc_encode_map(const DecView &dv, int slot, CUtensorMap *map);
+
 int tc_make_map(const DecView &dv, int slot, CUtensorMap *map) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const uint64_t key = (uint64_t)(uintptr_t)dv.tc_w[slot] ^ ((uint64_t)(dev & 0xff) << 56);
+  {
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *map = it->second;
+      return DIST_OK;
+    }
+  }
+  const int rc = tc_encode_map(dv, slot, map);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  g_maps[key] = *map;
+  return DIST_OK;
+}
+
+// a decoder's packs are freed with it: forget their maps (the blob address
+// can be reused by a later decoder)
+void tc_forget_maps(const DecView &dv) {
+  std::lock_guard<std::mutex> lk(g_map_mu);
+  for (int l = 0; l < kMaxLayers; ++l)
+    if (dv.tc_w[l])
+      for (auto it = g_maps.begin(); it != g_maps.end();)
+        it = ((it->first & ((1ull << 56) - 1)) == ((uint64_t)(uintptr_t)dv.tc_w[l] & ((1ull << 56) - 1)))
+                 ? g_maps.erase(it) : std::next(it);
+}
+
+static int tc_encode_map(const DecView &dv, int slot, CUtensorMap *map) {
   tc::EncodeTiledFn enc = tc::encode_fn();
   if (!enc) return fail(DIST_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const int G = dv.n_layers - 2;
@@ -1143,8 +1182,15 @@ static int launch_tc_t(const DecView &dv, const double *c0, int S, const Rows &r
     P.head_gain = hg ? atof(hg) : dv.tc_gain[slot == 0 ? 0 : 1];
   }
   const void *fn = (const void *)tc::k_tc_mlp<F16, Rows, PAIR>;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
-  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc)");
+  static int attr_dev = -1;   // per instantiation: set once per device
+  int cur_dev = 0;
+  cudaGetDevice(&cur_dev);
+  cudaError_t e = cudaSuccess;
+  if (attr_dev != cur_dev) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(tc)");
+    attr_dev = cur_dev;
+  }
   const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_bound, sm_count() / 2));
   static const bool pdl = [] {
     const char *v = getenv("DIST_TC_PDL");

@@ -402,6 +402,7 @@ __global__ void k_ext_apply(const dist_camera *__restrict__ cams, LevelState ls,
     vb_count(vb, v);
     warp_append(keep, (int32_t)g, out, &ctl->cnt[cur ^ 1]);
   }
+  __syncthreads();   // every warp's NaN count is in s_nan before thread 0 reads it
   step_epilogue(ctl, cur, vb, a, s_nan, stats);
 }
 

@@ -129,6 +129,13 @@ class NeuralField:
         self._handles[self.precision] = out.value
         return out.value
 
+    def head_gain(self) -> tuple:
+        """The calibrated accumulator-bias gain of the tensor-core head
+        (include/dist.h dist_decoder_head_gain): (march/eval, fp16 probes)."""
+        g = (C.c_double * 2)()
+        _lib.check(_lib.lib().dist_decoder_head_gain(self.handle(), g))
+        return float(g[0]), float(g[1])
+
     def __del__(self):
         try:
             lib = _lib._lib

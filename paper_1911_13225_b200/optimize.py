@@ -67,7 +67,7 @@ def adam_step(state: AdamState, params, grads):
     cfg = _lib.dist_adam_config(state.lr, state.beta1, state.beta2, state.eps)
     _lib.check(_lib.lib().dist_adam_step(1, D, P.data_ptr(), G.data_ptr(), M.data_ptr(),
                                          V.data_ptr(), t.data_ptr(), sk.data_ptr(), None, None, None,
-                                         None, 0, None, C.byref(cfg), _lib.stream_ptr()))
+                                         None, 0, None, C.byref(cfg), None, _lib.stream_ptr()))
     state.t, state.skipped = int(t.item()), int(sk.item())
     state.m, state.v = M.cpu().numpy().reshape(p.shape), V.cpu().numpy().reshape(p.shape)
     return P.cpu().numpy().reshape(p.shape)
@@ -205,6 +205,8 @@ class LatentOptimizer:
         self.last_trace = None
         self.timing = None      # a list: _sharded_objective appends (trace start, end, objective end) events
         self._colsum = None
+        self.iter_dev = torch.zeros(1, dtype=torch.int32, device=dev)   # Adam's iteration index
+        self._graph = None
         if shard is not None:
             sov_p = self._parent_shapes()
             oh = np.zeros((self.S, len(self.parent_views)))
@@ -322,7 +324,36 @@ class LatentOptimizer:
             self.v.data_ptr(), self.t.data_ptr(), self.skipped.data_ptr(),
             self.shape_terms.data_ptr(), self.best_loss.data_ptr(), self.best_code.data_ptr(),
             self.best_iter.data_ptr(), self.iter, self.hist.data_ptr(), C.byref(self.adam_cfg),
-            _lib.stream_ptr()))
+            self.iter_dev.data_ptr(), _lib.stream_ptr()))
+        self.iter += 1
+
+    def step_graph(self):
+        """step() replayed from a CUDA graph: the first call runs one eager
+        iterate (buffers, workspaces, lazily loaded kernels), the second
+        captures one iterate -- every launch of the trace slots, the heads, the
+        fused backward, the reductions and Adam, whose iteration index lives on
+        the device -- and every later call replays it with one launch.  Not for
+        sharded optimisers (their collectives run between launches)."""
+        import torch
+        if self.shard is not None:
+            raise ValueError("step_graph: sharded optimisers step eagerly")
+        if self.iter >= self.max_iters:
+            raise ValueError("max_iters exceeded")
+        if self.last_trace is None:
+            self.step()
+            return
+        if self._graph is None:
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.graph(g, stream=s):
+                self.objective()
+                self._adam()
+            self._graph, self._graph_stream = g, s
+            torch.cuda.current_stream().wait_stream(s)
+            # capture records the iterate without running it
+            self.iter -= 1
+        self._graph.replay()
         self.iter += 1
 
     def step(self, reduce_fn=None):

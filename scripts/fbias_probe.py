@@ -40,4 +40,6 @@ for prec in ("fp16x3", "bf16x3", "fp32"):
     out[prec] = {"mean": float(e.mean()), "median": float(np.median(e)), "std": float(e.std()),
                  "mean_near_surface": float(e[near].mean()), "std_near_surface": float(e[near].std()),
                  "maxabs": float(np.abs(e).max()), "fit_bias_slope": [float(c) for c in coef]}
+for prec in ("fp16x3", "bf16x3"):
+    out[prec]["head_gain"] = f64.with_precision(prec).head_gain()
 print(json.dumps(out))

@@ -213,3 +213,52 @@ def test_dynamic_mask_off_on_tensor_cores(st, prec):
     assert off.total_queries > on.total_queries
     # the reference's count without the mask: every ray of the level, each step
     assert all(c in (16 * 16, 32 * 32, 64 * 64) for c in off.live_counts)
+
+
+def test_tensor_core_precision_refuses_unsupported_shapes(st):
+    """A tensor-core precision on a decoder the tcgen05 kernels cannot tile
+    (skip layer, hidden width != 512) raises instead of silently running SIMT."""
+    with pytest.raises(ValueError):
+        st.NeuralField.geometric(256, (512,) * 8, 0, skip=4, precision="fp16x3").handle()
+    with pytest.raises(ValueError):
+        st.NeuralField.geometric(64, (256,) * 4, 0, precision="bf16x3").handle()
+    st.NeuralField.geometric(256, (512,) * 8, 0, skip=4, precision="fp32").handle()
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp16x3"])
+def test_graph_replayed_iterates_equal_eager(st, prec):
+    """LatentOptimizer.step_graph (one CUDA graph per iterate, the Adam
+    iteration index on the device) gives the eager iterates bit for bit: codes,
+    loss history and best iterate."""
+    import time
+    import torch
+    from paper_1911_13225_b200.workloads import render_depth_observations, ring_views, target_code
+    if prec == "fp64":
+        net, code = _tiny(st)
+        views = [(st.Intrinsics(width=64, height=64), st.look_at((0.0, 0.0, -2.0)))]
+        obs = render_depth_observations(net, code + 0.05, views, st.TraceConfig(k_samples=3))
+        z0 = np.zeros((1, 2))
+    else:
+        net = st.NeuralField.geometric(256, (512,) * 8, 0, precision=prec)
+        views = ring_views(2, 64)
+        obs = render_depth_observations(net, target_code(1), views, st.TraceConfig(k_samples=3))
+        z0 = np.zeros((1, 256))
+    cfg = st.TraceConfig(k_samples=3)
+    runs = {}
+    for mode in ("eager", "graph"):
+        opt = st.LatentOptimizer(net, views, {"depth": obs}, z0, cfg, max_iters=12)
+        codes = []
+        for _ in range(6):
+            (opt.step if mode == "eager" else opt.step_graph)()
+            codes.append(opt.code.cpu().numpy().copy())
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(6):
+            (opt.step if mode == "eager" else opt.step_graph)()
+        torch.cuda.synchronize()
+        runs[mode] = (np.stack(codes), opt.losses(), int(opt.best_iter[0].item()),
+                      (time.perf_counter() - t0) / 6 * 1e3)
+    assert np.array_equal(runs["eager"][0], runs["graph"][0])
+    assert np.array_equal(runs["eager"][1], runs["graph"][1])
+    assert runs["eager"][2] == runs["graph"][2]
+    print(f"{prec}: ms per iterate eager {runs['eager'][3]:.3f} graph {runs['graph'][3]:.3f}")
