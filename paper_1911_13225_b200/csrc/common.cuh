@@ -46,6 +46,8 @@ struct DecView {
   const void *W[2][kMaxLayers], *Wt[2][kMaxLayers], *bias[2][kMaxLayers];
   // skip layer extra input rows (code+xyz part) kept in fp64: Wsz [D][np], Wsp [3][np]
   const double *Wsz, *Wsp;
+  const float *Wspf;      // fp32 copy of Wsp for the tensor-core epilogues
+  float wsm[3];           // max |Wsp row a| (bounds the fp16 row scale of the skip layer)
   int nskip;              // np[skip] (0 if no skip)
   // output layer: w_out [kp_out] (fp64 / fp32 copies), b_out
   const void *w_out[2];

@@ -69,12 +69,16 @@ __global__ void k_code_bias(DecView dv, const double *__restrict__ codes, int S,
     atomicMax(reinterpret_cast<int *>(c0 + total) + total + s, __float_as_int(fabsf((float)v)));
   }
   if (dv.skip > 0) {
+    // the skip layer's code part, laid out like c0 (fp64, fp32 copy, per-shape max |.|)
     const int ns = dv.nskip;
     const int tot2 = S * ns;
     for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < tot2;
          idx += gridDim.x * blockDim.x) {
       const int s = idx / ns, j = idx % ns;
-      cskip[idx] = dot_ordered<16>(codes + (size_t)s * D, 1, dv.Wsz + j, ns, D, 0.0);
+      const double v = codes ? dot_ordered<16>(codes + (size_t)s * D, 1, dv.Wsz + j, ns, D, 0.0) : 0.0;
+      cskip[idx] = v;
+      reinterpret_cast<float *>(cskip + tot2)[idx] = (float)v;
+      atomicMax(reinterpret_cast<int *>(cskip + tot2) + tot2 + s, __float_as_int(fabsf((float)v)));
     }
   }
 }
@@ -84,6 +88,8 @@ int launch_code_bias(const DecView &dv, const double *codes, int S, double *c0, 
   if (S <= 0) return DIST_OK;
   const int n = S * dv.np[0];
   cudaError_t e = cudaMemsetAsync(const_cast<float *>(c0_absmax(c0, S, dv.np[0])), 0, sizeof(float) * S, st);
+  if (e == cudaSuccess && dv.skip > 0)
+    e = cudaMemsetAsync(const_cast<float *>(c0_absmax(cskip, S, dv.nskip)), 0, sizeof(float) * S, st);
   if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(c0 max)");
   const int nmax = std::max(n, S * std::max(dv.nskip, 0));
   k_code_bias<<<(int)std::min<int64_t>(ceil_div(nmax, 64), 4096), 64, 0, st>>>(dv, codes, S, c0, cskip);
@@ -201,7 +207,7 @@ size_t eval_ws(const DecView &dv, int64_t n, int S, bool vjp) {
   Carve cv{nullptr, 0, ~size_t(0)};
   const int s1 = std::max(S, 1);
   cv.take<double>(c0_doubles(s1, dv.np[0]));
-  cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
+  cv.take<double>(c0_doubles(s1, std::max(dv.nskip, 1)));
   if (vjp) {
     const int G = vjp_grid_cap(dv.prec);
     cv.take<fx_t>((size_t)G * s1 * dv.np[0]);
@@ -304,7 +310,7 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
     for (int j = 0; j < dims[1]; ++j) b0[j] = b[0][j];
   }
   size_t o_W[2][kMaxLayers] = {}, o_Wt[2][kMaxLayers] = {}, o_b[2][kMaxLayers] = {};
-  size_t o_Wsz = 0, o_Wsp = 0;
+  size_t o_Wsz = 0, o_Wsp = 0, o_Wspf = 0;
   for (int l = 1; l <= L - 2; ++l) {
     const int K = v.kp[l], N = v.np[l];
     const int kin = dims[l], nout = dims[l + 1];  // true h-part input width and output width
@@ -334,12 +340,22 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
     if (l == skip) {
       o_Wsz = put(sizeof(double) * std::max(D, 1) * N);
       o_Wsp = put(sizeof(double) * 3 * N);
+      o_Wspf = put(sizeof(float) * 3 * N);
       double *Wsz = (double *)(host.data() + o_Wsz);
       double *Wsp = (double *)(host.data() + o_Wsp);
+      float *Wspf = (float *)(host.data() + o_Wspf);
       for (int k = 0; k < D; ++k)
         for (int j = 0; j < nout; ++j) Wsz[(size_t)k * N + j] = W[l][(size_t)(kin + k) * nout + j];
-      for (int a = 0; a < 3; ++a)
-        for (int j = 0; j < nout; ++j) Wsp[(size_t)a * N + j] = W[l][(size_t)(kin + D + a) * nout + j];
+      for (int a = 0; a < 3; ++a) {
+        double m = 0.0;
+        for (int j = 0; j < nout; ++j) {
+          const double w = W[l][(size_t)(kin + D + a) * nout + j];
+          Wsp[(size_t)a * N + j] = w;
+          Wspf[(size_t)a * N + j] = (float)w;
+          m = std::max(m, std::fabs(w));
+        }
+        v.wsm[a] = (float)(m * (1.0 + 1e-6));   // rounded up: a bound
+      }
     }
   }
   const int Ko = v.np[L - 2];
@@ -384,6 +400,7 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
     }
   v.Wsz = skip > 0 ? (const double *)(base + o_Wsz) : nullptr;
   v.Wsp = skip > 0 ? (const double *)(base + o_Wsp) : nullptr;
+  v.Wspf = skip > 0 ? (const float *)(base + o_Wspf) : nullptr;
   v.w_out[0] = base + o_wo[0];
   v.w_out[1] = base + o_wo[1];
   if (prec >= DIST_PREC_BF16X3)
@@ -442,7 +459,7 @@ int dist_eval(const dist_decoder *dec, const double *codes, int S, const double 
   Carve cv{(char *)ws, 0, ws_bytes};
   const int s1 = std::max(S, 1);
   double *c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
-  double *cs = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
+  double *cs = cv.take<double>(c0_doubles(s1, std::max(dv.nskip, 1)));
   if (!cv.ok) return fail(DIST_ERR_CONFIG, "workspace too small");
   int rc;
   if (dv.latent_dim > 0) {
@@ -464,7 +481,7 @@ int dist_eval_vjp(const dist_decoder *dec, const double *codes, int S, const dou
   const int s1 = std::max(S, 1);
   Carve cv{(char *)ws, 0, ws_bytes};
   double *c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
-  double *cs = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
+  double *cs = cv.take<double>(c0_doubles(s1, std::max(dv.nskip, 1)));
   const int G = vjp_grid_cap(dv.prec);
   fx_t *part0 = cv.take<fx_t>((size_t)G * s1 * dv.np[0]);
   fx_t *parts = cv.take<fx_t>((size_t)G * s1 * std::max(dv.nskip, 1));

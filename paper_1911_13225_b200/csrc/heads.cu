@@ -357,7 +357,7 @@ static ObjLayout obj_layout(const DecView &dv, int V, int W, int H, int K, int S
   L.loss_part = cv.take<double>((size_t)V * std::max(kLossBlocks, 3 * kPrepBlocks));
   L.bcount = cv.take<int32_t>(ceil_div(n * K, kScanBlock) + 1);
   L.c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
-  L.cs = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
+  L.cs = cv.take<double>(c0_doubles(s1, std::max(dv.nskip, 1)));
   const int G = vjp_grid_cap(dv.prec);
   L.part0 = cv.take<fx_t>((size_t)G * s1 * dv.np[0]);
   L.parts = cv.take<fx_t>((size_t)G * s1 * std::max(dv.nskip, 1));

@@ -62,7 +62,7 @@ struct ObjGen;
 // backward-only head rows (f and ReLU masks from the march's mask record)
 int launch_tc_heads_bwd(const DecView &dv, const double *c0, const ObjGen &gen, int64_t n_bound, int S,
                         fx_t *part0, int *bad, int grid_cap, int *grid_out, cudaStream_t st);
-int tc_eval_probes(const DecView &dv, const double *c0, int S, const ProbeGen &gen, int64_t n_bound,
+int tc_eval_probes(const DecView &dv, const double *c0, const double *cs, int S, const ProbeGen &gen, int64_t n_bound,
                    cudaStream_t st);
 int normals_pass(const DecView &dv, const double *c0, const double *cs, int S, const dist_camera *cams,
                  const LevelState &ls, const dist_trace_config *cfg, double *normals, double *gdotv,

@@ -59,6 +59,12 @@ struct Params {
   const float *winv;      // [L-2] inverse power-of-2 weight scales (fp16x3), 1 for bf16x3
   const float *cn, *bm, *w0m;  // fp16 row-scale bounds (tc_mlp.cu fill_fwd)
   const float *c0max;     // [S] max |c0| per shape
+  // DeepSDF skip layer: GEMM skipg computes the skip
+  // layer's pre-activation, to which the epilogue adds the per-shape code part
+  // cskf[s] and the row's p . Wsp (the layer's concat(code, xyz) input rows)
+  int skipg;              // -1: no skip
+  const float *cskf;      // [S][512] fp32 (kernels.cuh c0 layout of cskip)
+  const float *cskmax;    // [S] max |cskip|
   int n_gemm;             // hidden GEMM layers (L-2)
   int acc_mode;           // 0: one accumulator; 1: two (even/odd K blocks); 2: hi*hi | corrections;
                           // 3 (default): as 2, stage-grouped; 4 (experiment): single pass, hi*hi only
@@ -626,6 +632,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       // columns just read -- they cannot go to A yet, the nh = 1 MMAs still read
       // A.  After the GEMM, the parked words are copied to A, K blocks 0..3 are
       // announced, then the nh = 1 columns are processed.
+      // The DeepSDF skip layer (GEMM P.skipg) also takes concat(code, p): its
+      // per-shape code part (cskf, folded like c0) and p . Wsp join the bias.
+      // Pair mode: the even row carries the midpoint's terms, the odd (diff)
+      // row only the half-offset's p . Wsp (no bias, no code part).
+      auto load_bias8 = [&](int l, const float *bias, int col, float (&bb)[8]) {
+        ldg8(bias + col, bb);
+        if constexpr (PAIR) {
+          if (odd) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) bb[e] = 0.f;
+          }
+        }
+        if (l == P.skipg) {
+          const int ns = P.dv.nskip;
+          float w0[8], w1[8], w2[8], cf[8];
+          ldg8(P.dv.Wspf + col, w0);
+          ldg8(P.dv.Wspf + ns + col, w1);
+          ldg8(P.dv.Wspf + 2 * ns + col, w2);
+          ldg8(P.cskf + (size_t)(s < 0 ? 0 : s) * ns + col, cf);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            if (PAIR && odd) bb[e] += fmaf(oz, w2[e], fmaf(oy, w1[e], ox * w0[e]));
+            else bb[e] += fmaf(pz, w2[e], fmaf(py, w1[e], fmaf(px, w0[e], cf[e])));
+          }
+        }
+      };
+      // |skip terms| <= max|cskip| + sum_a |p_a| max|Wsp row a| (the fp16 row-scale bound)
+      auto skip_bound = [&]() -> float {
+        return s >= 0 ? P.cskmax[s] + fabsf(px) * P.dv.wsm[0] + fabsf(py) * P.dv.wsm[1] + fabsf(pz) * P.dv.wsm[2]
+                      : 0.f;
+      };
       for (int l = 0; l < G; ++l, ++layer) {
         if (l == G - 1) fetch(t + nclusters, nx);
         const bool last = (l == G - 1);
@@ -634,7 +671,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         // bias + ReLU (pair mode: diff rows carry no bias; ReLU of the pair)
         auto act = [&](float v, float bb) -> float {
           if constexpr (PAIR) {
-            const float y = fmaf(v, unscale, odd ? 0.f : bb);
+            const float y = fmaf(v, unscale, bb);   // load_bias8: the diff row's bias is 0
             const float yp = __shfl_xor_sync(0xffffffffu, y, 1);
             return relu_pair_sel(odd ? yp : y, odd ? y : yp, odd);
           } else {
@@ -645,7 +682,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (kEarly && P.debug != 1) {
           float inv = 1.f, part = 0.f;
           if (!last && kBound) {
-            sc = pow2_scale((amax * P.cn[l] + P.bm[l]) * 1.000001f);
+            sc = pow2_scale((amax * P.cn[l] + P.bm[l] + (l == P.skipg ? skip_bound() : 0.f)) * 1.000001f);
             inv = 1.f / sc;
           }
           mbar_wait(&m.dfull[0], layer & 1);
@@ -664,7 +701,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
               for (int g8 = 0; g8 < 4; ++g8) {
                 float bb[8], x[8];
-                ldg8(bias + cb + c * 32 + g8 * 8, bb);
+                load_bias8(l, bias, cb + c * 32 + g8 * 8, bb);
                 if (last) {
                   float wo[8];
                   ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
@@ -782,7 +819,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
               for (int g8 = 0; g8 < 4; ++g8) {
                 float x[8], bb[8];
-                ldg8(bias + cb + c * 32 + g8 * 8, bb);
+                load_bias8(l, bias, cb + c * 32 + g8 * 8, bb);
                 if (last) {
                   float wo[8];
                   ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
@@ -848,7 +885,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
               for (int g8 = 0; g8 < 4; ++g8) {
                 float bb[8], wo[8];
-                ldg8(bias + cb + c * 32 + g8 * 8, bb);
+                load_bias8(l, bias, cb + c * 32 + g8 * 8, bb);
                 if (last) ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
@@ -872,7 +909,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
               for (int g8 = 0; g8 < 4; ++g8) {
                 float x[8], bb[8];
-                ldg8(bias + cb + c * 32 + g8 * 8, bb);
+                load_bias8(l, bias, cb + c * 32 + g8 * 8, bb);
 #pragma unroll
                 for (int e = 0; e < 8; ++e) x[e] = act(v[g8 * 8 + e], bb[e]) * sc;
                 put8<F16>(smem, row, cb + c * 32 + g8 * 8, x);
@@ -1154,7 +1191,7 @@ static int tc_encode_map(const DecView &dv, int slot, CUtensorMap *map) {
 }
 
 template <bool F16, class Rows, bool PAIR = false>
-static int launch_tc_t(const DecView &dv, const double *c0, int S, const Rows &rows,
+static int launch_tc_t(const DecView &dv, const double *c0, const double *cs, int S, const Rows &rows,
                        int64_t tiles_bound, cudaStream_t st, int slot = 0) {
   CUtensorMap map;
   int rc = tc_make_map(dv, slot, &map);
@@ -1171,6 +1208,9 @@ static int launch_tc_t(const DecView &dv, const double *c0, int S, const Rows &r
   P.bm = P.cn + (dv.n_layers - 2);
   P.w0m = P.bm + (dv.n_layers - 2);
   P.c0max = c0_absmax(c0, S, dv.np[0]);
+  P.skipg = dv.skip > 0 ? dv.skip - 1 : -1;
+  P.cskf = dv.skip > 0 ? c0_f32(cs, S, dv.nskip) : nullptr;
+  P.cskmax = dv.skip > 0 ? c0_absmax(cs, S, dv.nskip) : nullptr;
   {
     const char *am = getenv("DIST_TC_ACC");
     P.acc_mode = am ? atoi(am) : 3;
@@ -1213,10 +1253,10 @@ static int launch_tc_t(const DecView &dv, const double *c0, int S, const Rows &r
 }
 
 template <class Rows, bool PAIR = false>
-static int launch_tc(const DecView &dv, const double *c0, int S, const Rows &rows,
+static int launch_tc(const DecView &dv, const double *c0, const double *cs, int S, const Rows &rows,
                      int64_t tiles_bound, cudaStream_t st) {
-  if (dv.prec == DIST_PREC_FP16X3) return launch_tc_t<true, Rows, PAIR>(dv, c0, S, rows, tiles_bound, st);
-  return launch_tc_t<false, Rows, PAIR>(dv, c0, S, rows, tiles_bound, st);
+  if (dv.prec == DIST_PREC_FP16X3) return launch_tc_t<true, Rows, PAIR>(dv, c0, cs, S, rows, tiles_bound, st);
+  return launch_tc_t<false, Rows, PAIR>(dv, c0, cs, S, rows, tiles_bound, st);
 }
 
 extern "C" DIST_API int dist_debug_mlp_timeline(unsigned long long *out, int n) {
@@ -1224,13 +1264,13 @@ extern "C" DIST_API int dist_debug_mlp_timeline(unsigned long long *out, int n) 
                  cudaSuccess ? 0 : -1;
 }
 
-int tc_eval_probes(const DecView &dv, const double *c0, int S, const ProbeGen &gen, int64_t n_bound,
+int tc_eval_probes(const DecView &dv, const double *c0, const double *cs, int S, const ProbeGen &gen, int64_t n_bound,
                    cudaStream_t st) {
   tc::ProbeRows rows{gen};
   // always fp16x3: a bf16x3 decoder carries an fp16 probe pack in slot 2
   const int slot = dv.prec == DIST_PREC_FP16X3 ? 0 : 2;
   if (!dv.tc_w[slot]) return fail(DIST_ERR_CONFIG, "decoder has no fp16 probe pack");
-  return launch_tc_t<true, tc::ProbeRows, true>(dv, c0, S, rows, ceil_div(n_bound, 128), st, slot);
+  return launch_tc_t<true, tc::ProbeRows, true>(dv, c0, cs, S, rows, ceil_div(n_bound, 128), st, slot);
 }
 
 int tc_eval_points(const DecView &dv, const double *c0, const double *cskip, int S, const double *pts,
@@ -1240,7 +1280,7 @@ int tc_eval_points(const DecView &dv, const double *c0, const double *cskip, int
     return launch_eval_gen<float>(dv, c0, cskip, g, n, st);
   }
   tc::EvalRows rows{pts, shape, f, n};
-  return launch_tc(dv, c0, S, rows, ceil_div(n, 128), st);
+  return launch_tc(dv, c0, cskip, S, rows, ceil_div(n, 128), st);
 }
 
 // Accumulator-bias calibration.  tcgen05 accumulates fp32 in TMEM with
@@ -1287,7 +1327,7 @@ int tc_calibrate(DecView &dv) {
   cv.take<double>(N);
   cv.take<double>(N);
   cv.take<double>(c0_doubles(1, dv.np[0]));
-  cv.take<double>(std::max(dv.nskip, 1));
+  cv.take<double>(c0_doubles(1, std::max(dv.nskip, 1)));
   cv.take<double>(std::max(dv.latent_dim, 1));
   void *buf = nullptr;
   cudaError_t e = cudaMalloc(&buf, cv.off + 256);
@@ -1297,7 +1337,7 @@ int tc_calibrate(DecView &dv) {
   double *f64 = c2.take<double>(N);
   double *ftc = c2.take<double>(N);
   double *c0 = c2.take<double>(c0_doubles(1, dv.np[0]));
-  double *cs = c2.take<double>(std::max(dv.nskip, 1));
+  double *cs = c2.take<double>(c0_doubles(1, std::max(dv.nskip, 1)));
   double *z0 = c2.take<double>(std::max(dv.latent_dim, 1));   // code 0
   cudaStream_t st = 0;
   int rc = DIST_OK;
@@ -1319,8 +1359,8 @@ int tc_calibrate(DecView &dv) {
     const int slot = which == 0 ? 0 : (f16 ? 0 : 2);   // the pack each gain serves
     if (!dv.tc_w[slot]) continue;
     tc::EvalRows rows{pts, nullptr, ftc, N};
-    rc = (slot == 0 && !f16) ? launch_tc_t<false, tc::EvalRows>(dv, c0, 1, rows, ceil_div(N, 128), st, slot)
-                             : launch_tc_t<true, tc::EvalRows>(dv, c0, 1, rows, ceil_div(N, 128), st, slot);
+    rc = (slot == 0 && !f16) ? launch_tc_t<false, tc::EvalRows>(dv, c0, cs, 1, rows, ceil_div(N, 128), st, slot)
+                             : launch_tc_t<true, tc::EvalRows>(dv, c0, cs, 1, rows, ceil_div(N, 128), st, slot);
     if (rc) break;
     e = cudaMemcpy(htc.data(), ftc, sizeof(double) * N, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) {
@@ -1345,12 +1385,11 @@ int tc_calibrate(DecView &dv) {
 int tc_run_steps(const DecView &dv, const double *c0, const double *cskip, int S, const dist_camera *cams,
                  const LevelState &ls, Ctl *ctl, int32_t *l0, int32_t *l1, const MarchArgs &a,
                  int slots, const ViewBudget &vb, int64_t *stats, cudaStream_t st) {
-  (void)cskip;
   tc::MarchRows rows{cams, ls, ctl, l0, l1, a, vb, stats};
   tc::MarchRowsM rows_m{rows};
   for (int s = 0; s < slots; ++s) {
-    int rc = ls.masks ? launch_tc(dv, c0, S, rows_m, ceil_div(ls.n, 128), st)
-                      : launch_tc(dv, c0, S, rows, ceil_div(ls.n, 128), st);
+    int rc = ls.masks ? launch_tc(dv, c0, cskip, S, rows_m, ceil_div(ls.n, 128), st)
+                      : launch_tc(dv, c0, cskip, S, rows, ceil_div(ls.n, 128), st);
     if (rc) return rc;
   }
   return DIST_OK;

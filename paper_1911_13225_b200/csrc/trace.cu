@@ -339,7 +339,7 @@ int normals_pass(const DecView &dv, const double *c0, const double *cs, int S, c
   // On tensor-core decoders the pairs run through k_tc_mlp's pair mode.
   const int pair = dv.prec == DIST_PREC_FP64 ? 0 : 1;
   if (!pair) rc = launch_eval_gen<double>(dv, c0, cs, gen, n * 6, st);
-  else if (tc_supported(dv)) rc = tc_eval_probes(dv, c0, S, gen, n * 6, st);
+  else if (tc_supported(dv)) rc = tc_eval_probes(dv, c0, cs, S, gen, n * 6, st);
   else rc = launch_eval_gen<float, ProbeGen, true>(dv, c0, cs, gen, n * 6, st);
   if (rc) return rc;
   k_normals_assemble<<<grid_for(n, 256), 256, 0, st>>>(cams, ls, conv, count, f, cfg->normal_delta,
@@ -440,7 +440,7 @@ static TraceLayout layout(const DecView &dv, const dist_trace_config *cfg, int V
   Carve cv{ws, 0, cap};
   const int s1 = std::max(S, 1);
   L.c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
-  L.cskip = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
+  L.cskip = cv.take<double>(c0_doubles(s1, std::max(dv.nskip, 1)));
   int levels[3], nl = 0;
   for (int s = cfg->coarse_start_scale; s >= 1; s /= 2) levels[nl++] = s;
   L.n_levels = nl;
@@ -669,7 +669,7 @@ size_t dist_normals_workspace_size(const dist_decoder *dec, int V, int W, int H,
   Carve cv{nullptr, 0, ~size_t(0)};
   const int s1 = std::max(S, 1);
   cv.take<double>(c0_doubles(s1, dec->view.np[0]));
-  cv.take<double>((size_t)s1 * std::max(dec->view.nskip, 1));
+  cv.take<double>(c0_doubles(s1, std::max(dec->view.nskip, 1)));
   cv.take<int32_t>(n);
   cv.take<int32_t>(4);
   cv.take<int32_t>(ceil_div(n, kScanBlock) + 1);
@@ -687,7 +687,7 @@ int dist_normals(const dist_decoder *dec, const double *codes, int S, const dist
   const int s1 = std::max(S, 1);
   Carve cv{(char *)ws, 0, ws_bytes};
   double *c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
-  double *cs = cv.take<double>((size_t)s1 * std::max(dv.nskip, 1));
+  double *cs = cv.take<double>(c0_doubles(s1, std::max(dv.nskip, 1)));
   int32_t *conv = cv.take<int32_t>(n);
   int32_t *count = cv.take<int32_t>(4);
   int32_t *bcount = cv.take<int32_t>(ceil_div(n, kScanBlock) + 1);
