@@ -39,6 +39,22 @@ F_Q = 3_674_112      # algorithmic FLOP per decoder query (layer 0 folded, no sk
 F_B = 3_671_040      # algorithmic FLOP per differentiated sample (dgrad, no wgrad), SURVEY 8d
 
 
+def _flops(skip):
+    """(F_Q, F_B) of the 8x512 decoder; skip >= 0 (DeepSDF layout): layer
+    skip-1 is 512 -> 512-259 wide and layer `skip` reads concat(h, code, xyz)
+    with its code rows folded into a per-shape bias like layer 0's."""
+    if skip < 0:
+        return F_Q, F_B
+    hid = [512] * 8
+    outs = [hid[i] - (259 if i + 1 == skip else 0) for i in range(8)] + [1]
+    fwd = 3 * outs[0]
+    bwd = 0
+    for i in range(1, 9):
+        fwd += (outs[i - 1] + (3 if i == skip else 0)) * outs[i]
+        bwd += outs[i - 1] * outs[i]
+    return 2 * fwd, 2 * bwd
+
+
 def _traffic(queries):
     """DRAM bytes of the march kernel per trace phase: bytes/query from the
     committed ncu --set full capture (profiles/r01_ncu_traffic.json) x this
@@ -133,12 +149,14 @@ class _RefSample:
     geometric-init decoder, code 0, depth observation of z* -- the first C3
     iterate.  Falls back to the oracle's numpy port when the copy is absent."""
 
-    def __init__(self):
+    def __init__(self, skip=-1):
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import sdf_oracle as orc
         from paper_1911_13225_b200.workloads import ring_eye, target_code
-        self.kind = "reference" if os.path.isdir(os.path.join(REF_DIR, "sdftrace")) else "port"
-        ws = orc.geometric_init(256, (512,) * 8, 0)
+        # the reference decoder has no skip layer: the skip-4 layout times the port
+        self.kind = "reference" if skip < 0 and os.path.isdir(os.path.join(REF_DIR, "sdftrace")) else "port"
+        self.skip = skip
+        ws = orc.geometric_init(256, (512,) * 8, 0, skip=skip) if skip >= 0 else orc.geometric_init(256, (512,) * 8, 0)
         z_true = target_code(1)
         c = REF_CROP
         x0 = (RES - c) // 2
@@ -157,7 +175,7 @@ class _RefSample:
             self.obs = [ref.Observation("depth", obs)]
         else:
             self.orc = orc
-            self.dec = orc.Decoder(ws, 256)
+            self.dec = orc.Decoder(ws, 256, skip=skip) if skip >= 0 else orc.Decoder(ws, 256)
             self.cam = orc.cam_look_at(ring_eye(0, VIEWS_PER_RANK), c, c)   # port: a c x c view
             self.cfg = orc.Cfg(k_samples=3)
             self.obs = orc.depth_map(orc.trace(lambda p: self.dec(p, z_true), self.cam, self.cfg), self.cfg)
@@ -178,16 +196,17 @@ class _RefSample:
         return c * c / dt, {"cores": cores, "seconds": dt, "queries": q, "kind": self.kind,
                             "sample": f"the central {c}x{c} pixels of a 512^2 C3 ring view (same rays), one "
                                       f"full iterate (trace + heads + loss + backward) of {what}, "
-                                      f"8x512 decoder, numpy fp64 with {cores}-thread BLAS"}
+                                      f"8x512 decoder{'' if self.skip < 0 else f' (skip {self.skip})'}, "
+                                      f"numpy fp64 with {cores}-thread BLAS"}
 
 
 _REF = None
 
 
-def cpu_reference_sample():
+def cpu_reference_sample(skip=-1):
     global _REF
     if _REF is None:
-        _REF = _RefSample()
+        _REF = _RefSample(skip)
     return _REF()
 
 
@@ -196,10 +215,10 @@ def run_reference(args):
     if rank != 0:
         return 0
     for _ in range(args.warmup):
-        cpu_reference_sample()
+        cpu_reference_sample(args.skip)
     vals, infos = [], []
     for _ in range(args.steps):
-        v, info = cpu_reference_sample()
+        v, info = cpu_reference_sample(args.skip)
         vals.append(v)
         infos.append(info)
     val = float(np.mean(vals))
@@ -224,11 +243,12 @@ def _config(args, world=1):
            if strong else
            f"views sharded over {world} GPU(s) (ring interleaved, {VIEWS_PER_RANK} per GPU), latent all-reduce")
     return {"workload": f"C3: {VIEWS_PER_RANK} views x {RES}x{RES} depth-supervised latent "
-                        f"optimisation, 8x512 DeepSDF decoder (latent 256, geometric init seed 0), "
+                        f"optimisation, 8x512 DeepSDF decoder (latent 256, geometric init seed 0"
+                        f"{'' if getattr(args, 'skip', -1) < 0 else f', layer-{args.skip} skip'}), "
                         f"K=3, alpha 1.5, coarse 4, 100 steps" +
                         ("" if strong or world == 1 else f" (per GPU; {VIEWS_PER_RANK * world} views in all)"),
             "views_per_gpu": VIEWS_PER_RANK / world if strong else VIEWS_PER_RANK,
-            "resolution": RES, "precision": args.precision,
+            "resolution": RES, "precision": args.precision, "skip": getattr(args, "skip", -1),
             "parallelism": par,
             "l2": "working set > L2 (ray state ~320 MB per step)",
             "relu_mask_record": (not getattr(args, "no_relu_masks", False)) and args.precision in ("bf16x3", "fp16x3")}
@@ -250,6 +270,8 @@ def main():
     # the ranks; "weak" gives every rank 8 views of an 8N-view ring
     ap.add_argument("--scaling", default="strong", choices=["strong", "weak"])
     ap.add_argument("--tile", type=int, default=32)
+    ap.add_argument("--skip", type=int, default=-1,
+                    help="DeepSDF skip layer (4: concat(h, code, xyz) into layer 4); -1: the reference's plain MLP")
     ap.add_argument("--force-tiles", action="store_true",
                     help="run the tiled (sharded) path even at N=1 (measures its overhead)")
     args = ap.parse_args()
@@ -277,7 +299,9 @@ def main():
     from paper_1911_13225_b200.workloads import render_depth_observations, ring_views, target_code
 
     strong = (world > 1 and args.scaling == "strong") or args.force_tiles
-    field = st.NeuralField.geometric(256, (512,) * 8, 0, precision=args.precision)
+    field = (st.NeuralField.geometric(256, (512,) * 8, 0, precision=args.precision, skip=args.skip)
+             if args.skip >= 0 else st.NeuralField.geometric(256, (512,) * 8, 0, precision=args.precision))
+    f_q, f_b = _flops(args.skip)
     cfg = st.TraceConfig(k_samples=3)
     iters = args.warmup + args.steps
     relu = False if args.no_relu_masks else "auto"
@@ -421,7 +445,7 @@ def main():
     # march (k_tc_mlp in march mode for bf16x3).  achieved = algorithmic FLOP
     # (F_Q per query) / device time of the trace phase; executed MMA
     # FLOP are 3x for the split-precision scheme.
-    flops_trace = queries * F_Q
+    flops_trace = queries * f_q
     achieved = flops_trace / (trace_ms * 1e-3) / 1e12
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     split = 3.0 if args.precision in ("bf16x3", "fp16x3") else 1.0
@@ -448,7 +472,7 @@ def main():
                      "executed_frac": achieved * split / peak,
                      "kernel": "march step kernels (decoder + update), whole trace phase",
                      "peak_source": f"{peak_kind} bf16 sustained (MEASURED_PEAKS.json; fp16 MMAs run at the bf16 rate)",
-                     "algorithmic_flop_per_query": F_Q, "queries_per_step": queries,
+                     "algorithmic_flop_per_query": f_q, "queries_per_step": queries,
                      "trace_ms_per_step": trace_ms,
                      "objective_ms_per_step": obj_ms,
                      "step_ms": [round(x, 2) for x in step_ms],
@@ -456,13 +480,13 @@ def main():
                      "objective_step_ms": [round(a.elapsed_time(b), 2) for a, b in obj_ev],
                      "lead_ms": round(lead_ms, 3),
                      "head_samples_per_step": samples,
-                     "objective_achieved_tflops": samples * (F_Q + F_B) / (obj_ms * 1e-3) / 1e12,
+                     "objective_achieved_tflops": samples * (f_q + f_b) / (obj_ms * 1e-3) / 1e12,
                      "objective_achieved_note": "algorithmic: the reference's taped forward + dgrad per seeded sample (F_Q + F_B); the forward of samples the march itself queried is not recomputed (ReLU-mask record), so this exceeds the executed rate",
                      "objective_note": "heads + seeds + fused tcgen05 backward + reductions "
                                        "(k_tc_heads dominates; its ncu capture is in profiles/)"},
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:   # the contract: rank 0 at N=1 only
-        v, info = cpu_reference_sample()
+        v, info = cpu_reference_sample(args.skip)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": info["cores"], "kind": info["kind"],
                                 "sample": info["sample"]}
     if rank == 0:

@@ -112,7 +112,10 @@ DIST_API int dist_debug_heads_timeline(unsigned long long *out, int n);
  * b[l] its bias; dims has n_layers+1 entries (dims[0] = latent_dim + 3 +
  * 0, dims[n_layers] = 1).  skip_layer >= 0 selects the DeepSDF layout where
  * layer `skip_layer` consumes concat(h, code, xyz);
- * -1 is the reference's plain stack.  final_linear selects the head: 0 = tanh,
+ * -1 is the reference's plain stack.  The tensor-core precisions take
+ * skip_layer <= n_layers - 3 (a hidden layer follows the skip layer) with
+ * 512-wide hidden layers (the pre-skip layer may be narrower: it is
+ * zero-padded to 512) and return DIST_ERR_CONFIG for any other shape.  final_linear selects the head: 0 = tanh,
  * 1 = linear (fields.py:200-201, 245-246), 2 = sigmoid (AttributeField,
  * fields.py:332-338).  Hidden activation is ReLU. */
 DIST_API int dist_decoder_create(const double *const *W, const double *const *b, int n_layers,

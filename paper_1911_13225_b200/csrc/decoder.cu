@@ -183,7 +183,7 @@ int vjp_points(const DecView &dv, const double *c0, const double *cskip, const d
     return launch_vjp_gen<double>(dv, c0, cskip, g, n, S, part0, parts, gpts, bad, grid_cap, grid_out, st);
   // bf16x3: the fused tensor-core head kernel (forward, given seeds, fp16x2 dgrad)
   if (tc_heads_supported(dv))
-    return launch_tc_heads<ArrayGen>(dv, c0, g, n, S, part0, bad, grid_cap, grid_out, st, gpts);
+    return launch_tc_heads<ArrayGen>(dv, c0, cskip, g, n, S, part0, parts, bad, grid_cap, grid_out, st, gpts);
   return launch_vjp_gen<float>(dv, c0, cskip, g, n, S, part0, parts, gpts, bad, grid_cap, grid_out, st);
 }
 
@@ -274,16 +274,12 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
   v.np[L - 1] = 1;
   for (int l = 1; l < L; ++l) v.kp[l] = v.np[l - 1];
   v.nskip = skip > 0 ? v.np[skip] : 0;
-  if (prec >= DIST_PREC_BF16X3) {
-    // the tensor-core kernels tile 512-wide hidden layers without a skip
-    // input; any other shape would silently run SIMT fp32 -- refuse instead
-    bool ok = skip < 0 && L >= 3;
-    for (int l = 0; l <= L - 2 && ok; ++l) ok = v.np[l] == kMaxWidth && dims[l + 1] == kMaxWidth;
-    if (!ok)
-      return fail(DIST_ERR_CONFIG,
-                  "tensor-core precisions (bf16x3, fp16x3) need >= 2 hidden layers, all 512 wide, and no "
-                  "skip layer; use precision fp32 or fp64 for this decoder");
-  }
+  if (prec >= DIST_PREC_BF16X3 && !tc_shape_ok(v))
+    // any other shape would silently run SIMT fp32 -- refuse instead
+    return fail(DIST_ERR_CONFIG,
+                "tensor-core precisions (bf16x3, fp16x3) need >= 2 hidden layers, a 512-wide first "
+                "hidden layer (and skip layer), and a skip layer below the top hidden layer; use "
+                "precision fp32 or fp64 for this decoder");
 
   // host staging of every packed array, then one device blob
   std::vector<char> host;

@@ -525,11 +525,11 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
     goth.sel = L.sel_oth;
     goth.sel_count = L.sel_counts + 1;
     int grid2 = 0;
-    rc = launch_tc_heads_bwd(dv, L.c0, gown, n * K, s1, L.part0, L.bad, G, &grid, sm);
-    if (!rc) rc = launch_tc_heads<ObjGen>(dv, L.c0, goth, n * K, s1, L.part0, L.bad, G, &grid2, sm);
+    rc = launch_tc_heads_bwd(dv, L.c0, L.cs, gown, n * K, s1, L.part0, L.parts, L.bad, G, &grid, sm);
+    if (!rc) rc = launch_tc_heads<ObjGen>(dv, L.c0, L.cs, goth, n * K, s1, L.part0, L.parts, L.bad, G, &grid2, sm);
     grid = std::max(grid, grid2);
   } else if (tc_heads_supported(dv))
-    rc = launch_tc_heads<ObjGen>(dv, L.c0, gen, n * K, s1, L.part0, L.bad, G, &grid, sm);
+    rc = launch_tc_heads<ObjGen>(dv, L.c0, L.cs, gen, n * K, s1, L.part0, L.parts, L.bad, G, &grid, sm);
   else if (dv.prec == DIST_PREC_FP64)
     rc = launch_vjp_gen<double>(dv, L.c0, L.cs, gen, n * K, s1, L.part0, L.parts, nullptr, L.bad, G, &grid, sm);
   else

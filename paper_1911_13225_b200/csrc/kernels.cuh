@@ -43,6 +43,7 @@ void tc_pack_fill(const DecView &dv, const double *const *W, const double *const
                   const int32_t *dims, const std::function<void *(int)> &wdst,
                   const std::function<float *(int)> &bdst);
 bool tc_supported(const DecView &dv);
+bool tc_shape_ok(const DecView &dv);
 // measures DecView.tc_gain (the accumulator-bias gain of the head dot)
 int tc_calibrate(DecView &dv);
 bool tc_heads_supported(const DecView &dv);
@@ -52,16 +53,17 @@ namespace dist {
 int tc_make_map(const DecView &dv, int slot, CUtensorMap *map);
 void tc_forget_maps(const DecView &dv);
 template <class Gen>
-int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
-                    fx_t *part0, int *bad, int grid_cap, int *grid_out, cudaStream_t st,
+int launch_tc_heads(const DecView &dv, const double *c0, const double *cs, const Gen &gen, int64_t n_bound,
+                    int S, fx_t *part0, fx_t *parts, int *bad, int grid_cap, int *grid_out, cudaStream_t st,
                     double *gpts = nullptr);
 
 struct LevelState;
 struct ProbeGen;
 struct ObjGen;
 // backward-only head rows (f and ReLU masks from the march's mask record)
-int launch_tc_heads_bwd(const DecView &dv, const double *c0, const ObjGen &gen, int64_t n_bound, int S,
-                        fx_t *part0, int *bad, int grid_cap, int *grid_out, cudaStream_t st);
+int launch_tc_heads_bwd(const DecView &dv, const double *c0, const double *cs, const ObjGen &gen,
+                        int64_t n_bound, int S, fx_t *part0, fx_t *parts, int *bad, int grid_cap,
+                        int *grid_out, cudaStream_t st);
 int tc_eval_probes(const DecView &dv, const double *c0, const double *cs, int S, const ProbeGen &gen, int64_t n_bound,
                    cudaStream_t st);
 int normals_pass(const DecView &dv, const double *c0, const double *cs, int S, const dist_camera *cams,

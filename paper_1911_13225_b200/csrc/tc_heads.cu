@@ -46,7 +46,13 @@ struct HParams {
   int S;
   int timeline;        // DIST_TC_TIMELINE: CTA 0 / thread 64 records %globaltimer marks
   fx_t *part0;         // [grid][S][512] exact fixed-point column sums (common.cuh)
+  fx_t *parts;         // [grid][S][512] the same for the skip layer's pre-activation (DeepSDF)
   int *bad;            // set on a non-finite / out-of-range contribution
+  // DeepSDF skip layer: forward GEMM skipg adds the code part cskf[s] and p . Wsp
+  // to its bias; backward phase skipl produces the skip layer's pre-activation
+  // gradient, whose column sums (code) and . Wsp (points) it takes
+  int skipg, skipl;
+  const float *cskf;   // [S][512] fp32 (kernels.cuh c0 layout of cskip)
   double *gpts;        // [n][3] seed * df/dp per row, or null
 };
 
@@ -92,6 +98,22 @@ __device__ __forceinline__ void warp_colsum16d(double (&v)[16]) {
   v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
 }
 
+// exact column sums of a 16-column chunk over the warp's 32 rows (values v in
+// true units, zero for rows not counted): the fp64 butterfly when the warp's
+// nonzero values span at most 24 binades inside the fixed-point range (then
+// exact), else the 128-bit integer butterfly.  Lanes 2c, 2c+1 return the sum of
+// column c; nb is set on an out-of-range value.
+__device__ __forceinline__ fx_t chunk_sum16(const float (&v)[16], int &nb);
+
+__device__ __forceinline__ void fx_atomic_add(fx_t *dst, fx_t v) {
+  // two 64-bit atomics with an explicit carry: exact modulo 2^128 whatever the
+  // interleaving of concurrent adders
+  unsigned long long *w = reinterpret_cast<unsigned long long *>(dst);
+  const unsigned long long lo = (unsigned long long)v, hi = (unsigned long long)((unsigned __int128)v >> 64);
+  const unsigned long long old = atomicAdd(w, lo);
+  atomicAdd(w + 1, hi + ((old + lo < old) ? 1ull : 0ull));
+}
+
 // The butterfly on exact fixed-point integers (common.cuh fx_t) over a
 // 16-column chunk (registers: 64 per chunk): afterwards lanes 2c and 2c+1
 // both hold the sum of column c over the warp's 32 rows.
@@ -108,6 +130,32 @@ __device__ __forceinline__ void warp_colsum16x(fx_t (&v)[16]) {
     }
   }
   v[0] += fx_shfl_xor(v[0], 1);
+}
+
+__device__ __forceinline__ fx_t chunk_sum16(const float (&v)[16], int &nb) {
+  uint32_t emin = 255u, emax = 0u;
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const uint32_t ex = (__float_as_uint(v[e]) >> 23) & 0xffu;
+    if (v[e] != 0.f) {
+      emin = min(emin, ex);
+      emax = max(emax, ex);
+    }
+  }
+  emin = __reduce_min_sync(0xffffffffu, emin);
+  emax = __reduce_max_sync(0xffffffffu, emax);
+  if (emax < emin || (emax - emin <= 24u && emin >= 55u && emax <= 151u)) {
+    double w[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) w[e] = (double)v[e];
+    warp_colsum16d(w);
+    return fx_from_double(w[0], &nb);
+  }
+  fx_t w[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) w[e] = fx_from_float(v[e], nb);
+  warp_colsum16x(w);
+  return w[0];
 }
 
 // Sum v[0..63] over the 32 lanes of the warp; afterwards lane l holds the
@@ -359,6 +407,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       const uint32_t *const mrec = nxm;
 
       if (row_thread) m.shape[row] = s;
+      const float px = (float)p[0], py = (float)p[1], pz = (float)p[2];
+      // the DeepSDF skip layer's extra input terms (code part + p . Wsp) for n
+      // consecutive columns, added to the bias of forward GEMM P.skipg
+      auto skip_terms = [&](int col, float *bb, int n) {
+        const int ns = P.dv.nskip;
+        const float *cf = P.cskf + (size_t)(s < 0 ? 0 : s) * ns + col;
+        for (int e0 = 0; e0 < n; e0 += 8) {
+          float w0[8], w1[8], w2[8], c8[8];
+          ldg8(P.dv.Wspf + col + e0, w0);
+          ldg8(P.dv.Wspf + ns + col + e0, w1);
+          ldg8(P.dv.Wspf + 2 * ns + col + e0, w2);
+          ldg8(cf + e0, c8);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) bb[e0 + e] += fmaf(pz, w2[e], fmaf(py, w1[e], fmaf(px, w0[e], c8[e])));
+        }
+      };
       float head = 0.f;
       typename Gen::Prep sp{};
       float gr_b = 0.f;    // BWD: this row's seed, applied in the first backward epilogue
@@ -395,7 +459,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       // ---- layer 0 (folded bias + p . W0p, fp32) + mask 0 ----
       {
         const float *c0f = P.c0f + (size_t)(s < 0 ? 0 : s) * n0;
-        const float px = (float)p[0], py = (float)p[1], pz = (float)p[2];
         uint32_t mk[4] = {0, 0, 0, 0};
         for (int nh = 0; nh < 2; ++nh) {
           const int cb = nh * 256 + half * 128 + sub * 64;
@@ -447,6 +510,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           for (int g8 = 0; g8 < 4; ++g8) {
             float x[8], bb[8];
             ldg8(bias + cb + c * 32 + g8 * 8, bb);
+            if (l == P.skipg) skip_terms(cb + c * 32 + g8 * 8, bb, 8);
             if (last) {
               float wo[8];
               ldg8(P.w_out + cb + c * 32 + g8 * 8, wo);
@@ -479,6 +543,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const int cb = 256 + half * 128 + sub * 64;
           float v[32], bbc[32];
           ldg32(bias + cb + c * 32, bbc);
+          if (l == P.skipg) skip_terms(cb + c * 32, bbc, 32);
           tmem_ld32(tq + 128 + sub * 64 + c * 32, v);
           uint32_t bits = 0;
 #pragma unroll
@@ -598,6 +663,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       a_ready_all();
       TL(6);
       }   // !BWD
+      // The DeepSDF skip layer's share of the backward: its pre-activation
+      // gradient g_{z_skip} (the operand phase P.skipl just wrote to A, true
+      // units x * rinv) feeds the code gradient through W_skip's code rows
+      // (exact column sums into P.parts, per shape) and the sample points
+      // through its xyz rows (gps, added to d/dp with the layer-0 term).
+      float gps[3] = {0.f, 0.f, 0.f};
+      auto skip_backward = [&](float ri) {
+        const int ns = P.dv.nskip;
+        int nb = 0;
+        int shapes_done = 0;
+        for (int guard = 0; guard < ROWS; ++guard) {
+          int next = 0x7fffffff;
+          for (int r = 0; r < ROWS; ++r) {
+            const int sr = m.shape[r];
+            if (sr >= 0 && sr >= shapes_done && sr < next) next = sr;
+          }
+          if (next == 0x7fffffff) break;
+          const bool mine = (s == next);
+          for (int nh = 0; nh < 2; ++nh) {
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+              const int cb = nh * 256 + half * 128 + sub * 64 + c * 16;
+              float v[16];
+#pragma unroll
+              for (int g2 = 0; g2 < 2; ++g2) {
+                const uint4 q4 = *reinterpret_cast<const uint4 *>(smem + OFF_AHI + a_off(row, cb + g2 * 8));
+                const uint32_t wds[4] = {q4.x, q4.y, q4.z, q4.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float2 f2 = __half22float2(*reinterpret_cast<const __half2 *>(&wds[i]));
+                  v[g2 * 8 + 2 * i] = mine ? f2.x * ri : 0.f;
+                  v[g2 * 8 + 2 * i + 1] = mine ? f2.y * ri : 0.f;
+                }
+              }
+              if (P.gpts && mine) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) {
+                  gps[0] = fmaf(v[e], __ldg(P.dv.Wspf + cb + e), gps[0]);
+                  gps[1] = fmaf(v[e], __ldg(P.dv.Wspf + ns + cb + e), gps[1]);
+                  gps[2] = fmaf(v[e], __ldg(P.dv.Wspf + 2 * ns + cb + e), gps[2]);
+                }
+              }
+              const fx_t r = chunk_sum16(v, nb);
+              if (!(lane & 1)) fx_atomic_add(P.parts + ((size_t)blockIdx.x * P.S + next) * ns + cb + (lane >> 1), r);
+            }
+          }
+          shapes_done = next + 1;
+        }
+        if (nb) atomicOr(P.bad, 1);
+      };
       // ---- backward through GEMM layers G-1 .. 0 ----
       for (int gl = G - 1; gl >= 0; --gl, ++phase) {
         if (gl == 0) fetch(t + nclusters, nxp, nxs, nxm);
@@ -708,6 +823,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           if (gl >= 2) named_arrive(2, 2 * N_EPI_WARPS * 32);
           a_ready_hi();
           TL(8);
+          if (gl == P.skipl) skip_backward(rinv);
         } else {
           mbar_wait(&m.dfull[1], phase & 1);
           TL(7);
@@ -721,7 +837,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             // d loss / d p = g_pre0 . W0p^T per row: this thread's 128 columns,
             // then the row's four part sums through smem (after `red`)
             float *gp = red + 8 * KDIM;   // [3][4][64], after the [2][512] fixed-point column sums
-            float acc[3] = {0.f, 0.f, 0.f};
+            float acc[3] = {gps[0], gps[1], gps[2]};   // + the skip layer's xyz rows (skip_backward)
             for (int nh = 0; nh < 2; ++nh) {
               const int cb = nh * 256 + half * 128 + sub * 64;
 #pragma unroll 1
@@ -781,35 +897,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 float v[16];
                 tmem_ld16(tq + nh * 128 + sub * 64 + c * 16, v);
                 const uint32_t bits = mine ? (get4(mk, nh * 2 + (c >> 1)) >> ((c & 1) * 16)) : 0u;
-                uint32_t emin = 255u, emax = 0u;
 #pragma unroll
-                for (int e = 0; e < 16; ++e) {
-                  v[e] = ((bits >> e) & 1u) ? v[e] * unscale : 0.f;
-                  const uint32_t ex = (__float_as_uint(v[e]) >> 23) & 0xffu;
-                  if (v[e] != 0.f) {
-                    emin = min(emin, ex);
-                    emax = max(emax, ex);
-                  }
-                }
-                emin = __reduce_min_sync(0xffffffffu, emin);
-                emax = __reduce_max_sync(0xffffffffu, emax);
+                for (int e = 0; e < 16; ++e) v[e] = ((bits >> e) & 1u) ? v[e] * unscale : 0.f;
                 // lanes 2c', 2c'+1 end up holding column c' of the chunk; the
                 // two row-warps (q&1 = 0, 1) of the chunk combine in smem below
                 const int col = nh * 256 + half * 128 + sub * 64 + c * 16 + (lane >> 1);
-                fx_t r;
-                if (emax < emin || (emax - emin <= 24u && emin >= 55u && emax <= 151u)) {
-                  double w[16];
-#pragma unroll
-                  for (int e = 0; e < 16; ++e) w[e] = (double)v[e];
-                  warp_colsum16d(w);
-                  r = fx_from_double(w[0], &nb);
-                } else {
-                  fx_t w[16];
-#pragma unroll
-                  for (int e = 0; e < 16; ++e) w[e] = fx_from_float(v[e], nb);
-                  warp_colsum16x(w);
-                  r = w[0];
-                }
+                const fx_t r = chunk_sum16(v, nb);
                 if (!(lane & 1)) redx[(q & 1) * 512 + col] = r;
               }
             }
@@ -846,9 +939,9 @@ bool tc_heads_supported(const DecView &dv) {
 
 
 template <class Gen, bool BWD>
-static int launch_heads_impl(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
-                             fx_t *part0, int *bad, int grid_cap, int *grid_out, cudaStream_t st,
-                             double *gpts) {
+static int launch_heads_impl(const DecView &dv, const double *c0, const double *cs, const Gen &gen,
+                             int64_t n_bound, int S, fx_t *part0, fx_t *parts, int *bad, int grid_cap,
+                             int *grid_out, cudaStream_t st, double *gpts) {
   CUtensorMap mf, mb;
   const int fs = dv.prec == DIST_PREC_FP16X3 ? 3 : 0;   // bf16x3 forward pack
   int rc = tc_make_map(dv, fs, &mf);
@@ -870,7 +963,11 @@ static int launch_heads_impl(const DecView &dv, const double *c0, const Gen &gen
     P.timeline = tl ? atoi(tl) : 0;
   }
   P.part0 = part0;
+  P.parts = parts;
   P.bad = bad;
+  P.skipg = dv.skip > 0 ? dv.skip - 1 : -1;
+  P.skipl = dv.skip > 0 ? dv.skip : -1;
+  P.cskf = dv.skip > 0 ? c0_f32(cs, S, dv.nskip) : nullptr;
   P.gpts = gpts;
   const void *fn = (const void *)tc::k_tc_heads<Gen, BWD>;
   static int attr_dev = -1;   // per instantiation: set once per device
@@ -890,14 +987,17 @@ static int launch_heads_impl(const DecView &dv, const double *c0, const Gen &gen
 }
 
 template <class Gen>
-int launch_tc_heads(const DecView &dv, const double *c0, const Gen &gen, int64_t n_bound, int S,
-                    fx_t *part0, int *bad, int grid_cap, int *grid_out, cudaStream_t st, double *gpts) {
-  return launch_heads_impl<Gen, false>(dv, c0, gen, n_bound, S, part0, bad, grid_cap, grid_out, st, gpts);
+int launch_tc_heads(const DecView &dv, const double *c0, const double *cs, const Gen &gen, int64_t n_bound,
+                    int S, fx_t *part0, fx_t *parts, int *bad, int grid_cap, int *grid_out, cudaStream_t st,
+                    double *gpts) {
+  return launch_heads_impl<Gen, false>(dv, c0, cs, gen, n_bound, S, part0, parts, bad, grid_cap, grid_out, st,
+                                       gpts);
 }
 
-int launch_tc_heads_bwd(const DecView &dv, const double *c0, const ObjGen &gen, int64_t n_bound, int S,
-                        fx_t *part0, int *bad, int grid_cap, int *grid_out, cudaStream_t st) {
-  return launch_heads_impl<ObjGen, true>(dv, c0, gen, n_bound, S, part0, bad, grid_cap, grid_out, st,
+int launch_tc_heads_bwd(const DecView &dv, const double *c0, const double *cs, const ObjGen &gen,
+                        int64_t n_bound, int S, fx_t *part0, fx_t *parts, int *bad, int grid_cap,
+                        int *grid_out, cudaStream_t st) {
+  return launch_heads_impl<ObjGen, true>(dv, c0, cs, gen, n_bound, S, part0, parts, bad, grid_cap, grid_out, st,
                                          nullptr);
 }
 
@@ -906,9 +1006,9 @@ extern "C" DIST_API int dist_debug_heads_timeline(unsigned long long *out, int n
                  cudaSuccess ? 0 : -1;
 }
 
-template int launch_tc_heads<ObjGen>(const DecView &, const double *, const ObjGen &, int64_t, int,
-                                     fx_t *, int *, int, int *, cudaStream_t, double *);
-template int launch_tc_heads<ArrayGen>(const DecView &, const double *, const ArrayGen &, int64_t, int,
-                                       fx_t *, int *, int, int *, cudaStream_t, double *);
+template int launch_tc_heads<ObjGen>(const DecView &, const double *, const double *, const ObjGen &, int64_t,
+                                     int, fx_t *, fx_t *, int *, int, int *, cudaStream_t, double *);
+template int launch_tc_heads<ArrayGen>(const DecView &, const double *, const double *, const ArrayGen &,
+                                       int64_t, int, fx_t *, fx_t *, int *, int, int *, cudaStream_t, double *);
 
 }  // namespace dist

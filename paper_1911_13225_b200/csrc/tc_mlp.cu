@@ -992,11 +992,21 @@ static EncodeTiledFn encode_fn() {
 
 }  // namespace tc
 
-bool tc_supported(const DecView &dv) {
-  if (dv.skip >= 0 || dv.n_layers < 3) return false;
+// Shapes the tcgen05 kernels tile: every GEMM is 512 x 512 (narrower hidden
+// layers are zero-padded in the packs), layer 0 and the skip layer write all
+// 512 columns, and the skip layer (DeepSDF) is not the top hidden layer (the
+// head kernel's backward takes its column sums between two backward GEMMs).
+bool tc_shape_ok(const DecView &dv) {
+  if (dv.n_layers < 3 || dv.np[0] != tc::KDIM) return false;
   for (int l = 0; l <= dv.n_layers - 2; ++l)
-    if (dv.np[l] != tc::KDIM) return false;
-  return (dv.prec == DIST_PREC_BF16X3 || dv.prec == DIST_PREC_FP16X3) && dv.tc_w[0] != nullptr;
+    if (dv.np[l] > tc::KDIM) return false;
+  if (dv.skip >= 0 && (dv.skip > dv.n_layers - 3 || dv.nskip != tc::KDIM)) return false;
+  return true;
+}
+
+bool tc_supported(const DecView &dv) {
+  return tc_shape_ok(dv) && (dv.prec == DIST_PREC_BF16X3 || dv.prec == DIST_PREC_FP16X3) &&
+         dv.tc_w[0] != nullptr;
 }
 
 // Packs (slot: contents):
@@ -1015,9 +1025,7 @@ bool tc_supported(const DecView &dv) {
 //   3: fp16x3 only -- bf16x3 forward pack for the fused head kernel (its
 //      forward phases are bf16x3 in both modes)
 void tc_pack_sizes(const DecView &dv, const std::function<void(int, size_t, size_t)> &put) {
-  for (int l = 0; l <= dv.n_layers - 2; ++l)
-    if (dv.np[l] != tc::KDIM) return;
-  if (dv.skip >= 0 || dv.n_layers < 3) return;
+  if (!tc_shape_ok(dv)) return;
   const int G = dv.n_layers - 2;
   const size_t wb = (size_t)G * 2 * tc::KDIM * tc::KDIM * 2;
   // biases, w_out, winv[G], then the fp16 row-scale bounds cn[G], bm[G], w0m[3]
@@ -1033,9 +1041,7 @@ static void fill_fwd(const DecView &dv, const double *const *W, const double *co
 void tc_pack_fill(const DecView &dv, const double *const *W, const double *const *b,
                   const int32_t *dims, const std::function<void *(int)> &wdst,
                   const std::function<float *(int)> &bdst) {
-  for (int l = 0; l <= dv.n_layers - 2; ++l)
-    if (dv.np[l] != tc::KDIM) return;
-  if (dv.skip >= 0 || dv.n_layers < 3) return;
+  if (!tc_shape_ok(dv)) return;
   const bool f16 = dv.prec == DIST_PREC_FP16X3;
   fill_fwd(dv, W, b, dims, f16, reinterpret_cast<uint16_t *>(wdst(0)), bdst(0));
   const int other = f16 ? 3 : 2;   // the forward pack in the other 16-bit type

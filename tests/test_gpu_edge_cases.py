@@ -217,12 +217,14 @@ def test_dynamic_mask_off_on_tensor_cores(st, prec):
 
 def test_tensor_core_precision_refuses_unsupported_shapes(st):
     """A tensor-core precision on a decoder the tcgen05 kernels cannot tile
-    (skip layer, hidden width != 512) raises instead of silently running SIMT."""
-    with pytest.raises(ValueError):
-        st.NeuralField.geometric(256, (512,) * 8, 0, skip=4, precision="fp16x3").handle()
-    with pytest.raises(ValueError):
+    (a skip at the top hidden layer, a first hidden layer narrower than 512)
+    raises instead of silently running SIMT."""
+    with pytest.raises(ValueError):   # skip at the top hidden layer
+        st.NeuralField.geometric(256, (512,) * 8, 0, skip=7, precision="fp16x3").handle()
+    with pytest.raises(ValueError):   # a 256-wide first hidden layer
         st.NeuralField.geometric(64, (256,) * 4, 0, precision="bf16x3").handle()
-    st.NeuralField.geometric(256, (512,) * 8, 0, skip=4, precision="fp32").handle()
+    st.NeuralField.geometric(256, (512,) * 8, 0, skip=7, precision="fp32").handle()
+    st.NeuralField.geometric(256, (512,) * 8, 0, skip=4, precision="fp16x3").handle()   # DeepSDF: tiled
 
 
 @pytest.mark.parametrize("prec", ["fp64", "fp16x3"])
