@@ -225,9 +225,11 @@ typedef struct dist_objective_io {
   int32_t phase;
   int32_t reserved2;
   const double *view_norm;       /* [V*3] (phase 2) or NULL */
-  void *colsum_fixed;            /* optional out [S*np0] 16-byte two's-complement integers: the
-                                    layer-0 gradient column sums * 2^95 (exact, so ranks can add
-                                    them in any order); see dist_code_grad_fixed */
+  void *colsum_fixed;            /* optional out [S*w] (w = dist_decoder_colsum_width) 16-byte
+                                    two's-complement integers: the layer-0 gradient column sums
+                                    * 2^95 as [S][np0], then for a skip decoder the skip layer's
+                                    as [S][nskip] (exact, so ranks can add them in any order);
+                                    see dist_code_grad_fixed */
 } dist_objective_io;
 
 /* flags: bit 0 = a normal term will be requested (reserves its buffers) */
@@ -243,14 +245,15 @@ DIST_API int dist_objective(const dist_decoder *dec, const double *codes_dev, in
                             const dist_trace_config *cfg, const dist_ray_state *st,
                             const dist_objective_io *io, void *ws, size_t ws_bytes, void *stream);
 
-/* d/dz = W0[:D] colsum + w_latent * 2 z from exact column sums (the element-
+/* d/dz = W0[:D] colsum (+ W_skip[code rows] colsum_skip) + w_latent * 2 z from exact column sums (the element-
  * wise integer sum of every rank's dist_objective_io.colsum_fixed): the
  * reduction step of optimize.py:340-341 ("g += hg['code']", regulariser once)
  * with a result that is bit-identical for any number of ranks. */
 DIST_API int dist_code_grad_fixed(const dist_decoder *dec, int n_shapes, const void *colsum_fixed,
                                   const double *codes_dev, double w_latent, double *grad_dev,
                                   void *stream);
-/* padded width of layer 0 (the length of one shape's colsum_fixed row) */
+/* fixed-point column sums per shape: padded width of layer 0 (+ that of the
+ * skip layer for a skip decoder) -- colsum_fixed holds S times this many */
 DIST_API int dist_decoder_colsum_width(const dist_decoder *dec);
 /* The tensor-core decoders' calibrated head gain (measured at creation):
  * tcgen05 accumulates fp32 in TMEM with truncation toward zero, which shrinks

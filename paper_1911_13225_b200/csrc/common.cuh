@@ -38,6 +38,7 @@ struct DecView {
   int prec;
   int np[kMaxLayers + 1]; // padded output width of layer l (np[L-1] = 1)
   int kp[kMaxLayers + 1]; // padded input width of hidden layer l (GEMM K)
+  int nr[kMaxLayers + 1]; // true output width of layer l (dims[l + 1]; the h part for the skip input)
   // layer 0 in fp64: W0z [D][np0], W0p [3][np0], b0 [np0]
   const double *W0z, *W0p, *b0;
   const float *W0pf;       // fp32 copy of W0p for the tensor-core prologue

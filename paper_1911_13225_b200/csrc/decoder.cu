@@ -272,6 +272,7 @@ int dist_decoder_create(const double *const *W, const double *const *b, int L,
   v.prec = prec;
   for (int l = 0; l < L - 1; ++l) v.np[l] = (int)round_up(dims[l + 1], 64);
   v.np[L - 1] = 1;
+  for (int l = 0; l < L; ++l) v.nr[l] = dims[l + 1];
   for (int l = 1; l < L; ++l) v.kp[l] = v.np[l - 1];
   v.nskip = skip > 0 ? v.np[skip] : 0;
   if (prec >= DIST_PREC_BF16X3 && !tc_shape_ok(v))
@@ -432,7 +433,9 @@ int dist_decoder_destroy(dist_decoder *dec) {
 
 int dist_decoder_precision(const dist_decoder *dec) { return dec ? dec->view.prec : -1; }
 
-int dist_decoder_colsum_width(const dist_decoder *dec) { return dec ? dec->view.np[0] : -1; }
+int dist_decoder_colsum_width(const dist_decoder *dec) {
+  return dec ? dec->view.np[0] + std::max(dec->view.nskip, 0) : -1;
+}
 
 int dist_decoder_head_gain(const dist_decoder *dec, double *gain2) {
   if (!dec || !gain2) return fail(DIST_ERR_CONFIG, "null argument");

@@ -388,8 +388,6 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
   const DecView &dv = dec->view;
   if (dv.latent_dim > 0 && (!codes || S < 1)) return fail(DIST_ERR_CONFIG, "field expects a latent code");
   if (io->phase < 0 || io->phase > 2) return fail(DIST_ERR_CONFIG, "phase must be 0, 1 or 2");
-  if (io->colsum_fixed && dv.nskip)
-    return fail(DIST_ERR_CONFIG, "colsum_fixed is not defined for skip decoders");
   if (io->grad_mode < 0 || io->grad_mode > 2)
     return fail(DIST_ERR_CONFIG, "grad_mode must be 0 (surrogate), 1 (implicit) or 2 (implicit, unit normal)");
   const int K = cfg->k_samples;
@@ -557,13 +555,15 @@ int dist_objective(const dist_decoder *dec, const double *codes, int S, const di
   if (dv.latent_dim > 0) {
     // the caller may take the exact column sums (cross-rank reduction, then
     // dist_code_grad_fixed); grad is always formed from the local sums
+    // layout [S][np0] then (skip decoders) [S][nskip]
     fx_t *col0 = io->colsum_fixed ? reinterpret_cast<fx_t *>(io->colsum_fixed) : L.col0;
+    fx_t *cols = io->colsum_fixed ? col0 + (size_t)s1 * dv.np[0] : L.cols;
     if (grid == 0) {   // no seeded sample anywhere: zero sums
       e = cudaMemsetAsync(col0, 0, sizeof(fx_t) * s1 * dv.np[0], sm);
-      if (e == cudaSuccess && dv.nskip) e = cudaMemsetAsync(L.cols, 0, sizeof(fx_t) * s1 * dv.nskip, sm);
+      if (e == cudaSuccess && dv.nskip) e = cudaMemsetAsync(cols, 0, sizeof(fx_t) * s1 * dv.nskip, sm);
       if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(colsum)");
     }
-    rc = reduce_code_grad(dv, s1, grid, L.part0, L.parts, L.bad, col0, L.cols, io->grad, sm);
+    rc = reduce_code_grad(dv, s1, grid, L.part0, L.parts, L.bad, col0, cols, io->grad, sm);
     if (rc) return rc;
   }
   if (io->counts_out) {
@@ -582,13 +582,12 @@ int dist_code_grad_fixed(const dist_decoder *dec, int S, const void *colsum_fixe
                          const double *codes, double w_latent, double *grad, void *stream) {
   if (!dec || !colsum_fixed || !grad) return fail(DIST_ERR_CONFIG, "null argument");
   const DecView &dv = dec->view;
-  if (dv.nskip) return fail(DIST_ERR_CONFIG, "colsum_fixed is not defined for skip decoders");
   if (S < 1) return fail(DIST_ERR_CONFIG, "S must be >= 1");
   if (dv.latent_dim == 0) return DIST_OK;
   cudaStream_t sm = (cudaStream_t)stream;
-  int rc = reduce_code_grad(dv, S, 0, nullptr, nullptr, nullptr,
-                            const_cast<fx_t *>(reinterpret_cast<const fx_t *>(colsum_fixed)), nullptr,
-                            grad, sm);
+  fx_t *col0 = const_cast<fx_t *>(reinterpret_cast<const fx_t *>(colsum_fixed));
+  int rc = reduce_code_grad(dv, S, 0, nullptr, nullptr, nullptr, col0,
+                            dv.nskip ? col0 + (size_t)S * dv.np[0] : nullptr, grad, sm);
   if (rc) return rc;
   if (codes && w_latent != 0.0) {
     k_add_reg<<<S, 256, 0, sm>>>(S, dv.latent_dim, codes, w_latent, grad);

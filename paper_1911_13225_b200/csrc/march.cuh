@@ -90,47 +90,62 @@ __device__ __forceinline__ void warp_append(bool keep, int32_t value, int32_t *l
 }
 
 // --- the march update for one queried ray (tracer.py:170-192) -----------------
+// One ray's state, wherever it lives: the level arrays in HBM (stride 1 for
+// the top-K lists) or a CTA's shared-memory copy (k_march_resident: stride NT).
+struct RayRef {
+  double *d, *b;
+  uint8_t *status;
+  int32_t *steps;
+  double *ta, *tf, *td;   // top-K |f|, f, d; entry k at [k * ks]
+  int ks;
+  uint8_t *tp;            // ReLU-mask record slots [K+1] or nullptr
+};
+
+__device__ __forceinline__ RayRef ray_ref(const LevelState &ls, int K, int64_t g) {
+  return RayRef{ls.d + g, ls.b + g, ls.status + g, ls.steps + g, ls.tk_a + g * K, ls.tk_f + g * K,
+                ls.tk_d + g * K, 1, ls.tk_p ? ls.tk_p + g * (K + 1) : nullptr};
+}
+
 // Returns true if the ray is still marching.  Arithmetic is kept
 // uncontracted so that d' = d + alpha*f rounds exactly like numpy.
-__device__ __forceinline__ bool march_update(const LevelState &ls, const MarchArgs &a, int64_t g,
-                                             const double dir[3], const double *o, double f,
-                                             int *nan_count) {
+__device__ __forceinline__ bool march_update_at(const RayRef &r, const MarchArgs &a, const double dir[3],
+                                                const double *o, double f, int *nan_count) {
   if (!isfinite(f)) {
-    ls.status[g] = DIST_EXHAUSTED;
-    ls.b[g] = __longlong_as_double(0x7ff8000000000000ll);
-    ls.steps[g] += 1;
+    *r.status = DIST_EXHAUSTED;
+    *r.b = __longlong_as_double(0x7ff8000000000000ll);
+    *r.steps += 1;
     ++*nan_count;
     return false;
   }
-  const double dk = ls.d[g];
+  const double dk = *r.d;
   const double av = fabs(f);
-  const int K = a.K;
-  double *ta = ls.tk_a + g * K, *tf = ls.tk_f + g * K, *td = ls.tk_d + g * K;
-  if (av < ta[K - 1]) {  // strict: the earliest query wins ties (tracer.py:133-134)
-    uint8_t *tp = ls.tk_p ? ls.tk_p + g * (K + 1) : nullptr;
+  const int K = a.K, ks = r.ks;
+  double *ta = r.ta, *tf = r.tf, *td = r.td;
+  if (av < ta[(K - 1) * ks]) {  // strict: the earliest query wins ties (tracer.py:133-134)
+    uint8_t *tp = r.tp;
     const uint8_t evicted = tp ? tp[K - 1] : 0;
     int pos = K - 1;
-    while (pos > 0 && ta[pos - 1] > av) {
-      ta[pos] = ta[pos - 1];
-      tf[pos] = tf[pos - 1];
-      td[pos] = td[pos - 1];
+    while (pos > 0 && ta[(pos - 1) * ks] > av) {
+      ta[pos * ks] = ta[(pos - 1) * ks];
+      tf[pos * ks] = tf[(pos - 1) * ks];
+      td[pos * ks] = td[(pos - 1) * ks];
       if (tp) tp[pos] = tp[pos - 1];
       --pos;
     }
-    ta[pos] = av;
-    tf[pos] = f;
-    td[pos] = dk;
+    ta[pos * ks] = av;
+    tf[pos * ks] = f;
+    td[pos * ks] = dk;
     if (tp) {  // this query's masks sit in the spare slot; the evicted one's becomes spare
       tp[pos] = tp[K] | 0x80;
       tp[K] = evicted & 0x7f;
     }
   }
-  ls.steps[g] += 1;
-  ls.b[g] = f;
+  *r.steps += 1;
+  *r.b = f;
   const double dn = __dadd_rn(dk, __dmul_rn(a.alpha, f));
-  ls.d[g] = dn;
+  *r.d = dn;
   if (av < a.eps) {
-    ls.status[g] = DIST_CONVERGED;
+    *r.status = DIST_CONVERGED;
     return false;
   }
   double p[3];
@@ -138,10 +153,16 @@ __device__ __forceinline__ bool march_update(const LevelState &ls, const MarchAr
   const double r2 = __dadd_rn(__dadd_rn(__dmul_rn(p[0], p[0]), __dmul_rn(p[1], p[1])), __dmul_rn(p[2], p[2]));
   const double vp = __dadd_rn(__dadd_rn(__dmul_rn(dir[0], p[0]), __dmul_rn(dir[1], p[1])), __dmul_rn(dir[2], p[2]));
   if (r2 > 1.0 && f > 0.0 && vp > 0.0) {
-    ls.status[g] = DIST_ESCAPED;
+    *r.status = DIST_ESCAPED;
     return false;
   }
   return true;
+}
+
+__device__ __forceinline__ bool march_update(const LevelState &ls, const MarchArgs &a, int64_t g,
+                                             const double dir[3], const double *o, double f,
+                                             int *nan_count) {
+  return march_update_at(ray_ref(ls, a.K, g), a, dir, o, f, nan_count);
 }
 
 // Last CTA of a step slot records every stepping view's query count

@@ -12,17 +12,24 @@
 // the march update (NaN -> EXHAUSTED, top-K record, d += alpha f, converge /
 // escape tests) in the tile epilogue, and appends surviving rays to the next
 // live list with warp-aggregated atomics; the last CTA to finish records the
-// step's query count (TraceResult.live_counts) and flips the lists.
+// step's query count (TraceResult.live_counts) and flips the lists.  The
+// SIMT precisions run all slots of a level as ONE cooperative launch instead
+// (k_march_coop: the same step body, a grid barrier between steps).
+#include <cooperative_groups.h>
+
 #include <cmath>
 #include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
 #include "mlp_eval.cuh"
+#include "mlp_small.cuh"
 #include "scan.cuh"
 #include "march.cuh"
 
 namespace dist {
+
+namespace cg = cooperative_groups;
 
 // --- init (tracer.py:88-119) ----------------------------------------------
 __global__ void k_init(const dist_camera *__restrict__ cams, LevelState ls, int K,
@@ -189,23 +196,25 @@ __global__ void k_finalize(LevelState ls) {
 }
 
 // --- one step slot, SIMT decoder --------------------------------------------
+// Returns false (block-uniform) when the live list is empty: the slot is a
+// no-op and so is every later slot of the level.
 template <typename T>
-__global__ void __launch_bounds__(SimtTile<T>::NT)
-    k_step(DecView dv, const double *__restrict__ c0, const double *__restrict__ cskip,
-           const dist_camera *__restrict__ cams, LevelState ls, Ctl *ctl, int32_t *list0,
-           int32_t *list1, MarchArgs a, ViewBudget vb, int64_t *stats) {
-  extern __shared__ __align__(16) char smem[];
+__device__ __forceinline__ bool simt_step(char *smem, const DecView &dv, const double *__restrict__ c0,
+                                          const double *__restrict__ cskip,
+                                          const dist_camera *__restrict__ cams, const LevelState &ls,
+                                          Ctl *ctl, int32_t *list0, int32_t *list1, const MarchArgs &a,
+                                          const ViewBudget &vb, int64_t *stats) {
   using Tile = SimtTile<T>;
   Tile tile(smem);
   __shared__ int s_cur, s_cnt, s_go, s_nan;
   if (threadIdx.x == 0) {
-    s_cur = ctl->cur;
-    s_cnt = ctl->cnt[s_cur];
+    s_cur = *(volatile int *)&ctl->cur;
+    s_cnt = *(volatile int *)&ctl->cnt[s_cur];
     s_go = s_cnt > 0;   // per-view budgets gate the rays (ViewBudget)
     s_nan = 0;
   }
   __syncthreads();
-  if (!s_go) return;
+  if (!s_go) return false;
   const int cur = s_cur;
   const int32_t *in = cur ? list1 : list0;
   int32_t *out = cur ? list0 : list1;
@@ -249,6 +258,325 @@ __global__ void __launch_bounds__(SimtTile<T>::NT)
     __syncthreads();
   }
   step_epilogue(ctl, cur, vb, a, s_nan, stats);
+  return true;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(SimtTile<T>::NT)
+    k_step(DecView dv, const double *__restrict__ c0, const double *__restrict__ cskip,
+           const dist_camera *__restrict__ cams, LevelState ls, Ctl *ctl, int32_t *list0,
+           int32_t *list1, MarchArgs a, ViewBudget vb, int64_t *stats) {
+  extern __shared__ __align__(16) char smem[];
+  simt_step<T>(smem, dv, c0, cskip, cams, ls, ctl, list0, list1, a, vb, stats);
+}
+
+// All `slots` steps of a level in one cooperative launch (every CTA
+// co-resident): a grid barrier after each step's epilogue publishes the
+// flipped live list.  The same per-step code as k_step, without a launch per
+// slot -- what bounds small workloads (C1: ~100 slots of a few thousand rays).
+template <typename T>
+__global__ void __launch_bounds__(SimtTile<T>::NT)
+    k_march_coop(DecView dv, const double *__restrict__ c0, const double *__restrict__ cskip,
+                 const dist_camera *__restrict__ cams, LevelState ls, Ctl *ctl, int32_t *list0,
+                 int32_t *list1, MarchArgs a, ViewBudget vb, int64_t *stats, int slots) {
+  extern __shared__ __align__(16) char smem[];
+  cg::grid_group grid = cg::this_grid();
+  for (int s = 0; s < slots; ++s) {
+    if (!simt_step<T>(smem, dv, c0, cskip, cams, ls, ctl, list0, list1, a, vb, stats)) break;
+    grid.sync();
+  }
+}
+
+// All slots of a level for a NARROW decoder (mlp_small.cuh): one ray per
+// thread, the decoder staged in shared memory once, one cooperative launch
+// with a grid barrier after each step.  Same march update, compaction and
+// step bookkeeping as k_step.
+template <typename T>
+__global__ void __launch_bounds__(kSmallNT)
+    k_march_small(DecView dv, const double *__restrict__ c0, const double *__restrict__ cskip,
+                  const dist_camera *__restrict__ cams, LevelState ls, Ctl *ctl, int32_t *list0,
+                  int32_t *list1, MarchArgs a, ViewBudget vb, int64_t *stats, int slots) {
+  extern __shared__ __align__(16) char smem[];
+  cg::grid_group grid = cg::this_grid();
+  SmallNet<T> net;
+  net.stage(dv, smem);
+  __syncthreads();
+  __shared__ int s_cur, s_cnt, s_nan;
+  for (int sl = 0; sl < slots; ++sl) {
+    if (threadIdx.x == 0) {
+      s_cur = *(volatile int *)&ctl->cur;
+      s_cnt = *(volatile int *)&ctl->cnt[s_cur];
+      s_nan = 0;
+    }
+    __syncthreads();
+    if (s_cnt <= 0) break;   // grid-uniform: every CTA read the same controller
+    const int cur = s_cur;
+    const int32_t *in = cur ? list1 : list0;
+    int32_t *out = cur ? list0 : list1;
+    int32_t *out_cnt = &ctl->cnt[cur ^ 1];
+    const int64_t rows = a.dynamic ? (int64_t)s_cnt : ls.n;
+    for (int64_t base = (int64_t)blockIdx.x * kSmallNT; base < rows; base += (int64_t)gridDim.x * kSmallNT) {
+      const int64_t idx = base + threadIdx.x;
+      bool keep = false;
+      int v = -1;
+      int64_t g = -1;
+      if (idx < rows) {
+        g = a.dynamic ? in[idx] : idx;
+        if (ls.status[g] == DIST_MARCHING && vb_active(vb, a, g)) {
+          double dir[3], p[3];
+          const dist_camera *cam;
+          ray_of(cams, ls, g, dir, &cam);
+          const double dg = ls.d[g];
+          for (int i = 0; i < 3; ++i) p[i] = __dadd_rn(cam->origin[i], __dmul_rn(dg, dir[i]));
+          const double f = net.eval(dv, c0, cskip, p, cam->shape);
+          int nn = 0;
+          v = vb_view(vb, g);
+          keep = march_update(ls, a, g, dir, cam->origin, f, &nn) && vb_continues(vb, a, g);
+          if (nn) atomicAdd(&s_nan, nn);
+        }
+      }
+      vb_count(vb, v);
+      warp_append(keep, (int32_t)g, out, out_cnt);
+    }
+    step_epilogue(ctl, cur, vb, a, s_nan, stats);
+    grid.sync();
+  }
+}
+
+// Narrow decoder, level small enough for every ray to have a home thread
+// (<= kResidentR rays per thread over a co-resident grid): the level's ray
+// state is copied into shared memory at the start, each thread marches its
+// own rays for all slots (no live list: a ray is live while it is MARCHING and
+// its view has budget), and the state is written back once at the end.
+//
+// One grid barrier per step and no last-CTA hand-off: the step's per-view
+// query counts and its survivor count go to one of three rotating counter
+// rows (rcnt[3][V+1]); after the barrier every CTA reads the row and advances
+// its own shared copy of the per-view step counters identically, CTA 0
+// records live_counts and clears the row two steps ahead (read by everyone
+// before the previous barrier, written again only after the next).  The
+// bookkeeping is step_epilogue's (march.cuh), so the executed steps, the
+// per-view live_counts and the audit counters equal k_step's.
+constexpr int kResidentR = 4;
+constexpr int kResidentMaxViews = 1024;
+constexpr size_t kResidentCodeBytes = 48 * 1024;   // c0/cskip rows staged up to this size
+
+struct ResidentLayout {
+  int R, S, wb;          // rays per thread, shapes, register width bucket (64: shared activations)
+  int code_in_smem;      // c0 / cskip rows staged in shared memory
+  size_t off_vsteps, off_code, off_state, bytes;
+  // bytes per resident ray: d, b, top-K (3K), dir, origin (f64); steps, shape, view (i32); status
+  __host__ __device__ static size_t per_ray(int K) { return 8 * (2 + 3 * (size_t)K + 6) + 12 + 1; }
+};
+
+template <typename T, int WB>
+__global__ void __launch_bounds__(kSmallNT)
+    k_march_resident(DecView dv, const double *__restrict__ c0, const double *__restrict__ cskip,
+                     const dist_camera *__restrict__ cams, LevelState ls, Ctl *ctl, MarchArgs a,
+                     ViewBudget vb, int64_t *stats, int slots, ResidentLayout rl, int32_t *rcnt) {
+  extern __shared__ __align__(16) char smem[];
+  constexpr int NT = kSmallNT;
+  cg::grid_group grid = cg::this_grid();
+  SmallNet<T> net;
+  net.stage(dv, smem);
+  const int K = a.K, R = rl.R, t = threadIdx.x, V = a.V;
+  const int n0 = dv.nr[0], ns = dv.skip > 0 ? dv.nr[dv.skip] : 0;
+  // shared ray state, [field][R * NT] (slot i = r * NT + t)
+  const int M = R * NT;
+  double *sd = reinterpret_cast<double *>(smem + rl.off_state);
+  double *sb = sd + M;
+  double *sta = sb + M, *stf = sta + (size_t)K * M, *std_ = stf + (size_t)K * M;
+  double *sdir = std_ + (size_t)K * M, *sorg = sdir + 3 * M;
+  int32_t *ssteps = reinterpret_cast<int32_t *>(sorg + 3 * M);
+  int32_t *sshape = ssteps + M, *sview = sshape + M;
+  uint8_t *sstat = reinterpret_cast<uint8_t *>(sview + M);
+  int32_t *vsteps = reinterpret_cast<int32_t *>(smem + rl.off_vsteps);   // [V] this CTA's copy
+  double *scode = reinterpret_cast<double *>(smem + rl.off_code);       // [S][n0] then [S][ns]
+  if (rl.code_in_smem) {
+    for (int i = t; i < rl.S * n0; i += NT) scode[i] = c0[(size_t)(i / n0) * dv.np[0] + i % n0];
+    for (int i = t; i < rl.S * ns; i += NT)
+      scode[rl.S * n0 + i] = cskip[(size_t)(i / ns) * dv.np[dv.skip] + i % ns];
+  }
+  const int64_t g0 = (int64_t)blockIdx.x * M;
+  for (int i = t; i < M; i += NT) {
+    const int64_t g = g0 + i;
+    if (g < ls.n) {
+      sd[i] = ls.d[g];
+      sb[i] = ls.b[g];
+      ssteps[i] = ls.steps[g];
+      sstat[i] = ls.status[g];
+      for (int k = 0; k < K; ++k) {
+        sta[k * M + i] = ls.tk_a[g * K + k];
+        stf[k * M + i] = ls.tk_f[g * K + k];
+        std_[k * M + i] = ls.tk_d[g * K + k];
+      }
+      double dir[3];
+      const dist_camera *cam;
+      ray_of(cams, ls, g, dir, &cam);   // fixed for the level: once, not per step
+      for (int c = 0; c < 3; ++c) {
+        sdir[c * M + i] = dir[c];
+        sorg[c * M + i] = cam->origin[c];
+      }
+      sshape[i] = cam->shape;
+      sview[i] = vb_view(vb, g);
+    } else {
+      sstat[i] = DIST_CONVERGED;   // no ray: never live
+    }
+  }
+  for (int v = t; v < V; v += NT) vsteps[v] = vb.steps[v];
+  const int W = V + 1;   // counter row: [V] queried rows per view, [V] survivors
+  if (blockIdx.x == 0)
+    for (int i = t; i < 3 * W; i += NT) rcnt[i] = 0;
+  __shared__ int s_live, s_keep, s_nan, s_smax;
+  __shared__ unsigned long long s_q;
+  if (t == 0) {
+    s_live = ctl->cnt[ctl->cur];   // the level's initial live list (k_init / k_split)
+    s_q = 0;
+    s_smax = 0;
+  }
+  grid.sync();
+  int executed = 0;
+  for (int sl = 0; sl < slots; ++sl) {
+    if (s_live <= 0) break;   // grid-uniform: every CTA read the same row
+    int32_t *row = rcnt + (sl % 3) * W;
+    if (t == 0) {
+      s_keep = 0;
+      s_nan = 0;
+    }
+    __syncthreads();
+    int kept = 0;
+    for (int r = 0; r < R; ++r) {
+      const int i = r * NT + t;
+      int v = -1;
+      if (sstat[i] == DIST_MARCHING) {
+        const int vv = sview[i];
+        if (vsteps[vv] < a.max_steps) {
+          const double dir[3] = {sdir[i], sdir[M + i], sdir[2 * M + i]};
+          const double org[3] = {sorg[i], sorg[M + i], sorg[2 * M + i]};
+          const double dg = sd[i];
+          double p[3];
+          for (int c = 0; c < 3; ++c) p[c] = __dadd_rn(org[c], __dmul_rn(dg, dir[c]));
+          const int sh = sshape[i];
+          double f;
+          if constexpr (WB < 64) {
+            const double *cz = rl.code_in_smem ? scode + (size_t)sh * n0 : c0 + (size_t)sh * dv.np[0];
+            const double *cs = rl.code_in_smem ? scode + (size_t)rl.S * n0 + (size_t)sh * ns
+                                               : (ns ? cskip + (size_t)sh * dv.np[dv.skip] : nullptr);
+            f = net.template eval_reg<WB>(dv, cz, cs, p);
+          } else {
+            f = net.eval(dv, c0, cskip, p, sh);
+          }
+          int nn = 0;
+          v = vv;
+          const RayRef ref{sd + i, sb + i, sstat + i, ssteps + i, sta + i, stf + i, std_ + i, M, nullptr};
+          kept += (march_update_at(ref, a, dir, org, f, &nn) && vsteps[vv] + 1 < a.max_steps) ? 1 : 0;
+          if (nn) atomicAdd(&s_nan, nn);
+        }
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, v);
+      if (v >= 0 && (t & 31) == __ffs(peers) - 1) atomicAdd(&row[v], __popc(peers));
+    }
+    kept = __reduce_add_sync(0xffffffffu, kept);
+    if ((t & 31) == 0 && kept) atomicAdd(&s_keep, kept);
+    __syncthreads();
+    if (t == 0) {
+      if (s_keep) atomicAdd(&row[V], s_keep);
+      if (s_nan) atomicAdd((unsigned long long *)&stats[1], (unsigned long long)s_nan);
+    }
+    grid.sync();
+    // every CTA: advance its view step copies from the row
+    for (int v = t; v < V; v += NT) {
+      const int c = *(volatile int32_t *)&row[v];
+      if (!c) continue;
+      const int sv = vsteps[v];
+      if (blockIdx.x == 0) {
+        const int64_t n = a.dynamic ? (int64_t)c : vb.per;
+        vb.live[(int64_t)v * a.max_steps + sv] = n;
+        atomicAdd(&s_q, (unsigned long long)n);
+        atomicMax(&s_smax, sv + 1);
+      }
+      vsteps[v] = sv + 1;
+    }
+    if (t == 0) s_live = *(volatile int32_t *)&row[V];
+    if (blockIdx.x == 0) {   // the row two steps ahead: read by all before this barrier
+      int32_t *nxt = rcnt + ((sl + 2) % 3) * W;
+      for (int i = t; i < W; i += NT) nxt[i] = 0;
+    }
+    ++executed;
+    __syncthreads();
+  }
+  if (blockIdx.x == 0) {
+    for (int v = t; v < V; v += NT) vb.steps[v] = vsteps[v];
+    if (t == 0) {
+      ctl->steps_done += executed;
+      if (s_q) atomicAdd((unsigned long long *)&stats[0], s_q);
+      if (s_smax) atomicMax((unsigned long long *)&stats[2], (unsigned long long)s_smax);
+    }
+  }
+  for (int i = t; i < M; i += NT) {
+    const int64_t g = g0 + i;
+    if (g < ls.n) {
+      ls.d[g] = sd[i];
+      ls.b[g] = sb[i];
+      ls.steps[g] = ssteps[i];
+      ls.status[g] = sstat[i];
+      for (int k = 0; k < K; ++k) {
+        ls.tk_a[g * K + k] = sta[k * M + i];
+        ls.tk_f[g * K + k] = stf[k * M + i];
+        ls.tk_d[g * K + k] = std_[k * M + i];
+      }
+    }
+  }
+}
+
+template <typename T, int WB>
+static int launch_resident(const DecView &dv, const double *c0, const double *cskip,
+                           const dist_camera *cams, const LevelState &ls, Ctl *ctl, const MarchArgs &a,
+                           int slots, const ViewBudget &vb, int64_t *stats, int32_t *rcnt, int S,
+                           cudaStream_t st, bool *launched) {
+  *launched = false;
+  const int K = a.K;
+  const size_t wbytes = SmallNet<T>::weight_bytes(dv);
+  const size_t act = WB < 64 ? 0 : 2 * sizeof(T) * kSmallWidth * kSmallNT;
+  const int n0 = dv.nr[0], ns = dv.skip > 0 ? dv.nr[dv.skip] : 0;
+  const size_t code = sizeof(double) * (size_t)S * (n0 + ns);
+  ResidentLayout rl{};
+  rl.S = S;
+  rl.wb = WB;
+  rl.off_vsteps = round_up((int64_t)(wbytes + act), 16);
+  rl.off_code = round_up((int64_t)(rl.off_vsteps + sizeof(int32_t) * a.V), 16);
+  rl.code_in_smem = code <= kResidentCodeBytes;
+  rl.off_state = round_up((int64_t)(rl.off_code + (rl.code_in_smem ? code : 0)), 16);
+  for (int R = 1; R <= kResidentR; ++R) {
+    const size_t bytes = rl.off_state + (size_t)R * kSmallNT * ResidentLayout::per_ray(K);
+    if (bytes > 200 * 1024) break;
+    const void *rf = (const void *)k_march_resident<T, WB>;
+    cudaError_t e = cudaFuncSetAttribute(rf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(march_resident)");
+    int cap_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&cap_sm, rf, kSmallNT, bytes);
+    const int64_t grid = ceil_div(ls.n, (int64_t)R * kSmallNT);
+    if (cap_sm < 1 || grid > (int64_t)cap_sm * sm_count()) continue;
+    rl.R = R;
+    rl.bytes = bytes;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)grid);
+    lc.blockDim = dim3(kSmallNT);
+    lc.dynamicSmemBytes = bytes;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&lc, k_march_resident<T, WB>, dv, c0, cskip, cams, ls, ctl, a, vb, stats, slots,
+                           rl, rcnt);
+    if (e != cudaSuccess) return cuda_fail(e, "k_march_resident");
+    DIST_CHECK_LAUNCH("k_march_resident");
+    *launched = true;
+    return DIST_OK;
+  }
+  return DIST_OK;
 }
 
 // --- maps (shading.py:48-61, 97-113) ------------------------------------------
@@ -430,6 +758,7 @@ struct TraceLayout {
   int n_levels;
   int32_t *list0, *list1, *bcount;
   int32_t *vsteps, *vcnt;   // ViewBudget: per-view steps and this slot's counts
+  int32_t *rcnt;            // k_march_resident: three rotating [V+1] counter rows
   Ctl *ctl;
   size_t bytes;
 };
@@ -477,6 +806,7 @@ static TraceLayout layout(const DecView &dv, const dist_trace_config *cfg, int V
   L.bcount = cv.take<int32_t>(ceil_div(nmax * 6, kScanBlock) + 1);
   L.vsteps = cv.take<int32_t>(2 * (size_t)V);
   L.vcnt = L.vsteps ? L.vsteps + V : nullptr;
+  L.rcnt = cv.take<int32_t>(3 * ((size_t)V + 1));
   L.ctl = cv.take<Ctl>(1);
   L.bytes = cv.off + 256;
   return L;
@@ -486,8 +816,44 @@ template <typename T>
 static int run_steps(const DecView &dv, const double *c0, const double *cskip,
                      const dist_camera *cams, const LevelState &ls, Ctl *ctl, int32_t *l0,
                      int32_t *l1, const MarchArgs &a, int slots, const ViewBudget &vb, int64_t *stats,
-                     cudaStream_t st) {
+                     int32_t *rcnt, int S, cudaStream_t st) {
   using Tile = SimtTile<T>;
+  const size_t small = SmallNet<T>::smem_bytes(dv);
+  if (small && !ls.tk_p && rcnt && a.V <= kResidentMaxViews) {
+    // every ray resident in shared memory for the whole level?
+    bool done = false;
+    const int wb = SmallNet<T>::width_bucket(dv);
+    int rc = wb == 16 ? launch_resident<T, 16>(dv, c0, cskip, cams, ls, ctl, a, slots, vb, stats, rcnt, S, st, &done)
+           : wb == 32 ? launch_resident<T, 32>(dv, c0, cskip, cams, ls, ctl, a, slots, vb, stats, rcnt, S, st, &done)
+                      : launch_resident<T, 64>(dv, c0, cskip, cams, ls, ctl, a, slots, vb, stats, rcnt, S, st, &done);
+    if (rc || done) return rc;
+  }
+  if (small && small <= 200 * 1024) {
+    // narrow decoder: one ray per thread, the whole level in one cooperative launch
+    const void *sf = (const void *)k_march_small<T>;
+    cudaError_t e = cudaFuncSetAttribute(sf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(march_small)");
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, sf, kSmallNT, small);
+    if (per >= 1) {
+      const int64_t need = ceil_div(ls.n, kSmallNT);
+      const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)per * sm_count()));
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(grid);
+      lc.blockDim = dim3(kSmallNT);
+      lc.dynamicSmemBytes = small;
+      lc.stream = st;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeCooperative;
+      at[0].val.cooperative = 1;
+      lc.attrs = at;
+      lc.numAttrs = 1;
+      e = cudaLaunchKernelEx(&lc, k_march_small<T>, dv, c0, cskip, cams, ls, ctl, l0, l1, a, vb, stats, slots);
+      if (e != cudaSuccess) return cuda_fail(e, "k_march_small");
+      DIST_CHECK_LAUNCH("k_march_small");
+      return DIST_OK;
+    }
+  }
   const void *fn = (const void *)k_step<T>;
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)Tile::fwd_bytes);
@@ -496,6 +862,29 @@ static int run_steps(const DecView &dv, const double *c0, const double *cskip,
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, Tile::NT, Tile::fwd_bytes);
   const int64_t tiles = ceil_div(ls.n, Tile::TM);
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, (int64_t)std::max(per_sm, 1) * sm_count()));
+  if (slots > 1 && per_sm >= 1) {
+    // one cooperative launch for the level (grid <= co-resident CTAs)
+    const void *cf = (const void *)k_march_coop<T>;
+    e = cudaFuncSetAttribute(cf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Tile::fwd_bytes);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(march_coop)");
+    int coop_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&coop_sm, cf, Tile::NT, Tile::fwd_bytes);
+    const int cgrid = std::min(grid, std::max(coop_sm, 1) * sm_count());
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(cgrid);
+    lc.blockDim = dim3(Tile::NT);
+    lc.dynamicSmemBytes = Tile::fwd_bytes;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&lc, k_march_coop<T>, dv, c0, cskip, cams, ls, ctl, l0, l1, a, vb, stats, slots);
+    if (e != cudaSuccess) return cuda_fail(e, "k_march_coop");
+    DIST_CHECK_LAUNCH("k_march_coop");
+    return DIST_OK;
+  }
   for (int s = 0; s < slots; ++s) {
     k_step<T><<<grid, Tile::NT, Tile::fwd_bytes, st>>>(dv, c0, cskip, cams, ls, ctl, l0, l1, a, vb,
                                                       stats);
@@ -559,11 +948,11 @@ int dist_trace(const dist_decoder *dec, const double *codes, int S, const dist_c
     const int slots = std::min(ls.level > 1 ? cfg->split_interval : cfg->max_steps, cfg->max_steps);
     const ViewBudget vb{L.vsteps, L.vcnt, live, (int64_t)ls.lw * ls.lh};
     if (dv.prec == DIST_PREC_FP64)
-      rc = run_steps<double>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, vb, stats, st);
+      rc = run_steps<double>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, vb, stats, L.rcnt, std::max(S, 1), st);
     else if (tc_supported(dv))
       rc = tc_run_steps(dv, L.c0, L.cskip, std::max(S, 1), cams, ls, L.ctl, L.list0, L.list1, a, slots, vb, stats, st);
     else
-      rc = run_steps<float>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, vb, stats, st);
+      rc = run_steps<float>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, vb, stats, L.rcnt, std::max(S, 1), st);
     if (rc) return rc;
   }
   const LevelState &fin = L.lv[L.n_levels - 1];

@@ -23,9 +23,10 @@ pytestmark = pytest.mark.gpu
 ITERS = 3
 
 
-def _problem(st):
+def _problem(st, skip=-1):
     from paper_1911_13225_b200.workloads import render_depth_observations, ring_views, target_code
-    field = st.NeuralField.geometric(256, (512,) * 8, 0, precision="fp16x3")
+    field = (st.NeuralField.geometric(256, (512,) * 8, 0, precision="fp16x3", skip=skip) if skip >= 0
+             else st.NeuralField.geometric(256, (512,) * 8, 0, precision="fp16x3"))
     views = ring_views(2, 128)
     cfg = st.TraceConfig(k_samples=3)
     obs = render_depth_observations(field, target_code(1), views, cfg).cpu().numpy()
@@ -33,8 +34,8 @@ def _problem(st):
     return field, views, cfg, {"depth": obs, "silhouette": sil}
 
 
-def _run(st, shard=None):
-    field, views, cfg, obs = _problem(st)
+def _run(st, shard=None, skip=-1):
+    field, views, cfg, obs = _problem(st, skip)
     opt = st.LatentOptimizer(field, views, obs, np.zeros((1, 256)), cfg, max_iters=ITERS,
                              shard=shard)
     codes = []
@@ -44,7 +45,7 @@ def _run(st, shard=None):
     return np.stack(codes), opt.losses()[:, 0]
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, skip=-1):
     import torch
     import torch.distributed as dist
     import paper_1911_13225_b200 as st
@@ -52,12 +53,15 @@ def _worker(rank, world, port, out):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    codes, losses = _run(st, TileShard(rank, world, 32))
+    codes, losses = _run(st, TileShard(rank, world, 32), skip)
     out[rank] = (codes.tolist(), losses.tolist())
     dist.destroy_process_group()
 
 
-def test_two_ranks_one_gpu_bit_identical_iterates():
+@pytest.mark.parametrize("skip", [-1, 4])
+def test_two_ranks_one_gpu_bit_identical_iterates(skip):
+    """skip=4: the DeepSDF decoder, whose exact column sums carry the skip
+    layer's code rows as a second block."""
     import torch.multiprocessing as mp
     import paper_1911_13225_b200 as st
     from paper_1911_13225_b200.shard import TileShard
@@ -66,9 +70,9 @@ def test_two_ranks_one_gpu_bit_identical_iterates():
     port = s.getsockname()[1]
     s.close()
     out = mp.get_context("spawn").Manager().dict()
-    mp.spawn(_worker, args=(2, port, out), nprocs=2, join=True)
-    c1, l1 = _run(st, TileShard(0, 1, 32))      # one rank, the same tiles
-    c0, l0 = _run(st)                            # unsharded whole views
+    mp.spawn(_worker, args=(2, port, out, skip), nprocs=2, join=True)
+    c1, l1 = _run(st, TileShard(0, 1, 32), skip)      # one rank, the same tiles
+    c0, l0 = _run(st, None, skip)                      # unsharded whole views
     for r in range(2):
         assert np.array_equal(np.asarray(out[r][0]), c1), f"rank {r} iterates differ from world 1"
         assert np.array_equal(np.asarray(out[r][1]), l1), f"rank {r} losses differ from world 1"
