@@ -166,82 +166,6 @@ struct SmallNet {
     return head_act(dv.final_act, sum);
   }
 
-  // The same arithmetic with the activations in registers (every hidden
-  // width <= WB, a compile-time bucket): k outer / n inner, so each h_k feeds
-  // N independent FMA chains, each still summed over k ascending from (T)0.
-  // cz / cs: this ray's shape rows of c0 and cskip (either memory space).
-  template <int WB>
-  __device__ __forceinline__ double eval_reg(const DecView &dv, const double *cz, const double *cs,
-                                             const double p[3]) const {
-    const int L = dv.n_layers;
-    T h[WB], o[WB];
-    {
-      const int n0 = dv.nr[0];
-#pragma unroll
-      for (int n = 0; n < WB; ++n) {
-        double v = 0.0;
-        if (n < n0) {
-          v = cz[n];
-          v = fma(p[0], W0p[n], v);
-          v = fma(p[1], W0p[n0 + n], v);
-          v = fma(p[2], W0p[2 * n0 + n], v);
-        }
-        h[n] = (T)(!(v <= 0.0) ? v : 0.0);
-      }
-    }
-    const char *q = layers;
-    for (int l = 1; l <= L - 2; ++l) {
-      const int K = dv.nr[l - 1], N = dv.nr[l];
-      const T *w = reinterpret_cast<const T *>(q);
-      q += al8(sizeof(T) * K * N);
-      const T *bb = reinterpret_cast<const T *>(q);
-      q += al8(sizeof(T) * N);
-      const bool is_skip = (l == dv.skip);
-      const double *Wsp = reinterpret_cast<const double *>(q);
-      if (is_skip) q += al8(sizeof(double) * 3 * N);
-#pragma unroll
-      for (int n = 0; n < WB; ++n) o[n] = (T)0;
-#pragma unroll
-      for (int k = 0; k < WB; ++k) {
-        if (k < K) {
-          const T hk = h[k];
-          const T *wr = w + k * N;
-#pragma unroll
-          for (int n = 0; n < WB; ++n)
-            if (n < N) o[n] = fma(hk, wr[n], o[n]);
-        }
-      }
-#pragma unroll
-      for (int n = 0; n < WB; ++n) {
-        T v = (T)0;
-        if (n < N) {
-          v = o[n] + bb[n];
-          if (is_skip) {
-            double e = cs[n];
-            e = fma(p[0], Wsp[n], e);
-            e = fma(p[1], Wsp[N + n], e);
-            e = fma(p[2], Wsp[2 * N + n], e);
-            v = (T)((double)v + e);
-          }
-          v = !(v <= (T)0) ? v : (T)0;
-        }
-        h[n] = v;
-      }
-    }
-    const int Ko = dv.nr[L - 2];
-    T part[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) part[j] = (T)0;
-#pragma unroll
-    for (int k = 0; k < WB; ++k)
-      if (k < Ko) part[k & 7] = fma(h[k], wout[k], part[k & 7]);
-    double sum = 0.0;
-#pragma unroll
-    for (int j = 0; j < 8; ++j) sum += (double)part[j];
-    sum += dv.b_out;
-    return head_act(dv.final_act, sum);
-  }
-
   __host__ static int width_bucket(const DecView &dv) {
     int w = 0;
     for (int l = 0; l <= dv.n_layers - 2; ++l) w = w > dv.nr[l] ? w : dv.nr[l];
@@ -260,6 +184,123 @@ struct SmallNet {
       v = (T)((double)v + e);
     }
     return !(v <= (T)0) ? v : (T)0;
+  }
+};
+
+// The same arithmetic with the activations in registers, for decoders whose
+// every width is <= WB (16 or 32): the decoder is staged zero-padded to
+// WB x WB per layer, so the fully unrolled loops need no width guards and
+// read weight rows as 16-byte broadcasts.  The padding adds exact zeros
+// (h = 0 past a layer's width, w = 0 past its rows/columns; an accumulator
+// starting at +0 never becomes -0), so results equal SmallNet::eval's bits.
+// k outer / n inner: each h_k feeds WB independent FMA chains, each summed
+// over k ascending from (T)0.
+template <typename T, int WB>
+struct RegNet {
+  static constexpr int WI = sizeof(T) == 4 ? 1 : 0;
+
+  // staged layout: W0p [3][WB] f64; per hidden layer: W [WB][WB] T, b [WB] T,
+  // Wsp [3][WB] f64 (every layer: keeps the stride uniform); w_out [WB] T
+  __host__ __device__ static size_t layer_bytes() {
+    return sizeof(T) * (WB * WB + WB) + sizeof(double) * 3 * WB;
+  }
+  __host__ __device__ static size_t weight_bytes(const DecView &dv) {
+    return sizeof(double) * 3 * WB + (size_t)(dv.n_layers - 2) * layer_bytes() + sizeof(T) * WB;
+  }
+
+  const char *base;
+
+  __device__ void stage(const DecView &dv, char *smem) {
+    const int L = dv.n_layers, tid = threadIdx.x, nt = blockDim.x;
+    base = smem;
+    double *w0 = reinterpret_cast<double *>(smem);
+    const int n0 = dv.nr[0], s0 = dv.np[0];
+    for (int i = tid; i < 3 * WB; i += nt) {
+      const int a = i / WB, n = i % WB;
+      w0[i] = n < n0 ? dv.W0p[a * s0 + n] : 0.0;
+    }
+    char *q = smem + sizeof(double) * 3 * WB;
+    for (int l = 1; l <= L - 2; ++l, q += layer_bytes()) {
+      const int K = dv.nr[l - 1], N = dv.nr[l], ldw = dv.np[l];
+      T *w = reinterpret_cast<T *>(q);
+      T *bb = w + WB * WB;
+      double *ws = reinterpret_cast<double *>(bb + WB);
+      const T *gw = reinterpret_cast<const T *>(dv.W[WI][l]);
+      const T *gb = reinterpret_cast<const T *>(dv.bias[WI][l]);
+      for (int i = tid; i < WB * WB; i += nt) {
+        const int k = i / WB, n = i % WB;
+        w[i] = (k < K && n < N) ? gw[(size_t)k * ldw + n] : (T)0;
+      }
+      for (int i = tid; i < WB; i += nt) bb[i] = i < N ? gb[i] : (T)0;
+      for (int i = tid; i < 3 * WB; i += nt) {
+        const int a = i / WB, n = i % WB;
+        ws[i] = (l == dv.skip && n < N) ? dv.Wsp[(size_t)a * ldw + n] : 0.0;
+      }
+    }
+    T *wo = reinterpret_cast<T *>(q);
+    const int Ko = dv.nr[L - 2];
+    const T *gwo = reinterpret_cast<const T *>(dv.w_out[WI]);
+    for (int i = tid; i < WB; i += nt) wo[i] = i < Ko ? gwo[i] : (T)0;
+  }
+
+  // cz / cs: this ray's shape rows of c0 and cskip, zero past the widths
+  // (>= WB readable entries each)
+  __device__ __forceinline__ double eval(const DecView &dv, const double *cz, const double *cs,
+                                         const double p[3]) const {
+    const int L = dv.n_layers;
+    const double *W0p = reinterpret_cast<const double *>(base);
+    T h[WB], o[WB];
+#pragma unroll
+    for (int n = 0; n < WB; ++n) {
+      double v = cz[n];
+      v = fma(p[0], W0p[n], v);
+      v = fma(p[1], W0p[WB + n], v);
+      v = fma(p[2], W0p[2 * WB + n], v);
+      h[n] = (T)(!(v <= 0.0) ? v : 0.0);   // np.maximum: NaN propagates
+    }
+    const char *q = base + sizeof(double) * 3 * WB;
+    for (int l = 1; l <= L - 2; ++l, q += layer_bytes()) {
+      const T *w = reinterpret_cast<const T *>(q);
+      const T *bb = w + WB * WB;
+      const double *Wsp = reinterpret_cast<const double *>(bb + WB);
+#pragma unroll
+      for (int n = 0; n < WB; ++n) o[n] = (T)0;
+#pragma unroll
+      for (int k = 0; k < WB; ++k) {
+        const T hk = h[k];
+#pragma unroll
+        for (int n = 0; n < WB; ++n) o[n] = fma(hk, w[k * WB + n], o[n]);
+      }
+      if (l == dv.skip) {
+#pragma unroll
+        for (int n = 0; n < WB; ++n) {
+          T v = o[n] + bb[n];
+          double e = cs[n];
+          e = fma(p[0], Wsp[n], e);
+          e = fma(p[1], Wsp[WB + n], e);
+          e = fma(p[2], Wsp[2 * WB + n], e);
+          v = (T)((double)v + e);
+          h[n] = !(v <= (T)0) ? v : (T)0;
+        }
+      } else {
+#pragma unroll
+        for (int n = 0; n < WB; ++n) {
+          const T v = o[n] + bb[n];
+          h[n] = !(v <= (T)0) ? v : (T)0;
+        }
+      }
+    }
+    const T *wout = reinterpret_cast<const T *>(q);
+    T part[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) part[j] = (T)0;
+#pragma unroll
+    for (int k = 0; k < WB; ++k) part[k & 7] = fma(h[k], wout[k], part[k & 7]);
+    double sum = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sum += (double)part[j];
+    sum += dv.b_out;
+    return head_act(dv.final_act, sum);
   }
 };
 

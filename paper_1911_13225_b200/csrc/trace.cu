@@ -378,9 +378,14 @@ __global__ void __launch_bounds__(kSmallNT)
   constexpr int NT = kSmallNT;
   cg::grid_group grid = cg::this_grid();
   SmallNet<T> net;
-  net.stage(dv, smem);
+  RegNet<T, WB < 64 ? WB : 16> rnet;
+  if constexpr (WB < 64) rnet.stage(dv, smem);
+  else net.stage(dv, smem);
   const int K = a.K, R = rl.R, t = threadIdx.x, V = a.V;
+  // staged code rows: [S][cw] of c0 then [S][cw] of cskip (zero-padded to WB
+  // for the register path, the true widths otherwise)
   const int n0 = dv.nr[0], ns = dv.skip > 0 ? dv.nr[dv.skip] : 0;
+  const int cw0 = WB < 64 ? WB : n0, cws = WB < 64 ? (ns ? WB : 0) : ns;
   // shared ray state, [field][R * NT] (slot i = r * NT + t)
   const int M = R * NT;
   double *sd = reinterpret_cast<double *>(smem + rl.off_state);
@@ -392,10 +397,10 @@ __global__ void __launch_bounds__(kSmallNT)
   uint8_t *sstat = reinterpret_cast<uint8_t *>(sview + M);
   int32_t *vsteps = reinterpret_cast<int32_t *>(smem + rl.off_vsteps);   // [V] this CTA's copy
   double *scode = reinterpret_cast<double *>(smem + rl.off_code);       // [S][n0] then [S][ns]
-  if (rl.code_in_smem) {
-    for (int i = t; i < rl.S * n0; i += NT) scode[i] = c0[(size_t)(i / n0) * dv.np[0] + i % n0];
-    for (int i = t; i < rl.S * ns; i += NT)
-      scode[rl.S * n0 + i] = cskip[(size_t)(i / ns) * dv.np[dv.skip] + i % ns];
+  if (rl.code_in_smem) {   // the blob's rows are zero-padded to np >= 64 >= cw
+    for (int i = t; i < rl.S * cw0; i += NT) scode[i] = c0[(size_t)(i / cw0) * dv.np[0] + i % cw0];
+    for (int i = t; i < rl.S * cws; i += NT)
+      scode[rl.S * cw0 + i] = cskip[(size_t)(i / cws) * dv.np[dv.skip] + i % cws];
   }
   const int64_t g0 = (int64_t)blockIdx.x * M;
   for (int i = t; i < M; i += NT) {
@@ -459,10 +464,10 @@ __global__ void __launch_bounds__(kSmallNT)
           const int sh = sshape[i];
           double f;
           if constexpr (WB < 64) {
-            const double *cz = rl.code_in_smem ? scode + (size_t)sh * n0 : c0 + (size_t)sh * dv.np[0];
-            const double *cs = rl.code_in_smem ? scode + (size_t)rl.S * n0 + (size_t)sh * ns
+            const double *cz = rl.code_in_smem ? scode + (size_t)sh * cw0 : c0 + (size_t)sh * dv.np[0];
+            const double *cs = rl.code_in_smem ? scode + (size_t)rl.S * cw0 + (size_t)sh * cws
                                                : (ns ? cskip + (size_t)sh * dv.np[dv.skip] : nullptr);
-            f = net.template eval_reg<WB>(dv, cz, cs, p);
+            f = rnet.eval(dv, cz, cs, p);
           } else {
             f = net.eval(dv, c0, cskip, p, sh);
           }
@@ -536,10 +541,10 @@ static int launch_resident(const DecView &dv, const double *c0, const double *cs
                            cudaStream_t st, bool *launched) {
   *launched = false;
   const int K = a.K;
-  const size_t wbytes = SmallNet<T>::weight_bytes(dv);
+  const size_t wbytes = WB < 64 ? RegNet<T, WB < 64 ? WB : 16>::weight_bytes(dv) : SmallNet<T>::weight_bytes(dv);
   const size_t act = WB < 64 ? 0 : 2 * sizeof(T) * kSmallWidth * kSmallNT;
   const int n0 = dv.nr[0], ns = dv.skip > 0 ? dv.nr[dv.skip] : 0;
-  const size_t code = sizeof(double) * (size_t)S * (n0 + ns);
+  const size_t code = sizeof(double) * (size_t)S * (WB < 64 ? WB + (ns ? WB : 0) : n0 + ns);
   ResidentLayout rl{};
   rl.S = S;
   rl.wb = WB;

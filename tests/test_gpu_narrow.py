@@ -1,7 +1,9 @@
-"""The narrow-decoder march (csrc/mlp_small.cuh, k_march_small): decoders
-whose hidden layers are all <= 64 wide -- the reference's tiny_net (C1,
-conftest.py:33-39) -- march one ray per thread with the decoder staged in
-shared memory, all slots of a level in one cooperative launch.  Parity is
+"""The narrow-decoder march (csrc/mlp_small.cuh; trace.cu k_march_resident /
+k_march_small): decoders whose hidden layers are all <= 64 wide -- the
+reference's tiny_net (C1, conftest.py:33-39) -- march one ray per thread with
+the decoder staged in shared memory, all slots of a level in one cooperative
+launch (and, when the level fits the grid, the ray state resident in shared
+memory with activations in registers for widths <= 32).  Parity is
 the reference's: per-step query counts and ray status exactly, depth to
 1e-9 in fp64 (tracer.py:221-252 restated by the oracle)."""
 from __future__ import annotations
@@ -49,11 +51,13 @@ def test_tiny_net_trace(st, prec, dynamic):
     assert (T.status == 1).sum() > 100
 
 
-def test_narrow_skip_net_trace(st):
-    """A 4 x 48 decoder with a layer-2 skip (the pre-skip layer 37 wide):
-    the skip layer's folded code rows + xyz term in the one-ray-per-thread path."""
+@pytest.mark.parametrize("width", [32, 48])
+def test_narrow_skip_net_trace(st, width):
+    """A 4 x width decoder with a layer-2 skip (the pre-skip layer width-11
+    wide): the skip layer's folded code rows + xyz term in the one-ray-per-
+    thread path (32: register activations; 48: shared-memory activations)."""
     D = 8
-    ws = orc.geometric_init(D, (48,) * 4, 5, skip=2)
+    ws = orc.geometric_init(D, (width,) * 4, 5, skip=2)
     dec = orc.Decoder(ws, D, skip=2)
     net = st.NeuralField(ws, latent_dim=D, precision="fp64", skip=2)
     code = np.random.default_rng(2).normal(0, 0.1, D)
