@@ -253,8 +253,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int ph = BWD ? G : 0; ph < NPH; ++ph, ++phase) {
           mbar_wait(&m.aready, phase & 1);
           tc_fence_after();
+          // fully unrolled: a loop that waits on a barrier gets a YIELD on its
+          // back-edge, which costs the MMA issue ~25% of the tensor pipe
+          // (scripts/tc_pattern_bench.cu patterns 18 vs 27)
+#pragma unroll
           for (int nh = 0; nh < 2; ++nh) {
             const uint32_t d = tmem + nh * 128;
+#pragma unroll
             for (int kc = 0; kc < NKB; ++kc, ++it) {
               if (nh == 0 && kc == NKB / 2) {   // second half of A: written after the first
                 mbar_wait(&m.aready2, phase & 1);

@@ -71,7 +71,7 @@ struct Params {
   int timeline;           // DIST_TC_TIMELINE: phase marks of CTA 0 (debug)
   double head_gain;       // the 512 -> 1 head dot's gain (DecView.tc_gain; DIST_TC_HEAD_GAIN overrides)
   int debug;              // timing experiments: 1 = no epilogue math, 2 = no MMAs, 3 = no mask-record
-                          // stores (results invalid)
+                          // stores, 4 = no weight TMA (results invalid)
 };
 
 // ---------------------------------------------------------------------------
@@ -261,6 +261,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             for (int kc = 0; kc < NKB; ++kc, ++it) {
               const int s = it % STAGES;
               mbar_wait(&m.empty[s], ((it / STAGES) & 1) ^ 1);
+              if (P.debug == 4) {   // timing experiment: no weight stream (stale B, results invalid)
+                if (rank == 0) mbar_arrive_cluster(&m.full[s], 0);
+                continue;
+              }
               if (rank == 0) mbar_arrive_expect_tx(&m.full[s], 2 * STAGE_BYTES);
               const uint32_t dst = smem_u32(smem + OFF_B + s * STAGE_BYTES);
               const int y = nh * 256 + (int)rank * 128;
@@ -277,8 +281,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int l = 0; l < G; ++l, ++layer) {
           mbar_wait(&m.aready, layer & 1);
           tc_fence_after();
+          // fully unrolled: a loop that waits on a barrier gets a YIELD on its
+          // back-edge, which costs the MMA issue ~25% of the tensor pipe
+          // (scripts/tc_pattern_bench.cu patterns 18 vs 27)
+#pragma unroll
           for (int nh = 0; nh < 2; ++nh) {
             const uint32_t d = tmem + nh * 128;
+#pragma unroll
             for (int kc = 0; kc < NKB; ++kc, ++it) {
               if (nh == 0 && kc == NKB / 2) {   // second half of A: written after the first
                 mbar_wait(&m.aready2, layer & 1);
