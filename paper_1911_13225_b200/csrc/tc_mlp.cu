@@ -189,7 +189,12 @@ __device__ __forceinline__ float relu_pair_sel(float m, float d, bool odd) {
 }
 
 static __device__ unsigned long long g_mlp_tl[4096];
-#define TL(id) DIST_TL_MARK(g_mlp_tl, id)
+// epilogue marks in [0, 2048), the MMA thread's in [2048, 4096)
+#define TL(id)                                   \
+  do {                                           \
+    if (tl_i < 2048) DIST_TL_MARK(g_mlp_tl, id); \
+  } while (0)
+#define TL_MMA(id) DIST_TL_MARK(g_mlp_tl, id)
 
 // ---------------------------------------------------------------------------
 // PAIR: rows 2i / 2i+1 are the probes p+ / p- of one central difference and
@@ -277,10 +282,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (rank == 0 && lane == 0) {
       uint32_t it = 0, layer = 0;
       const uint32_t a_hi = smem_u32(smem + OFF_AHI), a_lo = smem_u32(smem + OFF_ALO);
+      // DIST_TC_TIMELINE: the MMA thread's own marks in the buffer's upper half
+      const bool tl_on = P.timeline && blockIdx.x == 0;
+      int tl_i = 2048;
       for (int64_t t = cluster; t < ntiles; t += nclusters)
         for (int l = 0; l < G; ++l, ++layer) {
           mbar_wait(&m.aready, layer & 1);
           tc_fence_after();
+          TL_MMA(20);
           // fully unrolled: a loop that waits on a barrier gets a YIELD on its
           // back-edge, which costs the MMA issue ~25% of the tensor pipe
           // (scripts/tc_pattern_bench.cu patterns 18 vs 27)
@@ -290,8 +299,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
             for (int kc = 0; kc < NKB; ++kc, ++it) {
               if (nh == 0 && kc == NKB / 2) {   // second half of A: written after the first
+                TL_MMA(21);
                 mbar_wait(&m.aready2, layer & 1);
                 tc_fence_after();
+                TL_MMA(22);
               }
               const int s = it % STAGES;
               mbar_wait(&m.full[s], (it / STAGES) & 1);

@@ -32,6 +32,16 @@
 //  25/26 done-wait sparse : 18 with the wait every 2nd / 4th K block
 //  27 done-wait unrolled : 18 with the K-block loop fully unrolled (the compiler
 //               puts a YIELD on the back-edge of a loop that waits on a barrier)
+//  28 +tmem-ld : 27 (no waits) while 8 other warps stream tcgen05.ld from TMEM
+//               columns the MMAs do not write (the epilogue's D reads)
+//  29 +st.shared : 27 while 8 warps stream 16-byte shared stores into A_lo
+//  30 +both   : 28 and 29 together
+//  31/32 ring unrolled : 6 / 7 (3- / 6-stage full/empty ring with a producer
+//               thread) with the MMA issuer's K loop unrolled
+//  33 ring, both unrolled : 31 with the producer's loop unrolled by 8 too
+//  34/35 ring pairs : 31/32 waiting for two stages at once on even K blocks
+//  36 ring, local arrive : 31 with the producer arriving by mbarrier.arrive.shared::cta
+//  37 ring, leader-only  : 36 with only the leader's producer (rank 1's idles)
 // FLOP per clock per SM of the slowest issuer; operand values are zeros.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1911_13225_b200/csrc \
@@ -87,13 +97,14 @@ __device__ __forceinline__ void wait_w(uint64_t *b, uint32_t parity) {
 constexpr int TILES = 24;   // x 7 layers x 2 N halves x 8 K blocks
 
 template <int PAT>
-__global__ void __launch_bounds__(128, 1) k_pat(unsigned long long *cycles, unsigned long long *nmma) {
+__global__ void __launch_bounds__(320, 1) k_pat(unsigned long long *cycles, unsigned long long *nmma) {
   extern __shared__ __align__(1024) char smem_raw[];
   char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int RS = PAT == 7 || PAT == 13 || PAT == 15 || PAT == 16 ? 6 : (PAT == 14 || PAT == 17 ? 12 : STAGES);
+  constexpr int RS = PAT == 7 || PAT == 13 || PAT == 15 || PAT == 16 || PAT == 32 || PAT == 35 ? 6
+                     : (PAT == 14 || PAT == 17 ? 12 : STAGES);
   constexpr bool SELF = PAT >= 12 && PAT <= 17;
   constexpr int WF = PAT == 10 ? 1 : (PAT == 11 ? 2 : 0);
-  constexpr bool RING = (PAT >= 6 && PAT <= 8) || PAT == 10 || PAT == 11 || SELF;
+  constexpr bool RING = (PAT >= 6 && PAT <= 8) || PAT == 10 || PAT == 11 || SELF || PAT == 31 || PAT == 32 || PAT == 33 || PAT == 34 || PAT == 35 || PAT == 36 || PAT == 37;
   __shared__ uint64_t bar, sbar, full[16], empty[16];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5;
@@ -167,8 +178,32 @@ __global__ void __launch_bounds__(128, 1) k_pat(unsigned long long *cycles, unsi
   } else if ((PAT == 23 || PAT == 24) && rank == 1 && threadIdx.x == 0) {
     mbar_wait(&bar, 0);
   }
-  if (PAT == 27 && threadIdx.x == 0 && rank == 0) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sbar)) : "memory");
+  __shared__ volatile int s_stop;
+  if (threadIdx.x == 0) s_stop = 0;
+  __syncthreads();
+  if (PAT >= 28 && PAT <= 30 && warp >= 2) {   // load generators: until the MMA thread is done
+    const int q = warp & 3;
+    const uint32_t tq = tmem + ((uint32_t)(q * 32) << 16) + 128u;   // D nh1 columns
+    float acc = 0.f;
+    int n = 0;
+    while (!s_stop) {
+      if (PAT == 28 || PAT == 30) {
+        float v[32];
+        tmem_ld32(tq + ((n & 3) * 32u), v);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) acc += v[e];
+      }
+      if (PAT == 29 || PAT == 30) {
+        uint4 *dst = reinterpret_cast<uint4 *>(smem + OFF_ALO) + ((threadIdx.x - 64) + (n & 15) * 256) % 4096;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) dst[e * 1024 % 4096] = make_uint4(0u, 0u, 0u, 0u);
+      }
+      ++n;
+    }
+    if (acc == 12345.f) cycles[0] = 1;   // keep the loads
+  }
+  if ((PAT == 27 || (PAT >= 28 && PAT <= 30)) && threadIdx.x == 0 && rank == 0) {
+    if (PAT == 27) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&sbar)) : "memory");
     const uint32_t a_hi = smem_u32(smem + OFF_AHI), a_lo = smem_u32(smem + OFF_ALO);
     uint32_t it = 0;
     const unsigned long long t0 = clock64();
@@ -180,7 +215,7 @@ __global__ void __launch_bounds__(128, 1) k_pat(unsigned long long *cycles, unsi
           for (int kc = 0; kc < NKB; ++kc, ++it) {
             const int s = it % STAGES;
             const uint32_t b_hi = smem_u32(smem + OFF_B + s * STAGE_BYTES), b_lo = b_hi + B_TILE;
-            mbar_wait(&sbar, 0);
+            if (PAT == 27) mbar_wait(&sbar, 0);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
               const uint32_t ak = kc * (ROWS * 128) + q * 32;
@@ -202,14 +237,34 @@ __global__ void __launch_bounds__(128, 1) k_pat(unsigned long long *cycles, unsi
     mbar_wait(&bar, 0);
     cycles[blockIdx.x] = clock64() - t0;
     nmma[blockIdx.x] = (unsigned long long)NIT * 12;
-  } else if (PAT == 27 && threadIdx.x == 0) {
+  } else if ((PAT == 27 || (PAT >= 28 && PAT <= 30)) && threadIdx.x == 0) {
     mbar_wait(&bar, 0);
   }
+  if (PAT >= 28 && PAT <= 30 && threadIdx.x == 0) s_stop = 1;
   if (RING && !SELF && threadIdx.x == 32) {   // producer (both CTAs)
-    for (int it = 0; it < NIT; ++it) {
-      const int s = it % RS;
-      wait_w<WF>(&empty[s], ((it / RS) & 1) ^ 1);
-      if (rank == 0) mbar_arrive_cluster(&full[s], 0);
+    if constexpr (PAT == 33) {
+      for (int i0 = 0; i0 < NIT; i0 += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int it = i0 + j;
+          const int s = it % RS;
+          wait_w<WF>(&empty[s], ((it / RS) & 1) ^ 1);
+          if (rank == 0) mbar_arrive_cluster(&full[s], 0);
+        }
+      }
+    } else if constexpr (PAT == 36 || PAT == 37) {
+      if (PAT == 36 || rank == 0)
+        for (int it = 0; it < NIT; ++it) {
+          const int s = it % RS;
+          wait_w<WF>(&empty[s], ((it / RS) & 1) ^ 1);
+          if (rank == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+        }
+    } else {
+      for (int it = 0; it < NIT; ++it) {
+        const int s = it % RS;
+        wait_w<WF>(&empty[s], ((it / RS) & 1) ^ 1);
+        if (rank == 0) mbar_arrive_cluster(&full[s], 0);
+      }
     }
   }
   if (RING && threadIdx.x == 0 && rank == 0) {   // MMA issuer through the ring
@@ -220,6 +275,7 @@ __global__ void __launch_bounds__(128, 1) k_pat(unsigned long long *cycles, unsi
       for (int l = 0; l < 7; ++l)
         for (int nh = 0; nh < 2; ++nh) {
           const uint32_t d = tmem + nh * 128;
+#pragma unroll (PAT >= 31 ? 8 : 1)
           for (int kc = 0; kc < NKB; ++kc, ++it) {
             const int s = it % RS;
             if constexpr (PAT == 16) {
@@ -228,6 +284,11 @@ __global__ void __launch_bounds__(128, 1) k_pat(unsigned long long *cycles, unsi
               if (it >= (uint32_t)RS && (it & 3) == 0) wait_w<0>(&empty[s], ((it / RS) - 1) & 1);
             } else if constexpr (SELF) {
               if (it >= (uint32_t)RS) wait_w<PAT == 15 ? 3 : 0>(&empty[s], ((it / RS) - 1) & 1);
+            } else if constexpr (PAT == 34 || PAT == 35) {
+              if (!(kc & 1)) {
+                wait_w<0>(&full[s], (it / RS) & 1);
+                wait_w<0>(&full[(it + 1) % RS], ((it + 1) / RS) & 1);
+              }
             } else {
               wait_w<WF>(&full[s], (it / RS) & 1);
             }
@@ -340,7 +401,7 @@ static void run(const char *name, int nsm) {
   cudaMemset(cyc, 0, sizeof(unsigned long long) * nsm);
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(nsm - (nsm % 2));
-  lc.blockDim = dim3(128);
+  lc.blockDim = dim3(PAT >= 28 && PAT <= 30 ? 320 : 128);
   lc.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -398,6 +459,16 @@ int main() {
   run<25>("no ring, a completed-barrier wait every 2nd K block", nsm);
   run<26>("no ring, a completed-barrier wait every 4th K block", nsm);
   run<27>("no ring, completed-barrier wait per K block, K loop unrolled", nsm);
+  run<28>("MMA stream + 8 warps of tcgen05.ld on other columns", nsm);
+  run<29>("MMA stream + 8 warps of shared stores", nsm);
+  run<30>("MMA stream + both", nsm);
+  run<31>("3-stage ring, K loop unrolled", nsm);
+  run<32>("6-stage ring, K loop unrolled", nsm);
+  run<33>("3-stage ring, MMA and producer loops unrolled", nsm);
+  run<34>("3-stage ring, unrolled, waits in pairs", nsm);
+  run<35>("6-stage ring, unrolled, waits in pairs", nsm);
+  run<36>("3-stage ring, unrolled, producer arrives CTA-locally", nsm);
+  run<37>("3-stage ring, unrolled, local arrive, leader producer only", nsm);
   run<1>("kernel (mode 3) again", nsm);
   return 0;
 }

@@ -27,7 +27,8 @@ from paper_1911_13225_b200 import _lib  # noqa: E402
 from paper_1911_13225_b200.workloads import render_depth_observations, ring_views, target_code  # noqa: E402
 
 MLP = {1: "tile start", 2: "layer0 A ready", 10: "prev tile rows done", 3: "D (nh=0 half) ready", 4: "A ready",
-       9: "head done", 11: "GEMM done", 12: "parked copied", 13: "K 0..3 announced", 14: "nh=1 half done"}
+       9: "head done", 11: "nh=1 MMAs past K 3 (afree)", 12: "parked copied", 13: "K 0..3 announced",
+       14: "nh=1 half done"}
 HEADS = {1: "tile start", 2: "layer0 A ready", 3: "fwd D ready", 4: "fwd A ready", 5: "seed done",
          6: "bwd A0 ready", 7: "bwd D ready", 8: "bwd A ready", 9: "colsum done"}
 
@@ -49,6 +50,27 @@ def show(fn, names, label):
             print(f"  {names[ids[i]]:20s} +{(t[i] - t[s]) / 1e3:7.2f} us  (dt {dt:6.2f})")
 
 
+MMA = {20: "MMA: K 0..3 of A seen", 21: "MMA: K 0..3 issued", 22: "MMA: K 4..7 of A seen"}
+
+
+def merged(fn, label, ntiles=1):
+    """The epilogue thread's marks and the MMA thread's (buffer upper half) on one clock."""
+    buf = (ctypes.c_ulonglong * 4096)()
+    fn(buf, 4096)
+    a = np.array(buf[:], dtype=np.uint64)
+    ids = (a >> np.uint64(56)).astype(int)
+    t = (a & np.uint64((1 << 56) - 1)).astype(np.int64)
+    ev = [(t[i], ids[i]) for i in range(4096) if ids[i] != 0]
+    ev.sort()
+    starts = [k for k, (_, i) in enumerate(ev) if i == 1]
+    names = {**MLP, **MMA}
+    for k in range(1, min(1 + ntiles, len(starts) - 1)):
+        s, e = starts[k], starts[k + 1]
+        print(f"--- {label} tile {k} (epilogue + MMA thread marks)")
+        for j in range(s, e):
+            print(f"  {names.get(ev[j][1], ev[j][1]):28s} +{(ev[j][0] - ev[s][0]) / 1e3:7.2f} us")
+
+
 def main():
     lib = _lib.lib()
     field = st.NeuralField.geometric(256, (512,) * 8, 0, precision="bf16x3")
@@ -57,6 +79,9 @@ def main():
     field.evaluate_device(pts, code)
     torch.cuda.synchronize()
     show(lib.dist_debug_mlp_timeline, MLP, "k_tc_mlp")
+    merged(lib.dist_debug_mlp_timeline, "k_tc_mlp")
+    if os.environ.get("TL_MLP_ONLY"):
+        return
     views = ring_views(8, 512)
     cfg = st.TraceConfig(k_samples=3)
     obs = render_depth_observations(field, target_code(1), views, cfg)
