@@ -66,8 +66,6 @@ struct Params {
   const float *cskf;      // [S][512] fp32 (kernels.cuh c0 layout of cskip)
   const float *cskmax;    // [S] max |cskip|
   int n_gemm;             // hidden GEMM layers (L-2)
-  int acc_mode;           // 0: one accumulator; 1: two (even/odd K blocks); 2: hi*hi | corrections;
-                          // 3 (default): as 2, stage-grouped; 4 (experiment): single pass, hi*hi only
   int timeline;           // DIST_TC_TIMELINE: phase marks of CTA 0 (debug)
   double head_gain;       // the 512 -> 1 head dot's gain (DecView.tc_gain; DIST_TC_HEAD_GAIN overrides)
   int debug;              // timing experiments: 1 = no epilogue math, 2 = no MMAs, 3 = no mask-record
@@ -308,9 +306,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               mbar_wait(&m.full[s], (it / STAGES) & 1);
               tc_fence_after();
               const uint32_t b_hi = smem_u32(smem + OFF_B + s * STAGE_BYTES), b_lo = b_hi + B_TILE;
-              if (P.acc_mode == 3 && P.debug != 2) {
+              if (P.debug != 2) {
                 // hi*hi of the whole stage into D, then the corrections into D2:
-                // two accumulator switches per stage instead of eight
+                // two accumulator switches per stage instead of eight.  (One
+                // product scheme only: with the K loop unrolled, every runtime
+                // variant would be replicated per stage -- 4x the issue code.)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                   const uint32_t ak = kc * (ROWS * 128) + q * 32;
@@ -321,29 +321,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                   const uint32_t ak = kc * (ROWS * 128) + q * 32;
                   mma_2sm<F16>(d + 256u, sdesc(a_hi + ak), sdesc(b_lo + q * 32), (kc | q) ? 1u : 0u);
                   mma_2sm<F16>(d + 256u, sdesc(a_lo + ak), sdesc(b_hi + q * 32), 1u);
-                }
-              } else
-#pragma unroll
-              for (int q = 0; q < 4; ++q) {
-                if (P.debug == 2) break;
-                const uint32_t ak = kc * (ROWS * 128) + q * 32;
-                const uint64_t dah = sdesc(a_hi + ak), dal = sdesc(a_lo + ak);
-                const uint64_t dbh = sdesc(b_hi + q * 32), dbl = sdesc(b_lo + q * 32);
-                if (P.acc_mode == 4) {   // experiment: single pass (hi x hi only)
-                  mma_2sm<F16>(d, dah, dbh, (kc | q) ? 1u : 0u);
-                } else if (P.acc_mode == 0) {
-                  mma_2sm<F16>(d, dah, dbh, (kc | q) ? 1u : 0u);
-                  mma_2sm<F16>(d, dah, dbl, 1u);
-                  mma_2sm<F16>(d, dal, dbh, 1u);
-                } else if (P.acc_mode == 1) {
-                  const uint32_t dd = d + ((kc & 1) ? 256u : 0u);
-                  mma_2sm<F16>(dd, dah, dbh, (kc >> 1 | q) ? 1u : 0u);
-                  mma_2sm<F16>(dd, dah, dbl, 1u);
-                  mma_2sm<F16>(dd, dal, dbh, 1u);
-                } else {
-                  mma_2sm<F16>(d, dah, dbh, (kc | q) ? 1u : 0u);
-                  mma_2sm<F16>(d + 256u, dah, dbl, (kc | q) ? 1u : 0u);
-                  mma_2sm<F16>(d + 256u, dal, dbh, 1u);
                 }
               }
               commit_2sm(&m.empty[s]);
@@ -373,14 +350,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     auto a_ready_all = [&] { a_ready_lo(); a_ready_hi(); };
     // D columns [col, col+32) of this thread's lane (+ the correction accumulator)
     auto load_d = [&](int col, float (&v)[32]) {
-      if (P.acc_mode >= 1 && P.acc_mode <= 3) {
-        float w2[32];
-        tmem_ld32x2(tq + col, tq + 256 + col, v, w2);
+      float w2[32];
+      tmem_ld32x2(tq + col, tq + 256 + col, v, w2);
 #pragma unroll
-        for (int e = 0; e < 32; ++e) v[e] += w2[e];
-      } else {
-        tmem_ld32(tq + col, v);
-      }
+      for (int e = 0; e < 32; ++e) v[e] += w2[e];
     };
     // Tile boundaries keep the tensor core busy: the next tile's rows are
     // fetched while the current tile's last GEMM runs, and a tile's row
@@ -1238,8 +1211,6 @@ static int launch_tc_t(const DecView &dv, const double *c0, const double *cs, in
   P.cskf = dv.skip > 0 ? c0_f32(cs, S, dv.nskip) : nullptr;
   P.cskmax = dv.skip > 0 ? c0_absmax(cs, S, dv.nskip) : nullptr;
   {
-    const char *am = getenv("DIST_TC_ACC");
-    P.acc_mode = am ? atoi(am) : 3;
     const char *dbg = getenv("DIST_TC_DEBUG");
     P.debug = dbg ? atoi(dbg) : 0;
     const char *tl = getenv("DIST_TC_TIMELINE");
