@@ -229,7 +229,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint32_t it = 0;
       for (int64_t t = cluster; t < ntiles; t += nclusters)
         for (int ph = BWD ? G : 0; ph < NPH; ++ph) {
-          const bool fwd = ph < G;
+          const bool fwd = !BWD && ph < G;   // compile-time false in the backward-only kernel
           const int l = fwd ? ph : 2 * G - 1 - ph;
           const CUtensorMap *map = fwd ? &wfwd : &wbwd;
           for (int nh = 0; nh < 2; ++nh)
@@ -269,7 +269,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               mbar_wait(&m.full[s], (it / STAGES) & 1);
               tc_fence_after();
               const uint32_t b_hi = smem_u32(smem + OFF_B + s * STAGE_BYTES), b_lo = b_hi + B_TILE;
-              if (ph < G) {   // forward: bf16x3
+              if (!BWD && ph < G) {   // forward: bf16x3 (never in the backward-only kernel)
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                   const uint32_t ak = kc * (ROWS * 128) + q * 32;
