@@ -105,6 +105,9 @@ DIST_API int64_t dist_launch_count(void);
  * when DIST_TC_TIMELINE=1 (entries: mark id << 56 | %globaltimer ns of CTA 0's
  * first epilogue thread; scripts/tile_timeline.py). Copies up to n entries. */
 DIST_API int dist_debug_mlp_timeline(unsigned long long *out, int n);
+/* DIST_TC_TIMELINE=4: one row per CTA of the fluid march's slot grids,
+ * {slot | block << 32, start ns, end ns, 0}; copies up to n rows. */
+DIST_API int dist_debug_fluid_timeline(unsigned long long *out, int n);
 DIST_API int dist_debug_heads_timeline(unsigned long long *out, int n);
 
 /* ---- decoder (NeuralField, fields.py:185-247) -------------------------- */

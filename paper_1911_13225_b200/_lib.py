@@ -67,6 +67,7 @@ _SIGS = {
     "dist_device_info": (C.c_int, [C.POINTER(C.c_int)] * 3),
     "dist_launch_count": (C.c_int64, []),
     "dist_debug_mlp_timeline": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int]),
+    "dist_debug_fluid_timeline": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int]),
     "dist_debug_heads_timeline": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_int]),
     "dist_decoder_create": (C.c_int, [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.c_int,
                                       C.POINTER(C.c_int32), C.c_int, C.c_int, C.c_int, C.c_int,

@@ -207,9 +207,17 @@ __device__ __forceinline__ void step_epilogue(Ctl *ctl, int cur, const ViewBudge
   }
 }
 
+// Buffers of the fluid tensor-core march (tc_mlp.cu MarchFluid): a third
+// live list and [4 (max_steps + 2)] per-slot counters; null disables it.
+struct FluidBufs {
+  int32_t *list2;
+  int32_t *ctr;
+};
+
 int tc_run_steps(const DecView &dv, const double *c0, const double *cskip, int S,
                  const dist_camera *cams, const LevelState &ls, Ctl *ctl, int32_t *l0, int32_t *l1,
-                 const MarchArgs &a, int slots, const ViewBudget &vb, int64_t *stats, cudaStream_t st);
+                 const MarchArgs &a, int slots, const ViewBudget &vb, int64_t *stats, cudaStream_t st,
+                 const FluidBufs &fb = FluidBufs{nullptr, nullptr});
 
 // Normal probes of the converged rays (shading.py:73-94): row 6r + 2a (+1)
 // is p +/- delta e_a of converged ray r, so consecutive rows form the

@@ -33,6 +33,9 @@ struct Misc {
   uint64_t aready;    // next layer's A, K blocks 0..3 (output columns 0..255) written
   uint64_t aready2;   // ... and K blocks 4..7
   uint64_t afree;     // the GEMM's nh = 1 MMAs have consumed A's K blocks 0..3
+  uint64_t tk_bar[2]; // fluid march: tile ticket k is in tk_base/tk_cnt[k & 1]
+  int64_t tk_base[2]; //   (published by CTA 0's scheduler thread into both CTAs)
+  int32_t tk_cnt[2];  //   rows in the tile; 0 = no more tiles
   uint32_t tmem_base;
   int32_t go, cur, cnt, nan;
   int32_t ray[ROWS];

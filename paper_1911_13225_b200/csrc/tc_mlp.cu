@@ -153,9 +153,138 @@ struct MarchRows {
 // so traces without the record pay nothing for it)
 struct MarchRowsM : MarchRows {};
 
+// ---------------------------------------------------------------------------
+// Fluid march (tc_run_steps, full-grid levels with the dynamic mask): slot s
+// of a level is still one launch, but the launches overlap.  Slot s + 1's
+// grid starts (programmatic dependent launch) on the CTA pairs slot s has
+// released and claims tiles of slot s's survivors as they are appended,
+// instead of waiting for slot s's last partial wave: a slot costs its work,
+// not ceil(tiles / pairs) tile-times (scripts/wave_model.py).  A kernel only
+// consumes its own slot's list and only produces the next one, so no pair
+// ever waits on rows it must produce itself.  Per-ray arithmetic is the
+// stepped march's (bit-identical states, tests/test_gpu_fluid.py); what
+// changes is the bookkeeping: a ray's step budget is its view's step count at
+// the level's start plus the slot index (every live ray of a view has stepped
+// in every slot of the level), live counts are atomics at that step index,
+// and the views' step counts are advanced once per level (k_fluid_finish).
+struct FluidCtl {
+  int32_t *cnt;    // [slots + 1] rows appended to slot s's list (cnt[0]: the level's start)
+  int32_t *head;   // [slots + 1] rows of slot s's list claimed by tiles
+  int32_t *dctr;   // [slots] CTAs of slot s's grid that have finished
+  int32_t *done;   // [slots + 1] done[s]: slot s - 1 complete, cnt[s] final (done[0] = 1)
+  int32_t *lists[3];   // slot s reads lists[s % 3], appends to lists[(s + 1) % 3]; -1 = empty entry
+};
+
+__device__ __forceinline__ int32_t ld_acquire_s32(const int32_t *p) {
+  int32_t v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_s32(int32_t *p, int32_t v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+struct MarchFluid : MarchRows {
+  FluidCtl f;
+  int slot;          // this launch's slot index within the level
+  int last_slot;     // slots - 1: survivors of the last slot are not queued
+  int level_coarse;  // coarse levels stop after `slots` slots (split_interval)
+  __device__ bool begin(Misc &m) {
+    if (threadIdx.x == 0) m.nan = 0;
+    __syncthreads();
+    return true;
+  }
+  // CTA 0's scheduler thread: the next tile of this slot's list, or cnt = 0
+  // once slot - 1 is complete and its list is exhausted.  Partial tiles are
+  // taken only when nothing more can come or at least half a tile is ready.
+  __device__ void claim(int64_t &base, int &cnt) const {
+    int32_t *cp = f.cnt + slot, *hp = f.head + slot;
+    const int32_t *dp = f.done + slot;
+    for (;;) {
+      const bool prev_done = ld_acquire_s32(dp) != 0;
+      const int32_t c = ld_acquire_s32(cp);
+      const int32_t h = *(volatile int32_t *)hp;
+      const int32_t avail = c - h;
+      if (avail <= 0) {
+        if (prev_done) {
+          base = h;
+          cnt = 0;
+          return;
+        }
+        __nanosleep(256);
+        continue;
+      }
+      const int take = avail < 128 ? avail : 128;
+      if (take < 64 && !prev_done) {
+        __nanosleep(256);
+        continue;
+      }
+      if (atomicCAS(hp, h, h + take) == h) {
+        base = h;
+        cnt = take;
+        return;
+      }
+    }
+  }
+  // entry i of this slot's list: wait until it is written (the four epilogue
+  // threads of a row all read it; finish() empties it for the list's reuse
+  // three slots later)
+  __device__ int load_f(int64_t i, double p[3], int &s) const {
+    const int32_t *in = f.lists[slot % 3] + i;
+    int32_t g;
+    while ((g = ld_acquire_s32(in)) < 0) __nanosleep(64);
+    double dir[3];
+    const dist_camera *cam;
+    ray_of(cams, ls, g, dir, &cam);
+    const double dg = ls.d[g];
+    for (int q = 0; q < 3; ++q) p[q] = __dadd_rn(cam->origin[q], __dmul_rn(dg, dir[q]));
+    s = cam->shape;
+    return (int)g;
+  }
+  __device__ void finish(Misc &m, int64_t gi, int g, bool valid, double fv) const {
+    if (g >= 0) f.lists[slot % 3][gi] = -1;   // this tile's entry: empty again
+    bool keep = false;
+    int v = -1, sv = 0;
+    if (valid && ls.status[g] == DIST_MARCHING) {
+      v = vb_view(vb, g);
+      sv = vb.steps[v] + slot;   // the view's step index of this query
+      if (sv < a.max_steps) {
+        double dir[3];
+        const dist_camera *cam;
+        ray_of(cams, ls, g, dir, &cam);
+        int nn = 0;
+        keep = march_update(ls, a, g, dir, cam->origin, fv, &nn) && sv + 1 < a.max_steps && slot < last_slot;
+        if (nn) atomicAdd(&m.nan, nn);
+      } else {
+        v = -1;
+      }
+    }
+    // live counts: rows of view v queried at its step sv (warp-aggregated)
+    const unsigned peers = __match_any_sync(0xffffffffu, v);
+    if (v >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1) {
+      atomicAdd((unsigned long long *)&vb.live[(int64_t)v * a.max_steps + sv], (unsigned long long)__popc(peers));
+      atomicAdd((unsigned long long *)&stats[0], (unsigned long long)__popc(peers));
+    }
+    if (keep) __threadfence();   // the ray's state before its list entry
+    warp_append(keep, g, f.lists[(slot + 1) % 3], f.cnt + slot + 1);
+  }
+  __device__ void end(Misc &m) {
+    if (threadIdx.x == 0) {
+      if (m.nan) atomicAdd((unsigned long long *)&stats[1], (unsigned long long)m.nan);
+      __threadfence();
+      if (atomicAdd(f.dctr + slot, 1) == (int)gridDim.x - 1) {
+        __threadfence();
+        st_release_s32(f.done + slot + 1, 1);
+      }
+    }
+  }
+};
+struct MarchFluidM : MarchFluid {};
+
 template <class Rows>
 __device__ __forceinline__ int load_row(const Rows &r, const Misc &m, int64_t i, double p[3], int &s) {
-  if constexpr (std::is_base_of<MarchRows, Rows>::value) return r.load_m(m, i, p, s);
+  if constexpr (std::is_base_of<MarchFluid, Rows>::value) return r.load_f(i, p, s);
+  else if constexpr (std::is_base_of<MarchRows, Rows>::value) return r.load_m(m, i, p, s);
   else return r.load(i, p, s);
 }
 
@@ -187,6 +316,9 @@ __device__ __forceinline__ float relu_pair_sel(float m, float d, bool odd) {
 }
 
 static __device__ unsigned long long g_mlp_tl[4096];
+// DIST_TC_TIMELINE=4 (fluid march): per CTA (slot, start, end, tiles) rows
+static __device__ unsigned long long g_fluid_tl[8192][4];
+static __device__ unsigned int g_fluid_tl_n;
 // epilogue marks in [0, 2048), the MMA thread's in [2048, 4096)
 #define TL(id)                                   \
   do {                                           \
@@ -226,6 +358,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     mbar_init(&m.aready, 2);
     mbar_init(&m.aready2, 2);
     mbar_init(&m.afree, 1);
+    mbar_init(&m.tk_bar[0], 1);
+    mbar_init(&m.tk_bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -239,7 +373,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   cluster_sync();
   tc_fence_after();
   const uint32_t tmem = m.tmem_base;
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  constexpr bool kFluid = std::is_base_of<MarchFluid, Rows>::value;
+  // a fluid slot after the first starts while the previous slot still runs:
+  // it reads that slot's survivors through the list's entries and flags
+  bool wait_grid = true;
+  if constexpr (kFluid) wait_grid = R.slot == 0;
+  if (wait_grid) asm volatile("griddepcontrol.wait;" ::: "memory");
+  unsigned long long t_start = 0;
+  if (P.timeline == 4 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   if (!R.begin(m)) {  // uniform across the grid (all CTAs read the same controller)
     tc_fence_before();
     __syncthreads();
@@ -249,16 +390,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     return;
   }
 
-  const int64_t nrows = R.rows(m);
-  const int64_t ntiles = ceil_div(nrows, 2 * ROWS);
+  const int64_t nrows = kFluid ? INT64_MAX : R.rows(m);
+  const int64_t ntiles = kFluid ? 0 : ceil_div(nrows, 2 * ROWS);
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   const int G = P.n_gemm;
+  // Tile k of this CTA pair: a static round-robin tile, or (fluid) the k-th
+  // ticket CTA 0's scheduler thread publishes into both CTAs.  Returns false
+  // when there is no tile k.
+  auto ticket = [&](int k, int64_t &base, int &cnt) -> bool {
+    if constexpr (kFluid) {
+      mbar_wait(&m.tk_bar[k & 1], (k >> 1) & 1);
+      asm volatile("fence.acq_rel.cluster;" ::: "memory");   // the scheduler's (remote) mailbox stores
+      base = *(volatile int64_t *)&m.tk_base[k & 1];
+      cnt = *(volatile int32_t *)&m.tk_cnt[k & 1];
+      return cnt > 0;
+    } else {
+      const int64_t t = cluster + (int64_t)k * nclusters;
+      base = t * (2 * ROWS);
+      cnt = (int)(nrows - base < 2 * ROWS ? nrows - base : 2 * ROWS);
+      return t < ntiles;
+    }
+  };
+  // fluid: claim tile k and publish it to both CTAs (CTA 0, one thread)
+  auto publish = [&](int k) {
+    if constexpr (kFluid) {
+      int64_t base;
+      int cnt;
+      R.claim(base, cnt);
+      const int b = k & 1;
+      m.tk_base[b] = base;
+      m.tk_cnt[b] = cnt;
+      uint32_t rb, rc;   // the peer CTA's mailbox
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(rb) : "r"(smem_u32(&m.tk_base[b])));
+      asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(rc) : "r"(smem_u32(&m.tk_cnt[b])));
+      asm volatile("st.shared::cluster.b64 [%0], %1;" ::"r"(rb), "l"(base) : "memory");
+      asm volatile("st.shared::cluster.b32 [%0], %1;" ::"r"(rc), "r"(cnt) : "memory");
+      asm volatile("fence.acq_rel.cluster;" ::: "memory");
+      asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&m.tk_bar[b])) : "memory");
+      mbar_arrive_cluster(&m.tk_bar[b], 1);
+    } else {
+      (void)k;
+    }
+  };
 
   if (warp == 0) {
     // ===== TMA producer (both CTAs) =====
     if (lane == 0) {
       uint32_t it = 0;
-      for (int64_t t = cluster; t < ntiles; t += nclusters)
+      int64_t tb;
+      int tc_;
+      for (int k = 0; ticket(k, tb, tc_); ++k)
         for (int l = 0; l < G; ++l)
           for (int nh = 0; nh < 2; ++nh)
             for (int kc = 0; kc < NKB; ++kc, ++it) {
@@ -283,7 +464,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       // DIST_TC_TIMELINE: the MMA thread's own marks in the buffer's upper half
       const bool tl_on = P.timeline && blockIdx.x == 0;
       int tl_i = 2048;
-      for (int64_t t = cluster; t < ntiles; t += nclusters)
+      int64_t tb;
+      int tc_;
+      for (int k = 0; ticket(k, tb, tc_); ++k)
         for (int l = 0; l < G; ++l, ++layer) {
           mbar_wait(&m.aready, layer & 1);
           tc_fence_after();
@@ -367,7 +550,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     };
     // ReLU masks (march with a mask record): this thread's 2 x 64 columns of a
     // layer are words 8 nh + 4 half + 2 sub + {0, 1} of the layer's 16
-    constexpr bool kMasks = std::is_same<Rows, MarchRowsM>::value && !PAIR;
+    constexpr bool kMasks = (std::is_same<Rows, MarchRowsM>::value || std::is_same<Rows, MarchFluidM>::value) && !PAIR;
     // Record layout per layer (16 words): thread quarter q4 = 2 half + sub owns
     // words 4 q4 .. 4 q4 + 3 = (nh 0: cols +0..31, +32..63; nh 1: the same),
     // columns nh 256 + 64 q4 + 32 c + bit -- one 16-byte store per layer
@@ -380,16 +563,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     };
     uint32_t me0 = 0u, me1 = 0u;   // this layer's nh = 0 mask words until its nh = 1 half
     uint32_t ms0 = 0u, ms1 = 0u;   // the stashed next tile's layer-0 nh = 0 mask words
-    auto fetch = [&](int64_t t, RowIn &r) {
-      r.gi = t * (2 * ROWS) + (int64_t)rank * ROWS + row;
+    // rows of ticket k (tile base, row count): this thread's row of the tile;
+    // returns whether tile k exists
+    auto fetch = [&](int k, RowIn &r) -> bool {
+      int64_t base;
+      int cnt;
+      const bool ok = ticket(k, base, cnt);
+      const int ri = (int)rank * ROWS + row;
+      r.gi = base + ri;
       r.p[0] = r.p[1] = r.p[2] = 0.0;
       r.s = -1;
       r.id = -1;
       r.md = nullptr;
-      if (t < ntiles && r.gi < nrows) r.id = load_row(R, m, r.gi, r.p, r.s);
+      if (ok && ri < cnt && r.gi < nrows) r.id = load_row(R, m, r.gi, r.p, r.s);
       if constexpr (kMasks) {
         if (r.id >= 0) r.md = R.mask_dst(r.id);
       }
+      return ok;
     };
     uint32_t afree_n = 0;  // afree phases consumed (one per non-last kEarly layer)
     bool xpend = false;   // an xch_read's barrier-2 arrive awaits its matching sync
@@ -418,9 +608,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int pid = -1;
     double pfv = 0.0;
     RowIn nx;
-    fetch(cluster, nx);
+    // fluid: the scheduler is CTA 0's thread 64 (an epilogue thread that owns no row)
+    const bool sched = kFluid && rank == 0 && threadIdx.x == 64;
+    if (sched) publish(0);
+    bool have = fetch(0, nx), next_have = false;
     uint32_t layer = 0;
-    for (int64_t t = cluster; t < ntiles; t += nclusters) {
+    for (int k = 0; have; ++k, have = next_have) {
       TL(1);
       // ---- rows and layer 0 (fp64, latent folded into c0) ----
       double p[3] = {nx.p[0], nx.p[1], nx.p[2]};
@@ -657,7 +850,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                       : 0.f;
       };
       for (int l = 0; l < G; ++l, ++layer) {
-        if (l == G - 1) fetch(t + nclusters, nx);
+        if (l == G - 1) {
+          if (sched) publish(k + 1);
+          next_have = fetch(k + 1, nx);
+        }
         const bool last = (l == G - 1);
         const float *bias = P.bias + (size_t)l * KDIM;
         const float unscale = rinv * P.winv[l];   // exact: both are powers of two
@@ -727,7 +923,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             }
             me0 = mwa;
             me1 = mwb;
-            if (last && t + nclusters < ntiles) {
+            if (last && next_have) {
               // the next tile's layer 0, columns 0..255, into the TMEM columns
               // the head just consumed (nx: its rows, fetched above)
               const float qx = (float)nx.p[0], qy = (float)nx.p[1], qz = (float)nx.p[2];
@@ -961,6 +1157,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
   R.end(m);
+  if constexpr (kFluid) {
+    if (P.timeline == 4 && threadIdx.x == 0) {
+      unsigned long long t_end;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+      const unsigned i = atomicAdd(&g_fluid_tl_n, 1u);
+      if (i < 8192) {
+        g_fluid_tl[i][0] = (unsigned long long)R.slot | ((unsigned long long)blockIdx.x << 32);
+        g_fluid_tl[i][1] = t_start;
+        g_fluid_tl[i][2] = t_end;
+        g_fluid_tl[i][3] = 0;
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1256,6 +1465,11 @@ static int launch_tc(const DecView &dv, const double *c0, const double *cs, int 
   return launch_tc_t<false, Rows, PAIR>(dv, c0, cs, S, rows, tiles_bound, st);
 }
 
+extern "C" DIST_API int dist_debug_fluid_timeline(unsigned long long *out, int n) {
+  return cudaMemcpyFromSymbol(out, tc::g_fluid_tl, sizeof(unsigned long long) * 4 * (size_t)std::min(n, 8192)) ==
+                 cudaSuccess ? 0 : -1;
+}
+
 extern "C" DIST_API int dist_debug_mlp_timeline(unsigned long long *out, int n) {
   return cudaMemcpyFromSymbol(out, tc::g_mlp_tl, sizeof(unsigned long long) * (size_t)std::min(n, 4096)) ==
                  cudaSuccess ? 0 : -1;
@@ -1379,14 +1593,75 @@ int tc_calibrate(DecView &dv) {
   return rc;
 }
 
+// fluid level prologue: the level's initial list count (k_init / k_split
+// leave it in the controller) and "slot -1 complete"
+__global__ void k_fluid_prep(const Ctl *ctl, int32_t *cnt, int32_t *done) {
+  cnt[0] = ctl->cnt[ctl->cur];
+  done[0] = 1;
+}
+
+// fluid level epilogue: every view advances by the slots in which it had live
+// rays (step_epilogue's per-slot increments, applied once), and the trace's
+// max-steps audit counter
+__global__ void k_fluid_finish(ViewBudget vb, MarchArgs a, int slots, int64_t *stats) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= a.V) return;
+  const int s0 = vb.steps[v];
+  int n = 0;
+  for (int s = 0; s < slots && s0 + s < a.max_steps; ++s)
+    if (vb.live[(int64_t)v * a.max_steps + s0 + s] > 0) n = s + 1;
+  if (n) {
+    vb.steps[v] = s0 + n;
+    atomicMax((unsigned long long *)&stats[2], (unsigned long long)(s0 + n));
+  }
+}
+
 int tc_run_steps(const DecView &dv, const double *c0, const double *cskip, int S, const dist_camera *cams,
                  const LevelState &ls, Ctl *ctl, int32_t *l0, int32_t *l1, const MarchArgs &a,
-                 int slots, const ViewBudget &vb, int64_t *stats, cudaStream_t st) {
+                 int slots, const ViewBudget &vb, int64_t *stats, cudaStream_t st, const FluidBufs &fb) {
+  const int64_t tiles = ceil_div(ls.n, 128);
+  const char *sv = getenv("DIST_TC_STEPPED");   // A/B switch (tests/test_gpu_fluid.py)
+  const bool stepped = sv && atoi(sv) != 0;
+  // fluid: the dynamic mask, the buffers, and a full grid in every slot (so
+  // no more than two consecutive slots' grids are ever resident together)
+  if (!stepped && fb.list2 && fb.ctr && a.dynamic && tiles >= sm_count() / 2 && slots > 1) {
+    const size_t n = (size_t)a.max_steps + 2;
+    tc::FluidCtl f;
+    f.cnt = fb.ctr;
+    f.head = fb.ctr + n;
+    f.dctr = fb.ctr + 2 * n;
+    f.done = fb.ctr + 3 * n;
+    f.lists[0] = l0;
+    f.lists[1] = l1;
+    f.lists[2] = fb.list2;
+    cudaError_t e = cudaMemsetAsync(fb.ctr, 0, sizeof(int32_t) * 4 * n, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(l1, 0xFF, sizeof(int32_t) * ls.n, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(fb.list2, 0xFF, sizeof(int32_t) * ls.n, st);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemsetAsync(fluid)");
+    k_fluid_prep<<<1, 1, 0, st>>>(ctl, f.cnt, f.done);
+    DIST_CHECK_LAUNCH("k_fluid_prep");
+    tc::MarchFluid rows;
+    static_cast<tc::MarchRows &>(rows) = tc::MarchRows{cams, ls, ctl, l0, l1, a, vb, stats};
+    rows.f = f;
+    rows.last_slot = slots - 1;
+    rows.level_coarse = ls.level > 1;
+    for (int s = 0; s < slots; ++s) {
+      rows.slot = s;
+      tc::MarchFluidM rows_m;
+      static_cast<tc::MarchFluid &>(rows_m) = rows;
+      int rc = ls.masks ? launch_tc(dv, c0, cskip, S, rows_m, tiles, st)
+                        : launch_tc(dv, c0, cskip, S, rows, tiles, st);
+      if (rc) return rc;
+    }
+    k_fluid_finish<<<(int)ceil_div(a.V, 128), 128, 0, st>>>(vb, a, slots, stats);
+    DIST_CHECK_LAUNCH("k_fluid_finish");
+    return DIST_OK;
+  }
   tc::MarchRows rows{cams, ls, ctl, l0, l1, a, vb, stats};
   tc::MarchRowsM rows_m{rows};
   for (int s = 0; s < slots; ++s) {
-    int rc = ls.masks ? launch_tc(dv, c0, cskip, S, rows_m, ceil_div(ls.n, 128), st)
-                      : launch_tc(dv, c0, cskip, S, rows, ceil_div(ls.n, 128), st);
+    int rc = ls.masks ? launch_tc(dv, c0, cskip, S, rows_m, tiles, st)
+                      : launch_tc(dv, c0, cskip, S, rows, tiles, st);
     if (rc) return rc;
   }
   return DIST_OK;

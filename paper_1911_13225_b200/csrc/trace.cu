@@ -764,6 +764,7 @@ struct TraceLayout {
   int32_t *list0, *list1, *bcount;
   int32_t *vsteps, *vcnt;   // ViewBudget: per-view steps and this slot's counts
   int32_t *rcnt;            // k_march_resident: three rotating [V+1] counter rows
+  FluidBufs fluid;          // the fluid tensor-core march (tc_mlp.cu), or nulls
   Ctl *ctl;
   size_t bytes;
 };
@@ -808,6 +809,10 @@ static TraceLayout layout(const DecView &dv, const dist_trace_config *cfg, int V
   const int64_t nmax = (int64_t)V * W * H;
   L.list0 = cv.take<int32_t>(nmax);
   L.list1 = cv.take<int32_t>(nmax);
+  if (tc_supported(dv) && cfg->use_dynamic_mask) {   // the fluid march's third list and counters
+    L.fluid.list2 = cv.take<int32_t>(nmax);
+    L.fluid.ctr = cv.take<int32_t>(4 * ((size_t)cfg->max_steps + 2));
+  }
   L.bcount = cv.take<int32_t>(ceil_div(nmax * 6, kScanBlock) + 1);
   L.vsteps = cv.take<int32_t>(2 * (size_t)V);
   L.vcnt = L.vsteps ? L.vsteps + V : nullptr;
@@ -955,7 +960,8 @@ int dist_trace(const dist_decoder *dec, const double *codes, int S, const dist_c
     if (dv.prec == DIST_PREC_FP64)
       rc = run_steps<double>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, vb, stats, L.rcnt, std::max(S, 1), st);
     else if (tc_supported(dv))
-      rc = tc_run_steps(dv, L.c0, L.cskip, std::max(S, 1), cams, ls, L.ctl, L.list0, L.list1, a, slots, vb, stats, st);
+      rc = tc_run_steps(dv, L.c0, L.cskip, std::max(S, 1), cams, ls, L.ctl, L.list0, L.list1, a, slots, vb, stats, st,
+                        L.fluid);
     else
       rc = run_steps<float>(dv, L.c0, L.cskip, cams, ls, L.ctl, L.list0, L.list1, a, slots, vb, stats, L.rcnt, std::max(S, 1), st);
     if (rc) return rc;
