@@ -71,3 +71,20 @@ def test_fluid_two_shapes_and_skip_layout(st):
     b = _trace(field, codes, views, cfg, False, stepped=True, shape_of_view=[0, 1])
     for k in a:
         np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+
+
+def test_fluid_budget_and_nan_rays(st):
+    """A tight step budget (max_steps 12: rays still marching at the end are
+    EXHAUSTED) and a shape whose code is NaN (every ray of its views stops at
+    its first query, counted as NaN) through the fluid march."""
+    from paper_1911_13225_b200.workloads import ring_views, target_code
+    field = st.NeuralField.geometric(256, (512,) * 8, 0, precision="fp16x3")
+    views = ring_views(2, 256)
+    codes = np.stack([target_code(1), np.full(256, np.nan)])
+    cfg = st.TraceConfig(k_samples=3, max_steps=12)
+    a = _trace(field, codes, views, cfg, False, stepped=False, shape_of_view=[0, 1])
+    b = _trace(field, codes, views, cfg, False, stepped=True, shape_of_view=[0, 1])
+    for k in a:
+        np.testing.assert_array_equal(a[k], b[k], err_msg=k)
+    assert a["stats_dev"][1] > 0              # NaN queries counted
+    assert (a["status"] == 3).sum() > 1000    # budget-exhausted rays (EXHAUSTED)
