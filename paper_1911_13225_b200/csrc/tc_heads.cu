@@ -22,6 +22,7 @@
 //     butterfly and adds the column sums into this CTA's slice of part0: the
 //     sums are independent of how rows are partitioned.
 #include <cmath>
+#include <type_traits>
 #include <cstring>
 
 #include "common.cuh"
@@ -253,51 +254,59 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int ph = BWD ? G : 0; ph < NPH; ++ph, ++phase) {
           mbar_wait(&m.aready, phase & 1);
           tc_fence_after();
-          // fully unrolled: a loop that waits on a barrier gets a YIELD on its
-          // back-edge, which costs the MMA issue ~25% of the tensor pipe
-          // (scripts/tc_pattern_bench.cu patterns 18 vs 27)
+          // One GEMM: the N-half and K loops fully unrolled (a loop that waits
+          // on a barrier gets a YIELD on its back-edge, which costs the MMA
+          // issue ~25% of the tensor pipe: scripts/tc_pattern_bench.cu), one
+          // copy per product scheme so each phase's issue code is contiguous
+          // (the forward and backward variants interleaved per stage doubled
+          // the instruction footprint of either).
+          auto gemm = [&](auto fwd_tag) {
+            constexpr bool FWD = decltype(fwd_tag)::value;
+            // BWD: a tile's first operand is built in A_lo (parked there during
+            // the previous tile's last GEMM); every later one in A_hi
+            const uint32_t ab = (!FWD && BWD && ph == G) ? a_lo : a_hi;
 #pragma unroll
-          for (int nh = 0; nh < 2; ++nh) {
-            const uint32_t d = tmem + nh * 128;
+            for (int nh = 0; nh < 2; ++nh) {
+              const uint32_t d = tmem + nh * 128;
 #pragma unroll
-            for (int kc = 0; kc < NKB; ++kc, ++it) {
-              if (nh == 0 && kc == NKB / 2) {   // second half of A: written after the first
-                mbar_wait(&m.aready2, phase & 1);
+              for (int kc = 0; kc < NKB; ++kc, ++it) {
+                if (nh == 0 && kc == NKB / 2) {   // second half of A: written after the first
+                  mbar_wait(&m.aready2, phase & 1);
+                  tc_fence_after();
+                }
+                const int s = it % STAGES;
+                mbar_wait(&m.full[s], (it / STAGES) & 1);
                 tc_fence_after();
-              }
-              const int s = it % STAGES;
-              mbar_wait(&m.full[s], (it / STAGES) & 1);
-              tc_fence_after();
-              const uint32_t b_hi = smem_u32(smem + OFF_B + s * STAGE_BYTES), b_lo = b_hi + B_TILE;
-              if (!BWD && ph < G) {   // forward: bf16x3 (never in the backward-only kernel)
+                const uint32_t b_hi = smem_u32(smem + OFF_B + s * STAGE_BYTES), b_lo = b_hi + B_TILE;
+                if constexpr (FWD) {   // forward: bf16x3
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const uint32_t ak = kc * (ROWS * 128) + q * 32;
-                  const uint64_t dah = sdesc(a_hi + ak), dal = sdesc(a_lo + ak);
-                  const uint64_t dbh = sdesc(b_hi + q * 32), dbl = sdesc(b_lo + q * 32);
-                  mma_2sm<false>(d, dah, dbh, (kc | q) ? 1u : 0u);
-                  mma_2sm<false>(d, dah, dbl, 1u);
-                  mma_2sm<false>(d, dal, dbh, 1u);
-                }
-              } else {        // backward: fp16x2, g x (W_hi + W_lo)
-                // BWD: a tile's first operand is built in A_lo (parked there
-                // during the previous tile's last GEMM); every later one in A_hi
-                const uint32_t ab = (BWD && ph == G) ? a_lo : a_hi;
+                  for (int q = 0; q < 4; ++q) {
+                    const uint32_t ak = kc * (ROWS * 128) + q * 32;
+                    const uint64_t dah = sdesc(a_hi + ak), dal = sdesc(a_lo + ak);
+                    const uint64_t dbh = sdesc(b_hi + q * 32), dbl = sdesc(b_lo + q * 32);
+                    mma_2sm<false>(d, dah, dbh, (kc | q) ? 1u : 0u);
+                    mma_2sm<false>(d, dah, dbl, 1u);
+                    mma_2sm<false>(d, dal, dbh, 1u);
+                  }
+                } else {               // backward: fp16x2, g x (W_hi + W_lo)
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                  const uint64_t dah = sdesc(ab + kc * (ROWS * 128) + q * 32);
-                  mma_2sm<true>(d, dah, sdesc(b_hi + q * 32), (kc | q) ? 1u : 0u);
-                  mma_2sm<true>(d, dah, sdesc(b_lo + q * 32), 1u);
+                  for (int q = 0; q < 4; ++q) {
+                    const uint64_t dah = sdesc(ab + kc * (ROWS * 128) + q * 32);
+                    mma_2sm<true>(d, dah, sdesc(b_hi + q * 32), (kc | q) ? 1u : 0u);
+                    mma_2sm<true>(d, dah, sdesc(b_lo + q * 32), 1u);
+                  }
                 }
+                commit_2sm(&m.empty[s]);
+                // phases that write the next operand: A's K blocks 0..3 are free
+                // once the nh = 1 MMAs are past them (tc_mlp.cu, same barrier)
+                if (nh == 1 && kc == NKB / 2 - 1 && (ph < G - 1 || (ph >= G && ph < 2 * G - 1)))
+                  commit_2sm(&m.afree);
               }
-              commit_2sm(&m.empty[s]);
-              // phases that write the next operand: A's K blocks 0..3 are free
-              // once the nh = 1 MMAs are past them (tc_mlp.cu, same barrier)
-              if (nh == 1 && kc == NKB / 2 - 1 && (ph < G - 1 || (ph >= G && ph < 2 * G - 1)))
-                commit_2sm(&m.afree);
+              commit_2sm(&m.dfull[nh]);
             }
-            commit_2sm(&m.dfull[nh]);
-          }
+          };
+          if (!BWD && ph < G) gemm(std::true_type{});   // never in the backward-only kernel
+          else gemm(std::false_type{});
         }
     }
   } else {
