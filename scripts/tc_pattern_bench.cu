@@ -42,6 +42,12 @@
 //  34/35 ring pairs : 31/32 waiting for two stages at once on even K blocks
 //  36 ring, local arrive : 31 with the producer arriving by mbarrier.arrive.shared::cta
 //  37 ring, leader-only  : 36 with only the leader's producer (rank 1's idles)
+//  38/39/40 self, unrolled : 12/13/14 (the MMA thread waits on its own commit
+//               of K block it-RS, RS = 3 / 6 / 12) with the K loop unrolled
+//  41 ring, spin producer : 31 with the producer's empty-wait a test_wait spin
+//  42 ring, spin both     : 41 with the MMA thread's full-wait a test_wait spin too
+//  43/44 ring, lazy producer : 31 with the producer polling empty by test_wait
+//               + __nanosleep(200 / 1000) between polls
 // FLOP per clock per SM of the slowest issuer; operand values are zeros.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1911_13225_b200/csrc \
@@ -65,7 +71,20 @@ __device__ __forceinline__ void mma_m256(uint32_t d, uint64_t a, uint64_t b, uin
 template <int W>
 __device__ __forceinline__ void wait_w(uint64_t *b, uint32_t parity) {
   const uint32_t a = smem_u32(b);
-  if constexpr (W == 0) {
+  if constexpr (W == 5 || W == 6) {
+    for (;;) {
+      uint32_t ok;
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(ok)
+          : "r"(a), "r"(parity)
+          : "memory");
+      if (ok) break;
+      __nanosleep(W == 5 ? 200 : 1000);
+    }
+  } else if constexpr (W == 0) {
     mbar_wait(b, parity);
   } else if constexpr (W == 1) {
     asm volatile(
@@ -100,11 +119,12 @@ template <int PAT>
 __global__ void __launch_bounds__(320, 1) k_pat(unsigned long long *cycles, unsigned long long *nmma) {
   extern __shared__ __align__(1024) char smem_raw[];
   char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  constexpr int RS = PAT == 7 || PAT == 13 || PAT == 15 || PAT == 16 || PAT == 32 || PAT == 35 ? 6
-                     : (PAT == 14 || PAT == 17 ? 12 : STAGES);
-  constexpr bool SELF = PAT >= 12 && PAT <= 17;
-  constexpr int WF = PAT == 10 ? 1 : (PAT == 11 ? 2 : 0);
-  constexpr bool RING = (PAT >= 6 && PAT <= 8) || PAT == 10 || PAT == 11 || SELF || PAT == 31 || PAT == 32 || PAT == 33 || PAT == 34 || PAT == 35 || PAT == 36 || PAT == 37;
+  constexpr int RS = PAT == 7 || PAT == 13 || PAT == 15 || PAT == 16 || PAT == 32 || PAT == 35 || PAT == 39 ? 6
+                     : (PAT == 14 || PAT == 17 || PAT == 40 ? 12 : STAGES);
+  constexpr bool SELF = (PAT >= 12 && PAT <= 17) || (PAT >= 38 && PAT <= 40);
+  constexpr int WF = PAT == 10 || PAT == 41 || PAT == 42 ? 1 : (PAT == 11 ? 2 : (PAT == 43 ? 5 : (PAT == 44 ? 6 : 0)));
+  constexpr bool RING = (PAT >= 6 && PAT <= 8) || PAT == 10 || PAT == 11 || SELF || PAT == 31 || PAT == 32 || PAT == 33 || PAT == 34 || PAT == 35 || PAT == 36 || PAT == 37 ||
+                       PAT == 41 || PAT == 42 || PAT == 43 || PAT == 44;
   __shared__ uint64_t bar, sbar, full[16], empty[16];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5;
@@ -290,7 +310,7 @@ __global__ void __launch_bounds__(320, 1) k_pat(unsigned long long *cycles, unsi
                 wait_w<0>(&full[(it + 1) % RS], ((it + 1) / RS) & 1);
               }
             } else {
-              wait_w<WF>(&full[s], (it / RS) & 1);
+              wait_w<PAT == 41 || PAT == 43 || PAT == 44 ? 0 : WF>(&full[s], (it / RS) & 1);
             }
             if (PAT != 8) tc_fence_after();
             const uint32_t b_hi = smem_u32(smem + OFF_B + (s % STAGES) * STAGE_BYTES), b_lo = b_hi + B_TILE;
@@ -469,6 +489,13 @@ int main() {
   run<35>("6-stage ring, unrolled, waits in pairs", nsm);
   run<36>("3-stage ring, unrolled, producer arrives CTA-locally", nsm);
   run<37>("3-stage ring, unrolled, local arrive, leader producer only", nsm);
+  run<38>("self-throttled 3 deep, unrolled", nsm);
+  run<39>("self-throttled 6 deep, unrolled", nsm);
+  run<40>("self-throttled 12 deep, unrolled", nsm);
+  run<41>("3-stage ring, unrolled, producer spins on test_wait", nsm);
+  run<42>("3-stage ring, unrolled, both spin on test_wait", nsm);
+  run<43>("3-stage ring, unrolled, producer polls every 200 ns", nsm);
+  run<44>("3-stage ring, unrolled, producer polls every 1000 ns", nsm);
   run<1>("kernel (mode 3) again", nsm);
   return 0;
 }
