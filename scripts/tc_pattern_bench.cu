@@ -48,6 +48,10 @@
 //  42 ring, spin both     : 41 with the MMA thread's full-wait a test_wait spin too
 //  43/44 ring, lazy producer : 31 with the producer polling empty by test_wait
 //               + __nanosleep(200 / 1000) between polls
+//  45 merged  : no producer thread: before K block it the MMA thread waits on
+//               its own commit of it-1 (the slot of it+2), arrives on that
+//               slot's full barrier itself (where the TMA issue would go), then
+//               waits on full[it] -- the producer role folded into the issuer
 // FLOP per clock per SM of the slowest issuer; operand values are zeros.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_1911_13225_b200/csrc \
@@ -124,7 +128,7 @@ __global__ void __launch_bounds__(320, 1) k_pat(unsigned long long *cycles, unsi
   constexpr bool SELF = (PAT >= 12 && PAT <= 17) || (PAT >= 38 && PAT <= 40);
   constexpr int WF = PAT == 10 || PAT == 41 || PAT == 42 ? 1 : (PAT == 11 ? 2 : (PAT == 43 ? 5 : (PAT == 44 ? 6 : 0)));
   constexpr bool RING = (PAT >= 6 && PAT <= 8) || PAT == 10 || PAT == 11 || SELF || PAT == 31 || PAT == 32 || PAT == 33 || PAT == 34 || PAT == 35 || PAT == 36 || PAT == 37 ||
-                       PAT == 41 || PAT == 42 || PAT == 43 || PAT == 44;
+                       PAT == 41 || PAT == 42 || PAT == 43 || PAT == 44 || PAT == 45;
   __shared__ uint64_t bar, sbar, full[16], empty[16];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x >> 5;
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(320, 1) k_pat(unsigned long long *cycles, unsi
     mbar_wait(&bar, 0);
   }
   if (PAT >= 28 && PAT <= 30 && threadIdx.x == 0) s_stop = 1;
-  if (RING && !SELF && threadIdx.x == 32) {   // producer (both CTAs)
+  if (RING && !SELF && PAT != 45 && threadIdx.x == 32) {   // producer (both CTAs)
     if constexpr (PAT == 33) {
       for (int i0 = 0; i0 < NIT; i0 += 8) {
 #pragma unroll
@@ -298,7 +302,17 @@ __global__ void __launch_bounds__(320, 1) k_pat(unsigned long long *cycles, unsi
 #pragma unroll (PAT >= 31 ? 8 : 1)
           for (int kc = 0; kc < NKB; ++kc, ++it) {
             const int s = it % RS;
-            if constexpr (PAT == 16) {
+            if constexpr (PAT == 45) {
+              // refill the slot of K block it+2 (freed by the commit of it-1)
+              const uint32_t nx = it + 2;
+              if (nx >= (uint32_t)RS) wait_w<0>(&empty[nx % RS], ((nx / RS) - 1) & 1);
+              asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[nx % RS])) : "memory");
+              if (it == 0) {   // the first two slots
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[0])) : "memory");
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[1])) : "memory");
+              }
+              wait_w<0>(&full[s], (it / RS) & 1);
+            } else if constexpr (PAT == 16) {
               if (it == 0) {}   // K block 0's wait: none (nothing committed yet)
             } else if constexpr (PAT == 17) {
               if (it >= (uint32_t)RS && (it & 3) == 0) wait_w<0>(&empty[s], ((it / RS) - 1) & 1);
@@ -496,6 +510,7 @@ int main() {
   run<42>("3-stage ring, unrolled, both spin on test_wait", nsm);
   run<43>("3-stage ring, unrolled, producer polls every 200 ns", nsm);
   run<44>("3-stage ring, unrolled, producer polls every 1000 ns", nsm);
+  run<45>("producer folded into the MMA thread (3 slots)", nsm);
   run<1>("kernel (mode 3) again", nsm);
   return 0;
 }
