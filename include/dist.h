@@ -106,7 +106,8 @@ DIST_API int64_t dist_launch_count(void);
  * first epilogue thread; scripts/tile_timeline.py). Copies up to n entries. */
 DIST_API int dist_debug_mlp_timeline(unsigned long long *out, int n);
 /* DIST_TC_TIMELINE=4: one row per CTA of the fluid march's slot grids,
- * {slot | block << 32, start ns, end ns, 0}; copies up to n rows. */
+ * {slot | block << 32, start ns, end ns, first rows ns | tiles << 48};
+ * copies up to n (<= 16384) rows. */
 DIST_API int dist_debug_fluid_timeline(unsigned long long *out, int n);
 DIST_API int dist_debug_heads_timeline(unsigned long long *out, int n);
 

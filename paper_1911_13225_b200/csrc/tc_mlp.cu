@@ -317,7 +317,7 @@ __device__ __forceinline__ float relu_pair_sel(float m, float d, bool odd) {
 
 static __device__ unsigned long long g_mlp_tl[4096];
 // DIST_TC_TIMELINE=4 (fluid march): per CTA (slot, start, end, tiles) rows
-static __device__ unsigned long long g_fluid_tl[8192][4];
+static __device__ unsigned long long g_fluid_tl[16384][4];
 static __device__ unsigned int g_fluid_tl_n;
 // epilogue marks in [0, 2048), the MMA thread's in [2048, 4096)
 #define TL(id)                                   \
@@ -380,6 +380,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   if constexpr (kFluid) wait_grid = R.slot == 0;
   if (wait_grid) asm volatile("griddepcontrol.wait;" ::: "memory");
   unsigned long long t_start = 0;
+  __shared__ unsigned long long s_t_rows, s_tiles;   // DIST_TC_TIMELINE=4: first rows loaded, tiles run
   if (P.timeline == 4 && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
   if (!R.begin(m)) {  // uniform across the grid (all CTAs read the same controller)
     tc_fence_before();
@@ -612,9 +613,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const bool sched = kFluid && rank == 0 && threadIdx.x == 64;
     if (sched) publish(0);
     bool have = fetch(0, nx), next_have = false;
+    if (kFluid && P.timeline == 4 && threadIdx.x == 64) {
+      unsigned long long tr;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr));
+      s_t_rows = tr;
+      s_tiles = 0;
+    }
     uint32_t layer = 0;
     for (int k = 0; have; ++k, have = next_have) {
       TL(1);
+      if (kFluid && P.timeline == 4 && threadIdx.x == 64) s_tiles = k + 1;
       // ---- rows and layer 0 (fp64, latent folded into c0) ----
       double p[3] = {nx.p[0], nx.p[1], nx.p[2]};
       const int s = nx.s, id = nx.id;
@@ -1162,11 +1170,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       unsigned long long t_end;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
       const unsigned i = atomicAdd(&g_fluid_tl_n, 1u);
-      if (i < 8192) {
+      if (i < 16384) {
         g_fluid_tl[i][0] = (unsigned long long)R.slot | ((unsigned long long)blockIdx.x << 32);
         g_fluid_tl[i][1] = t_start;
         g_fluid_tl[i][2] = t_end;
-        g_fluid_tl[i][3] = 0;
+        g_fluid_tl[i][3] = (s_t_rows & 0xFFFFFFFFFFFFull) | (s_tiles << 48);
       }
     }
   }
@@ -1466,7 +1474,7 @@ static int launch_tc(const DecView &dv, const double *c0, const double *cs, int 
 }
 
 extern "C" DIST_API int dist_debug_fluid_timeline(unsigned long long *out, int n) {
-  return cudaMemcpyFromSymbol(out, tc::g_fluid_tl, sizeof(unsigned long long) * 4 * (size_t)std::min(n, 8192)) ==
+  return cudaMemcpyFromSymbol(out, tc::g_fluid_tl, sizeof(unsigned long long) * 4 * (size_t)std::min(n, 16384)) ==
                  cudaSuccess ? 0 : -1;
 }
 

@@ -33,19 +33,21 @@ opt = st.LatentOptimizer(field, views, {"depth": obs}, np.zeros((1, 256)), cfg, 
                          shard=TileShard(0, args.world, 32, None))
 opt.step()
 torch.cuda.synchronize()
-os.environ["DIST_TC_TIMELINE"] = "4"   # the next iterate only (8192 CTA rows)
+os.environ["DIST_TC_TIMELINE"] = "4"   # the next iterate only (16384 CTA rows)
 opt.step()
 torch.cuda.synchronize()
 os.environ.pop("DIST_TC_TIMELINE")
 
-buf = (ctypes.c_ulonglong * (8192 * 4))()
-_lib.lib().dist_debug_fluid_timeline(buf, 8192)
-a = np.array(buf[:], dtype=np.uint64).reshape(8192, 4)
+buf = (ctypes.c_ulonglong * (16384 * 4))()
+_lib.lib().dist_debug_fluid_timeline(buf, 16384)
+a = np.array(buf[:], dtype=np.uint64).reshape(16384, 4)
 a = a[a[:, 1] > 0]
 slot = (a[:, 0] & np.uint64(0xFFFFFFFF)).astype(int)
 t0, t1 = a[:, 1].astype(np.int64), a[:, 2].astype(np.int64)
+tiles = (a[:, 3] >> np.uint64(48)).astype(int)
+trow = (a[:, 3] & np.uint64((1 << 48) - 1)).astype(np.int64)
 order = np.argsort(t0)
-slot, t0, t1 = slot[order], t0[order], t1[order]
+slot, t0, t1, tiles, trow = slot[order], t0[order], t1[order], tiles[order], trow[order]
 base = t0[0]
 level = np.cumsum(np.r_[0, np.diff(slot) < 0])
 print(f"CTA rows {len(slot)}; levels {level.max() + 1}")
@@ -54,6 +56,8 @@ for (lv, sl) in sorted(set(zip(level.tolist(), slot.tolist()))):
     m = (level == lv) & (slot == sl)
     st_, en = (t0[m].min() - base) / 1e3, (t1[m].max() - base) / 1e3
     ov = "" if prev_end is None else f"  overlap with previous {max(0.0, prev_end - st_):7.1f} us"
-    if sl < 6 or sl % 10 == 0:
-        print(f"level {lv} slot {sl:3d}: CTAs {m.sum():4d}  start {st_:9.1f}  end {en:9.1f}  dur {en - st_:7.1f} us{ov}")
+    busy = m & (tiles > 0)
+    if sl < 6 or sl % 10 == 0 or sl > 90:
+        print(f"level {lv} slot {sl:3d}: CTAs {m.sum():4d} busy {busy.sum():4d} tiles/CTA max {tiles[m].max()}  "
+              f"start {st_:9.1f}  end {en:9.1f}  dur {en - st_:7.1f} us{ov}")
     prev_end = en
