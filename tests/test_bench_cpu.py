@@ -37,3 +37,27 @@ def test_reference_arm_other_ranks_exit_quietly():
     r = _run({"RANK": "1"})
     assert r.returncode == 0
     assert not [l for l in r.stdout.splitlines() if l.strip().startswith("{")]
+
+
+def test_algorithmic_flops_per_query():
+    """SURVEY 8d's F_q / F_b for the plain 8x512 decoder, and the DeepSDF
+    skip-4 layout's (layer 3 is 512 -> 253, layer 4 reads 253 + 3 rows per
+    query: its code rows are folded into a per-shape bias like layer 0's)."""
+    sys.path.insert(0, ROOT)
+    import bench
+    assert bench._flops(-1) == (3_674_112, 3_671_040)
+    fq, fb = bench._flops(4)
+    assert fq == 2 * (3 * 512 + 2 * 512 * 512 + 512 * 253 + 256 * 512 + 3 * 512 * 512 + 512)
+    assert fb == 2 * (2 * 512 * 512 + 512 * 253 + 253 * 512 + 3 * 512 * 512 + 512)
+
+
+def test_reference_arm_skip_layout_times_the_port():
+    """The reference decoder has no skip layer: `--skip 4` times the oracle port."""
+    env = dict(os.environ, RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--skip", "4",
+                        "--steps", "1", "--warmup", "0"], capture_output=True, text=True, env=env,
+                       timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([l for l in r.stdout.splitlines() if l.strip().startswith("{")][0])
+    assert d["cpu_baseline"]["kind"] == "port" and d["config"]["skip"] == 4
+    assert "skip 4" in d["cpu_baseline"]["sample"]
