@@ -609,9 +609,19 @@ def reconstruct_multiview(field, images, cameras, code0=None, iters: int = 60,
         sel = rng.choice(n_views, size=min(views_per_iter, n_views), replace=False)
         needed = sorted(set(sel) | {neighbor[i] for i in sel})
         heads_by, z_by, queries = {}, {}, 0
+        # one batched device trace for the needed views when they share a
+        # resolution (per-view budgets: the same result as tracing each view)
+        if hasattr(field, "handle") and len({(cams[i][0].width, cams[i][0].height) for i in needed}) == 1:
+            from .tracer import host_result, trace_views
+            dt = trace_views(field, code, [cams[i] for i in needed], cfg)
+            if dt.stats()["warnings"] & 1:
+                _w.warn("camera center inside the unit sphere; rays start at d=0", RuntimeWarning)
+            results = {i: host_result(dt, k) for k, i in enumerate(needed)}
+        else:
+            results = {i: trace(field, code, cams[i][0], cams[i][1], cfg) for i in needed}
         for i in needed:
             intr, pose = cams[i]
-            res = trace(field, code, intr, pose, cfg)
+            res = results[i]
             h = diff_heads(res, field, code)
             heads_by[i] = h
             z_by[i] = h.depth_image(intr.height, intr.width)
