@@ -9,7 +9,7 @@ when the CUDA library is missing.
 
 Parity status: PINNED.  `oracle/make_golden.py` runs the unmodified reference
 (imported from /root/reference in the build container) on the cases committed
-under `tests/golden/`, and `tests/test_oracle.py` checks this restatement
+under `tests/golden/`, and `tests/test_oracle_cpu.py` checks this restatement
 against those fixtures (bitwise for ray state and query counts, 1e-12 for
 floating outputs).
 
