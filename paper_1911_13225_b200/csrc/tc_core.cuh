@@ -24,6 +24,11 @@ constexpr int OFF_B = 2 * A_PART;
 constexpr int OFF_MISC = OFF_B + STAGES * STAGE_BYTES;   // 229376
 constexpr int N_EPI_WARPS = 8;
 constexpr int THREADS = (2 + N_EPI_WARPS) * 32;          // producer, MMA, 8 epilogue warps
+// k_tc_mlp adds two "finish" warps that apply each tile's row results (the
+// march update, survivor append; the eval store) off the epilogue's critical
+// path.  12 warps keep the register cap of 10 (3 warps per SM sub-partition).
+constexpr int FIN0 = 2 + N_EPI_WARPS;
+constexpr int THREADS_MLP = (FIN0 + 2) * 32;
 constexpr int TMEM_COLS = 512;
 
 struct Misc {
@@ -36,6 +41,9 @@ struct Misc {
   uint64_t tk_bar[2]; // fluid march: tile ticket k is in tk_base/tk_cnt[k & 1]
   int64_t tk_base[2]; //   (published by CTA 0's scheduler thread into both CTAs)
   int32_t tk_cnt[2];  //   rows in the tile; 0 = no more tiles
+  uint64_t fin_full;  // k_tc_mlp: a tile's row results posted (g_fin) ...
+  uint64_t fin_empty; // ... and read by the finish warps
+  int32_t fin_stop;   // no more tiles
   uint32_t tmem_base;
   int32_t go, cur, cnt, nan;
   int32_t ray[ROWS];
@@ -66,6 +74,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t *b, uint32_t parity) {
       "@!p bra LAB_WAIT;\n\t}" ::"r"(a),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_local(uint64_t *b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *b, uint32_t tx) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(tx)

@@ -316,6 +316,19 @@ __device__ __forceinline__ float relu_pair_sel(float m, float d, bool odd) {
 }
 
 static __device__ unsigned long long g_mlp_tl[4096];
+// k_tc_mlp's row results of one tile, epilogue -> finish warps, per SM (one
+// tile-kernel CTA per SM at a time: its shared memory is all of the SM's)
+struct FinRow {
+  int32_t gi;   // row index (~gi: not a valid row)
+  int32_t id;
+  double fv;
+};
+static __device__ FinRow g_fin[256][ROWS];
+__device__ __forceinline__ uint32_t sm_id() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
 // DIST_TC_TIMELINE=4 (fluid march): per CTA (slot, start, end, tiles) rows
 static __device__ unsigned long long g_fluid_tl[16384][4];
 static __device__ unsigned int g_fluid_tl_n;
@@ -331,7 +344,7 @@ static __device__ unsigned int g_fluid_tl_n;
 // travel through the network as (mid, diff) -- adjacent TMEM lanes, so each
 // pair meets in one shfl.xor 1; the odd row's result is f(p+) - f(p-).
 template <bool F16, class Rows, bool PAIR = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_MLP, 1)
     k_tc_mlp(const __grid_constant__ CUtensorMap wmap, Params P, Rows R) {
   extern __shared__ __align__(16) char smem_raw[];
   char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -360,6 +373,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     mbar_init(&m.afree, 1);
     mbar_init(&m.tk_bar[0], 1);
     mbar_init(&m.tk_bar[1], 1);
+    mbar_init(&m.fin_full, 2 * 32);    // the two row-thread warps
+    mbar_init(&m.fin_empty, 2 * 32);   // the two finish warps
+    m.fin_stop = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -517,6 +533,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           }
         }
     }
+  } else if (warp >= FIN0) {
+    // ===== finish warps: apply each tile's row results (one thread per row) =====
+    const int frow = (warp - FIN0) * 32 + lane;
+    const uint32_t smid = sm_id();
+    for (uint32_t n = 0;; ++n) {
+      mbar_wait(&m.fin_full, n & 1);
+      if (*(volatile int32_t *)&m.fin_stop) break;
+      const volatile FinRow *vr = &g_fin[smid][frow];
+      const int32_t rgi = vr->gi, rid = vr->id;
+      const double rfv = vr->fv;
+      mbar_arrive_local(&m.fin_empty);
+      R.finish(m, rgi < 0 ? ~rgi : rgi, rid, rgi >= 0, rfv);
+    }
   } else {
     // ===== epilogue warps (both CTAs) =====
     const bool tl_on = P.timeline && blockIdx.x == 0 && threadIdx.x == 64;
@@ -608,6 +637,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     int64_t pgi = 0;
     int pid = -1;
     double pfv = 0.0;
+    // a tile's row results go to the finish warps (row threads, one per row):
+    // the march update no longer holds the epilogue at the next tile's start
+    uint32_t fin_n = 0;
+    const uint32_t fin_sm = sm_id();
+    auto post_fin = [&](bool stop) {
+      if (fin_n > 0) mbar_wait(&m.fin_empty, (fin_n - 1) & 1);
+      if (stop) {
+        if (row == 0) *(volatile int32_t *)&m.fin_stop = 1;
+      } else {
+        volatile FinRow *vr = &g_fin[fin_sm][row];
+        vr->gi = pvalid ? (int32_t)pgi : ~(int32_t)pgi;
+        vr->id = pid;
+        vr->fv = pfv;
+      }
+      mbar_arrive_local(&m.fin_full);
+      ++fin_n;
+    };
     RowIn nx;
     // fluid: the scheduler is CTA 0's thread 64 (an epilogue thread that owns no row)
     const bool sched = kFluid && rank == 0 && threadIdx.x == 64;
@@ -815,7 +861,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       TL(2);
       }
       // the previous tile's row results, while this tile's first GEMM runs
-      if (row_thread && pend) R.finish(m, pgi, pid, pvalid, pfv);
+      if (row_thread && pend) post_fin(false);
       pend = false;
       TL(10);
       // ---- hidden layers ----
@@ -1156,7 +1202,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         a_ready_all();
       }
     }
-    if (row_thread && pend) R.finish(m, pgi, pid, pvalid, pfv);
+    if (row_thread && pend) post_fin(false);
+    if (row_thread) post_fin(true);
   }
   // ---- teardown ----
   tc_fence_before();
@@ -1452,7 +1499,7 @@ static int launch_tc_t(const DecView &dv, const double *c0, const double *cs, in
   }();
   cudaLaunchConfig_t lc = {};
   lc.gridDim = dim3(2 * pairs);
-  lc.blockDim = dim3(tc::THREADS);
+  lc.blockDim = dim3(tc::THREADS_MLP);
   lc.dynamicSmemBytes = tc::SMEM_BYTES;
   lc.stream = st;
   cudaLaunchAttribute attr[1];

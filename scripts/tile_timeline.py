@@ -82,6 +82,16 @@ def main():
     merged(lib.dist_debug_mlp_timeline, "k_tc_mlp")
     if os.environ.get("TL_MLP_ONLY"):
         return
+    if os.environ.get("TL_MARCH"):
+        # a bulk march step: the last slot of a trace cut at max_steps = 8 is
+        # the second full-resolution slot (2 x 1e6 rays of 8 ring views)
+        f16 = st.NeuralField.geometric(256, (512,) * 8, 0, precision="fp16x3")
+        from paper_1911_13225_b200.tracer import trace_views
+        trace_views(f16, target_code(1), ring_views(8, 512), st.TraceConfig(k_samples=3, max_steps=8),
+                    relu_masks=True)
+        torch.cuda.synchronize()
+        merged(lib.dist_debug_mlp_timeline, "k_tc_mlp march (fluid, mask record)")
+        return
     views = ring_views(8, 512)
     cfg = st.TraceConfig(k_samples=3)
     obs = render_depth_observations(field, target_code(1), views, cfg)
