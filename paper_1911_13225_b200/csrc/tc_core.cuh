@@ -44,6 +44,8 @@ struct Misc {
   uint64_t fin_full;  // k_tc_mlp: a tile's row results posted (g_fin) ...
   uint64_t fin_empty; // ... and read by the finish warps
   int32_t fin_stop;   // no more tiles
+  uint64_t nx_full;   // k_tc_mlp: the next tile's rows are in g_next (finish warps) ...
+  uint64_t nx_empty;  // ... and were read by the epilogue
   uint32_t tmem_base;
   int32_t go, cur, cnt, nan;
   int32_t ray[ROWS];

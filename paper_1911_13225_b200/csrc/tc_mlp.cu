@@ -114,9 +114,15 @@ struct MarchRows {
     return m.go;
   }
   __device__ int64_t rows(const Misc &m) const { return a.dynamic ? (int64_t)m.cnt : ls.n; }
-  __device__ int load_m(const Misc &m, int64_t i, double p[3], int &s) const {
+  // the row's ray id (a list entry): the first of the row's two dependent loads
+  __device__ int64_t pre_m(const Misc &m, int64_t i) const {
     const int32_t *in = m.cur ? l1 : l0;
-    const int64_t g = a.dynamic ? in[i] : i;
+    return a.dynamic ? in[i] : i;
+  }
+  __device__ int load_m(const Misc &m, int64_t i, double p[3], int &s) const {
+    return load_mg(pre_m(m, i), p, s);
+  }
+  __device__ int load_mg(int64_t g, double p[3], int &s) const {
     double dir[3];
     const dist_camera *cam;
     ray_of(cams, ls, g, dir, &cam);
@@ -229,18 +235,13 @@ struct MarchFluid : MarchRows {
   // entry i of this slot's list: wait until it is written (the four epilogue
   // threads of a row all read it; finish() empties it for the list's reuse
   // three slots later)
-  __device__ int load_f(int64_t i, double p[3], int &s) const {
+  __device__ int64_t pre_f(int64_t i) const {
     const int32_t *in = f.lists[slot % 3] + i;
     int32_t g;
     while ((g = ld_acquire_s32(in)) < 0) __nanosleep(64);
-    double dir[3];
-    const dist_camera *cam;
-    ray_of(cams, ls, g, dir, &cam);
-    const double dg = ls.d[g];
-    for (int q = 0; q < 3; ++q) p[q] = __dadd_rn(cam->origin[q], __dmul_rn(dg, dir[q]));
-    s = cam->shape;
-    return (int)g;
+    return g;
   }
+  __device__ int load_f(int64_t i, double p[3], int &s) const { return load_mg(pre_f(i), p, s); }
   __device__ void finish(Misc &m, int64_t gi, int g, bool valid, double fv) const {
     if (g >= 0) f.lists[slot % 3][gi] = -1;   // this tile's entry: empty again
     bool keep = false;
@@ -287,6 +288,24 @@ __device__ __forceinline__ int load_row(const Rows &r, const Misc &m, int64_t i,
   else if constexpr (std::is_base_of<MarchRows, Rows>::value) return r.load_m(m, i, p, s);
   else return r.load(i, p, s);
 }
+// A row in two steps, a layer apart (the epilogue has a short wait at the end
+// of each layer): its id (march: the live-list entry), then the point.
+template <class Rows>
+__device__ __forceinline__ int64_t pre_row(const Rows &r, const Misc &m, int64_t i) {
+  if constexpr (std::is_base_of<MarchFluid, Rows>::value) return r.pre_f(i);
+  else if constexpr (std::is_base_of<MarchRows, Rows>::value) return r.pre_m(m, i);
+  else return i;
+}
+template <class Rows>
+__device__ __forceinline__ int load_row_g(const Rows &r, int64_t i, int64_t g, double p[3], int &s) {
+  if constexpr (std::is_base_of<MarchRows, Rows>::value) {
+    (void)i;
+    return r.load_mg(g, p, s);
+  } else {
+    (void)g;
+    return r.load(i, p, s);
+  }
+}
 
 // Normal probes (march.cuh ProbeGen) in (mid, diff) pair mode.
 struct ProbeRows {
@@ -324,6 +343,15 @@ struct FinRow {
   double fv;
 };
 static __device__ FinRow g_fin[256][ROWS];
+// the next tile's rows, finish warps -> epilogue, per SM
+struct NextRow {
+  double p[3];
+  int32_t s, id;
+  int32_t gi;    // the tile's row index (list / point index)
+  int32_t ok;    // the tile exists
+  uint32_t *md;  // ReLU-mask record of the query, or null
+};
+static __device__ NextRow g_next[256][ROWS];
 __device__ __forceinline__ uint32_t sm_id() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
@@ -375,6 +403,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_MLP, 1)
     mbar_init(&m.tk_bar[1], 1);
     mbar_init(&m.fin_full, 2 * 32);    // the two row-thread warps
     mbar_init(&m.fin_empty, 2 * 32);   // the two finish warps
+    mbar_init(&m.nx_full, 2 * 32);     // the finish warps
+    mbar_init(&m.nx_empty, N_EPI_WARPS * 32);   // every epilogue thread
     m.fin_stop = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -411,6 +441,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_MLP, 1)
   const int64_t ntiles = kFluid ? 0 : ceil_div(nrows, 2 * ROWS);
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
   const int G = P.n_gemm;
+  constexpr bool kMasks = (std::is_same<Rows, MarchRowsM>::value || std::is_same<Rows, MarchFluidM>::value) && !PAIR;
   // Tile k of this CTA pair: a static round-robin tile, or (fluid) the k-th
   // ticket CTA 0's scheduler thread publishes into both CTAs.  Returns false
   // when there is no tile k.
@@ -534,17 +565,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_MLP, 1)
         }
     }
   } else if (warp >= FIN0) {
-    // ===== finish warps: apply each tile's row results (one thread per row) =====
+    // ===== finish warps (one thread per tile row): fetch each tile's rows a
+    // tile ahead (fluid: CTA 0's first finish thread claims the tiles), and
+    // apply each tile's row results -- both off the epilogue's critical path
     const int frow = (warp - FIN0) * 32 + lane;
     const uint32_t smid = sm_id();
-    for (uint32_t n = 0;; ++n) {
-      mbar_wait(&m.fin_full, n & 1);
-      if (*(volatile int32_t *)&m.fin_stop) break;
+    const bool fsched = kFluid && rank == 0 && warp == FIN0 && lane == 0;
+    uint32_t n_res = 0;
+    auto results = [&]() -> bool {   // one post of the epilogue; false: stop
+      mbar_wait(&m.fin_full, n_res & 1);
+      ++n_res;
+      if (*(volatile int32_t *)&m.fin_stop) return false;
       const volatile FinRow *vr = &g_fin[smid][frow];
       const int32_t rgi = vr->gi, rid = vr->id;
       const double rfv = vr->fv;
       mbar_arrive_local(&m.fin_empty);
       R.finish(m, rgi < 0 ? ~rgi : rgi, rid, rgi >= 0, rfv);
+      return true;
+    };
+    for (int j = 0;; ++j) {
+      if constexpr (kFluid) {
+        if (fsched) publish(j);
+      }
+      int64_t base;
+      int cnt;
+      const bool ok = ticket(j, base, cnt);
+      if (j >= 1) mbar_wait(&m.nx_empty, (j - 1) & 1);   // tile j-1's rows were read
+      {
+        NextRow r;
+        const int ri = (int)rank * ROWS + frow;
+        const int64_t gi = base + ri;
+        r.p[0] = r.p[1] = r.p[2] = 0.0;
+        r.s = -1;
+        r.id = -1;
+        r.md = nullptr;
+        if (ok && ri < cnt && gi < nrows) r.id = load_row(R, m, gi, r.p, r.s);
+        if constexpr (kMasks) {
+          if (r.id >= 0) r.md = R.mask_dst(r.id);
+        }
+        volatile NextRow *w = &g_next[smid][frow];
+        w->p[0] = r.p[0];
+        w->p[1] = r.p[1];
+        w->p[2] = r.p[2];
+        w->s = r.s;
+        w->id = r.id;
+        w->gi = (int32_t)gi;
+        w->ok = ok ? 1 : 0;
+        w->md = r.md;
+      }
+      mbar_arrive_local(&m.nx_full);
+      if (j >= 1) results();   // tile j-1's row results
+      if (!ok) {               // no tile j: the epilogue's stop post
+        while (results()) {
+        }
+        break;
+      }
     }
   } else {
     // ===== epilogue warps (both CTAs) =====
@@ -575,12 +650,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_MLP, 1)
     struct RowIn {
       double p[3];
       int s, id;
-      int64_t gi;
+      int64_t gi, g0;  // g0: the row's prefetched id (-1: none)
       uint32_t *md;   // ReLU-mask record of this query (march with masks), else null
     };
     // ReLU masks (march with a mask record): this thread's 2 x 64 columns of a
     // layer are words 8 nh + 4 half + 2 sub + {0, 1} of the layer's 16
-    constexpr bool kMasks = (std::is_same<Rows, MarchRowsM>::value || std::is_same<Rows, MarchFluidM>::value) && !PAIR;
+
     // Record layout per layer (16 words): thread quarter q4 = 2 half + sub owns
     // words 4 q4 .. 4 q4 + 3 = (nh 0: cols +0..31, +32..63; nh 1: the same),
     // columns nh 256 + 64 q4 + 32 c + bit -- one 16-byte store per layer
@@ -595,20 +670,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_MLP, 1)
     uint32_t ms0 = 0u, ms1 = 0u;   // the stashed next tile's layer-0 nh = 0 mask words
     // rows of ticket k (tile base, row count): this thread's row of the tile;
     // returns whether tile k exists
-    auto fetch = [&](int k, RowIn &r) -> bool {
-      int64_t base;
-      int cnt;
-      const bool ok = ticket(k, base, cnt);
-      const int ri = (int)rank * ROWS + row;
-      r.gi = base + ri;
-      r.p[0] = r.p[1] = r.p[2] = 0.0;
-      r.s = -1;
-      r.id = -1;
-      r.md = nullptr;
-      if (ok && ri < cnt && r.gi < nrows) r.id = load_row(R, m, r.gi, r.p, r.s);
-      if constexpr (kMasks) {
-        if (r.id >= 0) r.md = R.mask_dst(r.id);
-      }
+    // the rows of tile k, fetched a tile ahead by the finish warps
+    auto take_next = [&](int k, RowIn &r) -> bool {
+      mbar_wait(&m.nx_full, k & 1);
+      const volatile NextRow *v = &g_next[sm_id()][row];
+      r.p[0] = v->p[0];
+      r.p[1] = v->p[1];
+      r.p[2] = v->p[2];
+      r.s = v->s;
+      r.id = v->id;
+      r.gi = v->gi;
+      r.md = v->md;
+      const bool ok = v->ok != 0;
+      mbar_arrive_local(&m.nx_empty);
       return ok;
     };
     uint32_t afree_n = 0;  // afree phases consumed (one per non-last kEarly layer)
@@ -656,9 +730,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_MLP, 1)
     };
     RowIn nx;
     // fluid: the scheduler is CTA 0's thread 64 (an epilogue thread that owns no row)
-    const bool sched = kFluid && rank == 0 && threadIdx.x == 64;
-    if (sched) publish(0);
-    bool have = fetch(0, nx), next_have = false;
+    bool have = take_next(0, nx), next_have = false;
     if (kFluid && P.timeline == 4 && threadIdx.x == 64) {
       unsigned long long tr;
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr));
@@ -903,11 +975,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_MLP, 1)
         return s >= 0 ? P.cskmax[s] + fabsf(px) * P.dv.wsm[0] + fabsf(py) * P.dv.wsm[1] + fabsf(pz) * P.dv.wsm[2]
                       : 0.f;
       };
+      // the next tile's rows (prefetched by the finish warps): taken at the
+      // end of layer G-2, where the epilogue waits for the last GEMM anyway
+      bool fetched_next = false;
       for (int l = 0; l < G; ++l, ++layer) {
-        if (l == G - 1) {
-          if (sched) publish(k + 1);
-          next_have = fetch(k + 1, nx);
-        }
+        if (l == G - 1 && !fetched_next) next_have = take_next(k + 1, nx);
         const bool last = (l == G - 1);
         const float *bias = P.bias + (size_t)l * KDIM;
         const float unscale = rinv * P.winv[l];   // exact: both are powers of two
@@ -1100,6 +1172,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS_MLP, 1)
             a_ready_hi();
             if constexpr (kBound) amax = xch_read();
             TL(4);
+          }
+          if (l == G - 2) {   // the next tile's rows (the epilogue now waits for the last GEMM)
+            next_have = take_next(k + 1, nx);
+            fetched_next = true;
           }
           continue;
         }
