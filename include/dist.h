@@ -279,6 +279,25 @@ DIST_API int dist_photometric(const dist_camera *cams_dev, int height, int width
                               double *loss_dev, double *dz_dev, uint8_t *vis_dev, void *ws,
                               size_t ws_bytes, void *stream);
 
+/* reconstruct_multiview on the device (optimize.py:272-358): the depth head
+ * of each converged recorded pixel's best sample (top-K slot 0;
+ * HeadBundle.depth_image, shading.py:156-281), one dense row per pixel of the
+ * V traced views (ray id (v*H + j)*W + i).
+ * dist_photo_heads: points_dev[g] = origin + topk_d[g][0] * dir, scale_dev[g]
+ *   = the ray's distance -> camera-z factor; a pixel without a converged
+ *   sample gets scale 0 and the origin as its point.
+ * dist_photo_depth: z_dev[g] = (topk_d[g][0] + f[g]) * scale, +inf where
+ *   scale is 0 (f = dist_eval at points_dev).
+ * dist_photo_seeds: seed_dev[g] = w_photo * dz[g] * scale (0 where scale is 0),
+ *   the depth seeds of optimize.py:340-341 for dist_eval_vjp. */
+DIST_API int dist_photo_heads(const dist_camera *cams_dev, int n_views, int width, int height,
+                              int k_samples, const dist_ray_state *st, double *points_dev,
+                              double *scale_dev, void *stream);
+DIST_API int dist_photo_depth(int64_t n, int k_samples, const double *topk_d, const double *f_dev,
+                              const double *scale_dev, double *z_dev, void *stream);
+DIST_API int dist_photo_seeds(int64_t n, const double *dz_dev, const double *scale_dev,
+                              double w_photo, double *seed_dev, void *stream);
+
 /* ---- Adam (AdamState/adam_step, optimize.py:35-63) ------------------------ */
 typedef struct dist_adam_config {
   double lr, beta1, beta2, eps;

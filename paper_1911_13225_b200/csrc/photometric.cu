@@ -132,6 +132,51 @@ __global__ void k_photo_scale(int64_t n, const double *__restrict__ graw,
     dz[p] = cnt > 0.0 ? graw[p] / cnt : 0.0;
 }
 
+// --- reconstruct_multiview's depth heads on the device (optimize.py:272-358) --
+// The photometric iterate only reads, per converged recorded pixel, the depth
+// head of its best sample (top-K slot 0): HeadBundle.depth_image
+// (shading.py:156-281) -> photometric_loss -> seed at that sample.  One dense
+// row per pixel: a pixel without a converged sample has scale 0 (its point is
+// the origin, its seed 0), so the reverse sweep needs no compaction.
+__global__ void k_photo_heads(const dist_camera *__restrict__ cams, int W, int H, int64_t n, int K,
+                              const uint8_t *__restrict__ status, const double *__restrict__ topk_d,
+                              const double *__restrict__ topk_absf, double *__restrict__ pts,
+                              double *__restrict__ scale) {
+  const int64_t per = (int64_t)W * H;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int v = (int)(g / per);
+    const int64_t pix = g - (int64_t)v * per;
+    const int j = (int)(pix / W), i = (int)(pix - (int64_t)j * W);
+    const bool ok = status[g] == DIST_CONVERGED && isfinite(topk_absf[g * K]);
+    double dir[3], sc;
+    pixel_ray(cams[v], i, j, 1, dir, &sc);
+    const double d = topk_d[g * K];
+    const double *o = cams[v].origin;
+    // origin + d * dir, rounded as numpy does (shading.py HeadBundle points)
+    for (int a = 0; a < 3; ++a) pts[g * 3 + a] = ok ? __dadd_rn(o[a], __dmul_rn(d, dir[a])) : 0.0;
+    scale[g] = ok ? sc : 0.0;
+  }
+}
+
+// z = (d + f) * scale at converged pixels, +inf elsewhere (depth_image)
+__global__ void k_photo_depth(int64_t n, int K, const double *__restrict__ topk_d,
+                              const double *__restrict__ f, const double *__restrict__ scale,
+                              double *__restrict__ z) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x)
+    z[g] = scale[g] > 0.0 ? __dmul_rn(__dadd_rn(topk_d[g * K], f[g]), scale[g])
+                          : __longlong_as_double(0x7ff0000000000000ll);
+}
+
+// depth seed of the best sample: w_photo * dL/dz * scale (optimize.py:340-341)
+__global__ void k_photo_seeds(int64_t n, const double *__restrict__ dz, const double *__restrict__ scale,
+                              double w, double *__restrict__ seed) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x)
+    seed[g] = scale[g] > 0.0 ? __dmul_rn(__dmul_rn(w, dz[g]), scale[g]) : 0.0;
+}
+
 }  // namespace dist
 
 using namespace dist;
@@ -163,6 +208,39 @@ int dist_photometric(const dist_camera *cams_dev, int H, int W, int Hj, int Wj, 
   DIST_CHECK_LAUNCH("k_photo_reduce");
   k_photo_scale<<<grid, 256, 0, st>>>(n, graw, loss_dev, dz_dev);
   DIST_CHECK_LAUNCH("k_photo_scale");
+  return DIST_OK;
+}
+
+int dist_photo_heads(const dist_camera *cams_dev, int n_views, int width, int height, int k_samples,
+                     const dist_ray_state *st, double *points_dev, double *scale_dev, void *stream) {
+  if (!cams_dev || !st || !st->status || !st->topk_d || !st->topk_absf || !points_dev || !scale_dev)
+    return fail(DIST_ERR_CONFIG, "null argument");
+  if (n_views <= 0 || width <= 0 || height <= 0 || k_samples <= 0) return fail(DIST_ERR_CONFIG, "empty trace");
+  const int64_t n = (int64_t)n_views * width * height;
+  const int grid = (int)std::min<int64_t>(ceil_div(n, 256), 4096);
+  k_photo_heads<<<grid, 256, 0, (cudaStream_t)stream>>>(cams_dev, width, height, n, k_samples, st->status,
+                                                        st->topk_d, st->topk_absf, points_dev, scale_dev);
+  DIST_CHECK_LAUNCH("k_photo_heads");
+  return DIST_OK;
+}
+
+int dist_photo_depth(int64_t n, int k_samples, const double *topk_d, const double *f_dev,
+                     const double *scale_dev, double *z_dev, void *stream) {
+  if (!topk_d || !f_dev || !scale_dev || !z_dev || k_samples <= 0) return fail(DIST_ERR_CONFIG, "null argument");
+  if (n <= 0) return DIST_OK;
+  const int grid = (int)std::min<int64_t>(ceil_div(n, 256), 4096);
+  k_photo_depth<<<grid, 256, 0, (cudaStream_t)stream>>>(n, k_samples, topk_d, f_dev, scale_dev, z_dev);
+  DIST_CHECK_LAUNCH("k_photo_depth");
+  return DIST_OK;
+}
+
+int dist_photo_seeds(int64_t n, const double *dz_dev, const double *scale_dev, double w_photo,
+                     double *seed_dev, void *stream) {
+  if (!dz_dev || !scale_dev || !seed_dev) return fail(DIST_ERR_CONFIG, "null argument");
+  if (n <= 0) return DIST_OK;
+  const int grid = (int)std::min<int64_t>(ceil_div(n, 256), 4096);
+  k_photo_seeds<<<grid, 256, 0, (cudaStream_t)stream>>>(n, dz_dev, scale_dev, w_photo, seed_dev);
+  DIST_CHECK_LAUNCH("k_photo_seeds");
   return DIST_OK;
 }
 

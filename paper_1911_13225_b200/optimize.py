@@ -568,6 +568,11 @@ def recover_pose(field, code, observations, intr, pose0, iters: int = 200,
 
 # === multi-view photometric reconstruction (optimize.py:272-358) ===
 
+# reconstruct_multiview runs its iterates on the device for a NeuralField whose
+# views share one resolution; False selects the per-view host loop (tests)
+_DEVICE_MULTIVIEW = True
+
+
 def _nearest_view(centers):
     unit = centers / np.linalg.norm(centers, axis=1, keepdims=True)
     cosine = unit @ unit.T
@@ -601,6 +606,11 @@ def reconstruct_multiview(field, images, cameras, code0=None, iters: int = 60,
     grays = [to_gray(im) for im in images]
     neighbor = _nearest_view(np.stack([c[1].center() for c in cams], axis=0))
     n_views = len(images)
+    if _DEVICE_MULTIVIEW and hasattr(field, "handle") and hasattr(field, "vjp_device") and \
+            field.latent_dim > 0 and \
+            len({(c[0].width, c[0].height) for c in cams}) == 1:
+        return _reconstruct_multiview_device(field, grays, cams, neighbor, code, iters,
+                                             views_per_iter, cfg, weights, lr, rng)
     report = OptimizeReport()
     adam = AdamState(lr=lr)
     best_code = code.copy()
@@ -658,3 +668,113 @@ def reconstruct_multiview(field, images, cameras, code0=None, iters: int = 60,
         report.non_identifiable = True
         _w.warn("photometric loss is flat; views carry no texture signal", RuntimeWarning)
     return best_code, report
+
+
+def _reconstruct_multiview_device(field, grays, cams, neighbor, code, iters, views_per_iter, cfg,
+                                  weights, lr, rng):
+    """reconstruct_multiview with every iterate on the device: one batched
+    trace of the needed views, the best-sample depth heads (dist_photo_heads ->
+    dist_eval -> dist_photo_depth), one dist_photometric warp per sampled view
+    into its neighbour, the depth seeds (dist_photo_seeds), one reverse sweep
+    over all views (dist_eval_vjp), the latent regulariser and Adam with the
+    best-iterate record (dist_adam_step).  The host only draws the view sample
+    (the same generator sequence as the host loop) and reads the history once
+    at the end.  Equals the per-view host loop up to summation order."""
+    import torch
+    import warnings as _w
+
+    from .camera import camera_struct
+    lib = _lib.lib()
+    sp = _lib.stream_ptr
+    intr0 = cams[0][0]
+    W, H = intr0.width, intr0.height
+    npx = W * H
+    K = cfg.k_samples
+    n_views = len(cams)
+    D = field.latent_dim
+    dev = dict(device="cuda", dtype=torch.float64)
+    gray = torch.from_numpy(np.ascontiguousarray(np.stack(grays), dtype=np.float64)).cuda()
+    pair_cams = {}
+    z = torch.from_numpy(np.asarray(code, dtype=np.float64).reshape(1, D).copy()).cuda()
+    m, v = torch.zeros((1, D), **dev), torch.zeros((1, D), **dev)
+    t = torch.zeros(1, dtype=torch.int32, device="cuda")
+    skipped = torch.zeros(1, dtype=torch.int32, device="cuda")
+    best_loss = torch.full((1,), np.inf, **dev)
+    best_code = z.clone()
+    best_iter = torch.full((1,), -1, dtype=torch.int32, device="cuda")
+    hist = torch.zeros(max(iters, 1), **dev)
+    terms = torch.zeros((max(iters, 1), 3), **dev)   # photometric, latent, |g|
+    queries = torch.zeros(1, dtype=torch.int64, device="cuda")
+    warn_bits = torch.zeros(1, dtype=torch.int64, device="cuda")
+    bad = torch.zeros(1, dtype=torch.bool, device="cuda")
+    shape_terms = torch.zeros((1, 2), **dev)
+    adam_cfg = _lib.dist_adam_config(lr, 0.9, 0.999, 1e-8)
+    thresh = 0.001   # photometric_loss default (losses.py:186)
+    t0 = time.perf_counter()
+    for it in range(iters):
+        sel = rng.choice(n_views, size=min(views_per_iter, n_views), replace=False)
+        needed = sorted(set(sel) | {neighbor[i] for i in sel})
+        slot = {i: k for k, i in enumerate(needed)}
+        dt = trace_views(field, z, [cams[i] for i in needed], cfg)
+        queries += dt.stats_dev[0]
+        warn_bits |= dt.stats_dev[3]
+        n = len(needed) * npx
+        pts = torch.empty((n, 3), **dev)
+        scale = torch.empty(n, **dev)
+        st = dt.state_struct()
+        _lib.check(lib.dist_photo_heads(dt.cams.data_ptr(), len(needed), W, H, K, C.byref(st),
+                                        pts.data_ptr(), scale.data_ptr(), sp()))
+        f = field.evaluate_device(pts, z)
+        zimg = torch.empty(n, **dev)
+        _lib.check(lib.dist_photo_depth(n, K, dt.topk_d.data_ptr(), f.data_ptr(), scale.data_ptr(),
+                                        zimg.data_ptr(), sp()))
+        dz = torch.zeros(n, **dev)
+        loss = torch.zeros((len(sel), 2), **dev)
+        vis = torch.empty(npx, dtype=torch.uint8, device="cuda")
+        ws = _lib.workspace(lib.dist_photometric_workspace_size(H, W))
+        for q, i in enumerate(sel):
+            j = int(neighbor[i])
+            key = (int(i), j)
+            if key not in pair_cams:
+                pair_cams[key] = _lib.cameras_to_device([camera_struct(*cams[i]), camera_struct(*cams[j])])
+            a, b = slot[i] * npx, slot[j] * npx
+            _lib.check(lib.dist_photometric(pair_cams[key].data_ptr(), H, W, H, W, zimg[a:].data_ptr(),
+                                            gray[int(i)].data_ptr(), gray[j].data_ptr(), zimg[b:].data_ptr(),
+                                            thresh, loss[q].data_ptr(), dz[a:].data_ptr(), vis.data_ptr(),
+                                            ws.data_ptr(), ws.numel(), sp()))
+        seeds = torch.empty(n, **dev)
+        _lib.check(lib.dist_photo_seeds(n, dz.data_ptr(), scale.data_ptr(), weights.photometric,
+                                        seeds.data_ptr(), sp()))
+        _, gc, _ = field.vjp_device(pts, z, seeds, want_points=False)
+        bad |= ~torch.isfinite(gc).all()
+        photo = loss[:, 0].sum()
+        reg = (z * z).sum()
+        g = gc + weights.latent * (2.0 * z)
+        shape_terms[0, 0] = weights.photometric * photo + weights.latent * reg
+        shape_terms[0, 1] = reg
+        terms[it, 0], terms[it, 1], terms[it, 2] = photo, reg, torch.linalg.vector_norm(g)
+        _lib.check(lib.dist_adam_step(1, D, z.data_ptr(), g.contiguous().data_ptr(), m.data_ptr(),
+                                      v.data_ptr(), t.data_ptr(), skipped.data_ptr(),
+                                      shape_terms.data_ptr(), best_loss.data_ptr(), best_code.data_ptr(),
+                                      best_iter.data_ptr(), it, hist.data_ptr(), C.byref(adam_cfg), None,
+                                      sp()))
+    torch.cuda.synchronize()
+    if bool(bad.item()):
+        raise FloatingPointError("non-finite gradient for leaf 'code'")
+    if int(warn_bits.item()) & 1:
+        _w.warn("camera center inside the unit sphere; rays start at d=0", RuntimeWarning)
+    report = OptimizeReport()
+    hl, tl = hist.cpu().numpy(), terms.cpu().numpy()
+    for it in range(iters):
+        report.record(float(hl[it]), {"photometric": float(tl[it, 0]), "latent": float(tl[it, 1])},
+                      float(tl[it, 2]))
+    report.best_iter = int(best_iter.item())
+    report.best_loss = float(best_loss.item())
+    report.total_queries = int(queries.item())
+    report.skipped_steps = int(skipped.item())
+    report.elapsed = time.perf_counter() - t0
+    if report.grad_norms and max(report.grad_norms) < 1e-10:
+        report.non_identifiable = True
+        _w.warn("photometric loss is flat; views carry no texture signal", RuntimeWarning)
+    best = best_code.cpu().numpy().reshape(D) if report.best_iter >= 0 else np.asarray(code, np.float64)
+    return best, report

@@ -44,6 +44,33 @@ def test_reconstruct_multiview_history_vs_reference(st):
     np.testing.assert_allclose(best, g["mv_best"], rtol=1e-9, atol=1e-12)
 
 
+def test_reconstruct_multiview_device_loop_equals_host_loop(st, monkeypatch):
+    """The device-resident iterate (dist_photo_heads/depth/seeds, one reverse
+    sweep over all views, Adam with the best-iterate record on the device)
+    against the per-view host loop (HeadBundle per view) on the reference's
+    multiview golden scene: same losses, terms, best iterate and code up to
+    summation order, and no host round trip inside the loop."""
+    from paper_1911_13225_b200 import _lib, optimize
+    g = load_golden("multiview24.npz")
+    intr, poses = _views(st, g)
+    net = st.NeuralField(golden_weights(g), latent_dim=2, precision="fp64")
+    cfg = st.TraceConfig(alpha=1.0, k_samples=1, coarse_start_scale=1)
+    kw = dict(code0=g["code"] + 0.1, iters=5, views_per_iter=3, cfg=cfg, seed=4)
+    images, views = list(g["images"]), [(intr, p) for p in poses]
+    n0 = _lib.lib().dist_launch_count()
+    best_d, rep_d = st.reconstruct_multiview(net, images, views, **kw)
+    assert _lib.lib().dist_launch_count() > n0
+    monkeypatch.setattr(optimize, "_DEVICE_MULTIVIEW", False)
+    best_h, rep_h = st.reconstruct_multiview(net, images, views, **kw)
+    np.testing.assert_allclose(rep_d.losses, rep_h.losses, rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose([t["photometric"] for t in rep_d.terms],
+                               [t["photometric"] for t in rep_h.terms], rtol=1e-12, atol=1e-15)
+    np.testing.assert_allclose(rep_d.grad_norms, rep_h.grad_norms, rtol=1e-10, atol=1e-15)
+    assert rep_d.best_iter == rep_h.best_iter
+    assert rep_d.total_queries == rep_h.total_queries
+    np.testing.assert_allclose(best_d, best_h, rtol=1e-12, atol=1e-15)
+
+
 def test_attribute_field_and_map_vs_reference(st):
     """sigmoid-head colour MLP at hit points."""
     g = load_golden("attr32.npz")
