@@ -298,6 +298,33 @@ DIST_API int dist_photo_depth(int64_t n, int k_samples, const double *topk_d, co
 DIST_API int dist_photo_seeds(int64_t n, const double *dz_dev, const double *scale_dev,
                               double w_photo, double *seed_dev, void *stream);
 
+/* pose_objective on the device (optimize.py:185-233): one
+ * traced view, dense rows K per pixel (row g*K + k is a head sample when pixel
+ * g is recorded and top-K slot k is finite; other rows: origin, seed 0).
+ * dist_pose_samples: points_dev[row] = origin + topk_d * dir.
+ * dist_pose_seeds: loss_dev[0] = depth_loss (losses.py:54-75; obs_depth [H*W]
+ *   camera z with obs_valid [H*W] = finite & trusted, or NULL for no depth
+ *   term), loss_dev[1] = silhouette_loss (losses.py:78-91; soft_sil = the
+ *   dist_maps silhouette, obs_sil the target, both NULL for no term),
+ *   loss_dev[2] = n_px; seed_dev[row] = w_depth * depth seed + w_sil *
+ *   silhouette seed (best sample), f_dev = dist_eval at points_dev.
+ * dist_pose_grad: grad_dev[6] = (dL/d omega, dL/d t) by camera.py:255-278 from
+ *   the rows' point gradients (dist_eval_vjp) and the unrecorded pixels'
+ *   silhouette term at the ray's closest point to the origin
+ *   (optimize.py:220-229); mats_dev = R, dR/d omega_0..2 (row-major 3x3) and t
+ *   (39 doubles, camera.rotation_derivatives). */
+DIST_API int dist_pose_samples(const dist_camera *cam_dev, int width, int height, int k_samples,
+                               const dist_ray_state *st, double *points_dev, void *stream);
+DIST_API int dist_pose_seeds(const dist_camera *cam_dev, int width, int height, int k_samples,
+                             const dist_ray_state *st, const double *f_dev, const double *obs_depth,
+                             const uint8_t *obs_valid, const double *soft_sil, const double *obs_sil,
+                             double w_depth, double w_sil, double *loss_dev, double *seed_dev,
+                             void *stream);
+DIST_API int dist_pose_grad(const dist_camera *cam_dev, int width, int height, int k_samples,
+                            const dist_ray_state *st, const double *point_grads_dev,
+                            const double *soft_sil, const double *obs_sil, double w_sil,
+                            const double *mats_dev, double *grad_dev, void *stream);
+
 /* ---- Adam (AdamState/adam_step, optimize.py:35-63) ------------------------ */
 typedef struct dist_adam_config {
   double lr, beta1, beta2, eps;

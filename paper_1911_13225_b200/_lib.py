@@ -117,6 +117,14 @@ _SIGS = {
                                    C.c_void_p]),
     "dist_photo_seeds": (C.c_int, [C.c_int64, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                    C.c_void_p]),
+    "dist_pose_samples": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(dist_ray_state),
+                                    C.c_void_p, C.c_void_p]),
+    "dist_pose_seeds": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(dist_ray_state),
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                  C.c_double, C.c_double, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "dist_pose_grad": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(dist_ray_state),
+                                 C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                                 C.c_void_p, C.c_void_p]),
     "dist_adam_step": (C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                  C.c_void_p, C.c_int, C.c_void_p, C.POINTER(dist_adam_config),

@@ -503,6 +503,8 @@ def pose_objective(field, code, observations, intr, params, cfg: TraceConfig,
     from .tracer import trace
     pose = Pose.from_params(params)
     obs = _split_observations(observations)
+    if _device_pose(field):
+        return _pose_objective_device(field, code, _pose_obs_device(obs, intr), intr, params, cfg, weights)
     result = trace(field, code, intr, pose, cfg)
     heads = diff_heads(result, field, code)
     terms = {}
@@ -548,10 +550,15 @@ def recover_pose(field, code, observations, intr, pose0, iters: int = 200,
     report = OptimizeReport()
     adam = AdamState(lr=lr)
     best = params.copy()
+    dev_obs = _pose_obs_device(_split_observations(observations), intr) if _device_pose(field) else None
     t0 = time.perf_counter()
     for it in range(iters):
-        total, terms, g, queries = pose_objective(field, code, observations, intr, params, cfg,
-                                                  weights)
+        if dev_obs is not None:
+            total, terms, g, queries = _pose_objective_device(field, code, dev_obs, intr, params, cfg,
+                                                              weights)
+        else:
+            total, terms, g, queries = pose_objective(field, code, observations, intr, params, cfg,
+                                                      weights)
         report.total_queries += queries
         report.record(total, terms, float(np.linalg.norm(g)))
         if total < report.best_loss:
@@ -567,6 +574,89 @@ def recover_pose(field, code, observations, intr, pose0, iters: int = 200,
 
 
 # === multi-view photometric reconstruction (optimize.py:272-358) ===
+
+# pose_objective / recover_pose run the objective on the device for a NeuralField
+# (dist_pose_*); False selects the HeadBundle host path (tests)
+_DEVICE_POSE = True
+
+
+def _device_pose(field) -> bool:
+    return _DEVICE_POSE and hasattr(field, "handle") and hasattr(field, "vjp_device")
+
+
+def _pose_obs_device(obs: dict, intr) -> dict:
+    """The depth / silhouette observations of a pose fit, resident on the device."""
+    import torch
+    out = {}
+    shape = (intr.height, intr.width)
+    if "depth" in obs:
+        o = obs["depth"]
+        if o.image.shape != shape:
+            raise ValueError("depth observation shape differs from the view")
+        out["depth"] = torch.from_numpy(np.ascontiguousarray(o.image, dtype=np.float64)).cuda()
+        out["depth_valid"] = torch.from_numpy(np.ascontiguousarray(o.valid(), dtype=np.uint8)).cuda()
+    if "silhouette" in obs:
+        t = np.asarray(obs["silhouette"].image, dtype=np.float64)
+        if t.shape != shape:
+            raise ValueError("silhouette shapes differ")
+        out["silhouette"] = torch.from_numpy(np.ascontiguousarray(t)).cuda()
+    return out
+
+
+def _pose_objective_device(field, code, obs, intr, params, cfg, weights):
+    """pose_objective with every per-pixel step on the device: the trace,
+    dense sample rows (dist_pose_samples), f (dist_eval), the depth and
+    silhouette losses and seeds (dist_pose_seeds, with the dist_maps soft
+    silhouette), the point gradients (dist_eval_vjp) and the 6-parameter chain
+    rule (dist_pose_grad).  The host reads 10 numbers per iterate."""
+    import torch
+    import warnings as _w
+
+    from .camera import Pose, rotation_derivatives
+    from .tracer import trace_views
+    pose = Pose.from_params(params)
+    lib = _lib.lib()
+    sp = _lib.stream_ptr()
+    W, H, K = intr.width, intr.height, cfg.k_samples
+    dev = dict(device="cuda", dtype=torch.float64)
+    dt = trace_views(field, code, [(intr, pose)], cfg)
+    st = dt.state_struct()
+    pts = torch.empty((W * H * K, 3), **dev)
+    _lib.check(lib.dist_pose_samples(dt.cams.data_ptr(), W, H, K, C.byref(st), pts.data_ptr(), sp))
+    f = field.evaluate_device(pts, code)
+    soft = None
+    if "silhouette" in obs:
+        soft = torch.empty(W * H, **dev)
+        c = _lib.config_struct(cfg)
+        _lib.check(lib.dist_maps(dt.cams.data_ptr(), 1, W, H, C.byref(c), C.byref(st), None, None,
+                                 soft.data_ptr(), sp))
+    out = torch.zeros(10, **dev)   # depth, silhouette, n_px, queries, grad[6]
+    seeds = torch.empty(W * H * K, **dev)
+    _lib.check(lib.dist_pose_seeds(dt.cams.data_ptr(), W, H, K, C.byref(st), f.data_ptr(),
+                                   _lib.ptr(obs.get("depth")), _lib.ptr(obs.get("depth_valid")),
+                                   _lib.ptr(soft), _lib.ptr(obs.get("silhouette")), weights.depth,
+                                   weights.silhouette, out.data_ptr(), seeds.data_ptr(), sp))
+    _, _, gp = field.vjp_device(pts, code, seeds, want_points=True)
+    R, dRs = rotation_derivatives(pose.omega)
+    mats = np.concatenate([R.ravel()] + [d.ravel() for d in dRs] + [np.asarray(pose.t, np.float64)])
+    mats_dev = torch.from_numpy(mats).cuda()
+    _lib.check(lib.dist_pose_grad(dt.cams.data_ptr(), W, H, K, C.byref(st), gp.data_ptr(),
+                                  _lib.ptr(soft), _lib.ptr(obs.get("silhouette")), weights.silhouette,
+                                  mats_dev.data_ptr(), out[4:].data_ptr(), sp))
+    out[3] = dt.stats_dev[0].to(torch.float64)
+    v = out.cpu().numpy()
+    if not np.all(np.isfinite(v[4:])):
+        raise FloatingPointError("non-finite gradient for leaf 'points'")
+    terms = {}
+    if "depth" in obs:
+        if v[2] == 0:
+            _w.warn("depth loss: no overlap between observation and render", RuntimeWarning)
+        terms["depth"] = float(v[0])
+    if "silhouette" in obs:
+        terms["silhouette"] = float(v[1])
+    total = weights.depth * terms.get("depth", 0.0) + weights.silhouette * terms.get("silhouette", 0.0)
+    return total, terms, v[4:10].copy(), int(v[3])
+
 
 # reconstruct_multiview runs its iterates on the device for a NeuralField whose
 # views share one resolution; False selects the per-view host loop (tests)
