@@ -4,7 +4,7 @@ The reference sums per-view gradients on one host (optimize.py:309-351,
 `g += hg["code"]` at :340, the regulariser once at :341).  Here every view is
 cut into `tile` x `tile` pixel tiles (a multiple of the coarse-to-fine block,
 so the split tree tracer.py:196-218 never crosses a tile) and the tiles of all
-views are dealt round-robin over the ranks, so every rank marches rays of
+views are dealt round-robin (skewed per tile row) over the ranks, so every rank marches rays of
 every view and the per-view cost skew averages out.
 
 A tile is traced as a view of its own: same rotation, centre and focal
@@ -63,8 +63,22 @@ class Tile:
     pose: object
 
 
+# Tile (tx, ty) of view v goes to rank (tx + DEAL_SKEW * ty + v) % world: each
+# row of tiles is dealt round-robin, shifted by DEAL_SKEW per row, so a rank's
+# tiles form diagonal stripes a few tiles apart instead of whole tile columns
+# (a centred object made the column deal uneven).  0: plain round-robin over
+# the global tile order.
+DEAL_SKEW = 3
+
+
+def _owner(t: int, tx: int, ty: int, v: int, world: int) -> int:
+    if DEAL_SKEW == 0:
+        return t % world
+    return (tx + DEAL_SKEW * ty + v) % world
+
+
 def tile_split(views, tile: int, rank: int, world: int, coarse: int = 4):
-    """The tiles of `rank` (round-robin over the global tile order) and the
+    """The tiles of `rank` (row-skewed round-robin, DEAL_SKEW) and the
     total tile count."""
     if tile % coarse:
         raise ValueError(f"tile {tile} must be a multiple of coarse_start_scale {coarse}")
@@ -77,7 +91,7 @@ def tile_split(views, tile: int, rank: int, world: int, coarse: int = 4):
         cx, cy = intr.center
         for y0 in range(0, intr.height, tile):
             for x0 in range(0, intr.width, tile):
-                if t % world == rank:
+                if _owner(t, x0 // tile, y0 // tile, v, world) == rank:
                     ti = TileIntrinsics(intr.focal_mm, intr.sensor_mm, tile, tile, cx - x0, cy - y0,
                                         fx_parent=intr.fx)
                     out.append(Tile(t, v, x0, y0, ti, pose))

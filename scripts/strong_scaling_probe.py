@@ -29,7 +29,10 @@ ap.add_argument("--tile", type=int, default=32)
 ap.add_argument("--steps", type=int, default=4)
 ap.add_argument("--warmup", type=int, default=2)
 ap.add_argument("--worlds", default="1,2,4,8")
+ap.add_argument("--skew", type=int, default=None, help="shard.DEAL_SKEW (0: plain round-robin)")
 args = ap.parse_args()
+if args.skew is not None:
+    shard_mod.DEAL_SKEW = args.skew
 
 shard_mod.all_reduce_sum = lambda t, group=None, world=1: t
 shard_mod.fixed_all_reduce = lambda b, group=None, world=1: b
@@ -66,7 +69,7 @@ for G in [int(x) for x in args.worlds.split(",")]:
     worst = max(p[0] for p in per_rank)
     val = rays / (worst * 1e-3)
     base = base or val
-    print(json.dumps({"G": G, "tile": args.tile, "max_rank_ms": worst,
+    print(json.dumps({"G": G, "tile": args.tile, "skew": shard_mod.DEAL_SKEW, "max_rank_ms": worst,
                       "rank_ms": [round(p[0], 2) for p in per_rank],
                       "rank_trace_ms": [round(p[1], 2) for p in per_rank],
                       "rank_queries": [p[2] for p in per_rank],

@@ -1,6 +1,6 @@
 """Multi-rank latent optimisation on the product path, run as two
 ranks on the one available GPU: each rank is a process that drives
-LatentOptimizer.step() on its round-robin share of the pixel tiles of every
+LatentOptimizer.step() on its skewed round-robin share of the pixel tiles of every
 view (paper_1911_13225_b200/shard.py), with gloo carrying the two tiny
 per-iterate collectives.  The ranks' kernels never wait on each other (the
 collectives are host-side), so sharing one GPU changes timing only.

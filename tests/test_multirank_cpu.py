@@ -108,8 +108,11 @@ def test_tile_split_partitions_every_pixel_once(world):
     for r in range(world):
         tiles, total = tile_split(views, 16, r, world)
         for t in tiles:
-            assert t.index % world == r
+            # skewed deal: row ty of view v shifted by 3 ty + v (shard.DEAL_SKEW)
+            assert (t.x0 // 16 + 3 * (t.y0 // 16) + t.view) % world == r
             seen[t.view, t.y0:t.y0 + 16, t.x0:t.x0 + 16] += 1
+        if world in (1, 2):   # 4 tiles per row: every rank gets the same count
+            assert len(tiles) == 3 * 16 // world
     assert total == 3 * 16 and np.all(seen == 1)
     with pytest.raises(ValueError):
         tile_split(views, 6, 0, world)   # not a multiple of the coarse block
