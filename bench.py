@@ -238,7 +238,7 @@ def run_reference(args):
 
 def _config(args, world=1):
     strong = (world > 1 and args.scaling == "strong") or getattr(args, "force_tiles", False)
-    par = (f"C3's {VIEWS_PER_RANK} views cut into {args.tile}x{args.tile} pixel tiles dealt round-robin "
+    par = (f"C3's {VIEWS_PER_RANK} views cut into {args.tile}x{args.tile} pixel tiles dealt round-robin (row-skewed) "
            f"over {world} GPUs (strong scaling), exact fixed-point gradient all-reduce"
            if strong else
            f"views sharded over {world} GPU(s) (ring interleaved, {VIEWS_PER_RANK} per GPU), latent all-reduce")
