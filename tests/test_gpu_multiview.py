@@ -81,3 +81,25 @@ def test_attribute_field_and_map_vs_reference(st):
     maps = st.render(net, g["code"], st.Intrinsics(width=32, height=32), st.look_at((0.0, 0.0, -2.0)),
                      st.TraceConfig(), attr_field=attr, attr_code=g["acode"])
     np.testing.assert_allclose(maps.attribute, g["amap"], rtol=0, atol=1e-12)
+
+
+def test_reconstruct_multiview_device_loop_tensor_core_decoder(st, monkeypatch):
+    """The device iterate on the 8x512 fp16x3 decoder (K = 3 records, the
+    default coarse-to-fine start) against the per-view host loop: the same
+    kernels evaluate the same sample points, so the histories agree to
+    summation order."""
+    from paper_1911_13225_b200 import optimize
+    from paper_1911_13225_b200.workloads import ring_views, target_code
+    net = st.NeuralField.geometric(256, (512,) * 8, 0, precision="fp16x3")
+    views = ring_views(6, 64)
+    yy, xx = np.mgrid[0:64, 0:64] / 64.0
+    images = [np.stack([0.5 + 0.5 * np.sin(9 * xx + k), 0.5 + 0.5 * np.cos(7 * yy - k), xx * yy], axis=2)
+              for k in range(6)]
+    kw = dict(code0=target_code(1) * 0.9, iters=3, views_per_iter=3, cfg=st.TraceConfig(k_samples=3), seed=2)
+    best_d, rep_d = st.reconstruct_multiview(net, images, views, **kw)
+    monkeypatch.setattr(optimize, "_DEVICE_MULTIVIEW", False)
+    best_h, rep_h = st.reconstruct_multiview(net, images, views, **kw)
+    np.testing.assert_allclose(rep_d.losses, rep_h.losses, rtol=1e-9)
+    np.testing.assert_allclose(best_d, best_h, rtol=1e-7, atol=1e-12)
+    assert rep_d.best_iter == rep_h.best_iter and rep_d.total_queries == rep_h.total_queries
+    assert min(rep_d.grad_norms) > 0
