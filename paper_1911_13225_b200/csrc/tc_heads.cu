@@ -923,6 +923,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             if (nb) atomicOr(P.bad, 1);
             tc_fence_before();
             epi_sync();
+            TL(10);
             fx_t *dst = P.part0 + ((size_t)blockIdx.x * P.S + next) * n0;
             for (int col = threadIdx.x - 64; col < KDIM; col += N_EPI_WARPS * 32)
               dst[col] += redx[col] + redx[512 + col];

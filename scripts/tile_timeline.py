@@ -30,7 +30,7 @@ MLP = {1: "tile start", 2: "layer0 A ready", 10: "prev tile rows done", 3: "D (n
        9: "head done", 11: "nh=1 MMAs past K 3 (afree)", 12: "parked copied", 13: "K 0..3 announced",
        14: "nh=1 half done"}
 HEADS = {1: "tile start", 2: "layer0 A ready", 3: "fwd D ready", 4: "fwd A ready", 5: "seed done",
-         6: "bwd A0 ready", 7: "bwd D ready", 8: "bwd A ready", 9: "colsum done"}
+         6: "bwd A0 ready", 7: "bwd D ready", 8: "bwd A ready", 9: "colsum done", 10: "colsum chunks done"}
 
 
 def show(fn, names, label):
