@@ -138,6 +138,16 @@ DIST_API int dist_eval(const dist_decoder *dec, const double *codes_dev, int n_s
               const double *points_dev, const int32_t *shape_dev, int64_t n,
               double *f_dev, void *ws, size_t ws_bytes, void *stream);
 
+/* AttributeField.evaluate (fields.py:332-338): m <= 8 decoders that share
+ * every layer but the last (the attribute field's channels, each a
+ * single-output sigmoid-head decoder over the same hidden stack), evaluated
+ * with the hidden stack of decs[0] computed once: out[i*m + c] = channel c at
+ * points[i], bit-identical to dist_eval of decs[c].  SIMT precisions only;
+ * the workspace is dist_eval_workspace_size(decs[0], n, n_shapes). */
+DIST_API int dist_eval_channels(const dist_decoder *const *decs, int m, const double *codes_dev,
+                                int n_shapes, const double *points_dev, const int32_t *shape_dev,
+                                int64_t n, double *out_dev, void *ws, size_t ws_bytes, void *stream);
+
 /* Taped evaluation + reverse sweep (fields.py:260-291 with
  * autodiff.py:220-255): f, d(sum seed*f)/d code [S,D] and d/d points [n,3]
  * (grad_points_dev may be NULL). */

@@ -107,6 +107,8 @@ _SIGS = {
     "dist_objective": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_int,
                                  C.c_int, C.POINTER(dist_trace_config), C.POINTER(dist_ray_state),
                                  C.POINTER(dist_objective_io), C.c_void_p, C.c_size_t, C.c_void_p]),
+    "dist_eval_channels": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                     C.c_int64, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "dist_photometric_workspace_size": (C.c_size_t, [C.c_int, C.c_int]),
     "dist_photometric": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,

@@ -470,6 +470,44 @@ int dist_eval(const dist_decoder *dec, const double *codes, int S, const double 
   return eval_points(dv, c0, cs, s1, pts, shape, n, f, st);
 }
 
+int dist_eval_channels(const dist_decoder *const *decs, int m, const double *codes, int S,
+                       const double *pts, const int32_t *shape, int64_t n, double *out, void *ws,
+                       size_t ws_bytes, void *stream) {
+  if (!decs || !decs[0] || !out) return fail(DIST_ERR_CONFIG, "null argument");
+  if (m < 1 || m > kMaxHeads) return fail(DIST_ERR_CONFIG, "channel count must be in [1, 8]");
+  const dist_decoder *d0 = decs[0];
+  const DecView &dv = d0->view;
+  if (dv.prec >= DIST_PREC_BF16X3)
+    return fail(DIST_ERR_CONFIG, "dist_eval_channels takes the SIMT precisions (fp64, fp32)");
+  HeadSet hs{};
+  hs.m = m;
+  const int wi = dv.prec == DIST_PREC_FP64 ? 0 : 1;
+  for (int c = 0; c < m; ++c) {
+    const dist_decoder *dc = decs[c];
+    if (!dc) return fail(DIST_ERR_CONFIG, "null decoder");
+    const DecView &v = dc->view;
+    bool same = v.n_layers == dv.n_layers && v.latent_dim == dv.latent_dim && v.skip == dv.skip &&
+                v.prec == dv.prec && v.final_act == dv.final_act;
+    for (int l = 0; same && l <= dv.n_layers; ++l) same = dc->dims[l] == d0->dims[l];
+    if (!same) return fail(DIST_ERR_CONFIG, "channel decoders must share layout, precision and head activation");
+    hs.w[c] = v.w_out[wi];
+    hs.b[c] = v.b_out;
+  }
+  if (dv.latent_dim > 0 && (!codes || S < 1)) return fail(DIST_ERR_CONFIG, "field expects a latent code");
+  if (n <= 0) return DIST_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  Carve cv{(char *)ws, 0, ws_bytes};
+  const int s1 = std::max(S, 1);
+  double *c0 = cv.take<double>(c0_doubles(s1, dv.np[0]));
+  double *cs = cv.take<double>(c0_doubles(s1, std::max(dv.nskip, 1)));
+  if (!cv.ok) return fail(DIST_ERR_CONFIG, "workspace too small");
+  int rc = launch_code_bias(dv, dv.latent_dim > 0 ? codes : nullptr, s1, c0, cs, st);
+  if (rc) return rc;
+  ArrayGen g{pts, shape, nullptr, nullptr, n};
+  if (dv.prec == DIST_PREC_FP64) return launch_eval_channels<double>(dv, c0, cs, g, hs, out, st);
+  return launch_eval_channels<float>(dv, c0, cs, g, hs, out, st);
+}
+
 int dist_eval_vjp(const dist_decoder *dec, const double *codes, int S, const double *pts,
                   const int32_t *shape, int64_t n, const double *seed, double *f,
                   double *grad_codes, double *gpts, void *ws, size_t ws_bytes, void *stream) {

@@ -148,6 +148,63 @@ struct ArrayGen {
 
 int sm_count();
 
+// Heads of up to kMaxHeads decoders that share every layer but the last
+// (AttributeField's channels, fields.py:332-338): the hidden stack runs once
+// per tile, then each head; out[i * m + c].
+constexpr int kMaxHeads = 8;
+struct HeadSet {
+  const void *w[kMaxHeads];   // head weights in the tile's arithmetic type
+  double b[kMaxHeads];
+  int m;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(SimtTile<T>::NT)
+    k_eval_channels(DecView dv, const double *__restrict__ c0, const double *__restrict__ cskip,
+                    ArrayGen gen, HeadSet hs, double *__restrict__ out) {
+  extern __shared__ __align__(16) char smem[];
+  using Tile = SimtTile<T>;
+  Tile tile(smem);
+  const int64_t n = gen.count();
+  const int64_t ntiles = ceil_div(n, Tile::TM);
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t base = t * Tile::TM;
+    if (threadIdx.x < Tile::TM) {
+      const int64_t i = base + threadIdx.x;
+      double p[3] = {0.0, 0.0, 0.0};
+      int s = -1;
+      if (i < n && !gen.point(i, p, s)) s = -1;
+      tile.shape[threadIdx.x] = s;
+      for (int a = 0; a < 3; ++a) tile.pts[threadIdx.x * 3 + a] = p[a];
+    }
+    __syncthreads();
+    tile.layer0(dv, c0, false);
+    for (int l = 1; l <= dv.n_layers - 2; ++l) tile.hidden(dv, l, cskip, false);
+    for (int c = 0; c < hs.m; ++c) {
+      tile.output_head(dv, reinterpret_cast<const T *>(hs.w[c]), hs.b[c]);
+      if (threadIdx.x < Tile::TM && base + threadIdx.x < n) out[(base + threadIdx.x) * hs.m + c] = tile.f[threadIdx.x];
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+int launch_eval_channels(const DecView &dv, const double *c0, const double *cskip, const ArrayGen &gen,
+                         const HeadSet &hs, double *out, cudaStream_t st) {
+  using Tile = SimtTile<T>;
+  const void *fn = (const void *)k_eval_channels<T>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)Tile::fwd_bytes);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaFuncSetAttribute(eval_channels)");
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, Tile::NT, Tile::fwd_bytes);
+  const int64_t tiles = std::max<int64_t>(1, ceil_div(gen.n, Tile::TM));
+  const int grid = (int)std::min<int64_t>(tiles, (int64_t)std::max(per_sm, 1) * sm_count());
+  k_eval_channels<T><<<grid, Tile::NT, Tile::fwd_bytes, st>>>(dv, c0, cskip, gen, hs, out);
+  DIST_CHECK_LAUNCH("k_eval_channels");
+  return DIST_OK;
+}
+
 template <typename T, class Gen, bool PAIR = false>
 int launch_eval_gen(const DecView &dv, const double *c0, const double *cskip, const Gen &gen,
                     int64_t n_bound, cudaStream_t st) {

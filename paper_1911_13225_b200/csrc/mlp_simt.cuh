@@ -175,9 +175,13 @@ struct SimtTile {
 
   // Output layer: f[row] = head(H[:,row] . w_out + b_out).
   __device__ void output(const DecView &dv) {
+    output_head(dv, reinterpret_cast<const T *>(dv.w_out[WI]), dv.b_out);
+  }
+  // the same with another head (w, b_out) on this decoder's last hidden layer
+  // (AttributeField channels, dist_eval_channels)
+  __device__ void output_head(const DecView &dv, const T *w, double b_out) {
     const int tid = threadIdx.x;
     const int K = dv.np[dv.n_layers - 2];
-    const T *w = reinterpret_cast<const T *>(dv.w_out[WI]);
     constexpr int P = NT / TM;  // threads per row
     const int row = tid % TM, part = tid / TM;
     T acc = (T)0;
@@ -188,7 +192,7 @@ struct SimtTile {
       double s = 0.0;
 #pragma unroll
       for (int p = 0; p < P; ++p) s += red[p * TM + tid];
-      s += dv.b_out;
+      s += b_out;
       f[tid] = head_act(dv.final_act, s);
     }
     __syncthreads();

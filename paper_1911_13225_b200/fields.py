@@ -211,8 +211,10 @@ class NeuralField:
 
 class AttributeField:
     """MLP from concat(shape code, attribute code, p) to an m-vector in [0, 1]
-    (fields.py:294-338).  Evaluated on the device as m
-    single-output sigmoid-head decoders sharing the hidden stack."""
+    (fields.py:294-338).  Held on the device as m
+    single-output sigmoid-head decoders over the same hidden stack;
+    `dist_eval_channels` runs that stack once per point and then the m heads
+    (SIMT precisions, m <= 8; otherwise each channel is evaluated in turn)."""
 
     def __init__(self, weights, shape_dim: int = 0, attr_dim: int = 0,
                  hidden_activation: str = "relu", precision: str = "fp64"):
@@ -247,7 +249,28 @@ class AttributeField:
             if code.shape != (d,):
                 raise ValueError(f"attribute code shape {code.shape} != ({d},)")
         p = _pts(points)
+        if self.out_dim <= 8 and self._channels[0].precision in ("fp64", "fp32"):
+            return self.evaluate_device(p, code if d else None).cpu().numpy()
         return np.stack([ch.evaluate(p, code if d else None) for ch in self._channels], axis=1)
+
+    def evaluate_device(self, points, code=None):
+        """[n, m] on the device: the hidden stack once, then the m heads."""
+        import torch
+        ch0 = self._channels[0]
+        z, S = ch0._codes_dev(code, torch)
+        P = points if isinstance(points, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(points))
+        P = P.to(device="cuda", dtype=torch.float64).reshape(-1, 3).contiguous()
+        n = P.shape[0]
+        out = torch.empty((n, self.out_dim), dtype=torch.float64, device="cuda")
+        if n == 0:
+            return out
+        lib = _lib.lib()
+        handles = (C.c_void_p * self.out_dim)(*[ch.handle() for ch in self._channels])
+        ws = _lib.workspace(lib.dist_eval_workspace_size(ch0.handle(), n, S))
+        _lib.check(lib.dist_eval_channels(C.cast(handles, C.c_void_p), self.out_dim, _lib.ptr(z), S,
+                                          P.data_ptr(), None, n, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                          _lib.stream_ptr()))
+        return out
 
 
 def eval_field(field, points, code=None):

@@ -103,3 +103,19 @@ def test_reconstruct_multiview_device_loop_tensor_core_decoder(st, monkeypatch):
     np.testing.assert_allclose(best_d, best_h, rtol=1e-7, atol=1e-12)
     assert rep_d.best_iter == rep_h.best_iter and rep_d.total_queries == rep_h.total_queries
     assert min(rep_d.grad_norms) > 0
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_attribute_channels_one_hidden_stack(st, prec):
+    """dist_eval_channels (the hidden stack once, then the m heads) equals each
+    channel's own single-output decoder bit for bit, with a shape+attribute
+    code and a 3-channel head."""
+    rng = np.random.default_rng(5)
+    attr = st.AttributeField.init(shape_dim=3, attr_dim=2, hidden=(32, 48, 32), out_dim=3, rng=rng,
+                                  precision=prec)
+    pts = rng.uniform(-1, 1, (1000, 3))
+    code = rng.normal(0, 0.3, 5)
+    got = attr.evaluate(pts, code)
+    ref = np.stack([ch.evaluate(pts, code) for ch in attr._channels], axis=1)
+    assert got.shape == (1000, 3)
+    np.testing.assert_array_equal(got, ref)
