@@ -119,3 +119,20 @@ def test_attribute_channels_one_hidden_stack(st, prec):
     ref = np.stack([ch.evaluate(pts, code) for ch in attr._channels], axis=1)
     assert got.shape == (1000, 3)
     np.testing.assert_array_equal(got, ref)
+
+
+def test_reconstruct_multiview_device_zero_iters_and_all_views(st):
+    """Edge cases of the device loop: no iterate returns the start code; every
+    view sampled each iterate (views_per_iter >= n_views)."""
+    g = load_golden("multiview24.npz")
+    intr, poses = _views(st, g)
+    net = st.NeuralField(golden_weights(g), latent_dim=2, precision="fp64")
+    cfg = st.TraceConfig(alpha=1.0, k_samples=1, coarse_start_scale=1)
+    views = [(intr, p) for p in poses]
+    best, rep = st.reconstruct_multiview(net, list(g["images"]), views, code0=g["code"] + 0.1, iters=0,
+                                         cfg=cfg)
+    np.testing.assert_array_equal(best, g["code"] + 0.1)
+    assert rep.losses == [] and rep.best_iter == -1
+    best, rep = st.reconstruct_multiview(net, list(g["images"]), views, code0=g["code"] + 0.1, iters=2,
+                                         views_per_iter=len(views) + 3, cfg=cfg)
+    assert len(rep.losses) == 2 and np.all(np.isfinite(rep.losses)) and rep.total_queries > 0

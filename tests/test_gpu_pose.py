@@ -89,3 +89,21 @@ def test_pose_objective_device_fp16x3_8x512(st, monkeypatch):
     np.testing.assert_allclose(a[2], b[2], rtol=1e-6, atol=1e-9)
     assert a[3] == b[3]
     assert np.linalg.norm(a[2]) > 0
+
+
+def test_recover_pose_device_equals_host_fp32_k3(st, monkeypatch):
+    """recover_pose through the device objective and the host path, fp32
+    decoder, K = 3, learning-rate decay: the same iterate history."""
+    from paper_1911_13225_b200 import optimize
+    g, _, obs, intr, _ = _setup(st, "fp64")
+    net = st.NeuralField(golden_weights(g), latent_dim=2, precision="fp32")
+    cfg = st.TraceConfig(alpha=1.0, k_samples=3, coarse_start_scale=1)
+    p0 = st.Pose.from_params(np.asarray(g["params"]) + np.array([0.02, 0.0, -0.01, 0.01, 0.02, 0.0]))
+    kw = dict(iters=6, cfg=cfg, lr_decay_every=3)
+    best_d, rep_d = st.recover_pose(net, g["code"], obs, intr, p0, **kw)
+    monkeypatch.setattr(optimize, "_DEVICE_POSE", False)
+    best_h, rep_h = st.recover_pose(net, g["code"], obs, intr, p0, **kw)
+    np.testing.assert_allclose(rep_d.losses, rep_h.losses, rtol=1e-9)
+    np.testing.assert_allclose(rep_d.grad_norms, rep_h.grad_norms, rtol=1e-6)
+    assert rep_d.best_iter == rep_h.best_iter and rep_d.total_queries == rep_h.total_queries
+    np.testing.assert_allclose(best_d.params(), best_h.params(), rtol=1e-9, atol=1e-12)
