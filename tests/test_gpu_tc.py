@@ -315,3 +315,33 @@ def test_ring_trace_parity_vs_fp64_north_star_band(st, prec):
     assert conv.sum() > 0.2 * n
     rel = np.abs(d1[conv] - d0[conv]) / np.abs(d0[conv])
     assert rel.max() <= 1e-4
+
+
+@pytest.mark.parametrize("kw", [
+    dict(alpha=1.0, k_samples=1, epsilon=1e-3, coarse_start_scale=1),
+    dict(alpha=1.9, k_samples=5, coarse_start_scale=2, split_interval=2),
+    dict(alpha=1.5, k_samples=3, max_steps=20),
+    dict(alpha=1.5, k_samples=2, use_dynamic_mask=False),
+])
+def test_tc_trace_config_variants_vs_oracle(st, kw):
+    """TraceConfig corners on the fp16x3 march (plain and strongly over-relaxed steps,
+    K = 1 and 5, coarse starts 1 / 2 / 4, split every 2 steps, a tight step
+    budget, the dynamic mask off) against the fp64 oracle under the module's
+    band contract, with per-pixel step counts and the query total."""
+    res, seed = 32, 3
+    net = st.NeuralField.geometric(256, (512,) * 8, seed, precision="fp16x3")
+    code = np.random.default_rng(11).normal(0, 0.1, 256) * 0.3
+    cam = orc.cam_look_at(orc.ring_eye(2, 8), res, res)
+    dec = orc.Decoder(orc.geometric_init(256, (512,) * 8, seed), 256)
+    T = orc.trace(lambda p: dec(p, code), cam, orc.Cfg(**kw))
+    r = st.trace(net, code, st.Intrinsics(width=res, height=res), st.Pose(cam.omega, cam.t),
+                 st.TraceConfig(**kw))
+    band = (T.margin_f < 1e-5) | (T.margin_esc < 1e-6)
+    mism = (r.state.status != T.status) | (r.state.steps != T.steps)
+    assert not np.any(((r.state.status == 1) != (T.status == 1)) & ~band)
+    assert (mism & ~band).sum() <= max(1, 1e-3 * mism.size), np.nonzero(mism & ~band)
+    tq = sum(T.live_counts)
+    assert abs(r.total_queries - tq) <= max(2, 2e-3 * tq)
+    if kw.get("max_steps", 100) == 20:
+        assert (T.status == 3).sum() > 0   # the budget exhausts rays
+    assert (T.status == 1).sum() > 50
